@@ -1,0 +1,186 @@
+/*
+ * svh.h -- C-ABI of libsvh, the B200 (sm_100a) hot path of SuperVoxHenry
+ * (arXiv 2105.08627; PAPER.md cited as P:<line>).
+ *
+ * The library computes, for a voxelised superconducting structure, the
+ * FFT-accelerated VIE matrix-vector product CC = Z.I of Eq. 9 with
+ * the two-fluid local term (Eq. 3, App. A Eq. 16-23), the saddle-system
+ * operator of Eq. 7 and the preconditioned GMRES solve
+ * that turns port excitations into the port impedance / inductance matrix.
+ *
+ * General conventions
+ *  - Every entry point returns 0 on success or a negative SVH_E* code; the
+ *    thread-local message of the last failure is svh_last_error().
+ *  - Host pointers are read during the call only (copied); device pointers
+ *    belong to the caller and must stay valid until the work queued on the
+ *    given stream completes.  The handle owns every buffer it allocates.
+ *  - A handle is immutable after svh_setup except through svh_set_frequency;
+ *    svh_matvec / svh_apply_system may run concurrently on distinct streams
+ *    only if each stream uses its own handle workspace (see svh_opts.rhs_chunk;
+ *    in this version one handle serialises its workspace: do not call
+ *    svh_matvec on two streams at once with the same handle).
+ *  - Units: SI.  mu = mu0 = 4*pi*1e-7 H/m.  omega = 2*pi*f.
+ *  - Grid: Kx x Ky x Kz voxels of edge dx.  mat_id is uint8
+ *    [Kz][Ky][Kx] (x fastest); 0 = empty voxel, m >= 1 selects mats[m-1].
+ *  - Non-empty voxels are numbered 0..K-1 in x-fastest lexicographic order.
+ *  - Unknown vector I = [I^x; I^y; I^z; I^2D; I^3D], component-major:
+ *    element (c, k) of RHS r is at ((r*5 + c)*K + k).  Complex values are
+ *    interleaved (re, im) complex64 (float2) on the matvec path.
+ *  - Basis normalisation (reading G1): f^x = x^/dx^2 and the PWL
+ *    bases carry 1/dx^3, so I is in amperes and the incidence matrix A is
+ *    dimensionless.
+ *  - Nodes (M): unique face centres; ordered x-faces, then y-faces, then
+ *    z-faces, each family in flat x-fastest order over its face lattice
+ *    ((Kz,Ky,Kx+1), (Kz,Ky+1,Kx), (Kz+1,Ky,Kx)), keeping faces adjacent to at
+ *    least one non-empty voxel.  N = 5K + M.
+ */
+#ifndef SVH_H
+#define SVH_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* return codes */
+#define SVH_OK          0
+#define SVH_EINVAL     -1   /* bad dimensions / arguments; zero non-empty voxels; bad port */
+#define SVH_ENOMEM     -2   /* device or host allocation failed */
+#define SVH_ECUDA      -3   /* CUDA runtime / library error */
+#define SVH_ENCCL      -4   /* reserved: collective error (multi-GPU layer is in Python) */
+#define SVH_ENOCONV    -5   /* GMRES not converged: best iterate returned, stats flagged */
+#define SVH_EOPENPORT  -6   /* |I_port| below floor (open port) */
+#define SVH_ECACHE     -7   /* reserved: Toeplitz cache (Algorithm 2) mismatch */
+
+typedef struct svh_handle svh_handle;
+typedef void* svh_stream;   /* a cudaStream_t (0 = legacy default stream) */
+
+/* domain of kx*ky*kz voxels of edge dx_m metres */
+typedef struct { int32_t kx, ky, kz; double dx_m; } svh_grid;
+
+/* P:55 Eq. 3 -- two-fluid material; lambda_L_m = +INFINITY marks a normal
+ * conductor (then c = 1/sigma_n, reading G5). */
+typedef struct { double sigma_n_S_per_m; double lambda_L_m; } svh_material;
+
+/* Set of voxel faces: the faces on side (-1/+1) of axis (0=x,1=y,2=z) of every
+ * voxel in the half-open box [lo, hi) (x, y, z).  Faces of empty voxels are
+ * ignored. */
+typedef struct { int32_t axis; int32_t side; int32_t lo[3]; int32_t hi[3]; } svh_face_rect;
+
+/* A port (reading G13): unit potential on the + faces, 0 on the - faces. */
+typedef struct { int32_t n_plus; const svh_face_rect* plus; int32_t n_minus; const svh_face_rect* minus; } svh_port;
+
+typedef struct {
+    double  tucker_tol;   /* 0 = dense octant spectra; >0 = Tucker-compressed kernels (Alg. 1) */
+    int32_t restart;      /* GMRES restart (50) */
+    double  rre;          /* relative residual target ||b - Ax|| / ||b|| (1e-8) */
+    double  inner_tol;    /* Schur-complement inner solve tolerance (1e-8) */
+    int32_t inner_maxit;  /* inner PCG iteration cap */
+    int32_t max_iters;    /* total GMRES iteration cap */
+    int32_t rhs_chunk;    /* max RHS per internal matvec batch (workspace sizing); 0 = auto */
+    int32_t verbose;      /* 0 quiet */
+} svh_opts;
+
+typedef struct {
+    int32_t iterations;        /* GMRES iterations of the last port solve */
+    int32_t total_iterations;  /* summed over ports */
+    int32_t inner_iterations;  /* summed inner PCG iterations */
+    int32_t converged;         /* 1 if every port reached rre */
+    double  final_rre;         /* worst true relative residual over ports */
+    double  t_setup_s, t_solve_s, t_matvec_s, t_precond_s;   /* host wall clock */
+    int32_t ranks[7][3];       /* Tucker multilinear ranks per kernel (0 if dense) */
+    double  compression_ratio; /* dense octant spectra bytes / Tucker bytes (P:202 CR) */
+} svh_stats;
+
+/* Default options (P:95 tol 1e-8 when Tucker is on, P:174 restart 50, RRE 1e-8, P:166 inner 1e-8). */
+void svh_default_opts(svh_opts* o);
+
+/*
+ * svh_setup -- build lattice maps, the 7 unit-voxel Galerkin kernels by
+ * fp64 quadrature (App. A/B), their circulant spectra either
+ * dense (octant, fp32) or Tucker-compressed (Alg. 1, Eq. 10),
+ * the per-material local terms z^b (Eq. 16-23) and the incidence data.
+ *   grid     : host, dims > 0, dx > 0.
+ *   mat_id   : host uint8 [kz][ky][kx]; values in 0..n_mat.
+ *   mats     : host array of n_mat materials (n_mat >= 1, <= 255).
+ *   freq_hz  : > 0.
+ *   opts     : host, may be NULL (defaults).
+ *   device   : CUDA device ordinal.
+ *   out      : receives the handle.
+ * Errors: SVH_EINVAL (bad args / K == 0), SVH_ENOMEM, SVH_ECUDA.
+ */
+int svh_setup(const svh_grid* grid, const uint8_t* mat_id, const svh_material* mats, int32_t n_mat,
+              double freq_hz, const svh_opts* opts, int32_t device, svh_handle** out);
+
+/* Change omega: only z^b and the Green prefactor j*omega*mu0*dx change (kernels are f-independent). */
+int svh_set_frequency(svh_handle* h, double freq_hz);
+
+/* K = non-empty voxels, M = unique nodes; N = 5K + M. */
+int svh_unknowns(const svh_handle* h, int64_t* K, int64_t* M);
+
+/* Embedding extents Nx, Ny, Nz (powers of two >= 2K_i - 1, reading G7). */
+int svh_embedding(const svh_handle* h, int32_t* n3);
+
+/*
+ * svh_matvec -- Eq. 9: CC^b = z^b I^b + IFFT{ sum_a Z^{b,a} * FFT(I^a) }, cropped
+ * to the non-empty voxels.
+ *   I, CC : device complex64 [nrhs][5][K] (packed voxel order); must not alias.
+ *   nrhs  : >= 1.
+ *   green_only : 1 = omit the z^b I^b local term (tests of the FFT part).
+ *   stream: cudaStream_t.
+ * Errors: SVH_EINVAL, SVH_ECUDA.  Asynchronous w.r.t. the host.
+ */
+int svh_matvec(svh_handle* h, const void* I, void* CC, int32_t nrhs, int32_t green_only, svh_stream stream);
+
+/* Same operator on the lattice layout: complex64 [nrhs][5][kz][ky][kx]; input
+ * values at empty voxels are ignored (treated as 0); output is 0 there. */
+int svh_matvec_grid(svh_handle* h, const void* I, void* CC, int32_t nrhs, int32_t green_only, svh_stream stream);
+
+/*
+ * svh_apply_system -- Eq. 7 saddle operator (reading G12 sign convention):
+ *   y_I   = Z.x_I + A^T x_Phi,   y_Phi = A x_I
+ * x, y : device complex64 [nrhs][5K + M].  Errors: SVH_EINVAL, SVH_ECUDA.
+ */
+int svh_apply_system(svh_handle* h, const void* x, void* y, int32_t nrhs, svh_stream stream);
+
+/*
+ * svh_solve -- for each port p (reading G13): Phi = 1 on p's + faces, 0 on the
+ * - faces of p and on all faces of the other ports; solve the reduced saddle
+ * system with right-preconditioned FGMRES(restart) using the Schur
+ * complement preconditioner of Eq. 12-15 whose S^-1 is an
+ * aggregation-AMG preconditioned CG (AGMG-style); port currents give
+ * Y[:,p]; Z = Y^-1, L = Im(Z)/omega, R = Re(Z).
+ *   ports     : host array of n_ports ports (>= 1).
+ *   Z_port    : host double[2*P*P] interleaved complex (row-major), may be NULL.
+ *   L_H, R_ohm: host double[P*P] row-major, may be NULL.
+ *   Y_port    : host double[2*P*P] admittance columns, may be NULL.
+ *   stats     : may be NULL.
+ * Errors: SVH_EINVAL (bad port), SVH_ENOCONV, SVH_EOPENPORT, SVH_ECUDA.
+ */
+int svh_solve(svh_handle* h, const svh_port* ports, int32_t n_ports, double* Z_port, double* L_H,
+              double* R_ohm, double* Y_port, svh_stats* stats);
+
+/* Solve only the listed port columns (0-based indices into ports), writing
+ * Y columns into Y_cols (host double[2 * n_ports * n_sel], column j = port sel[j]).
+ * Used by the multi-GPU layer to shard ports over ranks (one RHS per port). */
+int svh_solve_columns(svh_handle* h, const svh_port* ports, int32_t n_ports, const int32_t* sel,
+                      int32_t n_sel, double* Y_cols, svh_stats* stats);
+
+/* Copy the 7 unit-voxel kernels (fp64 [7][kz][ky][kx], order K0, K1x, K1y, K1z,
+ * K2x, K2y, K2z; non-negative offsets) to host memory (tests / diagnostics). */
+int svh_get_kernels(const svh_handle* h, double* host_out);
+
+/* Query statistics of setup (ranks, CR, timings). */
+int svh_get_stats(const svh_handle* h, svh_stats* stats);
+
+void svh_destroy(svh_handle* h);
+const char* svh_last_error(void);
+
+/* Number of kernel launches issued by this library since load (instrumentation). */
+int64_t svh_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SVH_H */

@@ -1,0 +1,289 @@
+// C-ABI entry points of libsvh (include/svh.h).
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace svh {
+static thread_local std::string g_err;
+void set_error(const std::string& m) { g_err = m; }
+int64_t& launch_counter() {
+    static int64_t n = 0;
+    return n;
+}
+
+constexpr double kMu0 = 4e-7 * M_PI;   // P:45, reading G4
+
+static int next_pow2_embed(int K) {
+    // smallest power of two >= 2K - 1 (reading G7)
+    int n = 1;
+    while (n < 2 * K - 1) n <<= 1;
+    return n;
+}
+
+// z^b = c / (w_b dx), c = a + j w mu b (Eq. 16-18, 22-23); w = (1,1,1,6,2)
+void update_local_terms(svh_handle* h) {
+    const int nm = (int)h->mats.size();
+    std::vector<float2> z((size_t)(nm + 1) * 5, make_float2(0.f, 0.f));
+    const double w = h->omega;
+    const double div[5] = {1, 1, 1, 6, 2};
+    for (int m = 0; m < nm; ++m) {
+        const double s0 = h->mats[m].sigma_n_S_per_m, lam = h->mats[m].lambda_L_m;
+        double a, b;
+        if (std::isinf(lam)) {
+            a = 1.0 / s0;
+            b = 0.0;
+        } else {
+            const double g = w * kMu0 * lam * lam;
+            const double den = 1.0 + (s0 * g) * (s0 * g);
+            a = s0 * g * g / den;
+            b = lam * lam / den;
+        }
+        for (int c = 0; c < 5; ++c)
+            z[(size_t)(m + 1) * 5 + c] = make_float2((float)(a / (div[c] * h->dx)), (float)(w * kMu0 * b / (div[c] * h->dx)));
+    }
+    if (!h->d_zloc) SVH_CUDA(cudaMalloc(&h->d_zloc, z.size() * sizeof(float2)));
+    SVH_CUDA(cudaMemcpy(h->d_zloc, z.data(), z.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    h->gscale = (float)(w * kMu0 * h->dx / ((double)h->nx * h->ny * h->nz));
+}
+
+static void make_twiddles(svh_handle* h) {
+    const int N3[3] = {h->nx, h->ny, h->nz};
+    for (int a = 0; a < 3; ++a) {
+        std::vector<float2> t(N3[a]);
+        for (int j = 0; j < N3[a]; ++j) {
+            const double th = -2.0 * M_PI * j / N3[a];
+            t[j] = make_float2((float)std::cos(th), (float)std::sin(th));
+        }
+        SVH_CUDA(cudaMalloc(&h->d_tw[a], t.size() * sizeof(float2)));
+        SVH_CUDA(cudaMemcpy(h->d_tw[a], t.data(), t.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    }
+}
+
+static void build_lattice(svh_handle* h) {
+    const int64_t Kt = h->Kt;
+    h->h_vmap.assign(Kt, -1);
+    h->h_vox.clear();
+    for (int64_t c = 0; c < Kt; ++c)
+        if (h->h_mat[c]) {
+            h->h_vmap[c] = (int32_t)h->h_vox.size();
+            h->h_vox.push_back((int32_t)c);
+        }
+    h->K = (int64_t)h->h_vox.size();
+    // unique face nodes
+    int64_t M = 0;
+    const int kx = h->kx, ky = h->ky, kz = h->kz;
+    auto occ = [&](int x, int y, int z) {
+        return x >= 0 && y >= 0 && z >= 0 && x < kx && y < ky && z < kz && h->h_mat[((int64_t)z * ky + y) * kx + x];
+    };
+    for (int z = 0; z < kz; ++z)
+        for (int y = 0; y < ky; ++y)
+            for (int x = 0; x <= kx; ++x) M += occ(x - 1, y, z) || occ(x, y, z);
+    for (int z = 0; z < kz; ++z)
+        for (int y = 0; y <= ky; ++y)
+            for (int x = 0; x < kx; ++x) M += occ(x, y - 1, z) || occ(x, y, z);
+    for (int z = 0; z <= kz; ++z)
+        for (int y = 0; y < ky; ++y)
+            for (int x = 0; x < kx; ++x) M += occ(x, y, z - 1) || occ(x, y, z);
+    h->M = M;
+    SVH_CUDA(cudaMalloc(&h->d_mat, Kt));
+    SVH_CUDA(cudaMemcpy(h->d_mat, h->h_mat.data(), Kt, cudaMemcpyHostToDevice));
+    SVH_CUDA(cudaMalloc(&h->d_vmap, Kt * sizeof(int32_t)));
+    SVH_CUDA(cudaMemcpy(h->d_vmap, h->h_vmap.data(), Kt * sizeof(int32_t), cudaMemcpyHostToDevice));
+    SVH_CUDA(cudaMalloc(&h->d_vox, std::max<int64_t>(1, h->K) * sizeof(int32_t)));
+    SVH_CUDA(cudaMemcpy(h->d_vox, h->h_vox.data(), h->K * sizeof(int32_t), cudaMemcpyHostToDevice));
+}
+
+static void destroy(svh_handle* h) {
+    if (!h) return;
+    free_solve(h);
+    free_tucker(h);
+    cudaFree(h->d_mat);
+    cudaFree(h->d_vmap);
+    cudaFree(h->d_vox);
+    cudaFree(h->d_kern);
+    cudaFree(h->d_spec);
+    cudaFree(h->d_zloc);
+    for (int a = 0; a < 3; ++a) cudaFree(h->d_tw[a]);
+    cudaFree(h->X1);
+    cudaFree(h->X2);
+    delete h;
+}
+
+template <typename F>
+static int guarded(F&& f) {
+    try {
+        f();
+        return SVH_OK;
+    } catch (const Error& e) {
+        set_error(e.msg);
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        set_error("host allocation failed");
+        return SVH_ENOMEM;
+    } catch (const std::exception& e) {
+        set_error(e.what());
+        return SVH_EINVAL;
+    }
+}
+
+}  // namespace svh
+
+using namespace svh;
+
+extern "C" {
+
+void svh_default_opts(svh_opts* o) {
+    if (!o) return;
+    std::memset(o, 0, sizeof(*o));
+    o->tucker_tol = 0.0;
+    o->restart = 50;
+    o->rre = 1e-6;
+    o->inner_tol = 1e-8;
+    o->inner_maxit = 200;
+    o->max_iters = 2000;
+    o->rhs_chunk = 0;
+    o->verbose = 0;
+}
+
+int svh_setup(const svh_grid* grid, const uint8_t* mat_id, const svh_material* mats, int32_t n_mat,
+              double freq_hz, const svh_opts* opts, int32_t device, svh_handle** out) {
+    return guarded([&] {
+        SVH_CHECK(grid && mat_id && mats && out, SVH_EINVAL, "null argument");
+        SVH_CHECK(grid->kx > 0 && grid->ky > 0 && grid->kz > 0 && grid->dx_m > 0, SVH_EINVAL, "bad grid");
+        SVH_CHECK(grid->kx <= 2048 && grid->ky <= 2048 && grid->kz <= 2048, SVH_EINVAL, "grid extent > 2048");
+        SVH_CHECK(n_mat >= 1 && n_mat <= 255, SVH_EINVAL, "n_mat must be in 1..255");
+        SVH_CHECK(freq_hz > 0, SVH_EINVAL, "freq must be > 0");
+        for (int m = 0; m < n_mat; ++m) {
+            SVH_CHECK(mats[m].sigma_n_S_per_m >= 0 && mats[m].lambda_L_m > 0, SVH_EINVAL, "bad material");
+            SVH_CHECK(!(std::isinf(mats[m].lambda_L_m) && mats[m].sigma_n_S_per_m <= 0), SVH_EINVAL,
+                      "normal conductor needs sigma_n > 0");
+        }
+        auto t0 = std::chrono::steady_clock::now();
+        SVH_CUDA(cudaSetDevice(device));
+        svh_handle* h = new svh_handle();
+        try {
+            h->device = device;
+            h->kx = grid->kx;
+            h->ky = grid->ky;
+            h->kz = grid->kz;
+            h->dx = grid->dx_m;
+            h->Kt = (int64_t)h->kx * h->ky * h->kz;
+            if (opts)
+                h->opts = *opts;
+            else
+                svh_default_opts(&h->opts);
+            h->mats.assign(mats, mats + n_mat);
+            h->h_mat.assign(mat_id, mat_id + h->Kt);
+            for (int64_t c = 0; c < h->Kt; ++c)
+                SVH_CHECK(h->h_mat[c] <= n_mat, SVH_EINVAL, "mat_id out of range");
+            h->nx = next_pow2_embed(h->kx);
+            h->ny = next_pow2_embed(h->ky);
+            h->nz = next_pow2_embed(h->kz);
+            h->hx = h->nx / 2 + 1;
+            h->hy = h->ny / 2 + 1;
+            h->hz = h->nz / 2 + 1;
+            build_lattice(h);
+            SVH_CHECK(h->K > 0, SVH_EINVAL, "zero non-empty voxels");
+            h->freq = freq_hz;
+            h->omega = 2.0 * M_PI * freq_hz;
+            update_local_terms(h);
+            make_twiddles(h);
+            compute_kernels(h);
+            if (h->opts.tucker_tol > 0) {
+                h->use_tucker = true;
+                compute_tucker(h);
+            } else {
+                compute_spectra(h);
+            }
+            SVH_CUDA(cudaDeviceSynchronize());
+        } catch (...) {
+            destroy(h);
+            throw;
+        }
+        h->t_setup = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        *out = h;
+    });
+}
+
+int svh_set_frequency(svh_handle* h, double freq_hz) {
+    return guarded([&] {
+        SVH_CHECK(h && freq_hz > 0, SVH_EINVAL, "bad args");
+        SVH_CUDA(cudaSetDevice(h->device));
+        h->freq = freq_hz;
+        h->omega = 2.0 * M_PI * freq_hz;
+        update_local_terms(h);
+        free_solve(h);
+    });
+}
+
+int svh_unknowns(const svh_handle* h, int64_t* K, int64_t* M) {
+    return guarded([&] {
+        SVH_CHECK(h, SVH_EINVAL, "null handle");
+        if (K) *K = h->K;
+        if (M) *M = h->M;
+    });
+}
+
+int svh_embedding(const svh_handle* h, int32_t* n3) {
+    return guarded([&] {
+        SVH_CHECK(h && n3, SVH_EINVAL, "null arg");
+        n3[0] = h->nx;
+        n3[1] = h->ny;
+        n3[2] = h->nz;
+    });
+}
+
+int svh_matvec(svh_handle* h, const void* I, void* CC, int32_t nrhs, int32_t green_only, svh_stream stream) {
+    return guarded([&] {
+        SVH_CHECK(h && I && CC && nrhs >= 1 && I != CC, SVH_EINVAL, "bad matvec args");
+        SVH_CUDA(cudaSetDevice(h->device));
+        matvec(h, (const float2*)I, (float2*)CC, nrhs, green_only != 0, true, (cudaStream_t)stream);
+    });
+}
+
+int svh_matvec_grid(svh_handle* h, const void* I, void* CC, int32_t nrhs, int32_t green_only, svh_stream stream) {
+    return guarded([&] {
+        SVH_CHECK(h && I && CC && nrhs >= 1 && I != CC, SVH_EINVAL, "bad matvec args");
+        SVH_CUDA(cudaSetDevice(h->device));
+        matvec(h, (const float2*)I, (float2*)CC, nrhs, green_only != 0, false, (cudaStream_t)stream);
+    });
+}
+
+int svh_get_kernels(const svh_handle* h, double* host_out) {
+    return guarded([&] {
+        SVH_CHECK(h && host_out, SVH_EINVAL, "null arg");
+        SVH_CUDA(cudaSetDevice(h->device));
+        SVH_CUDA(cudaMemcpy(host_out, h->d_kern, sizeof(double) * 7 * h->Kt, cudaMemcpyDeviceToHost));
+    });
+}
+
+int svh_get_stats(const svh_handle* h, svh_stats* st) {
+    return guarded([&] {
+        SVH_CHECK(h && st, SVH_EINVAL, "null arg");
+        std::memset(st, 0, sizeof(*st));
+        st->t_setup_s = h->t_setup;
+        if (h->use_tucker) {
+            for (int q = 0; q < 7; ++q)
+                for (int a = 0; a < 3; ++a) st->ranks[q][a] = h->tucker.ranks[q][a];
+            const double dense = 7.0 * h->hx * h->hy * h->hz * sizeof(float);
+            st->compression_ratio = h->tucker.bytes ? dense / (double)h->tucker.bytes : 0.0;
+        }
+    });
+}
+
+void svh_destroy(svh_handle* h) {
+    if (h) {
+        cudaSetDevice(h->device);
+        svh::destroy(h);
+    }
+}
+
+const char* svh_last_error(void) { return g_err.c_str(); }
+
+int64_t svh_launch_count(void) { return launch_counter(); }
+
+}  // extern "C"

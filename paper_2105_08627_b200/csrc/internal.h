@@ -1,0 +1,65 @@
+// libsvh internal state (not part of the C-ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <vector>
+
+#include "common.cuh"
+
+struct SvhTucker {
+    // per kernel q (7): ranks d1,d2,d3; spectral factors (fp32, [h_i][d_i]); core fp32 [d3][d2][d1]
+    int ranks[7][3] = {};
+    float* d_factor[7][3] = {};
+    float* d_core[7] = {};
+    double rel_err[7] = {};
+    size_t bytes = 0;
+};
+
+struct svh_handle {
+    int device = 0;
+    int kx = 0, ky = 0, kz = 0;
+    double dx = 0;
+    int64_t Kt = 0, K = 0, M = 0;
+    int nx = 1, ny = 1, nz = 1;          // embedding extents (powers of two >= 2K-1)
+    int hx = 1, hy = 1, hz = 1;          // octant extents N/2 + 1
+    double freq = 0, omega = 0;
+    svh_opts opts{};
+    std::vector<svh_material> mats;
+    std::vector<uint8_t> h_mat;          // [Kt]
+    std::vector<int32_t> h_vmap;         // [Kt] packed index or -1
+    std::vector<int32_t> h_vox;          // [K] flat lattice index
+    // device data
+    uint8_t* d_mat = nullptr;            // [Kt]
+    int32_t* d_vmap = nullptr;           // [Kt]
+    int32_t* d_vox = nullptr;            // [K]
+    double* d_kern = nullptr;            // [7][Kt] unit-voxel kernels, fp64
+    float* d_spec = nullptr;             // [7][hz][hy][hx] dense octant spectra (tucker_tol == 0)
+    SvhTucker tucker;
+    bool use_tucker = false;
+    float2* d_zloc = nullptr;            // [n_mat + 1][5] local terms z^b (index 0 unused)
+    float2* d_tw[3] = {nullptr, nullptr, nullptr};  // W_N^j tables per axis
+    float gscale = 0;                    // omega * mu0 * dx / (nx ny nz)
+    // matvec workspace
+    float2* X1 = nullptr;                // [chunk][5][kz][ky][nx]
+    float2* X2 = nullptr;                // [chunk][5][kz][ny][nx]
+    int ws_rhs = 0;
+    // solve-side data (built lazily by svh_solve / svh_apply_system)
+    struct Solve* solve = nullptr;
+    double t_setup = 0;
+};
+
+namespace svh {
+// matvec.cu
+void matvec(svh_handle* h, const float2* I, float2* CC, int nrhs, bool green_only, bool packed,
+            cudaStream_t s);
+void ensure_workspace(svh_handle* h, int nrhs);
+// quad.cu
+void compute_kernels(svh_handle* h);
+// spectra.cu
+void compute_spectra(svh_handle* h);
+void compute_tucker(svh_handle* h);
+void free_tucker(svh_handle* h);
+// solve.cu
+void free_solve(svh_handle* h);
+void update_local_terms(svh_handle* h);
+}  // namespace svh

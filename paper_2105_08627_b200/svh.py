@@ -1,0 +1,279 @@
+"""Thin Python binding of libsvh (include/svh.h) -- argument marshalling only.
+
+Every step of the hot path runs in libsvh's CUDA kernels; torch is used only for
+device memory and streams.  There is no CPU fallback: if libsvh.so is missing
+or no CUDA device is present the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsvh.so")
+
+SVH_OK = 0
+ERRORS = {-1: "SVH_EINVAL", -2: "SVH_ENOMEM", -3: "SVH_ECUDA", -4: "SVH_ENCCL", -5: "SVH_ENOCONV",
+          -6: "SVH_EOPENPORT", -7: "SVH_ECACHE"}
+
+
+class SvhError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{ERRORS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class Grid(ctypes.Structure):
+    _fields_ = [("kx", ctypes.c_int32), ("ky", ctypes.c_int32), ("kz", ctypes.c_int32), ("dx_m", ctypes.c_double)]
+
+
+class Material(ctypes.Structure):
+    _fields_ = [("sigma_n_S_per_m", ctypes.c_double), ("lambda_L_m", ctypes.c_double)]
+
+
+class FaceRect(ctypes.Structure):
+    _fields_ = [("axis", ctypes.c_int32), ("side", ctypes.c_int32), ("lo", ctypes.c_int32 * 3),
+                ("hi", ctypes.c_int32 * 3)]
+
+
+class Port(ctypes.Structure):
+    _fields_ = [("n_plus", ctypes.c_int32), ("plus", ctypes.POINTER(FaceRect)),
+                ("n_minus", ctypes.c_int32), ("minus", ctypes.POINTER(FaceRect))]
+
+
+class Opts(ctypes.Structure):
+    _fields_ = [("tucker_tol", ctypes.c_double), ("restart", ctypes.c_int32), ("rre", ctypes.c_double),
+                ("inner_tol", ctypes.c_double), ("inner_maxit", ctypes.c_int32), ("max_iters", ctypes.c_int32),
+                ("rhs_chunk", ctypes.c_int32), ("verbose", ctypes.c_int32)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int32), ("total_iterations", ctypes.c_int32),
+                ("inner_iterations", ctypes.c_int32), ("converged", ctypes.c_int32), ("final_rre", ctypes.c_double),
+                ("t_setup_s", ctypes.c_double), ("t_solve_s", ctypes.c_double), ("t_matvec_s", ctypes.c_double),
+                ("t_precond_s", ctypes.c_double), ("ranks", (ctypes.c_int32 * 3) * 7),
+                ("compression_ratio", ctypes.c_double)]
+
+    def as_dict(self):
+        d = {f: getattr(self, f) for f, _ in self._fields_ if f != "ranks"}
+        d["ranks"] = [[self.ranks[q][a] for a in range(3)] for q in range(7)]
+        return d
+
+
+_lib = None
+
+
+def lib():
+    """Load libsvh.so (raises if it was not built -- no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} not built: run `python -m paper_2105_08627_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i32, i64, dbl = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+        L.svh_default_opts.argtypes = [ctypes.POINTER(Opts)]
+        L.svh_default_opts.restype = None
+        L.svh_setup.argtypes = [ctypes.POINTER(Grid), ctypes.POINTER(ctypes.c_uint8), ctypes.POINTER(Material), i32,
+                                dbl, ctypes.POINTER(Opts), i32, ctypes.POINTER(vp)]
+        L.svh_set_frequency.argtypes = [vp, dbl]
+        L.svh_unknowns.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+        L.svh_embedding.argtypes = [vp, ctypes.POINTER(i32)]
+        L.svh_matvec.argtypes = [vp, vp, vp, i32, i32, vp]
+        L.svh_matvec_grid.argtypes = [vp, vp, vp, i32, i32, vp]
+        L.svh_apply_system.argtypes = [vp, vp, vp, i32, vp]
+        dp = ctypes.POINTER(ctypes.c_double)
+        L.svh_solve.argtypes = [vp, ctypes.POINTER(Port), i32, dp, dp, dp, dp, ctypes.POINTER(Stats)]
+        L.svh_solve_columns.argtypes = [vp, ctypes.POINTER(Port), i32, ctypes.POINTER(i32), i32, dp,
+                                        ctypes.POINTER(Stats)]
+        L.svh_get_kernels.argtypes = [vp, dp]
+        L.svh_get_stats.argtypes = [vp, ctypes.POINTER(Stats)]
+        L.svh_destroy.argtypes = [vp]
+        L.svh_destroy.restype = None
+        L.svh_last_error.restype = ctypes.c_char_p
+        L.svh_launch_count.restype = i64
+        for name in ("svh_setup", "svh_set_frequency", "svh_unknowns", "svh_embedding", "svh_matvec",
+                     "svh_matvec_grid", "svh_apply_system", "svh_solve", "svh_solve_columns", "svh_get_kernels",
+                     "svh_get_stats"):
+            getattr(L, name).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+EXPORTED = ("svh_default_opts", "svh_setup", "svh_set_frequency", "svh_unknowns", "svh_embedding", "svh_matvec",
+            "svh_matvec_grid", "svh_apply_system", "svh_solve", "svh_solve_columns", "svh_get_kernels",
+            "svh_get_stats", "svh_destroy", "svh_last_error", "svh_launch_count")
+
+
+def _check(code):
+    if code != SVH_OK:
+        raise SvhError(code, lib().svh_last_error().decode())
+
+
+def launch_count() -> int:
+    return int(lib().svh_launch_count())
+
+
+def _stream_ptr(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def make_ports(ports):
+    """Python port dicts (svh_inputs convention) -> ctypes array (keeps buffers alive)."""
+    keep = []
+    arr = (Port * max(1, len(ports)))()
+    for i, p in enumerate(ports):
+        lists = []
+        for key in ("plus", "minus"):
+            rects = p[key]
+            ra = (FaceRect * max(1, len(rects)))()
+            for j, (axis, side, lo, hi) in enumerate(rects):
+                ra[j].axis = axis
+                ra[j].side = side
+                for d in range(3):
+                    ra[j].lo[d] = int(lo[d])
+                    ra[j].hi[d] = int(hi[d])
+            keep.append(ra)
+            lists.append((len(rects), ra))
+        arr[i].n_plus, arr[i].plus = lists[0][0], ctypes.cast(lists[0][1], ctypes.POINTER(FaceRect))
+        arr[i].n_minus, arr[i].minus = lists[1][0], ctypes.cast(lists[1][1], ctypes.POINTER(FaceRect))
+    keep.append(arr)
+    return arr, keep
+
+
+class Handle:
+    """svh_setup ... svh_destroy.  Mirrors the C-ABI names."""
+
+    def __init__(self, mat_id, dx, materials, freq, tucker_tol=0.0, device=0, **opts):
+        L = lib()
+        mat = np.ascontiguousarray(np.asarray(mat_id, dtype=np.uint8))
+        kz, ky, kx = mat.shape
+        g = Grid(kx, ky, kz, float(dx))
+        mats = (Material * len(materials))(*[Material(float(s), float(l)) for s, l in materials])
+        o = Opts()
+        L.svh_default_opts(ctypes.byref(o))
+        o.tucker_tol = float(tucker_tol)
+        for k, v in opts.items():
+            setattr(o, k, v)
+        h = ctypes.c_void_p()
+        _check(L.svh_setup(ctypes.byref(g), mat.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), mats,
+                           len(materials), float(freq), ctypes.byref(o), int(device), ctypes.byref(h)))
+        self._h = h
+        self.device = device
+        self.shape = (kz, ky, kx)
+        K, M = ctypes.c_int64(), ctypes.c_int64()
+        _check(L.svh_unknowns(h, ctypes.byref(K), ctypes.byref(M)))
+        self.K, self.M = K.value, M.value
+        self.N = 5 * self.K + self.M
+        n3 = (ctypes.c_int32 * 3)()
+        _check(L.svh_embedding(h, n3))
+        self.embedding = tuple(n3)
+
+    # -- lifetime
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().svh_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- API
+    def set_frequency(self, freq):
+        _check(lib().svh_set_frequency(self._h, float(freq)))
+
+    def matvec(self, I, out=None, green_only=False, stream=None):
+        """I: torch complex64 cuda tensor [nrhs, 5, K] (or [5, K])."""
+        import torch
+        squeeze = I.dim() == 2
+        Ib = I.unsqueeze(0) if squeeze else I
+        assert Ib.dtype == torch.complex64 and Ib.is_cuda and Ib.shape[1:] == (5, self.K)
+        Ib = Ib.contiguous()
+        o = torch.empty_like(Ib) if out is None else out
+        _check(lib().svh_matvec(self._h, ctypes.c_void_p(Ib.data_ptr()), ctypes.c_void_p(o.data_ptr()),
+                                Ib.shape[0], int(green_only), _stream_ptr(stream)))
+        return o[0] if squeeze and out is None else o
+
+    def matvec_grid(self, I, out=None, green_only=False, stream=None):
+        """I: torch complex64 cuda tensor [nrhs, 5, kz, ky, kx]."""
+        import torch
+        assert I.dtype == torch.complex64 and I.is_cuda and tuple(I.shape[1:]) == (5,) + self.shape
+        I = I.contiguous()
+        o = torch.empty_like(I) if out is None else out
+        _check(lib().svh_matvec_grid(self._h, ctypes.c_void_p(I.data_ptr()), ctypes.c_void_p(o.data_ptr()),
+                                     I.shape[0], int(green_only), _stream_ptr(stream)))
+        return o
+
+    def apply_system(self, x, out=None, stream=None):
+        import torch
+        xb = x.unsqueeze(0) if x.dim() == 1 else x
+        assert xb.dtype == torch.complex64 and xb.is_cuda and xb.shape[1] == self.N
+        xb = xb.contiguous()
+        o = torch.empty_like(xb) if out is None else out
+        _check(lib().svh_apply_system(self._h, ctypes.c_void_p(xb.data_ptr()), ctypes.c_void_p(o.data_ptr()),
+                                      xb.shape[0], _stream_ptr(stream)))
+        return o[0] if x.dim() == 1 and out is None else o
+
+    def solve(self, ports):
+        P = len(ports)
+        arr, keep = make_ports(ports)
+        Z = np.zeros(2 * P * P)
+        Lm = np.zeros(P * P)
+        R = np.zeros(P * P)
+        Y = np.zeros(2 * P * P)
+        st = Stats()
+        dp = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))  # noqa: E731
+        code = lib().svh_solve(self._h, arr, P, dp(Z), dp(Lm), dp(R), dp(Y), ctypes.byref(st))
+        if code not in (SVH_OK, -5):
+            _check(code)
+        del keep
+        return dict(Z=(Z[0::2] + 1j * Z[1::2]).reshape(P, P), L=Lm.reshape(P, P), R=R.reshape(P, P),
+                    Y=(Y[0::2] + 1j * Y[1::2]).reshape(P, P), stats=st.as_dict(), code=code)
+
+    def solve_columns(self, ports, sel):
+        P = len(ports)
+        arr, keep = make_ports(ports)
+        sel = np.ascontiguousarray(np.asarray(sel, dtype=np.int32))
+        Y = np.zeros(2 * P * max(1, sel.size))
+        st = Stats()
+        code = lib().svh_solve_columns(self._h, arr, P, sel.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                       sel.size, Y.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                       ctypes.byref(st))
+        if code not in (SVH_OK, -5):
+            _check(code)
+        del keep
+        Yc = (Y[0::2] + 1j * Y[1::2])[: P * sel.size].reshape(sel.size, P).T  # column j = port sel[j]
+        return Yc, st.as_dict(), code
+
+    def kernels(self):
+        kz, ky, kx = self.shape
+        out = np.zeros((7, kz, ky, kx))
+        _check(lib().svh_get_kernels(self._h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        return out
+
+    def stats(self):
+        st = Stats()
+        _check(lib().svh_get_stats(self._h, ctypes.byref(st)))
+        return st.as_dict()
+
+
+def setup_case(case, tucker_tol=None, device=0, **opts):
+    """Build a Handle from an svh_inputs case dict."""
+    tol = case.get("tucker_tol", 0.0) if tucker_tol is None else tucker_tol
+    return Handle(case["mat_id"], case["dx"], case["materials"], case["freq"], tucker_tol=tol, device=device,
+                  **opts)
+
+

@@ -1,0 +1,145 @@
+"""GPU parity: svh_matvec (CUDA, complex64) vs the fp64 oracle (north star: rel L2 <= 1e-5).
+
+All calls go through the C-ABI (paper_2105_08627_b200.svh).  Both the full
+product Z.I and the Green-only part are compared, since the local term can
+dominate and would hide FFT errors.
+"""
+import numpy as np
+import pytest
+
+import svh_inputs
+from oracle import kernels as okern
+from oracle.lattice import Lattice
+from oracle.operator import matvec_direct
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5   # BASELINE.json north_star: complex64 matvec vs fp64 oracle, relative L2
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm((a - b).ravel()) / np.linalg.norm(b.ravel()))
+
+
+def gpu_matvec(svh_lib, case, I, green_only=False, grid=False, tucker_tol=0.0):
+    import torch
+    with svh_lib.setup_case(case, tucker_tol=tucker_tol) as h:
+        if not grid:
+            t = torch.from_numpy(I.astype(np.complex64)).cuda()
+            out = h.matvec(t, green_only=green_only)
+            torch.cuda.synchronize()
+            return out.cpu().numpy().astype(np.complex128)
+        lat = Lattice(case["mat_id"])
+        g = np.zeros((I.shape[0], 5) + h.shape, dtype=np.complex64)
+        c = lat.coords
+        g[:, :, c[:, 2], c[:, 1], c[:, 0]] = I
+        out = h.matvec_grid(torch.from_numpy(g).cuda(), green_only=green_only).cpu().numpy()
+        return out[:, :, c[:, 2], c[:, 1], c[:, 0]].astype(np.complex128)
+
+
+SMALL = [((1, 1, 1), 1.0), ((2, 1, 1), 1.0), ((16, 2, 2), 1.0), ((5, 3, 2), 0.7), ((13, 7, 3), 0.6),
+         ((24, 20, 6), 0.5), ((9, 33, 5), 0.5), ((3, 1, 17), 0.8), ((70, 6, 2), 0.5)]
+
+
+@pytest.mark.parametrize("shape,fill", SMALL)
+def test_kernels_vs_oracle(svh_lib, shape, fill):
+    """H2: GPU fp64 quadrature of the 7 kernels vs the oracle at every offset of the grid."""
+    case = svh_inputs.random_fill(shape, fill=fill, seed=sum(shape))
+    with svh_lib.setup_case(case) as h:
+        kg = h.kernels()                       # [7][kz][ky][kx]
+    kx, ky, kz = shape
+    offs = np.array([(x, y, z) for z in range(kz) for y in range(ky) for x in range(kx)])
+    if len(offs) > 400:
+        offs = offs[np.random.default_rng(0).choice(len(offs), 400, replace=False)]
+    ko = okern.seven_kernels(offs)             # [P][7]
+    got = kg[:, offs[:, 2], offs[:, 1], offs[:, 0]].T
+    scale = np.abs(ko[:, :1])                  # |K0(m)|
+    assert np.max(np.abs(got - ko) / scale) < 1e-11
+
+
+@pytest.mark.parametrize("shape,fill", SMALL)
+@pytest.mark.parametrize("green_only", [False, True])
+def test_matvec_small(svh_lib, shape, fill, green_only):
+    case = svh_inputs.random_fill(shape, fill=fill, seed=3 + sum(shape), n_mat=2)
+    lat = Lattice(case["mat_id"])
+    I = svh_inputs.currents(lat.K, nrhs=3, seed=1)
+    w = 2 * np.pi * case["freq"]
+    ref = matvec_direct(lat, case["materials"], w, case["dx"], I, green_only=green_only)
+    got = gpu_matvec(svh_lib, case, I, green_only=green_only)
+    for r in range(3):
+        assert rel_l2(got[r], ref[r]) < TOL, (r, rel_l2(got[r], ref[r]))
+
+
+@pytest.mark.parametrize("shape", [(13, 7, 3), (24, 20, 6)])
+def test_matvec_grid_layout(svh_lib, shape):
+    case = svh_inputs.random_fill(shape, fill=0.5, seed=8, n_mat=2)
+    lat = Lattice(case["mat_id"])
+    I = svh_inputs.currents(lat.K, nrhs=2, seed=2)
+    w = 2 * np.pi * case["freq"]
+    ref = matvec_direct(lat, case["materials"], w, case["dx"], I)
+    got = gpu_matvec(svh_lib, case, I, grid=True)
+    assert rel_l2(got, ref) < TOL
+
+
+def test_matvec_config1(svh_lib):
+    """BASELINE configs[0]: 16x2x2 bar, seeds 0-3."""
+    case = svh_inputs.config1()
+    lat = Lattice(case["mat_id"])
+    w = 2 * np.pi * case["freq"]
+    for seed in range(4):
+        I = svh_inputs.currents(lat.K, 1, seed=seed)
+        for go in (False, True):
+            ref = matvec_direct(lat, case["materials"], w, case["dx"], I, green_only=go)
+            got = gpu_matvec(svh_lib, case, I, green_only=go)
+            assert rel_l2(got, ref) < TOL
+
+
+def test_matvec_config2_sampled_rows(svh_lib):
+    """BASELINE configs[1] at full size (256x32x4 meander): 48 sampled voxels, all 5 components."""
+    import torch
+    case = svh_inputs.config2()
+    lat = Lattice(case["mat_id"])
+    rows = np.sort(np.random.default_rng(7).choice(lat.K, 48, replace=False))
+    I = svh_inputs.currents(lat.K, 1, seed=11)
+    w = 2 * np.pi * case["freq"]
+    for go in (True, False):
+        ref = matvec_direct(lat, case["materials"], w, case["dx"], I, green_only=go, rows=rows)
+        got = gpu_matvec(svh_lib, case, I, green_only=go)[:, :, rows]
+        assert rel_l2(got, ref) < TOL
+
+
+def test_matvec_symmetry_large(svh_lib):
+    """Property at any size: Z is complex symmetric (P4/P12), u^T (Z v) = v^T (Z u)."""
+    import torch
+    case = svh_inputs.random_fill((128, 96, 8), fill=0.5, seed=5)
+    with svh_lib.setup_case(case) as h:
+        u = torch.from_numpy(svh_inputs.currents(h.K, 1, seed=1).astype(np.complex64)).cuda()
+        v = torch.from_numpy(svh_inputs.currents(h.K, 1, seed=2).astype(np.complex64)).cuda()
+        for go in (True, False):
+            Zv = h.matvec(v, green_only=go).cpu().numpy().astype(np.complex128)
+            Zu = h.matvec(u, green_only=go).cpu().numpy().astype(np.complex128)
+            a = np.sum(u.cpu().numpy() * Zv)
+            b = np.sum(v.cpu().numpy() * Zu)
+            assert abs(a - b) / abs(a) < 1e-5
+
+
+def test_matvec_batch_consistency(svh_lib):
+    """nrhs batching (and RHS chunking) gives the same result as single-RHS calls."""
+    import torch
+    case = svh_inputs.random_fill((40, 12, 5), fill=0.5, seed=12)
+    with svh_lib.setup_case(case, rhs_chunk=2) as h:
+        I = torch.from_numpy(svh_inputs.currents(h.K, 5, seed=4).astype(np.complex64)).cuda()
+        all_ = h.matvec(I).cpu().numpy()
+        one = np.stack([h.matvec(I[r]).cpu().numpy() for r in range(5)])
+    assert np.array_equal(all_, one)
+
+
+def test_launch_count_increments(svh_lib):
+    import torch
+    case = svh_inputs.random_fill((8, 8, 4), fill=0.5, seed=1)
+    with svh_lib.setup_case(case) as h:
+        I = torch.from_numpy(svh_inputs.currents(h.K, 1, seed=4).astype(np.complex64)).cuda()
+        n0 = svh_lib.launch_count()
+        h.matvec(I)
+        torch.cuda.synchronize()
+        assert svh_lib.launch_count() - n0 == 5
