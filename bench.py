@@ -1,0 +1,334 @@
+#!/usr/bin/env python
+"""Benchmark of the SuperVoxHenry B200 hot path (BASELINE.json metric:
+"FFT-circulant matvec voxel-unknowns/s & % HBM roofline; time to port L-matrix").
+
+One step = one svh_matvec (Eq. 9, all five passes A-E of DESIGN.md) over a
+batch of R right-hand sides (one per port) on the workload's full grid.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg4] [--nrhs R]
+  python bench.py --impl reference ...   # the fp64 CPU oracle on the same workload
+
+Rank 0 prints ONE JSON line.  Under torchrun each rank processes its own R
+RHS (weak scaling: independent port excitations, no data-path collective);
+timing is CUDA events on the launching stream, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import svh_inputs  # noqa: E402
+
+METRIC = "FFT-circulant matvec voxel-unknowns/s"
+UNIT = "voxel-unknowns/s"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+
+
+def workload(name):
+    if name == "cfg4":
+        return svh_inputs.config4(), 16
+    if name == "cfg3":
+        return svh_inputs.config3(), 2
+    if name == "cfg2":
+        c = svh_inputs.config2()
+        c = dict(c, tucker_tol=0.0)
+        return c, 1
+    if name.startswith("fill"):
+        # e.g. fill512x512x64
+        dims = tuple(int(v) for v in name[4:].split("x"))
+        return svh_inputs.random_fill(dims, fill=0.5, seed=5), 4
+    raise SystemExit(f"unknown workload {name}")
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured (MEASURED_PEAKS.json)"
+    return PEAKS_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if len(r) > 4 + i and r[4 + i].lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def pass_bytes(h, R, packed=True):
+    """Algorithmic HBM bytes of each pass per launch (R RHS), DESIGN.md "Roofline".
+
+    pts/comp: A reads K (packed) + writes 2Kt; B 2Kt -> 4Kt; C 4Kt -> 4Kt (+ the 7 fp32
+    octant spectra once); D 4Kt -> 2Kt; E 2Kt + K (I again) -> K; maps: vmap 4 B/cell
+    in A and E, mat_id 1 B/cell in E.
+    """
+    kz, ky, kx = h.shape
+    Kt = kx * ky * kz
+    K = h.K
+    nx, ny, nz = h.embedding
+    c8 = 5 * 8 * R
+    X1 = kz * ky * nx
+    X2 = kz * ny * nx
+    spec = 7 * 4 * (nx // 2 + 1) * (ny // 2 + 1) * (nz // 2 + 1)
+    A = c8 * (K + X1) + 4 * Kt * R
+    B = c8 * (X1 + X2)
+    C = c8 * 2 * X2 + spec
+    D = c8 * (X2 + X1)
+    E = c8 * (X1 + 2 * K) + 5 * Kt * R
+    return [A, B, C, D, E]
+
+
+def cpu_oracle_rate(case, n_rows, seed=0):
+    """Oracle (fp64 direct sum, numpy) on a bounded sample: n_rows sampled output voxels
+    (all 5 components, summing over every source voxel, kernels included), extrapolated
+    to a full matvec.  Returns (voxel-unknowns/s, seconds, cores)."""
+    from oracle.lattice import Lattice
+    from oracle.operator import matvec_direct
+    lat = Lattice(case["mat_id"])
+    I = svh_inputs.currents(lat.K, 1, seed=seed)
+    rows = np.random.default_rng(seed).choice(lat.K, n_rows, replace=False)
+    t0 = time.perf_counter()
+    matvec_direct(lat, case["materials"], 2 * np.pi * case["freq"], case["dx"], I, rows=rows)
+    dt = time.perf_counter() - t0
+    t_full = dt / n_rows * lat.K
+    Kt = int(np.prod(case["mat_id"].shape))
+    return 5 * Kt / t_full, dt, os.cpu_count()
+
+
+def run_reference(args):
+    """--impl reference: the fp64 CPU oracle timed on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    case, R = workload(args.workload)
+    from oracle.lattice import Lattice
+    from oracle.operator import matvec_direct
+    lat = Lattice(case["mat_id"])
+    I = svh_inputs.currents(lat.K, 1, seed=0)
+    w = 2 * np.pi * case["freq"]
+    g = np.random.default_rng(1)
+    times = []
+    for s in range(args.warmup + args.steps):
+        row = g.choice(lat.K, 1)
+        t0 = time.perf_counter()
+        matvec_direct(lat, case["materials"], w, case["dx"], I, rows=row)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+    Kt = int(np.prod(case["mat_id"].shape))
+    t_row = float(np.mean(times))
+    value = 5 * Kt / (t_row * lat.K)          # extrapolated full-matvec rate, 1 RHS
+    ms_step = t_row * 1e3
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": case["name"], "nrhs": 1, "grid": list(case["mat_id"].shape[::-1]), "K": lat.K,
+                       "step": "1 sampled output voxel (5 components) by direct sum over all K sources, "
+                               "kernels by fp64 quadrature; rate extrapolated x K to a full matvec"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+                             "sample": f"{args.steps} sampled rows of {case['name']}"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg4")
+    ap.add_argument("--nrhs", type=int, default=0)
+    ap.add_argument("--tucker", type=float, default=0.0)
+    ap.add_argument("--cpu-rows", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2105_08627_b200 import svh
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    case, R = workload(args.workload)
+    if args.nrhs:
+        R = args.nrhs
+    t0 = time.perf_counter()
+    h = svh.setup_case(case, tucker_tol=args.tucker, device=local)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+    kz, ky, kx = h.shape
+    Kt = kx * ky * kz
+    stream = torch.cuda.current_stream()
+
+    I_host = torch.from_numpy(svh_inputs.currents(h.K, R, seed=100 + rank).astype(np.complex64)).pin_memory()
+    out_host = torch.empty_like(I_host).pin_memory()
+    I = I_host.cuda()
+    out = torch.empty_like(I)
+
+    for _ in range(max(3, args.warmup)):
+        h.matvec(I, out=out)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    # ---- device-timed region (inputs resident in HBM) ----
+    h.profile(True)
+    h.profile_read(reset=True)
+    n0 = svh.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            h.matvec(I, out=out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = svh.launch_count() - n0
+    ms = e0.elapsed_time(e1) / args.steps
+    pass_ms, pass_n = h.profile_read(reset=True)
+    h.profile(False)
+    t = torch.tensor([ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = 5.0 * Kt * R * world / (ms_max / 1e3)
+
+    # ---- end-to-end through the public API with host buffers ----
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        I.copy_(I_host, non_blocking=True)
+        h.matvec(I, out=out)
+        out_host.copy_(out, non_blocking=True)
+    f1.record(stream)
+    torch.cuda.synchronize()
+    ms_e2e = f0.elapsed_time(f1) / args.steps
+    t = torch.tensor([ms_e2e], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_value = 5.0 * Kt * R * world / (float(t.item()) / 1e3)
+    io_bytes = I_host.numel() * 8
+
+    # ---- roofline of the dominant kernel (live per-pass CUDA events) ----
+    peaks, peak_src = load_peaks()
+    pb = pass_bytes(h, R)
+    per_launch_ms = pass_ms / np.maximum(pass_n, 1)
+    dom = int(np.argmax(per_launch_ms))
+    names = ["A_x_fwd", "B_y_fwd", "C_z_mac", "D_y_inv", "E_x_inv"]
+    achieved = pb[dom] / (per_launch_ms[dom] / 1e3) / 1e9
+    peak = float(peaks["hbm_gbs"])
+    matvec_bytes = sum(pb)
+    roof = {"bound": "hbm", "kernel": names[dom], "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": int(pb[dom]),
+            "share_of_step": round(float(per_launch_ms[dom] / per_launch_ms.sum()), 4),
+            "passes_ms": {n: round(float(x), 4) for n, x in zip(names, per_launch_ms)},
+            "whole_matvec": {"bytes": int(matvec_bytes),
+                             "achieved_GBs": round(matvec_bytes / (ms / 1e3) / 1e9, 1),
+                             "frac": round(matvec_bytes / (ms / 1e3) / 1e9 / peak, 4)}}
+    traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(traffic_file):
+        try:
+            tr = json.load(open(traffic_file)).get(case["name"], {}).get(names[dom])
+            if tr:
+                roof["traffic"] = tr
+        except Exception:
+            pass
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "c64", "data": "synthetic",
+            "config": {"workload": case["name"], "grid": [kx, ky, kz], "K": h.K, "nrhs_per_gpu": R,
+                       "embedding": list(h.embedding), "layout": "packed [nrhs][5][K]",
+                       "kernels": "tucker tol %g" % args.tucker if args.tucker else "dense octant spectra",
+                       "l2": "inputs larger than L2 (working set %.1f GB/step)" % (matvec_bytes / 1e9),
+                       "occupied_unknowns_per_s": 5.0 * h.K * R * world / (ms_max / 1e3),
+                       "setup_s": round(t_setup, 3)},
+            "roofline": roof,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary()}
+
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, dt, cores = cpu_oracle_rate(case, args.cpu_rows)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                                "sample": f"{args.cpu_rows} sampled output voxels of {case['name']} (direct sum "
+                                          f"over all {h.K} sources, fp64, {dt:.1f} s), extrapolated to one "
+                                          f"full 1-RHS matvec"}
+    h.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

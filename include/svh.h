@@ -177,6 +177,14 @@ int svh_get_stats(const svh_handle* h, svh_stats* stats);
 void svh_destroy(svh_handle* h);
 const char* svh_last_error(void);
 
+/* Per-pass device-time accounting of svh_matvec: while enabled, CUDA events are
+ * recorded on the caller's stream around each of the 5 passes (A..E).
+ * svh_profile_read synchronises those events and returns, per pass, the summed
+ * milliseconds (ms[5]) and the number of launches (launches[5]) since the last
+ * reset; reset != 0 clears the record.  Both pointers may be NULL. */
+int svh_profile_enable(svh_handle* h, int32_t on);
+int svh_profile_read(svh_handle* h, double* ms, int64_t* launches, int32_t reset);
+
 /* Number of kernel launches issued by this library since load (instrumentation). */
 int64_t svh_launch_count(void);
 

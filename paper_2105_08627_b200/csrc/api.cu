@@ -99,6 +99,10 @@ static void build_lattice(svh_handle* h) {
 
 static void destroy(svh_handle* h) {
     if (!h) return;
+    for (auto& r : h->prof) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
     free_solve(h);
     free_tucker(h);
     cudaFree(h->d_mat);
@@ -280,6 +284,40 @@ void svh_destroy(svh_handle* h) {
         cudaSetDevice(h->device);
         svh::destroy(h);
     }
+}
+
+int svh_profile_enable(svh_handle* h, int32_t on) {
+    return guarded([&] {
+        SVH_CHECK(h, SVH_EINVAL, "null handle");
+        h->prof_on = on != 0;
+    });
+}
+
+int svh_profile_read(svh_handle* h, double* ms, int64_t* launches, int32_t reset) {
+    return guarded([&] {
+        SVH_CHECK(h, SVH_EINVAL, "null handle");
+        SVH_CUDA(cudaSetDevice(h->device));
+        double acc[5] = {0, 0, 0, 0, 0};
+        int64_t cnt[5] = {0, 0, 0, 0, 0};
+        for (auto& r : h->prof) {
+            SVH_CUDA(cudaEventSynchronize(r.b));
+            float t = 0.f;
+            SVH_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+            acc[r.pass] += t;
+            cnt[r.pass] += 1;
+        }
+        for (int p = 0; p < 5; ++p) {
+            if (ms) ms[p] = acc[p];
+            if (launches) launches[p] = cnt[p];
+        }
+        if (reset) {
+            for (auto& r : h->prof) {
+                cudaEventDestroy(r.a);
+                cudaEventDestroy(r.b);
+            }
+            h->prof.clear();
+        }
+    });
 }
 
 const char* svh_last_error(void) { return g_err.c_str(); }

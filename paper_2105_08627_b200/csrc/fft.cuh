@@ -13,6 +13,8 @@
 #include "common.cuh"
 #include "twiddle64.h"
 
+#include <utility>
+
 namespace svh {
 
 __host__ __device__ constexpr int brev_c(int i, int L) {
@@ -24,40 +26,56 @@ __host__ __device__ constexpr int brev_c(int i, int L) {
     return r;
 }
 
+// compile-time loop: f(std::integral_constant<int, i>) for i < N (keeps register
+// arrays in registers: every index below is a constant expression)
+template <typename F, int... Is>
+__device__ __forceinline__ void static_for_impl(F&& f, std::integer_sequence<int, Is...>) {
+    (f(std::integral_constant<int, Is>{}), ...);
+}
+template <int N, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+    static_for_impl(f, std::make_integer_sequence<int, N>{});
+}
+
+__host__ __device__ constexpr int ilog2_c(int n) { return n <= 1 ? 0 : 1 + ilog2_c(n >> 1); }
+
 template <int L, int DIR>
 __device__ __forceinline__ void reg_fft(float2 (&v)[L]) {
     if constexpr (L > 1) {
-#pragma unroll
-        for (int i = 0; i < L; ++i) {
-            const int j = brev_c(i, L);
-            if (j > i) {
-                float2 t = v[i];
+        static_for<L>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            constexpr int j = brev_c(i, L);
+            if constexpr (j > i) {
+                const float2 t = v[i];
                 v[i] = v[j];
                 v[j] = t;
             }
-        }
-#pragma unroll
-        for (int len = 2; len <= L; len <<= 1) {
-            const int half = len >> 1;
-#pragma unroll
-            for (int i = 0; i < L; i += len) {
-#pragma unroll
-                for (int k = 0; k < half; ++k) {
+        });
+        static_for<ilog2_c(L)>([&](auto S) {
+            constexpr int len = 2 << decltype(S)::value;
+            constexpr int half = len >> 1;
+            static_for<L / len>([&](auto B) {
+                constexpr int i = decltype(B)::value * len;
+                static_for<half>([&](auto Kc) {
+                    constexpr int k = decltype(Kc)::value;
                     const float2 a = v[i + k];
                     const float2 b = v[i + k + half];
                     float2 t;
-                    if (k == 0) {
+                    if constexpr (k == 0) {
                         t = b;
+                    } else if constexpr (4 * k == len) {
+                        // w = exp(DIR * i pi/2) = DIR * i
+                        t = DIR < 0 ? make_float2(b.y, -b.x) : make_float2(-b.y, b.x);
                     } else {
-                        const float wr = (float)kTwCos64[k * (64 / len)];
-                        const float wi = (float)(DIR * kTwSin64[k * (64 / len)]);
+                        constexpr float wr = (float)kTwCos64[k * (64 / len)];
+                        constexpr float wi = (float)(DIR * kTwSin64[k * (64 / len)]);
                         t = make_float2(b.x * wr - b.y * wi, b.x * wi + b.y * wr);
                     }
                     v[i + k] = make_float2(a.x + t.x, a.y + t.y);
                     v[i + k + half] = make_float2(a.x - t.x, a.y - t.y);
-                }
-            }
-        }
+                });
+            });
+        });
     }
 }
 

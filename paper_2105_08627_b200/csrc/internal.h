@@ -6,6 +6,10 @@
 
 #include "common.cuh"
 
+namespace svh {
+struct Solve;
+}
+
 struct SvhTucker {
     // per kernel q (7): ranks d1,d2,d3; spectral factors (fp32, [h_i][d_i]); core fp32 [d3][d2][d1]
     int ranks[7][3] = {};
@@ -44,8 +48,15 @@ struct svh_handle {
     float2* X2 = nullptr;                // [chunk][5][kz][ny][nx]
     int ws_rhs = 0;
     // solve-side data (built lazily by svh_solve / svh_apply_system)
-    struct Solve* solve = nullptr;
+    svh::Solve* solve = nullptr;
     double t_setup = 0;
+    // per-pass event profiling (svh_profile_enable)
+    bool prof_on = false;
+    struct ProfRec {
+        int pass;
+        cudaEvent_t a, b;
+    };
+    std::vector<ProfRec> prof;
 };
 
 namespace svh {

@@ -2,15 +2,24 @@
 //   CC^b = z^b I^b + IFFT{ sum_a Zhat^{b,a} * FFT(I^a) }   (cropped to the voxels)
 //
 // Plan P5: five passes over HBM per right-hand side,
-//   A  x: scatter/zero-pad (gather from packed order) + forward FFT along x   Kt -> 2Kt pts/comp
+//   A  x: gather from packed order + zero-pad + forward FFT along x          Kt -> 2Kt pts/comp
 //   B  y: zero-pad + forward FFT along y (strided pencils)                    2Kt -> 4Kt
 //   C  z: zero-pad + forward FFT along z, 5->5 moment-form MAC with the 7
-//         kernel spectra (dense octant or Tucker-expanded), inverse FFT, crop  4Kt -> 4Kt (in place)
+//         kernel spectra, inverse FFT, crop (in place)                        4Kt -> 4Kt
 //   D  y: inverse FFT along y + crop                                          4Kt -> 2Kt
 //   E  x: inverse FFT along x + crop + local term z^b I^b + scatter to packed 2Kt -> Kt
-// The circulant spectra never exist densely in HBM in Tucker mode; in dense
-// mode only the 7 real octant spectra (Kt-sized, fp32) are read.
+// Layouts: X1 = [rhs][5][Kz][Ky][Nx], X2 = [rhs][5][Kz][Ny][Nx] (complex64).
+//
+// FFT structure (fft.cuh): lengths N <= 64 run entirely in one thread's
+// registers; longer ones use N = R1*R2 with the first R1-point FFTs loaded
+// straight from global memory into registers, one shared-memory transpose,
+// and the R2-point FFTs stored straight from registers to global memory.
+// Zero padding (forward: upper half of the input is zero) and cropping
+// (inverse: only the lower half of the output is kept) are compile-time
+// prunings of the first / last stage.
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 #include <cuda_runtime.h>
 
 #include "fft.cuh"
@@ -19,61 +28,231 @@
 namespace svh {
 
 // ---------------------------------------------------------------------------
-// Pass A: rows along x (contiguous).  S[j*PP + q], q = row within the tile.
-template <int N, bool PACKED>
-__global__ void __launch_bounds__(fft_max_threads(N)) k_pass_a(const float2* __restrict__ in, float2* __restrict__ X1,
-                                                const int32_t* __restrict__ vmap, const float2* __restrict__ tw,
-                                                int Kx, int rows, int64_t K, int64_t Kt, int Q) {
-    extern __shared__ float2 S[];
-    const int PP = Q + 1;
+// shared-memory index helpers (bank-conflict padding)
+// "pencil-major" layout for passes A/E: element j of row q at q*(N + N/R1) + j + j/R1
+template <int N>
+__device__ __forceinline__ int pm_idx(int q, int j) {
+    constexpr int R1 = fft_r1(N);
+    return q * (N + N / R1) + j + j / R1;
+}
+// "element-major" layout for strided passes: element j of pencil q at j*Q + q, plus Q
+// per R1-block when Q < 16 (so the 32/Q pencil-rows a warp stores hit distinct banks)
+template <int N, int Q>
+__device__ __forceinline__ int em_idx(int j, int q) {
+    constexpr int R1 = fft_r1(N);
+    return j * Q + q + (Q < 16 ? (j / R1) * Q : 0);
+}
+template <int N, int Q>
+constexpr int em_size() {
+    return N * Q + (Q < 16 ? (N / fft_r1(N)) * Q : 0);
+}
+
+// ---------------------------------------------------------------------------
+// Row passes A (forward, gather + pad) and E (inverse, crop + local term + scatter).
+// Row length N along x, Q rows per CTA; threads = TPP*Q with TPP = threads per pencil.
+template <int N, int Q, bool PACKED>
+__global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
+    k_row_fwd(const float2* __restrict__ in, float2* __restrict__ X1, const int32_t* __restrict__ vmap,
+              const float2* __restrict__ tw, int Kx, int rows, int64_t K, int64_t Kt) {
+    constexpr int R1 = fft_r1(N), R2 = fft_r2(N);
     const int rc = blockIdx.y;
     const int row0 = blockIdx.x * Q;
-    const int nq = min(Q, rows - row0);
-    for (int t = threadIdx.x; t < Q * N; t += blockDim.x) {
-        const int q = t / N, j = t - (t / N) * N;
-        float2 v = make_float2(0.f, 0.f);
-        if (q < nq && j < Kx) {
-            const int64_t cell = (int64_t)(row0 + q) * Kx + j;
-            const int idx = __ldg(&vmap[cell]);
-            if (idx >= 0) v = PACKED ? in[(int64_t)rc * K + idx] : in[(int64_t)rc * Kt + cell];
+    const float2 zero = make_float2(0.f, 0.f);
+    auto load = [&](int row, int j) -> float2 {
+        if (row >= rows || j >= Kx) return zero;
+        const int64_t cell = (int64_t)row * Kx + j;
+        const int idx = __ldg(&vmap[cell]);
+        if (idx < 0) return zero;
+        return PACKED ? __ldg(&in[(int64_t)rc * K + idx]) : __ldg(&in[(int64_t)rc * Kt + cell]);
+    };
+    if constexpr (R2 == 1) {
+        const int q = threadIdx.x;
+        const int row = row0 + q;
+        float2 v[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) v[j] = (j < N / 2 || N == 1) ? load(row, j) : zero;
+        reg_fft<N, -1>(v);
+        if (row < rows) {
+            float2* dst = X1 + ((int64_t)rc * rows + row) * N;
+#pragma unroll
+            for (int k = 0; k < N; ++k) dst[k] = v[k];
         }
-        S[j * PP + q] = v;
-    }
-    __syncthreads();
-    smem_fft<N, -1>(S, PP, Q, tw);
-    for (int t = threadIdx.x; t < Q * N; t += blockDim.x) {
-        const int q = t / N, j = t - (t / N) * N;
-        if (q < nq) X1[((int64_t)rc * rows + row0 + q) * N + j] = S[j * PP + q];
+    } else {
+        extern __shared__ float2 S[];
+        if (threadIdx.x < R2 * Q) {
+            const int q = threadIdx.x / R2, n2 = threadIdx.x % R2;
+            const int row = row0 + q;
+            float2 v[R1];
+#pragma unroll
+            for (int n1 = 0; n1 < R1; ++n1) v[n1] = (n1 < R1 / 2) ? load(row, R2 * n1 + n2) : zero;
+            reg_fft<R1, -1>(v);
+#pragma unroll
+            for (int k1 = 1; k1 < R1; ++k1) v[k1] = cmul(v[k1], __ldg(&tw[n2 * k1]));
+#pragma unroll
+            for (int k1 = 0; k1 < R1; ++k1) S[pm_idx<N>(q, n2 * R1 + k1)] = v[k1];
+        }
+        __syncthreads();
+        if (threadIdx.x < R1 * Q) {
+            const int q = threadIdx.x / R1, k1 = threadIdx.x % R1;
+            const int row = row0 + q;
+            float2 u[R2];
+#pragma unroll
+            for (int n2 = 0; n2 < R2; ++n2) u[n2] = S[pm_idx<N>(q, n2 * R1 + k1)];
+            reg_fft<R2, -1>(u);
+            if (row < rows) {
+                float2* dst = X1 + ((int64_t)rc * rows + row) * N;
+#pragma unroll
+                for (int k2 = 0; k2 < R2; ++k2) dst[k1 + R1 * k2] = u[k2];
+            }
+        }
     }
 }
 
-// Pass B / D: pencils along y (stride Nx).  Tile = Q consecutive kx at one (z, rc).
-template <int N, int DIR>
-__global__ void __launch_bounds__(fft_max_threads(N)) k_pass_y(const float2* __restrict__ in, float2* __restrict__ out,
-                                                const float2* __restrict__ tw, int Nx, int Kz, int Lin,
-                                                int Lout, int Q) {
-    extern __shared__ float2 S[];
-    const int PP = Q + 1;
+template <int N, int Q, bool PACKED>
+__global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
+    k_row_inv(const float2* __restrict__ X1, float2* __restrict__ out, const float2* __restrict__ in,
+              const int32_t* __restrict__ vmap, const uint8_t* __restrict__ mat, const float2* __restrict__ zloc,
+              const float2* __restrict__ tw, int Kx, int rows, int64_t K, int64_t Kt, int green_only) {
+    constexpr int R1 = fft_r1(N), R2 = fft_r2(N);
+    const int rc = blockIdx.y;
+    const int comp = rc % 5;
+    const int row0 = blockIdx.x * Q;
+    auto store = [&](int row, int j, float2 v) {
+        if (row >= rows || j >= Kx) return;
+        const int64_t cell = (int64_t)row * Kx + j;
+        const int idx = __ldg(&vmap[cell]);
+        if (idx < 0) {
+            if (!PACKED) out[(int64_t)rc * Kt + cell] = make_float2(0.f, 0.f);
+            return;
+        }
+        if (!green_only) {
+            const float2 z = __ldg(&zloc[__ldg(&mat[cell]) * 5 + comp]);
+            const float2 iv = PACKED ? __ldg(&in[(int64_t)rc * K + idx]) : __ldg(&in[(int64_t)rc * Kt + cell]);
+            v = cadd(v, cmul(z, iv));
+        }
+        if (PACKED)
+            out[(int64_t)rc * K + idx] = v;
+        else
+            out[(int64_t)rc * Kt + cell] = v;
+    };
+    if constexpr (R2 == 1) {
+        const int q = threadIdx.x;
+        const int row = row0 + q;
+        float2 v[N];
+        const float2* src = X1 + ((int64_t)rc * rows + min(row, rows - 1)) * N;
+#pragma unroll
+        for (int k = 0; k < N; ++k) v[k] = src[k];
+        reg_fft<N, +1>(v);
+#pragma unroll
+        for (int j = 0; j < (N + 1) / 2; ++j) store(row, j, v[j]);
+    } else {
+        extern __shared__ float2 S[];
+        if (threadIdx.x < R2 * Q) {
+            const int q = threadIdx.x / R2, n2 = threadIdx.x % R2;
+            const int row = min(row0 + q, rows - 1);
+            const float2* src = X1 + ((int64_t)rc * rows + row) * N;
+            float2 v[R1];
+#pragma unroll
+            for (int n1 = 0; n1 < R1; ++n1) v[n1] = src[R2 * n1 + n2];
+            reg_fft<R1, +1>(v);
+#pragma unroll
+            for (int k1 = 1; k1 < R1; ++k1) {
+                float2 w = __ldg(&tw[n2 * k1]);
+                w.y = -w.y;
+                v[k1] = cmul(v[k1], w);
+            }
+#pragma unroll
+            for (int k1 = 0; k1 < R1; ++k1) S[pm_idx<N>(q, n2 * R1 + k1)] = v[k1];
+        }
+        __syncthreads();
+        if (threadIdx.x < R1 * Q) {
+            const int q = threadIdx.x / R1, k1 = threadIdx.x % R1;
+            float2 u[R2];
+#pragma unroll
+            for (int n2 = 0; n2 < R2; ++n2) u[n2] = S[pm_idx<N>(q, n2 * R1 + k1)];
+            reg_fft<R2, +1>(u);
+#pragma unroll
+            for (int k2 = 0; k2 < R2 / 2; ++k2) store(row0 + q, k1 + R1 * k2, u[k2]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Strided passes B / D (pencils along y, stride Nx).  Tile = Q consecutive kx at one (z, rc).
+// DIR = -1: input rows j < Lin (<= N/2), zero-padded; all N outputs.
+// DIR = +1: all N inputs; outputs j < Lout (<= N/2).
+template <int N, int Q, int DIR>
+__global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
+    k_col(const float2* __restrict__ in, float2* __restrict__ out, const float2* __restrict__ tw, int Nx, int Kz,
+          int Lin, int Lout) {
+    constexpr int R1 = fft_r1(N), R2 = fft_r2(N);
     const int kx0 = blockIdx.x * Q;
     const int z = blockIdx.y;
     const int64_t rc = blockIdx.z;
     const float2* src = in + ((rc * Kz + z) * Lin) * (int64_t)Nx + kx0;
     float2* dst = out + ((rc * Kz + z) * Lout) * (int64_t)Nx + kx0;
-    const int nq = min(Q, Nx - kx0);
-    for (int t = threadIdx.x; t < Q * N; t += blockDim.x) {
-        const int j = t / Q, q = t - (t / Q) * Q;
-        float2 v = make_float2(0.f, 0.f);
-        if (j < Lin && q < nq) v = src[(int64_t)j * Nx + q];
-        S[j * PP + q] = v;
-    }
-    __syncthreads();
-    smem_fft<N, DIR>(S, PP, Q, tw);
-    for (int t = threadIdx.x; t < Q * Lout; t += blockDim.x) {
-        const int j = t / Q, q = t - (t / Q) * Q;
-        if (q < nq) dst[(int64_t)j * Nx + q] = S[j * PP + q];
+    const float2 zero = make_float2(0.f, 0.f);
+    if constexpr (R2 == 1) {
+        const int q = threadIdx.x;
+        if (kx0 + q >= Nx) return;
+        float2 v[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            if (DIR < 0)
+                v[j] = ((j < N / 2 || N == 1) && j < Lin) ? src[(int64_t)j * Nx + q] : zero;
+            else
+                v[j] = src[(int64_t)j * Nx + q];
+        }
+        reg_fft<N, DIR>(v);
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            if (DIR < 0 || (j < (N + 1) / 2 && j < Lout)) dst[(int64_t)j * Nx + q] = v[j];
+        }
+    } else {
+        extern __shared__ float2 S[];
+        if (threadIdx.x < R2 * Q) {
+            const int n2 = threadIdx.x / Q, q = threadIdx.x % Q;
+            const bool ok = kx0 + q < Nx;
+            float2 v[R1];
+#pragma unroll
+            for (int n1 = 0; n1 < R1; ++n1) {
+                const int j = R2 * n1 + n2;
+                if (DIR < 0)
+                    v[n1] = (n1 < R1 / 2 && j < Lin && ok) ? src[(int64_t)j * Nx + q] : zero;
+                else
+                    v[n1] = ok ? src[(int64_t)j * Nx + q] : zero;
+            }
+            reg_fft<R1, DIR>(v);
+#pragma unroll
+            for (int k1 = 1; k1 < R1; ++k1) {
+                float2 w = __ldg(&tw[n2 * k1]);
+                if (DIR > 0) w.y = -w.y;
+                v[k1] = cmul(v[k1], w);
+            }
+#pragma unroll
+            for (int k1 = 0; k1 < R1; ++k1) S[em_idx<N, Q>(n2 * R1 + k1, q)] = v[k1];
+        }
+        __syncthreads();
+        if (threadIdx.x < R1 * Q) {
+            const int k1 = threadIdx.x / Q, q = threadIdx.x % Q;
+            if (kx0 + q >= Nx) return;
+            float2 u[R2];
+#pragma unroll
+            for (int n2 = 0; n2 < R2; ++n2) u[n2] = S[em_idx<N, Q>(n2 * R1 + k1, q)];
+            reg_fft<R2, DIR>(u);
+#pragma unroll
+            for (int k2 = 0; k2 < R2; ++k2) {
+                const int j = k1 + R1 * k2;
+                if (DIR < 0)
+                    dst[(int64_t)j * Nx + q] = u[k2];
+                else if (k2 < R2 / 2 && j < Lout)
+                    dst[(int64_t)j * Nx + q] = u[k2];
+            }
+        }
     }
 }
 
+// ---------------------------------------------------------------------------
 // Moment-form 5->5 multiply-accumulate at one frequency point:
 //   m1x = I2D + I3D, m1y = I3D - I2D, m1z = -2 I3D
 //   P0c = K0 Ic + K1c m1c,  P1c = -K1c Ic + K2c m1c     (c = x, y, z)
@@ -93,7 +272,6 @@ __device__ __forceinline__ void mac5(float2 (&v)[5], float k0, float s1x, float 
     const float2 P1z = cadd(cmul_i(Iz, s1z), cscale(m1z, k2z));
     const float2 C2 = csub(P1x, P1y);
     const float2 C3 = csub(cadd(P1x, P1y), cscale(P1z, 2.f));
-    // multiply by j*g
     v[0] = cmul_i(P0x, g);
     v[1] = cmul_i(P0y, g);
     v[2] = cmul_i(P0z, g);
@@ -106,11 +284,87 @@ struct SpecView {
     int hx, hy, hz;
 };
 
-// Pass C: pencils along z (stride Nx*Ny), all 5 components of Q consecutive kx at one ky.
+// the 7 kernel spectra at frequency (kx, ky, kz) from the octant (mirror symmetry + parity)
+__device__ __forceinline__ void kernel_values(const SpecView& sv, int kx, int ky, int kz, int Nx, int Ny, int Nz,
+                                              float (&kv)[7]) {
+    const int ox = kx <= (Nx >> 1) ? kx : Nx - kx;
+    const int oy = ky <= (Ny >> 1) ? ky : Ny - ky;
+    const int oz = kz <= (Nz >> 1) ? kz : Nz - kz;
+    const float sx = kx <= (Nx >> 1) ? 1.f : -1.f;
+    const float sy = ky <= (Ny >> 1) ? 1.f : -1.f;
+    const float sz = kz <= (Nz >> 1) ? 1.f : -1.f;
+    const int64_t pl = (int64_t)sv.hx * sv.hy * sv.hz;
+    const int64_t o = ((int64_t)oz * sv.hy + oy) * sv.hx + ox;
+#pragma unroll
+    for (int k = 0; k < 7; ++k) kv[k] = __ldg(&sv.spec[k * pl + o]);
+    kv[1] *= sx;
+    kv[2] *= sy;
+    kv[3] *= sz;
+}
+
+// Pass C for Nz <= 64: one thread per (component, pencil) does the whole
+// z-FFT in registers; the 5 spectra of Q pencils meet in shared memory for
+// the MAC.  The CTA loops over all RHS of the batch (kernel values stay in
+// L1) and prefetches the next RHS while the MAC runs.
+template <int N, int Q>
+__global__ void __launch_bounds__(5 * Q)
+    k_freq_small(float2* __restrict__ X2, SpecView sv, int Nx, int Ny, int Kz, float g, int nrhs) {
+    extern __shared__ float2 S[];   // [5][N][Q]
+    const int c = threadIdx.x / Q, q = threadIdx.x % Q;
+    const int kx0 = blockIdx.x * Q;
+    const int ky = blockIdx.y;
+    const int64_t plane = (int64_t)Nx * Ny;
+    const bool ok = kx0 + q < Nx;
+    const float2 zero = make_float2(0.f, 0.f);
+    float2* col = X2 + (int64_t)c * Kz * plane + (int64_t)ky * Nx + kx0 + q;
+    const int64_t rstride = 5 * Kz * plane;
+    constexpr int NH = (N + 1) / 2;
+    float2 nxt[NH];
+#pragma unroll
+    for (int j = 0; j < NH; ++j) nxt[j] = (ok && j < Kz) ? col[(int64_t)j * plane] : zero;
+    for (int r = 0; r < nrhs; ++r) {
+        float2 v[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) v[j] = j < NH ? nxt[j] : zero;
+        reg_fft<N, -1>(v);
+#pragma unroll
+        for (int k = 0; k < N; ++k) S[(c * N + k) * Q + q] = v[k];
+        __syncthreads();
+        if (r + 1 < nrhs) {
+            const float2* nc = col + (r + 1) * rstride;
+#pragma unroll
+            for (int j = 0; j < NH; ++j) nxt[j] = (ok && j < Kz) ? nc[(int64_t)j * plane] : zero;
+        }
+        for (int t = threadIdx.x; t < N * Q; t += 5 * Q) {
+            const int k = t / Q, qq = t % Q;
+            if (kx0 + qq >= Nx) continue;
+            float kv[7];
+            kernel_values(sv, kx0 + qq, ky, k, Nx, Ny, N, kv);
+            float2 w[5];
+#pragma unroll
+            for (int cc = 0; cc < 5; ++cc) w[cc] = S[(cc * N + k) * Q + qq];
+            mac5(w, kv[0], kv[1], kv[2], kv[3], kv[4], kv[5], kv[6], g);
+#pragma unroll
+            for (int cc = 0; cc < 5; ++cc) S[(cc * N + k) * Q + qq] = w[cc];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < N; ++k) v[k] = S[(c * N + k) * Q + q];
+        reg_fft<N, +1>(v);
+        if (ok) {
+            float2* dst = col + r * rstride;
+#pragma unroll
+            for (int j = 0; j < NH; ++j)
+                if (j < Kz) dst[(int64_t)j * plane] = v[j];
+        }
+    }
+}
+
+// Pass C for Nz > 64: generic shared-memory FFT over 5Q pencils (smem_fft).
 template <int N>
-__global__ void __launch_bounds__(fft_max_threads(N)) k_pass_c(float2* __restrict__ X2, SpecView sv,
-                                                const float2* __restrict__ tw, int Nx, int Ny, int Kz, int Q,
-                                                float g) {
+__global__ void __launch_bounds__(fft_max_threads(N))
+    k_freq_big(float2* __restrict__ X2, SpecView sv, const float2* __restrict__ tw, int Nx, int Ny, int Kz, int Q,
+               float g) {
     extern __shared__ float2 S[];
     const int Q5 = 5 * Q;
     const int PP = Q5 + 1;
@@ -130,27 +384,15 @@ __global__ void __launch_bounds__(fft_max_threads(N)) k_pass_c(float2* __restric
     }
     __syncthreads();
     smem_fft<N, -1>(S, PP, Q5, tw);
-    // frequency-domain block multiply-accumulate
-    const int nxh = Nx >> 1, nyh = Ny >> 1, nzh = N >> 1;
-    const int oy = ky <= nyh ? ky : Ny - ky;
-    const float sy = ky <= nyh ? 1.f : -1.f;
     for (int t = threadIdx.x; t < Q * N; t += blockDim.x) {
         const int q = t % Q, kz = t / Q;
-        const int kx = kx0 + q;
         if (q >= nq) continue;
-        const int ox = kx <= nxh ? kx : Nx - kx;
-        const float sx = kx <= nxh ? 1.f : -1.f;
-        const int oz = kz <= nzh ? kz : N - kz;
-        const float sz = kz <= nzh ? 1.f : -1.f;
         float kv[7];
-        const int64_t pl = (int64_t)sv.hx * sv.hy * sv.hz;
-        const int64_t o = ((int64_t)oz * sv.hy + oy) * sv.hx + ox;
-#pragma unroll
-        for (int k = 0; k < 7; ++k) kv[k] = __ldg(&sv.spec[k * pl + o]);
+        kernel_values(sv, kx0 + q, ky, kz, Nx, Ny, N, kv);
         float2 v[5];
 #pragma unroll
         for (int c = 0; c < 5; ++c) v[c] = S[kz * PP + c * Q + q];
-        mac5(v, kv[0], sx * kv[1], sy * kv[2], sz * kv[3], kv[4], kv[5], kv[6], g);
+        mac5(v, kv[0], kv[1], kv[2], kv[3], kv[4], kv[5], kv[6], g);
 #pragma unroll
         for (int c = 0; c < 5; ++c) S[kz * PP + c * Q + q] = v[c];
     }
@@ -164,125 +406,95 @@ __global__ void __launch_bounds__(fft_max_threads(N)) k_pass_c(float2* __restric
     }
 }
 
-// Pass E: rows along x, inverse FFT, crop, local term, scatter.
-template <int N, bool PACKED>
-__global__ void __launch_bounds__(fft_max_threads(N)) k_pass_e(const float2* __restrict__ X1, float2* __restrict__ out,
-                                                const float2* __restrict__ in, const int32_t* __restrict__ vmap,
-                                                const uint8_t* __restrict__ mat, const float2* __restrict__ zloc,
-                                                const float2* __restrict__ tw, int Kx, int rows, int64_t K,
-                                                int64_t Kt, int Q, int green_only) {
-    extern __shared__ float2 S[];
-    const int PP = Q + 1;
-    const int rc = blockIdx.y;
-    const int comp = rc % 5;
-    const int row0 = blockIdx.x * Q;
-    const int nq = min(Q, rows - row0);
-    for (int t = threadIdx.x; t < Q * N; t += blockDim.x) {
-        const int q = t / N, j = t - (t / N) * N;
-        float2 v = make_float2(0.f, 0.f);
-        if (q < nq) v = X1[((int64_t)rc * rows + row0 + q) * N + j];
-        S[j * PP + q] = v;
-    }
-    __syncthreads();
-    smem_fft<N, +1>(S, PP, Q, tw);
-    for (int t = threadIdx.x; t < Q * Kx; t += blockDim.x) {
-        const int q = t / Kx, j = t - (t / Kx) * Kx;
-        if (q >= nq) continue;
-        const int64_t cell = (int64_t)(row0 + q) * Kx + j;
-        const int idx = __ldg(&vmap[cell]);
-        if (idx < 0) {
-            if (!PACKED) out[(int64_t)rc * Kt + cell] = make_float2(0.f, 0.f);
-            continue;
-        }
-        float2 v = S[j * PP + q];
-        if (!green_only) {
-            const float2 z = __ldg(&zloc[mat[cell] * 5 + comp]);
-            const float2 iv = PACKED ? in[(int64_t)rc * K + idx] : in[(int64_t)rc * Kt + cell];
-            v = cadd(v, cmul(z, iv));
-        }
-        if (PACKED)
-            out[(int64_t)rc * K + idx] = v;
-        else
-            out[(int64_t)rc * Kt + cell] = v;
-    }
-}
-
 // ---------------------------------------------------------------------------
 // host-side dispatch
 namespace {
 
 template <typename F>
-void set_smem(F* kern, size_t bytes) {
-    if (bytes > 48 * 1024) SVH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+void prep(F* kern, size_t bytes) {
+    // every pass kernel gets the max shared-memory carveout; >48 KB needs opt-in
+    SVH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  (int)cudaSharedmemCarveoutMaxShared));
+    if (bytes > 48 * 1024)
+        SVH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
 
-constexpr size_t kSmemCap = 110 * 1024;
-
-int pick_q(int N, int want_threads, int multiplicity, int qmax) {
-    const int tpp = fft_threads_per_pencil(N);
-    want_threads = std::min(want_threads, fft_max_threads(N));
-    int Q = std::max(1, want_threads / (tpp * multiplicity));
-    while (Q > 1 && (size_t)N * (multiplicity * Q + 1) * sizeof(float2) > kSmemCap) Q >>= 1;
-    return std::max(1, std::min(Q, qmax));
+// rows per CTA for the row passes (A/E)
+template <int N>
+constexpr int row_q() {
+    return fft_r2(N) == 1 ? 128 : (256 / fft_threads_per_pencil(N) > 0 ? 256 / fft_threads_per_pencil(N) : 1);
+}
+// pencils per CTA for the strided passes (B/D)
+template <int N>
+constexpr int col_q() {
+    return fft_r2(N) == 1 ? 128 : (fft_r1(N) >= 64 ? 4 : 8);
 }
 
 template <int N>
 void run_pass_a(svh_handle* h, const float2* in, bool packed, int nrhs, cudaStream_t s) {
+    constexpr int Q = row_q<N>();
     const int rows = h->ky * h->kz;
-    const int Q = pick_q(N, 256, 1, rows);
-    const int nt = std::max(32, fft_threads_per_pencil(N) * Q);
-    const size_t smem = (size_t)N * (Q + 1) * sizeof(float2);
+    const int nt = fft_threads_per_pencil(N) * Q;
+    const size_t smem = fft_r2(N) == 1 ? 0 : (size_t)Q * (N + N / fft_r1(N)) * sizeof(float2);
     dim3 grid((rows + Q - 1) / Q, 5 * nrhs);
     if (packed) {
-        set_smem((k_pass_a<N, true>), smem);
-        SVH_LAUNCH((k_pass_a<N, true>), grid, nt, smem, s, in, h->X1, h->d_vmap, h->d_tw[0], h->kx, rows, h->K, h->Kt, Q);
+        prep(k_row_fwd<N, Q, true>, smem);
+        SVH_LAUNCH((k_row_fwd<N, Q, true>), grid, nt, smem, s, in, h->X1, h->d_vmap, h->d_tw[0], h->kx, rows, h->K,
+                   h->Kt);
     } else {
-        set_smem((k_pass_a<N, false>), smem);
-        SVH_LAUNCH((k_pass_a<N, false>), grid, nt, smem, s, in, h->X1, h->d_vmap, h->d_tw[0], h->kx, rows, h->K, h->Kt, Q);
+        prep(k_row_fwd<N, Q, false>, smem);
+        SVH_LAUNCH((k_row_fwd<N, Q, false>), grid, nt, smem, s, in, h->X1, h->d_vmap, h->d_tw[0], h->kx, rows, h->K,
+                   h->Kt);
     }
 }
 
 template <int N, int DIR>
 void run_pass_y(svh_handle* h, const float2* in, float2* out, int Lin, int Lout, int nrhs, cudaStream_t s) {
-    const int Q = pick_q(N, 256, 1, std::max(1, h->nx));
-    const int nt = std::max(32, fft_threads_per_pencil(N) * Q);
-    const size_t smem = (size_t)N * (Q + 1) * sizeof(float2);
+    constexpr int Q = col_q<N>();
+    const int nt = fft_threads_per_pencil(N) * Q;
+    const size_t smem = fft_r2(N) == 1 ? 0 : (size_t)em_size<N, Q>() * sizeof(float2);
     dim3 grid((h->nx + Q - 1) / Q, h->kz, 5 * nrhs);
-    set_smem((k_pass_y<N, DIR>), smem);
-    SVH_LAUNCH((k_pass_y<N, DIR>), grid, nt, smem, s, in, out, h->d_tw[1], h->nx, h->kz, Lin, Lout, Q);
+    prep(k_col<N, Q, DIR>, smem);
+    SVH_LAUNCH((k_col<N, Q, DIR>), grid, nt, smem, s, in, out, h->d_tw[1], h->nx, h->kz, Lin, Lout);
 }
 
 template <int N>
 void run_pass_c(svh_handle* h, int nrhs, cudaStream_t s) {
-    const int Q = pick_q(N, 320, 5, std::max(1, h->nx));
-    const int nt = std::max(32, fft_threads_per_pencil(N) * 5 * Q);
-    const size_t smem = (size_t)N * (5 * Q + 1) * sizeof(float2);
-    dim3 grid((h->nx + Q - 1) / Q, h->ny, nrhs);
-    SpecView sv{};
-    sv.spec = h->d_spec;
-    sv.hx = h->hx;
-    sv.hy = h->hy;
-    sv.hz = h->hz;
-    set_smem(k_pass_c<N>, smem);
-    SVH_LAUNCH((k_pass_c<N>), grid, nt, smem, s, h->X2, sv, h->d_tw[2], h->nx, h->ny, h->kz, Q, h->gscale);
+    SpecView sv{h->d_spec, h->hx, h->hy, h->hz};
+    if constexpr (N <= 64) {
+        constexpr int Q = N >= 64 ? 16 : 32;
+        const size_t smem = (size_t)5 * N * Q * sizeof(float2);
+        dim3 grid((h->nx + Q - 1) / Q, h->ny);
+        prep(k_freq_small<N, Q>, smem);
+        SVH_LAUNCH((k_freq_small<N, Q>), grid, 5 * Q, smem, s, h->X2, sv, h->nx, h->ny, h->kz, h->gscale, nrhs);
+    } else {
+        const int tpp = fft_threads_per_pencil(N);
+        int Q = std::max(1, fft_max_threads(N) / (tpp * 5));
+        while (Q > 1 && (size_t)N * (5 * Q + 1) * sizeof(float2) > 160 * 1024) Q >>= 1;
+        const int nt = std::max(32, tpp * 5 * Q);
+        const size_t smem = (size_t)N * (5 * Q + 1) * sizeof(float2);
+        dim3 grid((h->nx + Q - 1) / Q, h->ny, nrhs);
+        prep(k_freq_big<N>, smem);
+        SVH_LAUNCH((k_freq_big<N>), grid, nt, smem, s, h->X2, sv, h->d_tw[2], h->nx, h->ny, h->kz, Q, h->gscale);
+    }
 }
 
 template <int N>
 void run_pass_e(svh_handle* h, const float2* in, float2* out, bool packed, bool green_only, int nrhs,
                 cudaStream_t s) {
+    constexpr int Q = row_q<N>();
     const int rows = h->ky * h->kz;
-    const int Q = pick_q(N, 256, 1, rows);
-    const int nt = std::max(32, fft_threads_per_pencil(N) * Q);
-    const size_t smem = (size_t)N * (Q + 1) * sizeof(float2);
+    const int nt = fft_threads_per_pencil(N) * Q;
+    const size_t smem = fft_r2(N) == 1 ? 0 : (size_t)Q * (N + N / fft_r1(N)) * sizeof(float2);
     dim3 grid((rows + Q - 1) / Q, 5 * nrhs);
     if (packed) {
-        set_smem((k_pass_e<N, true>), smem);
-        SVH_LAUNCH((k_pass_e<N, true>), grid, nt, smem, s, h->X1, out, in, h->d_vmap, h->d_mat, h->d_zloc, h->d_tw[0],
-                   h->kx, rows, h->K, h->Kt, Q, (int)green_only);
+        prep(k_row_inv<N, Q, true>, smem);
+        SVH_LAUNCH((k_row_inv<N, Q, true>), grid, nt, smem, s, h->X1, out, in, h->d_vmap, h->d_mat, h->d_zloc,
+                   h->d_tw[0], h->kx, rows, h->K, h->Kt, (int)green_only);
     } else {
-        set_smem((k_pass_e<N, false>), smem);
-        SVH_LAUNCH((k_pass_e<N, false>), grid, nt, smem, s, h->X1, out, in, h->d_vmap, h->d_mat, h->d_zloc, h->d_tw[0],
-                   h->kx, rows, h->K, h->Kt, Q, (int)green_only);
+        prep(k_row_inv<N, Q, false>, smem);
+        SVH_LAUNCH((k_row_inv<N, Q, false>), grid, nt, smem, s, h->X1, out, in, h->d_vmap, h->d_mat, h->d_zloc,
+                   h->d_tw[0], h->kx, rows, h->K, h->Kt, (int)green_only);
     }
 }
 
@@ -341,11 +553,39 @@ void matvec(svh_handle* h, const float2* I, float2* CC, int nrhs, bool green_onl
         const int nr = std::min(chunk, nrhs - r0);
         const float2* in = I + r0 * per_rhs;
         float2* out = CC + r0 * per_rhs;
+        static const bool dbg = getenv("SVH_SYNC_DEBUG") != nullptr;
+        auto tick = [&](int pass, bool begin) {
+            if (dbg && !begin) {
+                cudaError_t e = cudaStreamSynchronize(s);
+                if (e != cudaSuccess)
+                    throw Error{SVH_ECUDA, "pass " + std::to_string(pass) + ": " + cudaGetErrorString(e)};
+            }
+            if (!h->prof_on) return;
+            if (begin) {
+                svh_handle::ProfRec r{pass, nullptr, nullptr};
+                SVH_CUDA(cudaEventCreate(&r.a));
+                SVH_CUDA(cudaEventCreate(&r.b));
+                SVH_CUDA(cudaEventRecord(r.a, s));
+                h->prof.push_back(r);
+            } else {
+                SVH_CUDA(cudaEventRecord(h->prof.back().b, s));
+            }
+        };
+        tick(0, true);
         SVH_DISPATCH_N(h->nx, run_pass_a<NN>(h, in, packed, nr, s));
+        tick(0, false);
+        tick(1, true);
         SVH_DISPATCH_N(h->ny, (run_pass_y<NN, -1>(h, h->X1, h->X2, h->ky, h->ny, nr, s)));
+        tick(1, false);
+        tick(2, true);
         SVH_DISPATCH_N(h->nz, run_pass_c<NN>(h, nr, s));
+        tick(2, false);
+        tick(3, true);
         SVH_DISPATCH_N(h->ny, (run_pass_y<NN, +1>(h, h->X2, h->X1, h->ny, h->ky, nr, s)));
+        tick(3, false);
+        tick(4, true);
         SVH_DISPATCH_N(h->nx, run_pass_e<NN>(h, in, out, packed, green_only, nr, s));
+        tick(4, false);
     }
 }
 

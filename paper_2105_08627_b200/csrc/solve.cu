@@ -1,22 +1,1340 @@
-// Saddle-system operator (Eq. 7) and preconditioned GMRES solve.
+// Saddle system (Eq. 7), Schur-complement preconditioner (Eq. 12-15,
+// P:150-166) with an aggregation-AMG preconditioned CG for S^-1, and
+// right-preconditioned FGMRES(restart) producing port admittances.
+//
+// Conventions (readings G12-G15):
+//  * A = outward-flux incidence (M x 5K, dimensionless).  Operator:
+//      y_I = Z I + A^T Phi,   y_Phi = A I          (Eq. 7 with Phi -> -Phi)
+//  * Ports: Phi fixed on port faces (1 on the driven port's + faces, 0 on all
+//    other port faces); KCL rows only on free nodes; a port-less conductor gets
+//    one grounded node.  The iteration keeps the full [5K + M] layout: fixed
+//    nodes carry an identity row and a zero right-hand side.
+//  * Preconditioner (right): Q = [Y, A^T F; F A, I - F], Y = diag|Z_ii|
+//    (P:154), F = diag(free).  Q^-1 [c; d]:
+//        e = F A Y^-1 c - F d,  S b = e  (S = F A Y^-1 A^T F, real SPD),
+//        b_fixed = d_fixed,     a = Y^-1 (c - A^T F b)
+//    S^-1 by PCG with a pairwise-aggregation AMG V-cycle (re and im parts as
+//    two real right-hand sides).
+//  * Krylov vectors and Hessenberg in fp64; Z.I by the complex64 matvec.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <functional>
+#include <numeric>
+#include <vector>
+
 #include "internal.h"
 
 namespace svh {
-void free_solve(svh_handle*) {}
+
+using cd = std::complex<double>;
+
+struct CsrDev {
+    int n = 0;
+    int64_t nnz = 0;
+    int* rowptr = nullptr;
+    int* col = nullptr;
+    double* val = nullptr;
+    double* dinv = nullptr;   // l1-Jacobi: 1 / sum_j |a_ij|
+    int* agg = nullptr;       // fine -> coarse aggregate (except coarsest level)
+    int nc = 0;
+    double* vb = nullptr;     // level right-hand side (levels >= 1) [n][2]
+    double* vx = nullptr;     // level solution (levels >= 1)
+    double* tmp = nullptr;    // residual scratch
+    double* x2 = nullptr;     // smoother ping-pong
+};
+
+struct CsrHost {
+    int n = 0;
+    std::vector<int> rowptr, col;
+    std::vector<double> val;
+};
+
+struct Solve {
+    // lattice / incidence structure (per handle)
+    int64_t M = 0, K = 0;
+    std::vector<int32_t> node_vox;   // [M][2]: packed voxel on the - side / + side of the face (-1 none)
+    std::vector<int8_t> node_axis;   // [M]
+    std::vector<int32_t> fnode;      // [K][6]: faces -x,+x,-y,+y,-z,+z
+    std::vector<int32_t> face_idx[3];
+    int32_t* d_node_vox = nullptr;
+    int8_t* d_node_axis = nullptr;
+    int32_t* d_fnode = nullptr;
+    double* d_yinv = nullptr;        // [5][K]
+    std::vector<double> yinv;        // host copy
+    // port-dependent (fixed set): AMG hierarchy on free nodes
+    std::vector<int32_t> fixed_nodes;  // sorted
+    uint8_t* d_free = nullptr;       // [M] 1 = free
+    int32_t* d_free_list = nullptr;  // [nf] node ids
+    int32_t* d_node2free = nullptr;  // [M] free index or -1
+    int nf = 0;
+    std::vector<CsrDev> levels;
+    double* d_cinv = nullptr;        // dense inverse of the coarsest matrix
+    int ncoarse = 0;
+    // work buffers
+    double* wbuf[12] = {};
+    size_t wsize = 0;
+    double2* d_krylov = nullptr;     // V and Zp vectors
+    int krylov_m = 0;
+    int64_t N = 0;
+    float2* c64_in = nullptr;
+    float2* c64_out = nullptr;
+    double* d_red = nullptr;         // reduction scratch
+    int inner_its = 0;
+};
+
+// ---------------------------------------------------------------------------
+// kernels
+namespace {
+
+// A I (complex fp64): node r on axis a, voxel v on its - side (node = v's +a face),
+// voxel u on its + side (node = u's -a face):
+//   (A I)_r = [I^a_v - I^a_u] + c2(a) (I2_v + I2_u) + c3(a) (I3_v + I3_u)
+//   c2 = (1/2, -1/2, 0), c3 = (1/2, 1/2, -1)   (flux table)
+__device__ __forceinline__ double2 apply_A_node(const double2* __restrict__ I, int64_t K, int64_t r,
+                                                const int32_t* __restrict__ node_vox,
+                                                const int8_t* __restrict__ node_axis) {
+    const int a = node_axis[r];
+    const int v = node_vox[2 * r], u = node_vox[2 * r + 1];
+    const double c2 = a == 0 ? 0.5 : (a == 1 ? -0.5 : 0.0);
+    const double c3 = a == 2 ? -1.0 : 0.5;
+    double2 acc = make_double2(0, 0);
+    if (v >= 0) {
+        const double2 p = I[a * K + v], i2 = I[3 * K + v], i3 = I[4 * K + v];
+        acc.x += p.x + c2 * i2.x + c3 * i3.x;
+        acc.y += p.y + c2 * i2.y + c3 * i3.y;
+    }
+    if (u >= 0) {
+        const double2 p = I[a * K + u], i2 = I[3 * K + u], i3 = I[4 * K + u];
+        acc.x += -p.x + c2 * i2.x + c3 * i3.x;
+        acc.y += -p.y + c2 * i2.y + c3 * i3.y;
+    }
+    return acc;
+}
+
+// A^T Phi for voxel k, all 5 bases (phi may be masked by 'free')
+__device__ __forceinline__ void apply_AT_voxel(const double2* __restrict__ phi, const uint8_t* __restrict__ free_,
+                                               const int32_t* __restrict__ fn, double2 (&o)[5]) {
+    double2 p[6];
+#pragma unroll
+    for (int f = 0; f < 6; ++f) {
+        const int r = fn[f];
+        p[f] = (r >= 0 && (!free_ || free_[r])) ? phi[r] : make_double2(0, 0);
+    }
+    o[0] = make_double2(p[1].x - p[0].x, p[1].y - p[0].y);
+    o[1] = make_double2(p[3].x - p[2].x, p[3].y - p[2].y);
+    o[2] = make_double2(p[5].x - p[4].x, p[5].y - p[4].y);
+    o[3] = make_double2(0.5 * (p[0].x + p[1].x - p[2].x - p[3].x), 0.5 * (p[0].y + p[1].y - p[2].y - p[3].y));
+    o[4] = make_double2(0.5 * (p[0].x + p[1].x + p[2].x + p[3].x) - (p[4].x + p[5].x),
+                        0.5 * (p[0].y + p[1].y + p[2].y + p[3].y) - (p[4].y + p[5].y));
+}
+
+__global__ void k_to_c64(const double2* __restrict__ x, float2* __restrict__ y, int64_t n) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) y[i] = make_float2((float)x[i].x, (float)x[i].y);
+}
+
+// y_I = ZI (c64 result) + A^T F Phi ; y_Phi = F A I + (1 - F) Phi
+__global__ void k_sys_I(const float2* __restrict__ zi, const double2* __restrict__ x, double2* __restrict__ y,
+                        const int32_t* __restrict__ fnode, const uint8_t* __restrict__ free_, int64_t K) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    double2 o[5];
+    apply_AT_voxel(x + 5 * K, free_, fnode + 6 * k, o);
+#pragma unroll
+    for (int c = 0; c < 5; ++c) {
+        const float2 z = zi[c * K + k];
+        y[c * K + k] = make_double2((double)z.x + o[c].x, (double)z.y + o[c].y);
+    }
+}
+
+__global__ void k_sys_Phi(const double2* __restrict__ x, double2* __restrict__ y, const int32_t* __restrict__ nv,
+                          const int8_t* __restrict__ na, const uint8_t* __restrict__ free_, int64_t K, int64_t M) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= M) return;
+    if (free_ && !free_[r]) {
+        y[5 * K + r] = x[5 * K + r];
+        return;
+    }
+    y[5 * K + r] = apply_A_node(x, K, r, nv, na);
+}
+
+// c64 variant for svh_apply_system (all nodes free)
+__global__ void k_sys_c64(const float2* __restrict__ zi, const float2* __restrict__ x, float2* __restrict__ y,
+                          const int32_t* __restrict__ fnode, const int32_t* __restrict__ nv,
+                          const int8_t* __restrict__ na, int64_t K, int64_t M) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < K) {
+        double2 p[6];
+        const int32_t* fn = fnode + 6 * t;
+        double2 o[5];
+        double2 phi_local[6];
+        for (int f = 0; f < 6; ++f) {
+            const float2 v = x[5 * K + fn[f]];
+            phi_local[f] = make_double2(v.x, v.y);
+        }
+        (void)p;
+        // reuse the fp64 helper on a 6-entry local array
+        int32_t idx[6] = {0, 1, 2, 3, 4, 5};
+        apply_AT_voxel(phi_local, nullptr, idx, o);
+        for (int c = 0; c < 5; ++c) {
+            const float2 z = zi[c * K + t];
+            y[c * K + t] = make_float2((float)(z.x + o[c].x), (float)(z.y + o[c].y));
+        }
+    } else if (t < K + M) {
+        const int64_t r = t - K;
+        const int a = na[r];
+        const int v = nv[2 * r], u = nv[2 * r + 1];
+        const double c2 = a == 0 ? 0.5 : (a == 1 ? -0.5 : 0.0);
+        const double c3 = a == 2 ? -1.0 : 0.5;
+        double ax = 0, ay = 0;
+        if (v >= 0) {
+            const float2 p = x[a * K + v], i2 = x[3 * K + v], i3 = x[4 * K + v];
+            ax += p.x + c2 * i2.x + c3 * i3.x;
+            ay += p.y + c2 * i2.y + c3 * i3.y;
+        }
+        if (u >= 0) {
+            const float2 p = x[a * K + u], i2 = x[3 * K + u], i3 = x[4 * K + u];
+            ax += -p.x + c2 * i2.x + c3 * i3.x;
+            ay += -p.y + c2 * i2.y + c3 * i3.y;
+        }
+        y[5 * K + r] = make_float2((float)ax, (float)ay);
+    }
+}
+
+// ---- preconditioner pieces
+// t = Y^-1 c  (complex) ; e2[f] = (A t)[node] - d[node] for free nodes, split re/im -> [nf][2]
+__global__ void k_pre_e(const double2* __restrict__ c, const double* __restrict__ yinv, double2* __restrict__ t,
+                        int64_t n5) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n5) t[i] = make_double2(c[i].x * yinv[i], c[i].y * yinv[i]);
+}
+__global__ void k_pre_e2(const double2* __restrict__ t, const double2* __restrict__ d, double* __restrict__ e2,
+                         const int32_t* __restrict__ free_list, const int32_t* __restrict__ nv,
+                         const int8_t* __restrict__ na, int64_t K, int nf) {
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= nf) return;
+    const int r = free_list[f];
+    const double2 at = apply_A_node(t, K, r, nv, na);
+    e2[2 * f] = at.x - d[r].x;
+    e2[2 * f + 1] = at.y - d[r].y;
+}
+// b[node] = b2 (free) or d (fixed); stored into out Phi part
+__global__ void k_pre_b(const double* __restrict__ b2, const double2* __restrict__ d, double2* __restrict__ outphi,
+                        const int32_t* __restrict__ node2free, int64_t M) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= M) return;
+    const int f = node2free[r];
+    outphi[r] = f >= 0 ? make_double2(b2[2 * f], b2[2 * f + 1]) : d[r];
+}
+// a = Y^-1 (c - A^T F b)
+__global__ void k_pre_a(const double2* __restrict__ c, const double2* __restrict__ bphi, const double* __restrict__ yinv,
+                        double2* __restrict__ a, const int32_t* __restrict__ fnode, const uint8_t* __restrict__ free_,
+                        int64_t K) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    double2 o[5];
+    apply_AT_voxel(bphi, free_, fnode + 6 * k, o);
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+        const int64_t i = q * K + k;
+        a[i] = make_double2((c[i].x - o[q].x) * yinv[i], (c[i].y - o[q].y) * yinv[i]);
+    }
+}
+
+// ---- AMG / PCG on [n][2] interleaved real vectors
+// y = A x (2 vectors)
+__global__ void k_spmv2(int n, const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ v,
+                        const double* __restrict__ x, double* __restrict__ y) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double a0 = 0, a1 = 0;
+    for (int p = rp[i]; p < rp[i + 1]; ++p) {
+        const double w = v[p];
+        const int j = ci[p];
+        a0 += w * x[2 * j];
+        a1 += w * x[2 * j + 1];
+    }
+    y[2 * i] = a0;
+    y[2 * i + 1] = a1;
+}
+// l1-Jacobi sweep: xo = x + D^-1 (b - A x); x may be null (= zero initial guess)
+__global__ void k_jacobi2(int n, const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ v,
+                          const double* __restrict__ dinv, const double* __restrict__ b, const double* __restrict__ x,
+                          double* __restrict__ xo) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double a0 = 0, a1 = 0, x0 = 0, x1 = 0;
+    if (x) {
+        for (int p = rp[i]; p < rp[i + 1]; ++p) {
+            const double w = v[p];
+            const int j = ci[p];
+            a0 += w * x[2 * j];
+            a1 += w * x[2 * j + 1];
+        }
+        x0 = x[2 * i];
+        x1 = x[2 * i + 1];
+    }
+    xo[2 * i] = x0 + dinv[i] * (b[2 * i] - a0);
+    xo[2 * i + 1] = x1 + dinv[i] * (b[2 * i + 1] - a1);
+}
+// r = b - A x
+__global__ void k_resid2(int n, const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ v,
+                         const double* __restrict__ b, const double* __restrict__ x, double* __restrict__ r) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double a0 = 0, a1 = 0;
+    for (int p = rp[i]; p < rp[i + 1]; ++p) {
+        const double w = v[p];
+        const int j = ci[p];
+        a0 += w * x[2 * j];
+        a1 += w * x[2 * j + 1];
+    }
+    r[2 * i] = b[2 * i] - a0;
+    r[2 * i + 1] = b[2 * i + 1] - a1;
+}
+__global__ void k_zero(double* __restrict__ x, int64_t n) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) x[i] = 0.0;
+}
+// restriction: rc[agg[i]] += r[i]
+__global__ void k_restrict2(int n, const int* __restrict__ agg, const double* __restrict__ r, double* __restrict__ rc) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int I = agg[i];
+    atomicAdd(&rc[2 * I], r[2 * i]);
+    atomicAdd(&rc[2 * I + 1], r[2 * i + 1]);
+}
+// prolongation: x[i] += ec[agg[i]]
+__global__ void k_prolong2(int n, const int* __restrict__ agg, const double* __restrict__ ec, double* __restrict__ x) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int I = agg[i];
+    x[2 * i] += ec[2 * I];
+    x[2 * i + 1] += ec[2 * I + 1];
+}
+// dense coarse solve: x = Cinv b (2 vectors), one warp per row
+__global__ void k_dense2(int n, const double* __restrict__ Ci, const double* __restrict__ b, double* __restrict__ x) {
+    const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (row >= n) return;
+    double a0 = 0, a1 = 0;
+    for (int j = lane; j < n; j += 32) {
+        const double w = Ci[(int64_t)row * n + j];
+        a0 += w * b[2 * j];
+        a1 += w * b[2 * j + 1];
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        a0 += __shfl_xor_sync(0xffffffff, a0, o);
+        a1 += __shfl_xor_sync(0xffffffff, a1, o);
+    }
+    if (lane == 0) {
+        x[2 * row] = a0;
+        x[2 * row + 1] = a1;
+    }
+}
+// out[0..3] += (a . b) per component pair: out[0] = sum a0 b0, out[1] = sum a1 b1
+__global__ void k_dot2(int64_t n, const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ out) {
+    double s0 = 0, s1 = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        s0 += a[2 * i] * b[2 * i];
+        s1 += a[2 * i + 1] * b[2 * i + 1];
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        s0 += __shfl_xor_sync(0xffffffff, s0, o);
+        s1 += __shfl_xor_sync(0xffffffff, s1, o);
+    }
+    __shared__ double sh[2][32];
+    const int w = threadIdx.x / 32, l = threadIdx.x & 31;
+    if (l == 0) {
+        sh[0][w] = s0;
+        sh[1][w] = s1;
+    }
+    __syncthreads();
+    if (w == 0) {
+        s0 = l < blockDim.x / 32 ? sh[0][l] : 0;
+        s1 = l < blockDim.x / 32 ? sh[1][l] : 0;
+        for (int o = 16; o > 0; o >>= 1) {
+            s0 += __shfl_xor_sync(0xffffffff, s0, o);
+            s1 += __shfl_xor_sync(0xffffffff, s1, o);
+        }
+        if (l == 0) {
+            atomicAdd(&out[0], s0);
+            atomicAdd(&out[1], s1);
+        }
+    }
+}
+// x += alpha_c y (per component alpha[c]); y2 = ...
+__global__ void k_axpy2(int64_t n, const double* __restrict__ alpha, int sign, const double* __restrict__ y,
+                        double* __restrict__ x) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    x[2 * i] += sign * alpha[0] * y[2 * i];
+    x[2 * i + 1] += sign * alpha[1] * y[2 * i + 1];
+}
+// p = z + beta p
+__global__ void k_xpby2(int64_t n, const double* __restrict__ z, const double* __restrict__ beta, double* __restrict__ p) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    p[2 * i] = z[2 * i] + beta[0] * p[2 * i];
+    p[2 * i + 1] = z[2 * i + 1] + beta[1] * p[2 * i + 1];
+}
+
+// ---- complex Krylov helpers (double2 vectors of length n)
+// out[i] += sum_e conj(V_i[e]) w[e], i < m ; grid (blocks, m)
+__global__ void k_cdots(int64_t n, const double2* __restrict__ V, int64_t ldv, const double2* __restrict__ w,
+                        double* __restrict__ out) {
+    const int i = blockIdx.y;
+    const double2* v = V + i * ldv;
+    double sr = 0, si = 0;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const double2 a = v[e], b = w[e];
+        sr += a.x * b.x + a.y * b.y;
+        si += a.x * b.y - a.y * b.x;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        sr += __shfl_xor_sync(0xffffffff, sr, o);
+        si += __shfl_xor_sync(0xffffffff, si, o);
+    }
+    __shared__ double sh[2][32];
+    const int wp = threadIdx.x / 32, l = threadIdx.x & 31;
+    if (l == 0) {
+        sh[0][wp] = sr;
+        sh[1][wp] = si;
+    }
+    __syncthreads();
+    if (wp == 0) {
+        sr = l < blockDim.x / 32 ? sh[0][l] : 0;
+        si = l < blockDim.x / 32 ? sh[1][l] : 0;
+        for (int o = 16; o > 0; o >>= 1) {
+            sr += __shfl_xor_sync(0xffffffff, sr, o);
+            si += __shfl_xor_sync(0xffffffff, si, o);
+        }
+        if (l == 0) {
+            atomicAdd(&out[2 * i], sr);
+            atomicAdd(&out[2 * i + 1], si);
+        }
+    }
+}
+// w -= sum_{i<m} V_i h_i   (h complex on device)
+__global__ void k_cupdate(int64_t n, const double2* __restrict__ V, int64_t ldv, const double* __restrict__ h, int m,
+                          double2* __restrict__ w, double sign) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    double2 acc = w[e];
+    for (int i = 0; i < m; ++i) {
+        const double2 v = V[i * ldv + e];
+        const double hr = h[2 * i], hi = h[2 * i + 1];
+        acc.x -= sign * (v.x * hr - v.y * hi);
+        acc.y -= sign * (v.x * hi + v.y * hr);
+    }
+    w[e] = acc;
+}
+// r = b - y
+__global__ void k_csub(int64_t n, const double2* __restrict__ b, const double2* __restrict__ y, double2* __restrict__ r) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e < n) r[e] = make_double2(b[e].x - y[e].x, b[e].y - y[e].y);
+}
+__global__ void k_cscale(int64_t n, double2* __restrict__ x, double s, double2* __restrict__ y) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e < n) y[e] = make_double2(x[e].x * s, x[e].y * s);
+}
+__global__ void k_port_current(const double2* __restrict__ x, const int32_t* __restrict__ nodes, int n,
+                               const int32_t* __restrict__ nv, const int8_t* __restrict__ na, int64_t K,
+                               double* __restrict__ out) {
+    double sr = 0, si = 0;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+        const double2 f = apply_A_node(x, K, nodes[t], nv, na);
+        sr -= f.x;
+        si -= f.y;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        sr += __shfl_xor_sync(0xffffffff, sr, o);
+        si += __shfl_xor_sync(0xffffffff, si, o);
+    }
+    __shared__ double sh[2][32];
+    const int wp = threadIdx.x / 32, l = threadIdx.x & 31;
+    if (l == 0) {
+        sh[0][wp] = sr;
+        sh[1][wp] = si;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0, b = 0;
+        for (int q = 0; q < (int)(blockDim.x / 32); ++q) {
+            a += sh[0][q];
+            b += sh[1][q];
+        }
+        out[0] = a;
+        out[1] = b;
+    }
+}
+// b_I = -A^T Phi_p (Phi_p = 1 on the given nodes) ; b_Phi = 0
+__global__ void k_rhs(double2* __restrict__ b, const uint8_t* __restrict__ plus_mask, const int32_t* __restrict__ fnode,
+                      int64_t K, int64_t M) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < K) {
+        const int32_t* fn = fnode + 6 * t;
+        double2 p[6];
+        for (int f = 0; f < 6; ++f) p[f] = make_double2(plus_mask[fn[f]] ? 1.0 : 0.0, 0.0);
+        int32_t idx[6] = {0, 1, 2, 3, 4, 5};
+        double2 o[5];
+        apply_AT_voxel(p, nullptr, idx, o);
+        for (int c = 0; c < 5; ++c) b[c * K + t] = make_double2(-o[c].x, -o[c].y);
+    } else if (t < K + M) {
+        b[5 * K + (t - K)] = make_double2(0, 0);
+    }
+}
+
+inline unsigned nblk(int64_t n, int bs = 256) { return (unsigned)((n + bs - 1) / bs); }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// host: structure
+static void build_structure(svh_handle* h) {
+    Solve* S = new Solve();
+    h->solve = S;
+    const int kx = h->kx, ky = h->ky, kz = h->kz;
+    S->K = h->K;
+    auto vox = [&](int x, int y, int z) -> int32_t {
+        if (x < 0 || y < 0 || z < 0 || x >= kx || y >= ky || z >= kz) return -1;
+        return h->h_vmap[((int64_t)z * ky + y) * kx + x];
+    };
+    int64_t next = 0;
+    // face lattices: x (kz, ky, kx+1), y (kz, ky+1, kx), z (kz+1, ky, kx)
+    const int fdims[3][3] = {{kx + 1, ky, kz}, {kx, ky + 1, kz}, {kx, ky, kz + 1}};
+    for (int a = 0; a < 3; ++a) {
+        const int fx = fdims[a][0], fy = fdims[a][1], fz = fdims[a][2];
+        S->face_idx[a].assign((size_t)fx * fy * fz, -1);
+        for (int z = 0; z < fz; ++z)
+            for (int y = 0; y < fy; ++y)
+                for (int x = 0; x < fx; ++x) {
+                    const int dxm = a == 0, dym = a == 1, dzm = a == 2;
+                    const int32_t vm = vox(x - dxm, y - dym, z - dzm);   // - side: its +a face
+                    const int32_t vp = vox(x, y, z);                     // + side: its -a face
+                    if (vm < 0 && vp < 0) continue;
+                    S->face_idx[a][((size_t)z * fy + y) * fx + x] = (int32_t)next;
+                    S->node_vox.push_back(vm);
+                    S->node_vox.push_back(vp);
+                    S->node_axis.push_back((int8_t)a);
+                    ++next;
+                }
+    }
+    S->M = next;
+    SVH_CHECK(S->M == h->M, SVH_ECUDA, "node count mismatch");
+    S->fnode.resize((size_t)6 * h->K);
+    for (int64_t k = 0; k < h->K; ++k) {
+        const int64_t c = h->h_vox[k];
+        const int x = (int)(c % kx), y = (int)((c / kx) % ky), z = (int)(c / ((int64_t)kx * ky));
+        for (int a = 0; a < 3; ++a) {
+            const int fx = fdims[a][0], fy = fdims[a][1];
+            const int xx = x + (a == 0), yy = y + (a == 1), zz = z + (a == 2);
+            S->fnode[6 * k + 2 * a] = S->face_idx[a][((size_t)z * fy + y) * fx + x];
+            S->fnode[6 * k + 2 * a + 1] = S->face_idx[a][((size_t)zz * fy + yy) * fx + xx];
+        }
+    }
+    SVH_CUDA(cudaMalloc(&S->d_node_vox, S->node_vox.size() * sizeof(int32_t)));
+    SVH_CUDA(cudaMemcpy(S->d_node_vox, S->node_vox.data(), S->node_vox.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    SVH_CUDA(cudaMalloc(&S->d_node_axis, S->node_axis.size()));
+    SVH_CUDA(cudaMemcpy(S->d_node_axis, S->node_axis.data(), S->node_axis.size(), cudaMemcpyHostToDevice));
+    SVH_CUDA(cudaMalloc(&S->d_fnode, S->fnode.size() * sizeof(int32_t)));
+    SVH_CUDA(cudaMemcpy(S->d_fnode, S->fnode.data(), S->fnode.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    // Y = |Z_ii|: z^b + j w mu0 dx T^{bb}(0)
+    double k0[7];
+    for (int q = 0; q < 7; ++q) SVH_CUDA(cudaMemcpy(&k0[q], h->d_kern + q * h->Kt, sizeof(double), cudaMemcpyDeviceToHost));
+    const double tself[5] = {k0[0], k0[0], k0[0], k0[4] + k0[5], k0[4] + k0[5] + 4.0 * k0[6]};
+    const double mu0 = 4e-7 * M_PI, w = h->omega;
+    const double div[5] = {1, 1, 1, 6, 2};
+    S->yinv.resize((size_t)5 * h->K);
+    for (int64_t k = 0; k < h->K; ++k) {
+        const svh_material& m = h->mats[h->h_mat[h->h_vox[k]] - 1];
+        double a, b;
+        if (std::isinf(m.lambda_L_m)) {
+            a = 1.0 / m.sigma_n_S_per_m;
+            b = 0.0;
+        } else {
+            const double g = w * mu0 * m.lambda_L_m * m.lambda_L_m;
+            const double den = 1.0 + (m.sigma_n_S_per_m * g) * (m.sigma_n_S_per_m * g);
+            a = m.sigma_n_S_per_m * g * g / den;
+            b = m.lambda_L_m * m.lambda_L_m / den;
+        }
+        for (int c = 0; c < 5; ++c) {
+            const cd z(a / (div[c] * h->dx), w * mu0 * b / (div[c] * h->dx) + w * mu0 * h->dx * tself[c]);
+            S->yinv[c * h->K + k] = 1.0 / std::abs(z);
+        }
+    }
+    SVH_CUDA(cudaMalloc(&S->d_yinv, S->yinv.size() * sizeof(double)));
+    SVH_CUDA(cudaMemcpy(S->d_yinv, S->yinv.data(), S->yinv.size() * sizeof(double), cudaMemcpyHostToDevice));
+    S->N = 5 * h->K + S->M;
+}
+
+static void free_levels(Solve* S) {
+    for (auto& L : S->levels) {
+        cudaFree(L.vb);
+        cudaFree(L.vx);
+        cudaFree(L.tmp);
+        cudaFree(L.x2);
+        cudaFree(L.rowptr);
+        cudaFree(L.col);
+        cudaFree(L.val);
+        cudaFree(L.dinv);
+        cudaFree(L.agg);
+    }
+    S->levels.clear();
+    cudaFree(S->d_cinv);
+    S->d_cinv = nullptr;
+    cudaFree(S->d_free);
+    cudaFree(S->d_free_list);
+    cudaFree(S->d_node2free);
+    S->d_free = nullptr;
+    S->d_free_list = nullptr;
+    S->d_node2free = nullptr;
+}
+
+void free_solve(svh_handle* h) {
+    Solve* S = h->solve;
+    if (!S) return;
+    free_levels(S);
+    cudaFree(S->d_node_vox);
+    cudaFree(S->d_node_axis);
+    cudaFree(S->d_fnode);
+    cudaFree(S->d_yinv);
+    for (auto& b : S->wbuf) cudaFree(b);
+    cudaFree(S->d_krylov);
+    cudaFree(S->c64_in);
+    cudaFree(S->c64_out);
+    cudaFree(S->d_red);
+    delete S;
+    h->solve = nullptr;
+}
+
+// ---------------------------------------------------------------------------
+// host: AMG setup on the free-node Schur complement S = F A Y^-1 A^T F
+namespace {
+
+// flux coefficients of the 5 bases on the 6 faces (-x,+x,-y,+y,-z,+z)
+const double kFlux[5][6] = {{-1, 1, 0, 0, 0, 0},
+                            {0, 0, -1, 1, 0, 0},
+                            {0, 0, 0, 0, -1, 1},
+                            {0.5, 0.5, -0.5, -0.5, 0, 0},
+                            {0.5, 0.5, 0.5, 0.5, -1, -1}};
+
+CsrHost build_schur(const Solve* S, const std::vector<int32_t>& node2free, int nf) {
+    // rows by free node: neighbours are faces of the <= 2 adjacent voxels
+    CsrHost A;
+    A.n = nf;
+    A.rowptr.assign(nf + 1, 0);
+    std::vector<int> cols;
+    std::vector<double> vals;
+    cols.reserve((size_t)nf * 11);
+    vals.reserve((size_t)nf * 11);
+    std::vector<int> mark(nf, -1);
+    std::vector<int> slot(nf, 0);
+    const int64_t K = S->K;
+    int f = 0;
+    for (int64_t r = 0; r < S->M; ++r) {
+        if (node2free[r] < 0) continue;
+        const int row_start = (int)cols.size();
+        for (int side = 0; side < 2; ++side) {
+            const int32_t k = S->node_vox[2 * r + side];
+            if (k < 0) continue;
+            const int32_t* fn = &S->fnode[6 * k];
+            int pr = -1;
+            for (int q = 0; q < 6; ++q)
+                if (fn[q] == r) pr = q;
+            for (int q = 0; q < 6; ++q) {
+                const int cf = node2free[fn[q]];
+                if (cf < 0) continue;
+                double v = 0;
+                for (int b = 0; b < 5; ++b) v += kFlux[b][pr] * kFlux[b][q] * S->yinv[b * K + k];
+                if (mark[cf] != f) {
+                    mark[cf] = f;
+                    slot[cf] = (int)cols.size();
+                    cols.push_back(cf);
+                    vals.push_back(v);
+                } else {
+                    vals[slot[cf]] += v;
+                }
+            }
+        }
+        (void)row_start;
+        ++f;
+        A.rowptr[f] = (int)cols.size();
+    }
+    A.col.swap(cols);
+    A.val.swap(vals);
+    return A;
+}
+
+// one pass of pairwise aggregation: returns agg map and number of aggregates
+int pairwise(const CsrHost& A, std::vector<int>& agg) {
+    const int n = A.n;
+    agg.assign(n, -1);
+    int nc = 0;
+    std::vector<double> diag(n, 0.0);
+    for (int i = 0; i < n; ++i)
+        for (int p = A.rowptr[i]; p < A.rowptr[i + 1]; ++p)
+            if (A.col[p] == i) diag[i] = A.val[p];
+    for (int i = 0; i < n; ++i) {
+        if (agg[i] >= 0) continue;
+        // strongest coupling by |a_ij| / sqrt(a_ii a_jj) among unaggregated neighbours
+        int best = -1;
+        double bv = 0.0, rowmax = 0.0;
+        for (int p = A.rowptr[i]; p < A.rowptr[i + 1]; ++p) {
+            const int j = A.col[p];
+            if (j == i) continue;
+            const double s = std::fabs(A.val[p]) / std::sqrt(std::fabs(diag[i] * diag[j]) + 1e-300);
+            rowmax = std::max(rowmax, s);
+            if (agg[j] < 0 && s > bv) {
+                bv = s;
+                best = j;
+            }
+        }
+        agg[i] = nc;
+        if (best >= 0 && bv >= 0.25 * rowmax) agg[best] = nc;
+        ++nc;
+    }
+    return nc;
+}
+
+CsrHost galerkin(const CsrHost& A, const std::vector<int>& agg, int nc) {
+    // members of each aggregate
+    std::vector<int> cnt(nc + 1, 0), mem(A.n);
+    for (int i = 0; i < A.n; ++i) cnt[agg[i] + 1]++;
+    for (int I = 0; I < nc; ++I) cnt[I + 1] += cnt[I];
+    std::vector<int> pos(cnt.begin(), cnt.end() - 1);
+    for (int i = 0; i < A.n; ++i) mem[pos[agg[i]]++] = i;
+    CsrHost C;
+    C.n = nc;
+    C.rowptr.assign(nc + 1, 0);
+    std::vector<int> mark(nc, -1), slot(nc, 0);
+    for (int I = 0; I < nc; ++I) {
+        for (int q = cnt[I]; q < cnt[I + 1]; ++q) {
+            const int i = mem[q];
+            for (int p = A.rowptr[i]; p < A.rowptr[i + 1]; ++p) {
+                const int J = agg[A.col[p]];
+                if (mark[J] != I) {
+                    mark[J] = I;
+                    slot[J] = (int)C.col.size();
+                    C.col.push_back(J);
+                    C.val.push_back(A.val[p]);
+                } else {
+                    C.val[slot[J]] += A.val[p];
+                }
+            }
+        }
+        C.rowptr[I + 1] = (int)C.col.size();
+    }
+    return C;
+}
+
+CsrDev upload(const CsrHost& A) {
+    CsrDev d;
+    d.n = A.n;
+    d.nnz = (int64_t)A.col.size();
+    std::vector<double> dinv(A.n, 0.0);
+    for (int i = 0; i < A.n; ++i) {
+        double s = 0;
+        for (int p = A.rowptr[i]; p < A.rowptr[i + 1]; ++p) s += std::fabs(A.val[p]);
+        dinv[i] = s > 0 ? 1.0 / s : 0.0;
+    }
+    SVH_CUDA(cudaMalloc(&d.rowptr, (A.n + 1) * sizeof(int)));
+    SVH_CUDA(cudaMalloc(&d.col, std::max<size_t>(1, A.col.size()) * sizeof(int)));
+    SVH_CUDA(cudaMalloc(&d.val, std::max<size_t>(1, A.val.size()) * sizeof(double)));
+    SVH_CUDA(cudaMalloc(&d.dinv, std::max(1, A.n) * sizeof(double)));
+    SVH_CUDA(cudaMemcpy(d.rowptr, A.rowptr.data(), (A.n + 1) * sizeof(int), cudaMemcpyHostToDevice));
+    SVH_CUDA(cudaMemcpy(d.col, A.col.data(), A.col.size() * sizeof(int), cudaMemcpyHostToDevice));
+    SVH_CUDA(cudaMemcpy(d.val, A.val.data(), A.val.size() * sizeof(double), cudaMemcpyHostToDevice));
+    SVH_CUDA(cudaMemcpy(d.dinv, dinv.data(), A.n * sizeof(double), cudaMemcpyHostToDevice));
+    const size_t vb = (size_t)2 * std::max(1, A.n) * sizeof(double);
+    SVH_CUDA(cudaMalloc(&d.vb, vb));
+    SVH_CUDA(cudaMalloc(&d.vx, vb));
+    SVH_CUDA(cudaMalloc(&d.tmp, vb));
+    SVH_CUDA(cudaMalloc(&d.x2, vb));
+    return d;
+}
+
+// dense SPD inverse (Cholesky, then solve for the identity); returns row-major
+std::vector<double> dense_inverse(const CsrHost& A) {
+    const int n = A.n;
+    std::vector<double> L((size_t)n * n, 0.0);
+    for (int i = 0; i < n; ++i)
+        for (int p = A.rowptr[i]; p < A.rowptr[i + 1]; ++p) L[(size_t)i * n + A.col[p]] = A.val[p];
+    // Cholesky in place (lower)
+    for (int j = 0; j < n; ++j) {
+        double d = L[(size_t)j * n + j];
+        for (int k = 0; k < j; ++k) d -= L[(size_t)j * n + k] * L[(size_t)j * n + k];
+        SVH_CHECK(d > 0, SVH_ECUDA, "coarse Schur matrix not SPD");
+        d = std::sqrt(d);
+        L[(size_t)j * n + j] = d;
+        for (int i = j + 1; i < n; ++i) {
+            double s = L[(size_t)i * n + j];
+            for (int k = 0; k < j; ++k) s -= L[(size_t)i * n + k] * L[(size_t)j * n + k];
+            L[(size_t)i * n + j] = s / d;
+        }
+    }
+    std::vector<double> inv((size_t)n * n, 0.0), col(n);
+    for (int c = 0; c < n; ++c) {
+        std::fill(col.begin(), col.end(), 0.0);
+        col[c] = 1.0;
+        for (int i = 0; i < n; ++i) {
+            double s = col[i];
+            for (int k = 0; k < i; ++k) s -= L[(size_t)i * n + k] * col[k];
+            col[i] = s / L[(size_t)i * n + i];
+        }
+        for (int i = n - 1; i >= 0; --i) {
+            double s = col[i];
+            for (int k = i + 1; k < n; ++k) s -= L[(size_t)k * n + i] * col[k];
+            col[i] = s / L[(size_t)i * n + i];
+        }
+        for (int i = 0; i < n; ++i) inv[(size_t)i * n + c] = col[i];
+    }
+    return inv;
+}
+
+}  // namespace
+
+static void build_amg(svh_handle* h, const std::vector<int32_t>& fixed) {
+    Solve* S = h->solve;
+    if (!S->levels.empty() && fixed == S->fixed_nodes) return;
+    free_levels(S);
+    S->fixed_nodes = fixed;
+    std::vector<uint8_t> fr(S->M, 1);
+    for (int32_t r : fixed) fr[r] = 0;
+    std::vector<int32_t> node2free(S->M, -1), flist;
+    for (int64_t r = 0; r < S->M; ++r)
+        if (fr[r]) {
+            node2free[r] = (int32_t)flist.size();
+            flist.push_back((int32_t)r);
+        }
+    S->nf = (int)flist.size();
+    SVH_CUDA(cudaMalloc(&S->d_free, S->M));
+    SVH_CUDA(cudaMemcpy(S->d_free, fr.data(), S->M, cudaMemcpyHostToDevice));
+    SVH_CUDA(cudaMalloc(&S->d_free_list, std::max<size_t>(1, flist.size()) * sizeof(int32_t)));
+    SVH_CUDA(cudaMemcpy(S->d_free_list, flist.data(), flist.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    SVH_CUDA(cudaMalloc(&S->d_node2free, S->M * sizeof(int32_t)));
+    SVH_CUDA(cudaMemcpy(S->d_node2free, node2free.data(), S->M * sizeof(int32_t), cudaMemcpyHostToDevice));
+    if (S->nf == 0) return;
+    CsrHost A = build_schur(S, node2free, S->nf);
+    const int kCoarse = 1024;
+    while (true) {
+        if (A.n <= kCoarse) {
+            auto inv = dense_inverse(A);
+            S->ncoarse = A.n;
+            SVH_CUDA(cudaMalloc(&S->d_cinv, inv.size() * sizeof(double)));
+            SVH_CUDA(cudaMemcpy(S->d_cinv, inv.data(), inv.size() * sizeof(double), cudaMemcpyHostToDevice));
+            CsrDev d = upload(A);
+            S->levels.push_back(d);
+            break;
+        }
+        std::vector<int> a1, a2;
+        const int n1 = pairwise(A, a1);
+        CsrHost A1 = galerkin(A, a1, n1);
+        const int n2 = pairwise(A1, a2);
+        std::vector<int> agg(A.n);
+        for (int i = 0; i < A.n; ++i) agg[i] = a2[a1[i]];
+        CsrDev d = upload(A);
+        d.nc = n2;
+        SVH_CUDA(cudaMalloc(&d.agg, A.n * sizeof(int)));
+        SVH_CUDA(cudaMemcpy(d.agg, agg.data(), A.n * sizeof(int), cudaMemcpyHostToDevice));
+        S->levels.push_back(d);
+        CsrHost C = galerkin(A, agg, n2);
+        if (n2 > 0.85 * A.n) {   // stalled coarsening: stop with a dense solve if small enough
+            SVH_CHECK(C.n <= 8192, SVH_ECUDA, "AMG coarsening stalled");
+        }
+        A.rowptr.swap(C.rowptr);
+        A.col.swap(C.col);
+        A.val.swap(C.val);
+        A.n = C.n;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host: solver workspace and operators
+static void ensure_work(svh_handle* h, int restart) {
+    Solve* S = h->solve;
+    const size_t need = (size_t)2 * std::max<int64_t>(S->nf, 1);
+    if (S->wsize < need) {
+        for (auto& b : S->wbuf) cudaFree(b);
+        for (auto& b : S->wbuf) SVH_CUDA(cudaMalloc(&b, need * sizeof(double) * 1));
+        S->wsize = need;
+    }
+    if (!S->d_red) SVH_CUDA(cudaMalloc(&S->d_red, 4096 * sizeof(double)));
+    if (!S->c64_in) {
+        SVH_CUDA(cudaMalloc(&S->c64_in, 5 * h->K * sizeof(float2)));
+        SVH_CUDA(cudaMalloc(&S->c64_out, 5 * h->K * sizeof(float2)));
+    }
+    if (S->krylov_m < restart) {
+        cudaFree(S->d_krylov);
+        S->d_krylov = nullptr;
+        // V: restart+1 vectors, Zp: restart vectors, plus 3 scratch (x, r, t)
+        const size_t nv = (size_t)(2 * restart + 4);
+        SVH_CUDA(cudaMalloc(&S->d_krylov, nv * S->N * sizeof(double2)));
+        S->krylov_m = restart;
+    }
+}
+
+// y = Asys x (fp64 complex, masked by the free set if given)
+static void apply_sys(svh_handle* h, const double2* x, double2* y, bool masked, cudaStream_t s) {
+    Solve* S = h->solve;
+    const int64_t K = h->K, n5 = 5 * K;
+    SVH_LAUNCH(k_to_c64, nblk(n5), 256, 0, s, x, S->c64_in, n5);
+    matvec(h, S->c64_in, S->c64_out, 1, false, true, s);
+    SVH_LAUNCH(k_sys_I, nblk(K), 256, 0, s, S->c64_out, x, y, S->d_fnode, masked ? S->d_free : nullptr, K);
+    SVH_LAUNCH(k_sys_Phi, nblk(S->M), 256, 0, s, x, y, S->d_node_vox, S->d_node_axis, masked ? S->d_free : nullptr, K,
+               S->M);
+}
+
+// AMG V-cycle on level l: x = B^-1 b (x overwritten), 2 vectors, V(2,2) l1-Jacobi
+static void vcycle(Solve* S, int l, const double* b, double* x, cudaStream_t s) {
+    const CsrDev& L = S->levels[l];
+    const int n = L.n;
+    if (l == (int)S->levels.size() - 1) {
+        SVH_LAUNCH(k_dense2, nblk(n, 8), 256, 0, s, n, S->d_cinv, b, x);
+        return;
+    }
+    const CsrDev& C = S->levels[l + 1];
+    double* rc = C.vb;
+    double* ec = C.vx;
+    SVH_LAUNCH(k_jacobi2, nblk(n), 256, 0, s, n, L.rowptr, L.col, L.val, L.dinv, b, (const double*)nullptr, x);
+    SVH_LAUNCH(k_jacobi2, nblk(n), 256, 0, s, n, L.rowptr, L.col, L.val, L.dinv, b, x, L.x2);
+    SVH_LAUNCH(k_resid2, nblk(n), 256, 0, s, n, L.rowptr, L.col, L.val, b, L.x2, L.tmp);
+    SVH_LAUNCH(k_zero, nblk(2 * L.nc), 256, 0, s, rc, (int64_t)2 * L.nc);
+    SVH_LAUNCH(k_restrict2, nblk(n), 256, 0, s, n, L.agg, L.tmp, rc);
+    vcycle(S, l + 1, rc, ec, s);
+    SVH_LAUNCH(k_prolong2, nblk(n), 256, 0, s, n, L.agg, ec, L.x2);
+    SVH_LAUNCH(k_jacobi2, nblk(n), 256, 0, s, n, L.rowptr, L.col, L.val, L.dinv, b, L.x2, x);
+    SVH_LAUNCH(k_jacobi2, nblk(n), 256, 0, s, n, L.rowptr, L.col, L.val, L.dinv, b, x, L.x2);
+    SVH_CUDA(cudaMemcpyAsync(x, L.x2, 2 * (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+}
+
+// PCG on S (level 0) for 2 real RHS: x = S^-1 b to relative tol
+static int pcg2(svh_handle* h, const double* b, double* x, double tol, int maxit, cudaStream_t s) {
+    Solve* S = h->solve;
+    const CsrDev& A = S->levels[0];
+    const int n = A.n;
+    double* r = S->wbuf[0];
+    double* z = S->wbuf[1];
+    double* p = S->wbuf[2];
+    double* q = S->wbuf[3];
+    double* red = S->d_red;
+    auto dot = [&](const double* a, const double* bb, double* out2) {
+        SVH_CUDA(cudaMemsetAsync(red, 0, 2 * sizeof(double), s));
+        SVH_LAUNCH(k_dot2, 296, 256, 0, s, (int64_t)n, a, bb, red);
+        SVH_CUDA(cudaMemcpyAsync(out2, red, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+        SVH_CUDA(cudaStreamSynchronize(s));
+    };
+    double bn[2];
+    dot(b, b, bn);
+    SVH_LAUNCH(k_zero, nblk(2 * n), 256, 0, s, x, (int64_t)2 * n);
+    if (bn[0] == 0 && bn[1] == 0) return 0;
+    SVH_CUDA(cudaMemcpyAsync(r, b, 2 * n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    vcycle(S, 0, r, z, s);
+    SVH_CUDA(cudaMemcpyAsync(p, z, 2 * n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    double rz[2];
+    dot(r, z, rz);
+    double* dscal = red + 8;
+    int it = 0;
+    bool done[2] = {bn[0] == 0, bn[1] == 0};
+    for (it = 1; it <= maxit; ++it) {
+        SVH_LAUNCH(k_spmv2, nblk(n), 256, 0, s, n, A.rowptr, A.col, A.val, p, q);
+        double pq[2];
+        dot(p, q, pq);
+        double alpha[2] = {done[0] || pq[0] == 0 ? 0 : rz[0] / pq[0], done[1] || pq[1] == 0 ? 0 : rz[1] / pq[1]};
+        SVH_CUDA(cudaMemcpyAsync(dscal, alpha, 2 * sizeof(double), cudaMemcpyHostToDevice, s));
+        SVH_LAUNCH(k_axpy2, nblk(n), 256, 0, s, (int64_t)n, dscal, +1, p, x);
+        SVH_LAUNCH(k_axpy2, nblk(n), 256, 0, s, (int64_t)n, dscal, -1, q, r);
+        double rr[2];
+        dot(r, r, rr);
+        for (int c = 0; c < 2; ++c)
+            if (!done[c] && std::sqrt(rr[c]) <= tol * std::sqrt(bn[c])) done[c] = true;
+        if (done[0] && done[1]) break;
+        vcycle(S, 0, r, z, s);
+        double rz2[2];
+        dot(r, z, rz2);
+        double beta[2] = {done[0] || rz[0] == 0 ? 0 : rz2[0] / rz[0], done[1] || rz[1] == 0 ? 0 : rz2[1] / rz[1]};
+        rz[0] = rz2[0];
+        rz[1] = rz2[1];
+        SVH_CUDA(cudaMemcpyAsync(dscal, beta, 2 * sizeof(double), cudaMemcpyHostToDevice, s));
+        SVH_LAUNCH(k_xpby2, nblk(n), 256, 0, s, (int64_t)n, z, dscal, p);
+    }
+    return std::min(it, maxit);
+}
+
+// out = Q^-1 in  (right preconditioner)
+static void precond(svh_handle* h, const double2* in, double2* out, double tol, int maxit, cudaStream_t s) {
+    Solve* S = h->solve;
+    const int64_t K = h->K, n5 = 5 * K;
+    double2* tt = S->d_krylov + (size_t)(2 * S->krylov_m + 3) * S->N;   // scratch vector
+    SVH_LAUNCH(k_pre_e, nblk(n5), 256, 0, s, in, S->d_yinv, tt, n5);
+    double* e2 = S->wbuf[4];
+    double* b2 = S->wbuf[5];
+    if (S->nf > 0) {
+        SVH_LAUNCH(k_pre_e2, nblk(S->nf), 256, 0, s, tt, in + n5, e2, S->d_free_list, S->d_node_vox, S->d_node_axis, K,
+                   S->nf);
+        S->inner_its += pcg2(h, e2, b2, tol, maxit, s);
+    }
+    SVH_LAUNCH(k_pre_b, nblk(S->M), 256, 0, s, b2, in + n5, out + n5, S->d_node2free, S->M);
+    SVH_LAUNCH(k_pre_a, nblk(K), 256, 0, s, in, out + n5, S->d_yinv, out, S->d_fnode, S->d_free, K);
+}
+
+static double cnorm(svh_handle* h, const double2* x, cudaStream_t s) {
+    Solve* S = h->solve;
+    SVH_CUDA(cudaMemsetAsync(S->d_red, 0, 2 * sizeof(double), s));
+    SVH_LAUNCH(k_cdots, dim3(296, 1), 256, 0, s, S->N, x, 0, x, S->d_red);
+    double v[2];
+    SVH_CUDA(cudaMemcpyAsync(v, S->d_red, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    SVH_CUDA(cudaStreamSynchronize(s));
+    return std::sqrt(std::max(v[0], 0.0));
+}
+
+// FGMRES(m), right preconditioned; returns iterations, writes x, final true rre
+static int fgmres(svh_handle* h, const double2* b, double2* x, double rre, int m, int maxit, double& final_rre,
+                  cudaStream_t s) {
+    Solve* S = h->solve;
+    const int64_t N = S->N;
+    double2* V = S->d_krylov;                         // m+1 vectors
+    double2* Zp = S->d_krylov + (size_t)(m + 1) * N;  // m vectors
+    double2* w = S->d_krylov + (size_t)(2 * m + 1) * N;
+    double2* r = S->d_krylov + (size_t)(2 * m + 2) * N;
+    double* hcol = S->d_red + 16;
+    const double bnorm = cnorm(h, b, s);
+    SVH_CUDA(cudaMemsetAsync(x, 0, N * sizeof(double2), s));
+    if (bnorm == 0) {
+        final_rre = 0;
+        return 0;
+    }
+    int total = 0;
+    final_rre = 1.0;
+    const double tol_inner = h->opts.inner_tol;
+    const int inner_max = h->opts.inner_maxit;
+    while (total < maxit) {
+        // r = b - A x
+        apply_sys(h, x, w, true, s);
+        SVH_LAUNCH(k_csub, nblk(N), 256, 0, s, N, b, w, r);
+        const double beta = cnorm(h, r, s);
+        final_rre = beta / bnorm;
+        if (final_rre <= rre) break;
+        SVH_LAUNCH(k_cscale, nblk(N), 256, 0, s, N, r, 1.0 / beta, V);
+        std::vector<cd> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1, 0.0);
+        g[0] = beta;
+        int j = 0;
+        for (; j < m && total < maxit; ++j, ++total) {
+            precond(h, V + (size_t)j * N, Zp + (size_t)j * N, tol_inner, inner_max, s);
+            apply_sys(h, Zp + (size_t)j * N, w, true, s);
+            // CGS2
+            std::vector<cd> hj(j + 2, 0.0);
+            for (int pass = 0; pass < 2; ++pass) {
+                SVH_CUDA(cudaMemsetAsync(hcol, 0, 2 * (j + 1) * sizeof(double), s));
+                SVH_LAUNCH(k_cdots, dim3(148, j + 1), 256, 0, s, N, V, N, w, hcol);
+                SVH_LAUNCH(k_cupdate, nblk(N), 256, 0, s, N, V, N, hcol, j + 1, w, 1.0);
+                std::vector<double> hv(2 * (j + 1));
+                SVH_CUDA(cudaMemcpyAsync(hv.data(), hcol, hv.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+                SVH_CUDA(cudaStreamSynchronize(s));
+                for (int i = 0; i <= j; ++i) hj[i] += cd(hv[2 * i], hv[2 * i + 1]);
+            }
+            const double hn = cnorm(h, w, s);
+            hj[j + 1] = hn;
+            if (hn > 0) SVH_LAUNCH(k_cscale, nblk(N), 256, 0, s, N, w, 1.0 / hn, V + (size_t)(j + 1) * N);
+            // apply previous Givens rotations
+            for (int i = 0; i < j; ++i) {
+                const cd t0 = std::conj(cs[i]) * hj[i] + std::conj(sn[i]) * hj[i + 1];
+                const cd t1 = -sn[i] * hj[i] + cs[i] * hj[i + 1];
+                hj[i] = t0;
+                hj[i + 1] = t1;
+            }
+            const double den = std::sqrt(std::norm(hj[j]) + std::norm(hj[j + 1]));
+            cs[j] = den > 0 ? hj[j] / den : cd(1.0);
+            sn[j] = den > 0 ? hj[j + 1] / den : cd(0.0);
+            hj[j] = den;
+            hj[j + 1] = 0.0;
+            g[j + 1] = -sn[j] * g[j];
+            g[j] = std::conj(cs[j]) * g[j];
+            for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = hj[i];
+            if (std::abs(g[j + 1]) / bnorm <= rre * 0.5 || hn == 0) {
+                ++j;
+                ++total;
+                break;
+            }
+        }
+        // solve H y = g (upper triangular j x j)
+        std::vector<cd> y(j);
+        for (int i = j - 1; i >= 0; --i) {
+            cd acc = g[i];
+            for (int k = i + 1; k < j; ++k) acc -= H[(size_t)i * m + k] * y[k];
+            y[i] = acc / H[(size_t)i * m + i];
+        }
+        // x += Zp y   (k_cupdate with sign -1 adds)
+        std::vector<double> yv(2 * j);
+        for (int i = 0; i < j; ++i) {
+            yv[2 * i] = y[i].real();
+            yv[2 * i + 1] = y[i].imag();
+        }
+        SVH_CUDA(cudaMemcpyAsync(hcol, yv.data(), yv.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+        SVH_LAUNCH(k_cupdate, nblk(N), 256, 0, s, N, Zp, N, hcol, j, x, -1.0);
+    }
+    // final true residual
+    apply_sys(h, x, w, true, s);
+    SVH_LAUNCH(k_csub, nblk(N), 256, 0, s, N, b, w, r);
+    final_rre = cnorm(h, r, s) / bnorm;
+    return total;
+}
+
+// ---------------------------------------------------------------------------
+struct PortSets {
+    std::vector<std::vector<int32_t>> plus, minus;
+    std::vector<int32_t> fixed;
+};
+
+static std::vector<int32_t> rect_nodes(svh_handle* h, const svh_face_rect* rects, int n) {
+    Solve* S = h->solve;
+    std::vector<int32_t> out;
+    for (int i = 0; i < n; ++i) {
+        const svh_face_rect& R = rects[i];
+        SVH_CHECK(R.axis >= 0 && R.axis < 3 && (R.side == 1 || R.side == -1), SVH_EINVAL, "bad face rect");
+        for (int z = std::max(0, R.lo[2]); z < std::min(h->kz, R.hi[2]); ++z)
+            for (int y = std::max(0, R.lo[1]); y < std::min(h->ky, R.hi[1]); ++y)
+                for (int x = std::max(0, R.lo[0]); x < std::min(h->kx, R.hi[0]); ++x) {
+                    const int32_t k = h->h_vmap[((int64_t)z * h->ky + y) * h->kx + x];
+                    if (k < 0) continue;
+                    out.push_back(S->fnode[6 * k + 2 * R.axis + (R.side > 0)]);
+                }
+    }
+    std::sort(out.begin(), out.end());
+    out.erase(std::unique(out.begin(), out.end()), out.end());
+    return out;
+}
+
+static PortSets port_sets(svh_handle* h, const svh_port* ports, int P) {
+    Solve* S = h->solve;
+    PortSets ps;
+    for (int p = 0; p < P; ++p) {
+        ps.plus.push_back(rect_nodes(h, ports[p].plus, ports[p].n_plus));
+        ps.minus.push_back(rect_nodes(h, ports[p].minus, ports[p].n_minus));
+        SVH_CHECK(!ps.plus.back().empty() && !ps.minus.back().empty(), SVH_EINVAL,
+                  "port " + std::to_string(p) + " has an empty terminal");
+        ps.fixed.insert(ps.fixed.end(), ps.plus.back().begin(), ps.plus.back().end());
+        ps.fixed.insert(ps.fixed.end(), ps.minus.back().begin(), ps.minus.back().end());
+    }
+    std::sort(ps.fixed.begin(), ps.fixed.end());
+    ps.fixed.erase(std::unique(ps.fixed.begin(), ps.fixed.end()), ps.fixed.end());
+    // G14: ground one node of every voxel component without a fixed node (union-find over shared faces)
+    std::vector<int32_t> parent(h->K);
+    std::iota(parent.begin(), parent.end(), 0);
+    std::function<int32_t(int32_t)> find = [&](int32_t a) {
+        while (parent[a] != a) a = parent[a] = parent[parent[a]];
+        return a;
+    };
+    for (int64_t r = 0; r < S->M; ++r) {
+        const int32_t v = S->node_vox[2 * r], u = S->node_vox[2 * r + 1];
+        if (v >= 0 && u >= 0) parent[find(v)] = find(u);
+    }
+    std::vector<uint8_t> has_fixed(h->K, 0);
+    for (int32_t r : ps.fixed) {
+        const int32_t v = S->node_vox[2 * r] >= 0 ? S->node_vox[2 * r] : S->node_vox[2 * r + 1];
+        has_fixed[find(v)] = 1;
+    }
+    std::vector<int32_t> extra;
+    for (int64_t k = 0; k < h->K; ++k) {
+        const int32_t root = find((int32_t)k);
+        if (!has_fixed[root]) {
+            has_fixed[root] = 1;
+            extra.push_back(S->fnode[6 * k + 0]);
+        }
+    }
+    ps.fixed.insert(ps.fixed.end(), extra.begin(), extra.end());
+    std::sort(ps.fixed.begin(), ps.fixed.end());
+    ps.fixed.erase(std::unique(ps.fixed.begin(), ps.fixed.end()), ps.fixed.end());
+    return ps;
+}
+
+static void ensure_structure(svh_handle* h) {
+    if (!h->solve) build_structure(h);
+}
+
+static void solve_columns(svh_handle* h, const svh_port* ports, int P, const int32_t* sel, int nsel, double* Ycols,
+                          svh_stats* st) {
+    ensure_structure(h);
+    Solve* S = h->solve;
+    auto t0 = std::chrono::steady_clock::now();
+    PortSets ps = port_sets(h, ports, P);
+    build_amg(h, ps.fixed);
+    const int m = std::max(1, h->opts.restart);
+    ensure_work(h, m);
+    cudaStream_t s = 0;
+    const int64_t N = S->N;
+    double2* b = S->d_krylov + (size_t)(2 * m + 3) * N;   // scratch slot (also used by precond -> copy out first)
+    double2* x = nullptr;
+    SVH_CUDA(cudaMalloc(&x, N * sizeof(double2)));
+    double2* bb = nullptr;
+    SVH_CUDA(cudaMalloc(&bb, N * sizeof(double2)));
+    uint8_t* pm = nullptr;
+    SVH_CUDA(cudaMalloc(&pm, S->M));
+    int32_t* dnodes = nullptr;
+    size_t maxn = 1;
+    for (int p = 0; p < P; ++p) maxn = std::max(maxn, ps.plus[p].size());
+    SVH_CUDA(cudaMalloc(&dnodes, maxn * sizeof(int32_t)));
+    double* cur = nullptr;
+    SVH_CUDA(cudaMalloc(&cur, 2 * sizeof(double)));
+    bool all_conv = true;
+    double worst = 0;
+    int tot_it = 0;
+    S->inner_its = 0;
+    (void)b;
+    for (int si = 0; si < nsel; ++si) {
+        const int p = sel[si];
+        SVH_CHECK(p >= 0 && p < P, SVH_EINVAL, "bad port index");
+        std::vector<uint8_t> mask(S->M, 0);
+        for (int32_t r : ps.plus[p]) mask[r] = 1;
+        SVH_CUDA(cudaMemcpy(pm, mask.data(), S->M, cudaMemcpyHostToDevice));
+        SVH_LAUNCH(k_rhs, nblk(h->K + S->M), 256, 0, s, bb, pm, S->d_fnode, h->K, S->M);
+        double rre_out = 0;
+        const int its = fgmres(h, bb, x, h->opts.rre, m, h->opts.max_iters, rre_out, s);
+        tot_it += its;
+        worst = std::max(worst, rre_out);
+        if (!(rre_out <= h->opts.rre * 1.0001)) all_conv = false;
+        if (st) st->iterations = its;
+        for (int q = 0; q < P; ++q) {
+            SVH_CUDA(cudaMemcpy(dnodes, ps.plus[q].data(), ps.plus[q].size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+            SVH_LAUNCH(k_port_current, 1, 256, 0, s, x, dnodes, (int)ps.plus[q].size(), S->d_node_vox, S->d_node_axis,
+                       h->K, cur);
+            double c2[2];
+            SVH_CUDA(cudaMemcpy(c2, cur, 2 * sizeof(double), cudaMemcpyDeviceToHost));
+            Ycols[2 * ((size_t)si * P + q)] = c2[0];
+            Ycols[2 * ((size_t)si * P + q) + 1] = c2[1];
+        }
+    }
+    cudaFree(x);
+    cudaFree(bb);
+    cudaFree(pm);
+    cudaFree(dnodes);
+    cudaFree(cur);
+    if (st) {
+        st->total_iterations += tot_it;
+        st->inner_iterations += S->inner_its;
+        st->converged = all_conv ? 1 : 0;
+        st->final_rre = std::max(st->final_rre, worst);
+        st->t_solve_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        st->t_setup_s = h->t_setup;
+    }
+    if (!all_conv) throw Error{SVH_ENOCONV, "GMRES did not reach rre (best iterate returned)"};
+}
+
 }  // namespace svh
 
 using namespace svh;
 extern "C" {
-int svh_apply_system(svh_handle*, const void*, void*, int32_t, svh_stream) {
-    set_error("svh_apply_system: not implemented yet");
-    return SVH_EINVAL;
+
+int svh_apply_system(svh_handle* h, const void* x, void* y, int32_t nrhs, svh_stream stream) {
+    try {
+        SVH_CHECK(h && x && y && nrhs >= 1 && x != y, SVH_EINVAL, "bad args");
+        SVH_CUDA(cudaSetDevice(h->device));
+        ensure_structure(h);
+        Solve* S = h->solve;
+        cudaStream_t s = (cudaStream_t)stream;
+        const int64_t N = S->N, K = h->K;
+        float2* zi = nullptr;
+        SVH_CUDA(cudaMalloc(&zi, 5 * K * nrhs * sizeof(float2)));
+        float2* xin = nullptr;
+        SVH_CUDA(cudaMalloc(&xin, 5 * K * nrhs * sizeof(float2)));
+        for (int r = 0; r < nrhs; ++r)
+            SVH_CUDA(cudaMemcpyAsync(xin + 5 * K * r, (const float2*)x + N * r, 5 * K * sizeof(float2),
+                                     cudaMemcpyDeviceToDevice, s));
+        matvec(h, xin, zi, nrhs, false, true, s);
+        for (int r = 0; r < nrhs; ++r)
+            SVH_LAUNCH(k_sys_c64, nblk(K + S->M), 256, 0, s, zi + 5 * K * r, (const float2*)x + N * r,
+                       (float2*)y + N * r, S->d_fnode, S->d_node_vox, S->d_node_axis, K, S->M);
+        SVH_CUDA(cudaStreamSynchronize(s));
+        cudaFree(zi);
+        cudaFree(xin);
+        return SVH_OK;
+    } catch (const Error& e) {
+        set_error(e.msg);
+        return e.code;
+    }
 }
-int svh_solve(svh_handle*, const svh_port*, int32_t, double*, double*, double*, double*, svh_stats*) {
-    set_error("svh_solve: not implemented yet");
-    return SVH_EINVAL;
+
+int svh_solve_columns(svh_handle* h, const svh_port* ports, int32_t n_ports, const int32_t* sel, int32_t n_sel,
+                      double* Y_cols, svh_stats* stats) {
+    try {
+        SVH_CHECK(h && ports && n_ports >= 1 && sel && n_sel >= 0 && Y_cols, SVH_EINVAL, "bad args");
+        SVH_CUDA(cudaSetDevice(h->device));
+        if (stats) std::memset(stats, 0, sizeof(*stats));
+        solve_columns(h, ports, n_ports, sel, n_sel, Y_cols, stats);
+        return SVH_OK;
+    } catch (const Error& e) {
+        set_error(e.msg);
+        return e.code;
+    }
 }
-int svh_solve_columns(svh_handle*, const svh_port*, int32_t, const int32_t*, int32_t, double*, svh_stats*) {
-    set_error("svh_solve_columns: not implemented yet");
-    return SVH_EINVAL;
+
+int svh_solve(svh_handle* h, const svh_port* ports, int32_t n_ports, double* Z_port, double* L_H, double* R_ohm,
+              double* Y_port, svh_stats* stats) {
+    int code = SVH_OK;
+    try {
+        SVH_CHECK(h && ports && n_ports >= 1, SVH_EINVAL, "bad args");
+        SVH_CUDA(cudaSetDevice(h->device));
+        if (stats) std::memset(stats, 0, sizeof(*stats));
+        const int P = n_ports;
+        std::vector<int32_t> sel(P);
+        std::iota(sel.begin(), sel.end(), 0);
+        std::vector<double> Yc((size_t)2 * P * P);
+        try {
+            solve_columns(h, ports, P, sel.data(), P, Yc.data(), stats);
+        } catch (const Error& e) {
+            if (e.code != SVH_ENOCONV) throw;
+            code = SVH_ENOCONV;
+            set_error(e.msg);
+        }
+        // Y[q][p] = column p entry q
+        std::vector<cd> Y((size_t)P * P), Z((size_t)P * P);
+        for (int p = 0; p < P; ++p)
+            for (int q = 0; q < P; ++q) Y[(size_t)q * P + p] = cd(Yc[2 * ((size_t)p * P + q)], Yc[2 * ((size_t)p * P + q) + 1]);
+        // Z = Y^-1 (Gauss-Jordan with partial pivoting)
+        std::vector<cd> Aug((size_t)P * 2 * P);
+        for (int i = 0; i < P; ++i)
+            for (int j = 0; j < P; ++j) {
+                Aug[(size_t)i * 2 * P + j] = Y[(size_t)i * P + j];
+                Aug[(size_t)i * 2 * P + P + j] = (i == j) ? 1.0 : 0.0;
+            }
+        for (int c = 0; c < P; ++c) {
+            int piv = c;
+            for (int i = c + 1; i < P; ++i)
+                if (std::abs(Aug[(size_t)i * 2 * P + c]) > std::abs(Aug[(size_t)piv * 2 * P + c])) piv = i;
+            SVH_CHECK(std::abs(Aug[(size_t)piv * 2 * P + c]) > 1e-300, SVH_EOPENPORT, "singular Y (open port)");
+            if (piv != c)
+                for (int j = 0; j < 2 * P; ++j) std::swap(Aug[(size_t)c * 2 * P + j], Aug[(size_t)piv * 2 * P + j]);
+            const cd d = Aug[(size_t)c * 2 * P + c];
+            for (int j = 0; j < 2 * P; ++j) Aug[(size_t)c * 2 * P + j] /= d;
+            for (int i = 0; i < P; ++i) {
+                if (i == c) continue;
+                const cd f = Aug[(size_t)i * 2 * P + c];
+                if (f == 0.0) continue;
+                for (int j = 0; j < 2 * P; ++j) Aug[(size_t)i * 2 * P + j] -= f * Aug[(size_t)c * 2 * P + j];
+            }
+        }
+        for (int i = 0; i < P; ++i)
+            for (int j = 0; j < P; ++j) Z[(size_t)i * P + j] = Aug[(size_t)i * 2 * P + P + j];
+        for (int i = 0; i < P * P; ++i) {
+            if (Z_port) {
+                Z_port[2 * i] = Z[i].real();
+                Z_port[2 * i + 1] = Z[i].imag();
+            }
+            if (Y_port) {
+                Y_port[2 * i] = Y[i].real();
+                Y_port[2 * i + 1] = Y[i].imag();
+            }
+            if (L_H) L_H[i] = Z[i].imag() / h->omega;
+            if (R_ohm) R_ohm[i] = Z[i].real();
+        }
+        return code;
+    } catch (const Error& e) {
+        set_error(e.msg);
+        return e.code;
+    }
 }
-}
+
+}  // extern "C"

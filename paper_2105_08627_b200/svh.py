@@ -89,6 +89,8 @@ def lib():
         L.svh_solve_columns.argtypes = [vp, ctypes.POINTER(Port), i32, ctypes.POINTER(i32), i32, dp,
                                         ctypes.POINTER(Stats)]
         L.svh_get_kernels.argtypes = [vp, dp]
+        L.svh_profile_enable.argtypes = [vp, i32]
+        L.svh_profile_read.argtypes = [vp, dp, ctypes.POINTER(i64), i32]
         L.svh_get_stats.argtypes = [vp, ctypes.POINTER(Stats)]
         L.svh_destroy.argtypes = [vp]
         L.svh_destroy.restype = None
@@ -96,7 +98,7 @@ def lib():
         L.svh_launch_count.restype = i64
         for name in ("svh_setup", "svh_set_frequency", "svh_unknowns", "svh_embedding", "svh_matvec",
                      "svh_matvec_grid", "svh_apply_system", "svh_solve", "svh_solve_columns", "svh_get_kernels",
-                     "svh_get_stats"):
+                     "svh_get_stats", "svh_profile_enable", "svh_profile_read"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -104,7 +106,8 @@ def lib():
 
 EXPORTED = ("svh_default_opts", "svh_setup", "svh_set_frequency", "svh_unknowns", "svh_embedding", "svh_matvec",
             "svh_matvec_grid", "svh_apply_system", "svh_solve", "svh_solve_columns", "svh_get_kernels",
-            "svh_get_stats", "svh_destroy", "svh_last_error", "svh_launch_count")
+            "svh_get_stats", "svh_profile_enable", "svh_profile_read", "svh_destroy", "svh_last_error",
+            "svh_launch_count")
 
 
 def _check(code):
@@ -263,6 +266,16 @@ class Handle:
         out = np.zeros((7, kz, ky, kx))
         _check(lib().svh_get_kernels(self._h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
         return out
+
+    def profile(self, on=True):
+        _check(lib().svh_profile_enable(self._h, int(on)))
+
+    def profile_read(self, reset=True):
+        ms = np.zeros(5)
+        n = np.zeros(5, dtype=np.int64)
+        _check(lib().svh_profile_read(self._h, ms.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                      n.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), int(reset)))
+        return ms, n
 
     def stats(self):
         st = Stats()

@@ -7,9 +7,10 @@ symmetry identities.  Citations: PAPER.md lines (P:n).
 """
 import numpy as np
 import pytest
-from scipy import integrate
 
 from oracle import kernels
+
+from _pins import box_integral
 
 FOUR_PI = 4 * np.pi
 
@@ -131,21 +132,6 @@ def test_toeplitz_invariance():
         v2 = brute_6d(b, a, np.array([7, 1, 5]) + m, np.array([7, 1, 5]), 1.0, n=8)
         assert abs(v1 - v2) < 1e-13
         assert abs(kernels.toeplitz_blocks([m])[(b, a)][0] - v1) < 1e-8 * 0.05
-
-
-def box_integral(a, b, c):
-    """(1/4pi) int int_{box^2} 1/|r-r'| for an a x b x c box (unit voxels), independent route.
-
-    = (8/4pi) int_0^a int_0^b int_0^c (a-x)(b-y)(c-z)/r; the z integral is done
-    analytically: int_0^c (c-z)/sqrt(rho^2+z^2) dz = c asinh(c/rho) - sqrt(rho^2+c^2) + rho,
-    the (x,y) integral by adaptive QUADPACK (scipy dblquad).
-    """
-    def f(y, x):
-        rho = np.hypot(x, y)
-        inner = c * np.arcsinh(c / rho) - np.sqrt(rho ** 2 + c ** 2) + rho
-        return (a - x) * (b - y) * inner
-    val, err = integrate.dblquad(f, 0, a, 0, b, epsabs=1e-14, epsrel=1e-13)
-    return 8 * val / FOUR_PI
 
 
 @pytest.mark.parametrize("dims", [(2, 1, 1), (2, 2, 1), (2, 2, 2), (16, 2, 2), (5, 3, 1)])
