@@ -167,6 +167,12 @@ int svh_solve(svh_handle* h, const svh_port* ports, int32_t n_ports, double* Z_p
 int svh_solve_columns(svh_handle* h, const svh_port* ports, int32_t n_ports, const int32_t* sel,
                       int32_t n_sel, double* Y_cols, svh_stats* stats);
 
+/* Port post-processing (reading G13): Z = Y^-1, L = Im(Z)/omega, R = Re(Z).
+ *   Y_port : host double[2*P*P] interleaved complex, row-major (Y[q][p] = current at
+ *            port q for a 1 V drive of port p).  Outputs as in svh_solve (any may be NULL).
+ * Errors: SVH_EINVAL, SVH_EOPENPORT (singular Y).  Host only, no device work. */
+int svh_y_to_zl(const double* Y_port, int32_t P, double freq_hz, double* Z_port, double* L_H, double* R_ohm);
+
 /* Copy the 7 unit-voxel kernels (fp64 [7][kz][ky][kx], order K0, K1x, K1y, K1z,
  * K2x, K2y, K2z; non-negative offsets) to host memory (tests / diagnostics). */
 int svh_get_kernels(const svh_handle* h, double* host_out);

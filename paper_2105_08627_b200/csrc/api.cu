@@ -93,6 +93,32 @@ static void build_lattice(svh_handle* h) {
     SVH_CUDA(cudaMemcpy(h->d_mat, h->h_mat.data(), Kt, cudaMemcpyHostToDevice));
     SVH_CUDA(cudaMalloc(&h->d_vmap, Kt * sizeof(int32_t)));
     SVH_CUDA(cudaMemcpy(h->d_vmap, h->h_vmap.data(), Kt * sizeof(int32_t), cudaMemcpyHostToDevice));
+    // row occupancy words for the gather/scatter of passes A/E
+    h->rowW = (kx + 31) / 32;
+    const int64_t rows = (int64_t)ky * kz;
+    std::vector<int2> ri((size_t)rows * h->rowW);
+    std::vector<uint8_t> matp(std::max<int64_t>(1, h->K));
+    int64_t run = 0;   // packed index of the next occupied voxel (x-fastest order)
+    for (int64_t r = 0; r < rows; ++r)
+        for (int w = 0; w < h->rowW; ++w) {
+            unsigned m = 0;
+            const int64_t first = run;
+            for (int b = 0; b < 32; ++b) {
+                const int x = 32 * w + b;
+                if (x >= kx) break;
+                const int64_t c = r * kx + x;
+                if (h->h_vmap[c] >= 0) {
+                    m |= 1u << b;
+                    matp[h->h_vmap[c]] = h->h_mat[c];
+                    ++run;
+                }
+            }
+            ri[(size_t)r * h->rowW + w] = make_int2((int)m, (int)first);
+        }
+    SVH_CUDA(cudaMalloc(&h->d_rowinfo, ri.size() * sizeof(int2)));
+    SVH_CUDA(cudaMemcpy(h->d_rowinfo, ri.data(), ri.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    SVH_CUDA(cudaMalloc(&h->d_matp, matp.size()));
+    SVH_CUDA(cudaMemcpy(h->d_matp, matp.data(), matp.size(), cudaMemcpyHostToDevice));
     SVH_CUDA(cudaMalloc(&h->d_vox, std::max<int64_t>(1, h->K) * sizeof(int32_t)));
     SVH_CUDA(cudaMemcpy(h->d_vox, h->h_vox.data(), h->K * sizeof(int32_t), cudaMemcpyHostToDevice));
 }
@@ -107,6 +133,8 @@ static void destroy(svh_handle* h) {
     free_tucker(h);
     cudaFree(h->d_mat);
     cudaFree(h->d_vmap);
+    cudaFree(h->d_rowinfo);
+    cudaFree(h->d_matp);
     cudaFree(h->d_vox);
     cudaFree(h->d_kern);
     cudaFree(h->d_spec);

@@ -36,6 +36,9 @@ struct svh_handle {
     uint8_t* d_mat = nullptr;            // [Kt]
     int32_t* d_vmap = nullptr;           // [Kt]
     int32_t* d_vox = nullptr;            // [K]
+    int2* d_rowinfo = nullptr;           // [Ky*Kz][W]: {occupancy bits of 32 voxels, packed index of the first}
+    int rowW = 1;                        // words per row = ceil(Kx/32)
+    uint8_t* d_matp = nullptr;           // [K] material id in packed order
     double* d_kern = nullptr;            // [7][Kt] unit-voxel kernels, fp64
     float* d_spec = nullptr;             // [7][hz][hy][hx] dense octant spectra (tucker_tol == 0)
     SvhTucker tucker;

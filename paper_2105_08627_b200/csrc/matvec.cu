@@ -50,9 +50,18 @@ constexpr int em_size() {
 // ---------------------------------------------------------------------------
 // Row passes A (forward, gather + pad) and E (inverse, crop + local term + scatter).
 // Row length N along x, Q rows per CTA; threads = TPP*Q with TPP = threads per pencil.
+// Row occupancy words (rowinfo[row][j/32] = {bits, packed index of the word's first voxel})
+// give the packed index of voxel j of a row as pre + popc(bits below j): one tiny,
+// L1-resident load instead of a Kt-sized index map.
+__device__ __forceinline__ int packed_index(const int2* __restrict__ rowinfo, int W, int row, int j) {
+    const int2 mp = __ldg(&rowinfo[(int64_t)row * W + (j >> 5)]);
+    const unsigned bits = (unsigned)mp.x, b = (unsigned)(j & 31);
+    return ((bits >> b) & 1u) ? mp.y + __popc(bits & ((1u << b) - 1u)) : -1;
+}
+
 template <int N, int Q, bool PACKED>
 __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
-    k_row_fwd(const float2* __restrict__ in, float2* __restrict__ X1, const int32_t* __restrict__ vmap,
+    k_row_fwd(const float2* __restrict__ in, float2* __restrict__ X1, const int2* __restrict__ rowinfo, int W,
               const float2* __restrict__ tw, int Kx, int rows, int64_t K, int64_t Kt) {
     constexpr int R1 = fft_r1(N), R2 = fft_r2(N);
     const int rc = blockIdx.y;
@@ -60,10 +69,9 @@ __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
     const float2 zero = make_float2(0.f, 0.f);
     auto load = [&](int row, int j) -> float2 {
         if (row >= rows || j >= Kx) return zero;
-        const int64_t cell = (int64_t)row * Kx + j;
-        const int idx = __ldg(&vmap[cell]);
+        const int idx = packed_index(rowinfo, W, row, j);
         if (idx < 0) return zero;
-        return PACKED ? __ldg(&in[(int64_t)rc * K + idx]) : __ldg(&in[(int64_t)rc * Kt + cell]);
+        return PACKED ? __ldg(&in[(int64_t)rc * K + idx]) : __ldg(&in[(int64_t)rc * Kt + (int64_t)row * Kx + j]);
     };
     if constexpr (R2 == 1) {
         const int q = threadIdx.x;
@@ -111,22 +119,26 @@ __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
 template <int N, int Q, bool PACKED>
 __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
     k_row_inv(const float2* __restrict__ X1, float2* __restrict__ out, const float2* __restrict__ in,
-              const int32_t* __restrict__ vmap, const uint8_t* __restrict__ mat, const float2* __restrict__ zloc,
-              const float2* __restrict__ tw, int Kx, int rows, int64_t K, int64_t Kt, int green_only) {
+              const int2* __restrict__ rowinfo, int W, const uint8_t* __restrict__ matp,
+              const float2* __restrict__ zloc, int nzl, const float2* __restrict__ tw, int Kx, int rows, int64_t K,
+              int64_t Kt, int green_only) {
     constexpr int R1 = fft_r1(N), R2 = fft_r2(N);
     const int rc = blockIdx.y;
     const int comp = rc % 5;
     const int row0 = blockIdx.x * Q;
+    __shared__ float2 zs[256];   // z^b of this component per material
+    for (int m = threadIdx.x; m < nzl; m += blockDim.x) zs[m] = zloc[m * 5 + comp];
+    __syncthreads();
     auto store = [&](int row, int j, float2 v) {
         if (row >= rows || j >= Kx) return;
         const int64_t cell = (int64_t)row * Kx + j;
-        const int idx = __ldg(&vmap[cell]);
+        const int idx = packed_index(rowinfo, W, row, j);
         if (idx < 0) {
             if (!PACKED) out[(int64_t)rc * Kt + cell] = make_float2(0.f, 0.f);
             return;
         }
         if (!green_only) {
-            const float2 z = __ldg(&zloc[__ldg(&mat[cell]) * 5 + comp]);
+            const float2 z = zs[__ldg(&matp[idx])];
             const float2 iv = PACKED ? __ldg(&in[(int64_t)rc * K + idx]) : __ldg(&in[(int64_t)rc * Kt + cell]);
             v = cadd(v, cmul(z, iv));
         }
@@ -309,7 +321,8 @@ __device__ __forceinline__ void kernel_values(const SpecView& sv, int kx, int ky
 template <int N, int Q>
 __global__ void __launch_bounds__(5 * Q)
     k_freq_small(float2* __restrict__ X2, SpecView sv, int Nx, int Ny, int Kz, float g, int nrhs) {
-    extern __shared__ float2 S[];   // [5][N][Q]
+    extern __shared__ float2 S[];   // [5][N][Q] spectra, then [7][N][Q] kernel values (float)
+    float* KV = reinterpret_cast<float*>(S + 5 * N * Q);
     const int c = threadIdx.x / Q, q = threadIdx.x % Q;
     const int kx0 = blockIdx.x * Q;
     const int ky = blockIdx.y;
@@ -322,6 +335,14 @@ __global__ void __launch_bounds__(5 * Q)
     float2 nxt[NH];
 #pragma unroll
     for (int j = 0; j < NH; ++j) nxt[j] = (ok && j < Kz) ? col[(int64_t)j * plane] : zero;
+    // the 7 kernel spectra of this CTA's (kz, kx) points, reused by every RHS
+    for (int t = threadIdx.x; t < N * Q; t += 5 * Q) {
+        const int k = t / Q, qq = t % Q;
+        float kv[7];
+        kernel_values(sv, min(kx0 + qq, Nx - 1), ky, k, Nx, Ny, N, kv);
+#pragma unroll
+        for (int m = 0; m < 7; ++m) KV[(m * N + k) * Q + qq] = kv[m];
+    }
     for (int r = 0; r < nrhs; ++r) {
         float2 v[N];
 #pragma unroll
@@ -337,13 +358,12 @@ __global__ void __launch_bounds__(5 * Q)
         }
         for (int t = threadIdx.x; t < N * Q; t += 5 * Q) {
             const int k = t / Q, qq = t % Q;
-            if (kx0 + qq >= Nx) continue;
-            float kv[7];
-            kernel_values(sv, kx0 + qq, ky, k, Nx, Ny, N, kv);
             float2 w[5];
 #pragma unroll
             for (int cc = 0; cc < 5; ++cc) w[cc] = S[(cc * N + k) * Q + qq];
-            mac5(w, kv[0], kv[1], kv[2], kv[3], kv[4], kv[5], kv[6], g);
+            mac5(w, KV[(0 * N + k) * Q + qq], KV[(1 * N + k) * Q + qq], KV[(2 * N + k) * Q + qq],
+                 KV[(3 * N + k) * Q + qq], KV[(4 * N + k) * Q + qq], KV[(5 * N + k) * Q + qq],
+                 KV[(6 * N + k) * Q + qq], g);
 #pragma unroll
             for (int cc = 0; cc < 5; ++cc) S[(cc * N + k) * Q + qq] = w[cc];
         }
@@ -439,12 +459,12 @@ void run_pass_a(svh_handle* h, const float2* in, bool packed, int nrhs, cudaStre
     dim3 grid((rows + Q - 1) / Q, 5 * nrhs);
     if (packed) {
         prep(k_row_fwd<N, Q, true>, smem);
-        SVH_LAUNCH((k_row_fwd<N, Q, true>), grid, nt, smem, s, in, h->X1, h->d_vmap, h->d_tw[0], h->kx, rows, h->K,
-                   h->Kt);
+        SVH_LAUNCH((k_row_fwd<N, Q, true>), grid, nt, smem, s, in, h->X1, h->d_rowinfo, h->rowW, h->d_tw[0], h->kx,
+                   rows, h->K, h->Kt);
     } else {
         prep(k_row_fwd<N, Q, false>, smem);
-        SVH_LAUNCH((k_row_fwd<N, Q, false>), grid, nt, smem, s, in, h->X1, h->d_vmap, h->d_tw[0], h->kx, rows, h->K,
-                   h->Kt);
+        SVH_LAUNCH((k_row_fwd<N, Q, false>), grid, nt, smem, s, in, h->X1, h->d_rowinfo, h->rowW, h->d_tw[0], h->kx,
+                   rows, h->K, h->Kt);
     }
 }
 
@@ -463,7 +483,7 @@ void run_pass_c(svh_handle* h, int nrhs, cudaStream_t s) {
     SpecView sv{h->d_spec, h->hx, h->hy, h->hz};
     if constexpr (N <= 64) {
         constexpr int Q = N >= 64 ? 16 : 32;
-        const size_t smem = (size_t)5 * N * Q * sizeof(float2);
+        const size_t smem = (size_t)5 * N * Q * sizeof(float2) + (size_t)7 * N * Q * sizeof(float);
         dim3 grid((h->nx + Q - 1) / Q, h->ny);
         prep(k_freq_small<N, Q>, smem);
         SVH_LAUNCH((k_freq_small<N, Q>), grid, 5 * Q, smem, s, h->X2, sv, h->nx, h->ny, h->kz, h->gscale, nrhs);
@@ -487,14 +507,15 @@ void run_pass_e(svh_handle* h, const float2* in, float2* out, bool packed, bool 
     const int nt = fft_threads_per_pencil(N) * Q;
     const size_t smem = fft_r2(N) == 1 ? 0 : (size_t)Q * (N + N / fft_r1(N)) * sizeof(float2);
     dim3 grid((rows + Q - 1) / Q, 5 * nrhs);
+    const int nzl = (int)h->mats.size() + 1;
     if (packed) {
         prep(k_row_inv<N, Q, true>, smem);
-        SVH_LAUNCH((k_row_inv<N, Q, true>), grid, nt, smem, s, h->X1, out, in, h->d_vmap, h->d_mat, h->d_zloc,
-                   h->d_tw[0], h->kx, rows, h->K, h->Kt, (int)green_only);
+        SVH_LAUNCH((k_row_inv<N, Q, true>), grid, nt, smem, s, h->X1, out, in, h->d_rowinfo, h->rowW, h->d_matp,
+                   h->d_zloc, nzl, h->d_tw[0], h->kx, rows, h->K, h->Kt, (int)green_only);
     } else {
         prep(k_row_inv<N, Q, false>, smem);
-        SVH_LAUNCH((k_row_inv<N, Q, false>), grid, nt, smem, s, h->X1, out, in, h->d_vmap, h->d_mat, h->d_zloc,
-                   h->d_tw[0], h->kx, rows, h->K, h->Kt, (int)green_only);
+        SVH_LAUNCH((k_row_inv<N, Q, false>), grid, nt, smem, s, h->X1, out, in, h->d_rowinfo, h->rowW, h->d_matp,
+                   h->d_zloc, nzl, h->d_tw[0], h->kx, rows, h->K, h->Kt, (int)green_only);
     }
 }
 

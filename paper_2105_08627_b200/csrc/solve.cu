@@ -1290,14 +1290,31 @@ int svh_solve(svh_handle* h, const svh_port* ports, int32_t n_ports, double* Z_p
             set_error(e.msg);
         }
         // Y[q][p] = column p entry q
-        std::vector<cd> Y((size_t)P * P), Z((size_t)P * P);
+        std::vector<double> Yr((size_t)2 * P * P);
         for (int p = 0; p < P; ++p)
-            for (int q = 0; q < P; ++q) Y[(size_t)q * P + p] = cd(Yc[2 * ((size_t)p * P + q)], Yc[2 * ((size_t)p * P + q) + 1]);
+            for (int q = 0; q < P; ++q) {
+                Yr[2 * ((size_t)q * P + p)] = Yc[2 * ((size_t)p * P + q)];
+                Yr[2 * ((size_t)q * P + p) + 1] = Yc[2 * ((size_t)p * P + q) + 1];
+            }
+        if (Y_port) std::memcpy(Y_port, Yr.data(), Yr.size() * sizeof(double));
+        const int c2 = svh_y_to_zl(Yr.data(), P, h->freq, Z_port, L_H, R_ohm);
+        if (c2 != SVH_OK) return c2;
+        return code;
+    } catch (const Error& e) {
+        set_error(e.msg);
+        return e.code;
+    }
+}
+
+int svh_y_to_zl(const double* Yp, int32_t P, double freq_hz, double* Z_port, double* L_H, double* R_ohm) {
+    try {
+        SVH_CHECK(Yp && P >= 1 && freq_hz > 0, SVH_EINVAL, "bad args");
+        const double omega = 2.0 * M_PI * freq_hz;
         // Z = Y^-1 (Gauss-Jordan with partial pivoting)
         std::vector<cd> Aug((size_t)P * 2 * P);
         for (int i = 0; i < P; ++i)
             for (int j = 0; j < P; ++j) {
-                Aug[(size_t)i * 2 * P + j] = Y[(size_t)i * P + j];
+                Aug[(size_t)i * 2 * P + j] = cd(Yp[2 * ((size_t)i * P + j)], Yp[2 * ((size_t)i * P + j) + 1]);
                 Aug[(size_t)i * 2 * P + P + j] = (i == j) ? 1.0 : 0.0;
             }
         for (int c = 0; c < P; ++c) {
@@ -1317,20 +1334,17 @@ int svh_solve(svh_handle* h, const svh_port* ports, int32_t n_ports, double* Z_p
             }
         }
         for (int i = 0; i < P; ++i)
-            for (int j = 0; j < P; ++j) Z[(size_t)i * P + j] = Aug[(size_t)i * 2 * P + P + j];
-        for (int i = 0; i < P * P; ++i) {
-            if (Z_port) {
-                Z_port[2 * i] = Z[i].real();
-                Z_port[2 * i + 1] = Z[i].imag();
+            for (int j = 0; j < P; ++j) {
+                const cd z = Aug[(size_t)i * 2 * P + P + j];
+                const size_t k = (size_t)i * P + j;
+                if (Z_port) {
+                    Z_port[2 * k] = z.real();
+                    Z_port[2 * k + 1] = z.imag();
+                }
+                if (L_H) L_H[k] = z.imag() / omega;
+                if (R_ohm) R_ohm[k] = z.real();
             }
-            if (Y_port) {
-                Y_port[2 * i] = Y[i].real();
-                Y_port[2 * i + 1] = Y[i].imag();
-            }
-            if (L_H) L_H[i] = Z[i].imag() / h->omega;
-            if (R_ohm) R_ohm[i] = Z[i].real();
-        }
-        return code;
+        return SVH_OK;
     } catch (const Error& e) {
         set_error(e.msg);
         return e.code;

@@ -89,6 +89,7 @@ def lib():
         L.svh_solve_columns.argtypes = [vp, ctypes.POINTER(Port), i32, ctypes.POINTER(i32), i32, dp,
                                         ctypes.POINTER(Stats)]
         L.svh_get_kernels.argtypes = [vp, dp]
+        L.svh_y_to_zl.argtypes = [dp, i32, dbl, dp, dp, dp]
         L.svh_profile_enable.argtypes = [vp, i32]
         L.svh_profile_read.argtypes = [vp, dp, ctypes.POINTER(i64), i32]
         L.svh_get_stats.argtypes = [vp, ctypes.POINTER(Stats)]
@@ -98,7 +99,7 @@ def lib():
         L.svh_launch_count.restype = i64
         for name in ("svh_setup", "svh_set_frequency", "svh_unknowns", "svh_embedding", "svh_matvec",
                      "svh_matvec_grid", "svh_apply_system", "svh_solve", "svh_solve_columns", "svh_get_kernels",
-                     "svh_get_stats", "svh_profile_enable", "svh_profile_read"):
+                     "svh_get_stats", "svh_profile_enable", "svh_profile_read", "svh_y_to_zl"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -106,13 +107,28 @@ def lib():
 
 EXPORTED = ("svh_default_opts", "svh_setup", "svh_set_frequency", "svh_unknowns", "svh_embedding", "svh_matvec",
             "svh_matvec_grid", "svh_apply_system", "svh_solve", "svh_solve_columns", "svh_get_kernels",
-            "svh_get_stats", "svh_profile_enable", "svh_profile_read", "svh_destroy", "svh_last_error",
-            "svh_launch_count")
+            "svh_get_stats", "svh_profile_enable", "svh_profile_read", "svh_y_to_zl", "svh_destroy",
+            "svh_last_error", "svh_launch_count")
 
 
 def _check(code):
     if code != SVH_OK:
         raise SvhError(code, lib().svh_last_error().decode())
+
+
+def y_to_zl(Y, freq):
+    """svh_y_to_zl: Z = Y^-1, L = Im Z / omega, R = Re Z (host, in libsvh)."""
+    Y = np.asarray(Y, dtype=np.complex128)
+    P = Y.shape[0]
+    Yi = np.empty(2 * P * P)
+    Yi[0::2] = Y.real.ravel()
+    Yi[1::2] = Y.imag.ravel()
+    Z = np.zeros(2 * P * P)
+    L = np.zeros(P * P)
+    R = np.zeros(P * P)
+    dp = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))  # noqa: E731
+    _check(lib().svh_y_to_zl(dp(Yi), P, float(freq), dp(Z), dp(L), dp(R)))
+    return (Z[0::2] + 1j * Z[1::2]).reshape(P, P), L.reshape(P, P), R.reshape(P, P)
 
 
 def launch_count() -> int:
@@ -167,6 +183,7 @@ class Handle:
                            len(materials), float(freq), ctypes.byref(o), int(device), ctypes.byref(h)))
         self._h = h
         self.device = device
+        self.freq = float(freq)
         self.shape = (kz, ky, kx)
         K, M = ctypes.c_int64(), ctypes.c_int64()
         _check(L.svh_unknowns(h, ctypes.byref(K), ctypes.byref(M)))
@@ -197,6 +214,7 @@ class Handle:
     # -- API
     def set_frequency(self, freq):
         _check(lib().svh_set_frequency(self._h, float(freq)))
+        self.freq = float(freq)
 
     def matvec(self, I, out=None, green_only=False, stream=None):
         """I: torch complex64 cuda tensor [nrhs, 5, K] (or [5, K])."""
