@@ -292,9 +292,62 @@ __device__ __forceinline__ void mac5(float2 (&v)[5], float k0, float s1x, float 
 }
 
 struct SpecView {
-    const float* spec;   // dense [7][hz][hy][hx]
+    const float* spec;   // dense [7][hz][hy][hx]; null in Tucker mode
     int hx, hy, hz;
+    // Tucker mode (Eq. 10): factors [7][3] -> fp32 [h_i][d_i], cores [7] -> fp32 [d3][d2][d1]
+    const float* fac[7][3];
+    const float* core[7];
+    int rk[7][3];
 };
+
+// Tucker expansion of the 7 kernel spectra for a CTA tile (fixed ky, Q consecutive kx, all N kz)
+// into KV[m][kz][q]: G = core x2 F2[oy] (d3 x d1), H[q] = G x1 F1[ox_q] (d3), KV = H x3 F3[oz].
+// scratch: >= 2 * 32 * max(Q, 32) floats of shared memory.
+template <int N, int Q>
+__device__ void tucker_tile(const SpecView& sv, int kx0, int ky, int Nx, int Ny, float* KV, float* scratch) {
+    const int oy = ky <= (Ny >> 1) ? ky : Ny - ky;
+    const float sy = ky <= (Ny >> 1) ? 1.f : -1.f;
+    float* G = scratch;            // [d3][d1]
+    float* H = scratch + 32 * 32;  // [Q][d3]
+    for (int m = 0; m < 7; ++m) {
+        const int d1 = sv.rk[m][0], d2 = sv.rk[m][1], d3 = sv.rk[m][2];
+        const float* C = sv.core[m];
+        const float* F1 = sv.fac[m][0];
+        const float* F2 = sv.fac[m][1] + (int64_t)oy * d2;
+        const float* F3 = sv.fac[m][2];
+        for (int t = threadIdx.x; t < d3 * d1; t += blockDim.x) {
+            const int c3 = t / d1, c1 = t % d1;
+            float acc = 0.f;
+            for (int c2 = 0; c2 < d2; ++c2) acc = fmaf(__ldg(&C[((int64_t)c3 * d2 + c2) * d1 + c1]), __ldg(&F2[c2]), acc);
+            G[t] = acc;
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < Q * d3; t += blockDim.x) {
+            const int q = t / d3, c3 = t % d3;
+            const int kx = min(kx0 + q, Nx - 1);
+            const int ox = kx <= (Nx >> 1) ? kx : Nx - kx;
+            const float* f1 = F1 + (int64_t)ox * d1;
+            float acc = 0.f;
+            for (int c1 = 0; c1 < d1; ++c1) acc = fmaf(G[c3 * d1 + c1], __ldg(&f1[c1]), acc);
+            H[t] = acc;
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < N * Q; t += blockDim.x) {
+            const int k = t / Q, q = t % Q;
+            const int kx = min(kx0 + q, Nx - 1);
+            const int oz = k <= (N >> 1) ? k : N - k;
+            const float* f3 = F3 + (int64_t)oz * d3;
+            float acc = 0.f;
+            for (int c3 = 0; c3 < d3; ++c3) acc = fmaf(H[q * d3 + c3], __ldg(&f3[c3]), acc);
+            float sgn = 1.f;
+            if (m == 1) sgn = kx <= (Nx >> 1) ? 1.f : -1.f;
+            if (m == 2) sgn = sy;
+            if (m == 3) sgn = k <= (N >> 1) ? 1.f : -1.f;
+            KV[(m * N + k) * Q + q] = sgn * acc;
+        }
+        __syncthreads();
+    }
+}
 
 // the 7 kernel spectra at frequency (kx, ky, kz) from the octant (mirror symmetry + parity)
 __device__ __forceinline__ void kernel_values(const SpecView& sv, int kx, int ky, int kz, int Nx, int Ny, int Nz,
@@ -314,6 +367,11 @@ __device__ __forceinline__ void kernel_values(const SpecView& sv, int kx, int ky
     kv[3] *= sz;
 }
 
+template <int N, int Q>
+__host__ __device__ constexpr int freq_small_spec_f2() {
+    return 5 * N * Q > (1024 + 32 * Q + 1) / 2 ? 5 * N * Q : (1024 + 32 * Q + 1) / 2;
+}
+
 // Pass C for Nz <= 64: one thread per (component, pencil) does the whole
 // z-FFT in registers; the 5 spectra of Q pencils meet in shared memory for
 // the MAC.  The CTA loops over all RHS of the batch (kernel values stay in
@@ -321,8 +379,8 @@ __device__ __forceinline__ void kernel_values(const SpecView& sv, int kx, int ky
 template <int N, int Q>
 __global__ void __launch_bounds__(5 * Q)
     k_freq_small(float2* __restrict__ X2, SpecView sv, int Nx, int Ny, int Kz, float g, int nrhs) {
-    extern __shared__ float2 S[];   // [5][N][Q] spectra, then [7][N][Q] kernel values (float)
-    float* KV = reinterpret_cast<float*>(S + 5 * N * Q);
+    extern __shared__ float2 S[];   // [5][N][Q] spectra (also Tucker scratch), then [7][N][Q] kernel values
+    float* KV = reinterpret_cast<float*>(S + freq_small_spec_f2<N, Q>());
     const int c = threadIdx.x / Q, q = threadIdx.x % Q;
     const int kx0 = blockIdx.x * Q;
     const int ky = blockIdx.y;
@@ -335,13 +393,18 @@ __global__ void __launch_bounds__(5 * Q)
     float2 nxt[NH];
 #pragma unroll
     for (int j = 0; j < NH; ++j) nxt[j] = (ok && j < Kz) ? col[(int64_t)j * plane] : zero;
-    // the 7 kernel spectra of this CTA's (kz, kx) points, reused by every RHS
-    for (int t = threadIdx.x; t < N * Q; t += 5 * Q) {
-        const int k = t / Q, qq = t % Q;
-        float kv[7];
-        kernel_values(sv, min(kx0 + qq, Nx - 1), ky, k, Nx, Ny, N, kv);
+    // the 7 kernel spectra of this CTA's (kz, kx) points, reused by every RHS:
+    // dense octant lookup, or Tucker expansion on chip (scratch = the spectra buffer)
+    if (sv.spec) {
+        for (int t = threadIdx.x; t < N * Q; t += 5 * Q) {
+            const int k = t / Q, qq = t % Q;
+            float kv[7];
+            kernel_values(sv, min(kx0 + qq, Nx - 1), ky, k, Nx, Ny, N, kv);
 #pragma unroll
-        for (int m = 0; m < 7; ++m) KV[(m * N + k) * Q + qq] = kv[m];
+            for (int m = 0; m < 7; ++m) KV[(m * N + k) * Q + qq] = kv[m];
+        }
+    } else {
+        tucker_tile<N, Q>(sv, kx0, ky, Nx, Ny, KV, reinterpret_cast<float*>(S));
     }
     for (int r = 0; r < nrhs; ++r) {
         float2 v[N];
@@ -408,7 +471,35 @@ __global__ void __launch_bounds__(fft_max_threads(N))
         const int q = t % Q, kz = t / Q;
         if (q >= nq) continue;
         float kv[7];
-        kernel_values(sv, kx0 + q, ky, kz, Nx, Ny, N, kv);
+        if (sv.spec) {
+            kernel_values(sv, kx0 + q, ky, kz, Nx, Ny, N, kv);
+        } else {
+            // Tucker: direct contraction per point (Eq. 10)
+            const int kx = kx0 + q;
+            const int o3[3] = {kx <= (Nx >> 1) ? kx : Nx - kx, ky <= (Ny >> 1) ? ky : Ny - ky,
+                               kz <= (N >> 1) ? kz : N - kz};
+            for (int m = 0; m < 7; ++m) {
+                const int d1 = sv.rk[m][0], d2 = sv.rk[m][1], d3 = sv.rk[m][2];
+                const float* f1 = sv.fac[m][0] + (int64_t)o3[0] * d1;
+                const float* f2 = sv.fac[m][1] + (int64_t)o3[1] * d2;
+                const float* f3 = sv.fac[m][2] + (int64_t)o3[2] * d3;
+                float acc = 0.f;
+                for (int c3 = 0; c3 < d3; ++c3) {
+                    float a2 = 0.f;
+                    for (int c2 = 0; c2 < d2; ++c2) {
+                        float a1 = 0.f;
+                        const float* Cr = sv.core[m] + ((int64_t)c3 * d2 + c2) * d1;
+                        for (int c1 = 0; c1 < d1; ++c1) a1 = fmaf(__ldg(&Cr[c1]), __ldg(&f1[c1]), a1);
+                        a2 = fmaf(a1, __ldg(&f2[c2]), a2);
+                    }
+                    acc = fmaf(a2, __ldg(&f3[c3]), acc);
+                }
+                kv[m] = acc;
+            }
+            kv[1] *= kx <= (Nx >> 1) ? 1.f : -1.f;
+            kv[2] *= ky <= (Ny >> 1) ? 1.f : -1.f;
+            kv[3] *= kz <= (N >> 1) ? 1.f : -1.f;
+        }
         float2 v[5];
 #pragma unroll
         for (int c = 0; c < 5; ++c) v[c] = S[kz * PP + c * Q + q];
@@ -480,10 +571,22 @@ void run_pass_y(svh_handle* h, const float2* in, float2* out, int Lin, int Lout,
 
 template <int N>
 void run_pass_c(svh_handle* h, int nrhs, cudaStream_t s) {
-    SpecView sv{h->d_spec, h->hx, h->hy, h->hz};
+    SpecView sv{};
+    sv.spec = h->use_tucker ? nullptr : h->d_spec;
+    sv.hx = h->hx;
+    sv.hy = h->hy;
+    sv.hz = h->hz;
+    if (h->use_tucker)
+        for (int m = 0; m < 7; ++m) {
+            sv.core[m] = h->tucker.d_core[m];
+            for (int a = 0; a < 3; ++a) {
+                sv.fac[m][a] = h->tucker.d_factor[m][a];
+                sv.rk[m][a] = h->tucker.ranks[m][a];
+            }
+        }
     if constexpr (N <= 64) {
         constexpr int Q = N >= 64 ? 16 : 32;
-        const size_t smem = (size_t)5 * N * Q * sizeof(float2) + (size_t)7 * N * Q * sizeof(float);
+        const size_t smem = (size_t)freq_small_spec_f2<N, Q>() * sizeof(float2) + (size_t)7 * N * Q * sizeof(float);
         dim3 grid((h->nx + Q - 1) / Q, h->ny);
         prep(k_freq_small<N, Q>, smem);
         SVH_LAUNCH((k_freq_small<N, Q>), grid, 5 * Q, smem, s, h->X2, sv, h->nx, h->ny, h->kz, h->gscale, nrhs);

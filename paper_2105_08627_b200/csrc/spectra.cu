@@ -145,7 +145,9 @@ void compute_spectra(svh_handle* h) {
         for (int o = 0; o < 2; ++o) cudaFree(dC[a][o]);
 }
 
-void compute_tucker(svh_handle*) { throw Error{SVH_EINVAL, "Tucker mode not built yet"}; }
-void free_tucker(svh_handle*) {}
+void dgemm_nt(int m, int n, int k, const double* A, int lda, const double* B, int ldb, double* C, int ldc) {
+    dgemm(true, m, n, k, A, lda, 0, B, ldb, 0, C, ldc, 0, 1);
+}
+std::vector<double> embed_dft_matrix_host(int K, int N, bool odd) { return embed_dft_matrix(K, N, odd); }
 
 }  // namespace svh

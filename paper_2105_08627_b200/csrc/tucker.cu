@@ -1,0 +1,345 @@
+// H3 (Tucker mode): Algorithm 1 on the weighted Toeplitz tensors and
+// spectral factors for on-the-fly expansion in pass C (Eq. 10).
+//
+// Reading G8: the circulant embedding and the DFT act mode-wise, so the Tucker
+// ranks and relative Frobenius error of the spectrum equal those of the
+// Toeplitz tensor weighted by 1 (offset 0) / sqrt(2) (offset > 0) on each axis,
+// O = T x_i D_i.  With O ~ C x_i U_i (HOSVD, truncated at tol/sqrt(3) per mode
+// by tail energy, reading G9), the octant spectrum is
+//   Khat = (-i)^{#odd} C x_i F_i,   F_i = E_i D_i^-1 U_i   (h_i x d_i)
+// where E_i is the real even/odd embed+DFT matrix of spectra.cu.  Pass C
+// contracts C with the three factor rows at each (kx, ky, kz) on chip; the
+// dense circulant spectra never exist in HBM.
+//
+// Mode unfoldings: the Gram matrices G_i = O_(i) O_(i)^T are formed on the GPU
+// (fp64) and eigen-decomposed on the host (Householder tridiagonalisation +
+// implicit QL).  The final relative error ||O - C x_i U_i||_F / ||O||_F is
+// measured explicitly on the GPU (no cancellation) and ranks are raised until
+// it is <= tol; a Gram eigensolve cannot resolve singular values below
+// ~sqrt(eps) s_1, so for tol < ~1e-7 ranks may come out larger than a direct
+// SVD would give, but the error bound always holds.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "internal.h"
+
+namespace svh {
+
+void mode_products(const double* T, int Kx, int Ky, int Kz, const double* A, int hx, const double* B, int hy,
+                   const double* C, int hz, double* w1, double* w2, double* out);
+void dgemm_nt(int m, int n, int k, const double* A, int lda, const double* B, int ldb, double* C, int ldc);
+std::vector<double> embed_dft_matrix_host(int K, int N, bool odd);
+
+namespace {
+
+// out (mode-i unfolding, column-major K_i x rest) = weighted T
+__global__ void k_unfold(const double* __restrict__ T, double* __restrict__ out, int Kx, int Ky, int Kz, int mode,
+                         int weighted) {
+    const int64_t Kt = (int64_t)Kx * Ky * Kz;
+    const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (id >= Kt) return;
+    const int x = (int)(id % Kx), y = (int)((id / Kx) % Ky), z = (int)(id / ((int64_t)Kx * Ky));
+    double v = T[id];
+    if (weighted) v *= (x ? M_SQRT2 : 1.0) * (y ? M_SQRT2 : 1.0) * (z ? M_SQRT2 : 1.0);
+    int64_t o;
+    if (mode == 0)
+        o = id;                                        // [z][y][x]: x fastest already
+    else if (mode == 1)
+        o = ((int64_t)z * Kx + x) * Ky + y;            // y fastest
+    else
+        o = ((int64_t)y * Kx + x) * Kz + z;            // z fastest
+    out[o] = v;
+}
+
+__global__ void k_sqdiff(const double* __restrict__ a, const double* __restrict__ b, int64_t n,
+                         double* __restrict__ out) {
+    double s0 = 0, s1 = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double d = a[i] - b[i];
+        s0 += d * d;
+        s1 += b[i] * b[i];
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        s0 += __shfl_xor_sync(0xffffffff, s0, o);
+        s1 += __shfl_xor_sync(0xffffffff, s1, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&out[0], s0);
+        atomicAdd(&out[1], s1);
+    }
+}
+
+__global__ void k_to_f32t(const double* __restrict__ a, float* __restrict__ b, int64_t n) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) b[i] = (float)a[i];
+}
+
+// Householder tridiagonalisation (a row-major n x n, replaced by Q), d diag, e sub-diag.
+void tred2(std::vector<double>& a, int n, std::vector<double>& d, std::vector<double>& e) {
+    auto A = [&](int i, int j) -> double& { return a[(size_t)i * n + j]; };
+    for (int i = n - 1; i > 0; --i) {
+        const int l = i - 1;
+        double h = 0.0, scale = 0.0;
+        if (l > 0) {
+            for (int k = 0; k <= l; ++k) scale += std::fabs(A(i, k));
+            if (scale == 0.0) {
+                e[i] = A(i, l);
+            } else {
+                for (int k = 0; k <= l; ++k) {
+                    A(i, k) /= scale;
+                    h += A(i, k) * A(i, k);
+                }
+                double f = A(i, l);
+                double g = f >= 0 ? -std::sqrt(h) : std::sqrt(h);
+                e[i] = scale * g;
+                h -= f * g;
+                A(i, l) = f - g;
+                f = 0.0;
+                for (int j = 0; j <= l; ++j) {
+                    A(j, i) = A(i, j) / h;
+                    g = 0.0;
+                    for (int k = 0; k <= j; ++k) g += A(j, k) * A(i, k);
+                    for (int k = j + 1; k <= l; ++k) g += A(k, j) * A(i, k);
+                    e[j] = g / h;
+                    f += e[j] * A(i, j);
+                }
+                const double hh = f / (h + h);
+                for (int j = 0; j <= l; ++j) {
+                    f = A(i, j);
+                    e[j] = g = e[j] - hh * f;
+                    for (int k = 0; k <= j; ++k) A(j, k) -= (f * e[k] + g * A(i, k));
+                }
+            }
+        } else {
+            e[i] = A(i, l);
+        }
+        d[i] = h;
+    }
+    d[0] = 0.0;
+    e[0] = 0.0;
+    for (int i = 0; i < n; ++i) {
+        const int l = i - 1;
+        if (d[i] != 0.0) {
+            for (int j = 0; j <= l; ++j) {
+                double g = 0.0;
+                for (int k = 0; k <= l; ++k) g += A(i, k) * A(k, j);
+                for (int k = 0; k <= l; ++k) A(k, j) -= g * A(k, i);
+            }
+        }
+        d[i] = A(i, i);
+        A(i, i) = 1.0;
+        for (int j = 0; j <= l; ++j) A(j, i) = A(i, j) = 0.0;
+    }
+}
+
+// implicit QL on the tridiagonal (d, e); z (row-major) accumulates eigenvectors (columns)
+void tqli(std::vector<double>& d, std::vector<double>& e, int n, std::vector<double>& z) {
+    auto Z = [&](int i, int j) -> double& { return z[(size_t)i * n + j]; };
+    for (int i = 1; i < n; ++i) e[i - 1] = e[i];
+    e[n - 1] = 0.0;
+    for (int l = 0; l < n; ++l) {
+        int iter = 0, m;
+        do {
+            for (m = l; m < n - 1; ++m) {
+                const double dd = std::fabs(d[m]) + std::fabs(d[m + 1]);
+                if (std::fabs(e[m]) <= 1e-16 * dd) break;
+            }
+            if (m != l) {
+                SVH_CHECK(iter++ < 100, SVH_ECUDA, "tqli: no convergence");
+                double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+                double r = std::hypot(g, 1.0);
+                g = d[m] - d[l] + e[l] / (g + (g >= 0 ? std::fabs(r) : -std::fabs(r)));
+                double s = 1.0, c = 1.0, p = 0.0;
+                int i;
+                for (i = m - 1; i >= l; --i) {
+                    double f = s * e[i];
+                    const double b = c * e[i];
+                    e[i + 1] = (r = std::hypot(f, g));
+                    if (r == 0.0) {
+                        d[i + 1] -= p;
+                        e[m] = 0.0;
+                        break;
+                    }
+                    s = f / r;
+                    c = g / r;
+                    g = d[i + 1] - p;
+                    r = (d[i] - g) * s + 2.0 * c * b;
+                    d[i + 1] = g + (p = s * r);
+                    g = c * r - b;
+                    for (int k = 0; k < n; ++k) {
+                        f = Z(k, i + 1);
+                        Z(k, i + 1) = s * Z(k, i) + c * f;
+                        Z(k, i) = c * Z(k, i) - s * f;
+                    }
+                }
+                if (r == 0.0 && i >= l) continue;
+                d[l] -= p;
+                e[l] = g;
+                e[m] = 0.0;
+            }
+        } while (m != l);
+    }
+}
+
+// eigenpairs of symmetric G (n x n, row-major), sorted by decreasing eigenvalue;
+// U column-major (U[k + n*j] = component k of eigenvector j)
+void sym_eig(std::vector<double> G, int n, std::vector<double>& lam, std::vector<double>& U) {
+    std::vector<double> d(n), e(n);
+    if (n == 1) {
+        lam = {G[0]};
+        U = {1.0};
+        return;
+    }
+    tred2(G, n, d, e);
+    tqli(d, e, n, G);
+    std::vector<int> order(n);
+    for (int i = 0; i < n; ++i) order[i] = i;
+    std::sort(order.begin(), order.end(), [&](int a, int b) { return d[a] > d[b]; });
+    lam.resize(n);
+    U.resize((size_t)n * n);
+    for (int j = 0; j < n; ++j) {
+        lam[j] = d[order[j]];
+        for (int k = 0; k < n; ++k) U[(size_t)j * n + k] = G[(size_t)k * n + order[j]];
+    }
+}
+
+}  // namespace
+
+void free_tucker(svh_handle* h) {
+    for (int q = 0; q < 7; ++q) {
+        for (int a = 0; a < 3; ++a) {
+            cudaFree(h->tucker.d_factor[q][a]);
+            h->tucker.d_factor[q][a] = nullptr;
+        }
+        cudaFree(h->tucker.d_core[q]);
+        h->tucker.d_core[q] = nullptr;
+    }
+}
+
+void compute_tucker(svh_handle* h) {
+    const double tol = h->opts.tucker_tol;
+    const int K3[3] = {h->kx, h->ky, h->kz};
+    const int N3[3] = {h->nx, h->ny, h->nz};
+    const int H3[3] = {h->hx, h->hy, h->hz};
+    const int64_t Kt = h->Kt;
+    double *dO, *dU, *dG, *w1, *w2, *dRec, *dCore, *dred;
+    const int kmax = std::max(h->kx, std::max(h->ky, h->kz));
+    SVH_CUDA(cudaMalloc(&dO, Kt * sizeof(double)));
+    SVH_CUDA(cudaMalloc(&dU, Kt * sizeof(double)));
+    SVH_CUDA(cudaMalloc(&dG, (size_t)kmax * kmax * sizeof(double)));
+    SVH_CUDA(cudaMalloc(&w1, Kt * sizeof(double)));
+    SVH_CUDA(cudaMalloc(&w2, Kt * sizeof(double)));
+    SVH_CUDA(cudaMalloc(&dRec, Kt * sizeof(double)));
+    SVH_CUDA(cudaMalloc(&dCore, Kt * sizeof(double)));
+    SVH_CUDA(cudaMalloc(&dred, 2 * sizeof(double)));
+    double *dA[3], *dAt[3];
+    for (int a = 0; a < 3; ++a) {
+        SVH_CUDA(cudaMalloc(&dA[a], (size_t)K3[a] * K3[a] * sizeof(double)));
+        SVH_CUDA(cudaMalloc(&dAt[a], (size_t)K3[a] * K3[a] * sizeof(double)));
+    }
+    size_t bytes = 0;
+    const unsigned nb = (unsigned)((Kt + 255) / 256);
+    for (int q = 0; q < 7; ++q) {
+        const int odd_axis = (q >= 1 && q <= 3) ? q - 1 : -1;
+        const double* T = h->d_kern + q * Kt;
+        std::vector<double> lam[3], U[3];
+        double trace = 0;
+        for (int a = 0; a < 3; ++a) {
+            SVH_LAUNCH(k_unfold, nb, 256, 0, 0, T, dU, h->kx, h->ky, h->kz, a, 1);
+            const int n = K3[a];
+            const int rest = (int)(Kt / n);
+            dgemm_nt(n, n, rest, dU, n, dU, n, dG, n);
+            std::vector<double> G((size_t)n * n);
+            SVH_CUDA(cudaMemcpy(G.data(), dG, G.size() * sizeof(double), cudaMemcpyDeviceToHost));
+            trace = 0;
+            for (int i = 0; i < n; ++i) trace += G[(size_t)i * n + i];
+            sym_eig(G, n, lam[a], U[a]);
+        }
+        SVH_LAUNCH(k_unfold, nb, 256, 0, 0, T, dO, h->kx, h->ky, h->kz, 0, 1);   // weighted O, [z][y][x]
+        // ranks by tail energy (reading G9), then verified explicitly
+        int d[3];
+        for (int a = 0; a < 3; ++a) {
+            const int n = K3[a];
+            d[a] = n;
+            double tail = 0;
+            for (int k = n - 1; k >= 1; --k) {
+                tail += std::max(lam[a][k], 0.0);
+                if (tail > tol * tol / 3.0 * trace) break;
+                d[a] = k;
+            }
+        }
+        double err = 0;
+        for (int attempt = 0; attempt < 8; ++attempt) {
+            // U_i^T (d_i x K_i) and U_i (K_i x d_i), column-major
+            for (int a = 0; a < 3; ++a) {
+                const int n = K3[a], r = d[a];
+                std::vector<double> Ut((size_t)r * n), Uc((size_t)n * r);
+                for (int j = 0; j < r; ++j)
+                    for (int k = 0; k < n; ++k) {
+                        Ut[(size_t)k * r + j] = U[a][(size_t)j * n + k];
+                        Uc[(size_t)j * n + k] = U[a][(size_t)j * n + k];
+                    }
+                SVH_CUDA(cudaMemcpy(dAt[a], Ut.data(), Ut.size() * sizeof(double), cudaMemcpyHostToDevice));
+                SVH_CUDA(cudaMemcpy(dA[a], Uc.data(), Uc.size() * sizeof(double), cudaMemcpyHostToDevice));
+            }
+            // core = O x1 U1^T x2 U2^T x3 U3^T   [d3][d2][d1]
+            mode_products(dO, h->kx, h->ky, h->kz, dAt[0], d[0], dAt[1], d[1], dAt[2], d[2], w1, w2, dCore);
+            // reconstruction O_hat = core x_i U_i
+            mode_products(dCore, d[0], d[1], d[2], dA[0], h->kx, dA[1], h->ky, dA[2], h->kz, w1, w2, dRec);
+            SVH_CUDA(cudaMemset(dred, 0, 2 * sizeof(double)));
+            SVH_LAUNCH(k_sqdiff, 296, 256, 0, 0, dRec, dO, Kt, dred);
+            double r2[2];
+            SVH_CUDA(cudaMemcpy(r2, dred, sizeof(r2), cudaMemcpyDeviceToHost));
+            err = r2[1] > 0 ? std::sqrt(r2[0] / r2[1]) : 0.0;
+            if (err <= tol) break;
+            bool grown = false;
+            for (int a = 0; a < 3; ++a)
+                if (d[a] < K3[a]) {
+                    d[a] = std::min(K3[a], d[a] + 2);
+                    grown = true;
+                }
+            if (!grown) break;
+        }
+        h->tucker.rel_err[q] = err;
+        SVH_CHECK(d[0] <= 32 && d[2] <= 32, SVH_EINVAL,
+                  "Tucker rank > 32 (raise tucker_tol or use dense spectra)");
+        // spectral factors F_i = E_i D_i^-1 U_i  (h_i x d_i), stored row-major [h_i][d_i] fp32
+        for (int a = 0; a < 3; ++a) {
+            const int n = K3[a], r = d[a], hh = H3[a];
+            const auto E = embed_dft_matrix_host(n, N3[a], odd_axis == a);   // column-major hh x n
+            std::vector<float> F((size_t)hh * r);
+            for (int k = 0; k < hh; ++k)
+                for (int j = 0; j < r; ++j) {
+                    double acc = 0;
+                    for (int m = 0; m < n; ++m)
+                        acc += E[(size_t)m * hh + k] * (m ? 1.0 / M_SQRT2 : 1.0) * U[a][(size_t)j * n + m];
+                    F[(size_t)k * r + j] = (float)acc;
+                }
+            SVH_CUDA(cudaMalloc(&h->tucker.d_factor[q][a], F.size() * sizeof(float)));
+            SVH_CUDA(cudaMemcpy(h->tucker.d_factor[q][a], F.data(), F.size() * sizeof(float), cudaMemcpyHostToDevice));
+            h->tucker.ranks[q][a] = r;
+            bytes += F.size() * sizeof(float);
+        }
+        const int64_t nc = (int64_t)d[0] * d[1] * d[2];
+        SVH_CUDA(cudaMalloc(&h->tucker.d_core[q], nc * sizeof(float)));
+        SVH_LAUNCH(k_to_f32t, (unsigned)((nc + 255) / 256), 256, 0, 0, dCore, h->tucker.d_core[q], nc);
+        bytes += nc * sizeof(float);
+    }
+    SVH_CUDA(cudaDeviceSynchronize());
+    h->tucker.bytes = bytes;
+    cudaFree(dO);
+    cudaFree(dU);
+    cudaFree(dG);
+    cudaFree(w1);
+    cudaFree(w2);
+    cudaFree(dRec);
+    cudaFree(dCore);
+    cudaFree(dred);
+    for (int a = 0; a < 3; ++a) {
+        cudaFree(dA[a]);
+        cudaFree(dAt[a]);
+    }
+}
+
+}  // namespace svh
