@@ -115,8 +115,9 @@ def pass_bytes(h, R, packed=True):
     """Algorithmic HBM bytes of each pass per launch (R RHS), DESIGN.md "Roofline".
 
     pts/comp: A reads K (packed) + writes 2Kt; B 2Kt -> 4Kt; C 4Kt -> 4Kt (+ the 7 fp32
-    octant spectra once); D 4Kt -> 2Kt; E 2Kt + K (I again) -> K; maps: vmap 4 B/cell
-    in A and E, mat_id 1 B/cell in E.
+    octant spectra once, dense mode); D 4Kt -> 2Kt; E 2Kt + K (I again) -> K; maps: the
+    row-occupancy words (8 B per 32 cells) in A and E, the packed material ids (1 B per
+    voxel) in E -- each counted once per launch (compulsory bytes).
     """
     kz, ky, kx = h.shape
     Kt = kx * ky * kz
@@ -126,11 +127,12 @@ def pass_bytes(h, R, packed=True):
     X1 = kz * ky * nx
     X2 = kz * ny * nx
     spec = 7 * 4 * (nx // 2 + 1) * (ny // 2 + 1) * (nz // 2 + 1)
-    A = c8 * (K + X1) + 4 * Kt * R
+    rowinfo = 8 * ky * kz * ((kx + 31) // 32)
+    A = c8 * (K + X1) + rowinfo
     B = c8 * (X1 + X2)
-    C = c8 * 2 * X2 + spec
+    C = c8 * 2 * X2 + (0 if h.tucker else spec)
     D = c8 * (X2 + X1)
-    E = c8 * (X1 + 2 * K) + 5 * Kt * R
+    E = c8 * (X1 + 2 * K) + rowinfo + K
     return [A, B, C, D, E]
 
 
@@ -187,6 +189,32 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def time_to_L(name, device, world, rank):
+    """Time to the port L-matrix (BASELINE metric, 3rd part): svh_setup + svh_solve on a
+    BASELINE config, wall clock around the public API calls (ports sharded over ranks)."""
+    import torch
+    from paper_2105_08627_b200 import parallel, svh
+    case = {"cfg1": svh_inputs.config1, "cfg2": svh_inputs.config2, "cfg3": svh_inputs.config3,
+            "cfg4": svh_inputs.config4}[name]()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    h = svh.setup_case(case, tucker_tol=0.0, device=device, inner_tol=1e-3)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    if world > 1:
+        res = parallel.solve_sharded(h, case["ports"])
+    else:
+        res = h.solve(case["ports"])
+    t2 = time.perf_counter()
+    h.close()
+    st = res["stats"]
+    return {"workload": case["name"], "seconds": round(t2 - t0, 4), "setup_s": round(t1 - t0, 4),
+            "solve_s": round(t2 - t1, 4), "n_ports": len(case["ports"]),
+            "L_pH_diag": [round(float(v) * 1e12, 6) for v in np.diag(res["L"])],
+            "gmres_iterations": st.get("total_iterations"), "inner_pcg_iterations": st.get("inner_iterations"),
+            "rre": st.get("final_rre"), "converged": st.get("converged")}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -198,6 +226,8 @@ def main():
     ap.add_argument("--tucker", type=float, default=0.0)
     ap.add_argument("--cpu-rows", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-solve", action="store_true", help="skip the time-to-L measurement")
+    ap.add_argument("--solve-workload", default="cfg2")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -315,6 +345,9 @@ def main():
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes},
             "gpu_launches": int(launches),
             "clocks": clk.summary()}
+
+    if not args.no_solve:
+        line["time_to_L"] = time_to_L(args.solve_workload, local, world, rank)
 
     if rank == 0 and world == 1 and not args.no_cpu:
         v, dt, cores = cpu_oracle_rate(case, args.cpu_rows)

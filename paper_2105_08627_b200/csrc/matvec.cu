@@ -264,6 +264,104 @@ __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
     }
 }
 
+// Persistent, software-pipelined variant of the strided pass for N > 64: every CTA
+// loops over tiles; the input tile of the next iteration is copied HBM -> shared
+// memory with cp.async (16-byte LDGSTS, no register cost) while the current tile is
+// transformed, so a full tile of loads is always in flight per SM.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+
+template <int N, int Q, int DIR>
+constexpr int colpipe_stage_rows() {
+    return DIR < 0 ? N / 2 : N;
+}
+template <int N, int Q, int DIR>
+constexpr size_t colpipe_smem() {
+    return (size_t)(2 * colpipe_stage_rows<N, Q, DIR>() * Q + em_size<N, Q>()) * sizeof(float2);
+}
+
+template <int N, int Q, int DIR>
+__global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q, 1)
+    k_col_pipe(const float2* __restrict__ in, float2* __restrict__ out, const float2* __restrict__ tw, int Nx,
+               int Kz, int Lin, int Lout, int ntiles, int tiles_x) {
+    constexpr int R1 = fft_r1(N), R2 = fft_r2(N);
+    constexpr int SR = colpipe_stage_rows<N, Q, DIR>();
+    constexpr int NT = fft_threads_per_pencil(N) * Q;
+    extern __shared__ float2 sm[];
+    float2* T = sm + 2 * SR * Q;
+    const float2 zero = make_float2(0.f, 0.f);
+    const int lin = min(Lin, SR);
+    auto tile_src = [&](int t) {
+        const int xt = t % tiles_x, rest = t / tiles_x;
+        const int z = rest % Kz, rc = rest / Kz;
+        return in + (((int64_t)rc * Kz + z) * Lin) * (int64_t)Nx + (int64_t)xt * Q;
+    };
+    auto issue = [&](int t, int buf) {
+        const float2* src = tile_src(t);
+        float2* st = sm + buf * SR * Q;
+        for (int e = threadIdx.x; e < lin * (Q / 2); e += NT) {
+            const int j = e / (Q / 2), p = e % (Q / 2);
+            cp_async16(st + j * Q + 2 * p, src + (int64_t)j * Nx + 2 * p);
+        }
+    };
+    int t = blockIdx.x;
+    if (t < ntiles) issue(t, 0);
+    cp_async_commit();
+    for (int it = 0; t < ntiles; t += gridDim.x, ++it) {
+        const int buf = it & 1;
+        if (t + (int)gridDim.x < ntiles) issue(t + gridDim.x, buf ^ 1);
+        cp_async_commit();
+        cp_async_wait1();
+        __syncthreads();
+        const float2* st = sm + buf * SR * Q;
+        if (threadIdx.x < R2 * Q) {
+            const int n2 = threadIdx.x / Q, q = threadIdx.x % Q;
+            float2 v[R1];
+#pragma unroll
+            for (int n1 = 0; n1 < R1; ++n1) {
+                const int j = R2 * n1 + n2;
+                if (DIR < 0)
+                    v[n1] = (n1 < R1 / 2 && j < lin) ? st[j * Q + q] : zero;
+                else
+                    v[n1] = st[j * Q + q];
+            }
+            reg_fft<R1, DIR>(v);
+#pragma unroll
+            for (int k1 = 1; k1 < R1; ++k1) {
+                float2 w = __ldg(&tw[n2 * k1]);
+                if (DIR > 0) w.y = -w.y;
+                v[k1] = cmul(v[k1], w);
+            }
+#pragma unroll
+            for (int k1 = 0; k1 < R1; ++k1) T[em_idx<N, Q>(n2 * R1 + k1, q)] = v[k1];
+        }
+        __syncthreads();
+        if (threadIdx.x < R1 * Q) {
+            const int k1 = threadIdx.x / Q, q = threadIdx.x % Q;
+            const int xt = t % tiles_x, rest = t / tiles_x;
+            const int z = rest % Kz, rc = rest / Kz;
+            float2* dst = out + (((int64_t)rc * Kz + z) * Lout) * (int64_t)Nx + (int64_t)xt * Q;
+            float2 u[R2];
+#pragma unroll
+            for (int n2 = 0; n2 < R2; ++n2) u[n2] = T[em_idx<N, Q>(n2 * R1 + k1, q)];
+            reg_fft<R2, DIR>(u);
+#pragma unroll
+            for (int k2 = 0; k2 < R2; ++k2) {
+                const int j = k1 + R1 * k2;
+                if (DIR < 0)
+                    dst[(int64_t)j * Nx + q] = u[k2];
+                else if (k2 < R2 / 2 && j < Lout)
+                    dst[(int64_t)j * Nx + q] = u[k2];
+            }
+        }
+    }
+    cp_async_commit();
+}
+
 // ---------------------------------------------------------------------------
 // Moment-form 5->5 multiply-accumulate at one frequency point:
 //   m1x = I2D + I3D, m1y = I3D - I2D, m1z = -2 I3D
@@ -371,16 +469,25 @@ template <int N, int Q>
 __host__ __device__ constexpr int freq_small_spec_f2() {
     return 5 * N * Q > (1024 + 32 * Q + 1) / 2 ? 5 * N * Q : (1024 + 32 * Q + 1) / 2;
 }
+template <int N, int Q, bool ASYNC>
+constexpr size_t freq_small_smem() {
+    return (size_t)freq_small_spec_f2<N, Q>() * sizeof(float2) + (size_t)7 * N * Q * sizeof(float) +
+           (ASYNC ? (size_t)5 * ((N + 1) / 2) * Q * sizeof(float2) : 0);
+}
 
 // Pass C for Nz <= 64: one thread per (component, pencil) does the whole
 // z-FFT in registers; the 5 spectra of Q pencils meet in shared memory for
-// the MAC.  The CTA loops over all RHS of the batch (kernel values stay in
-// L1) and prefetches the next RHS while the MAC runs.
-template <int N, int Q>
+// the MAC.  The CTA loops over all RHS of the batch (the 7 kernel spectra of
+// its points are computed once into shared memory) and prefetches the next
+// RHS while the current one is transformed: into registers (ASYNC = false) or
+// into a shared staging tile with cp.async (ASYNC = true).
+template <int N, int Q, bool ASYNC>
 __global__ void __launch_bounds__(5 * Q)
     k_freq_small(float2* __restrict__ X2, SpecView sv, int Nx, int Ny, int Kz, float g, int nrhs) {
-    extern __shared__ float2 S[];   // [5][N][Q] spectra (also Tucker scratch), then [7][N][Q] kernel values
+    extern __shared__ float2 S[];   // [5][N][Q] spectra (also Tucker scratch), [7][N][Q] kernel values, stage
     float* KV = reinterpret_cast<float*>(S + freq_small_spec_f2<N, Q>());
+    constexpr int NH = (N + 1) / 2;
+    float2* stage = reinterpret_cast<float2*>(KV + 7 * N * Q);   // [5][NH][Q]
     const int c = threadIdx.x / Q, q = threadIdx.x % Q;
     const int kx0 = blockIdx.x * Q;
     const int ky = blockIdx.y;
@@ -389,10 +496,23 @@ __global__ void __launch_bounds__(5 * Q)
     const float2 zero = make_float2(0.f, 0.f);
     float2* col = X2 + (int64_t)c * Kz * plane + (int64_t)ky * Nx + kx0 + q;
     const int64_t rstride = 5 * Kz * plane;
-    constexpr int NH = (N + 1) / 2;
-    float2 nxt[NH];
+    const int kz_ld = min(Kz, NH);
+    auto issue = [&](int r) {   // cp.async the RHS r tile: 5 comps x kz_ld rows x Q columns (16-byte chunks)
+        const float2* base = X2 + r * rstride + (int64_t)ky * Nx + kx0;
+        for (int e = threadIdx.x; e < 5 * kz_ld * (Q / 2); e += 5 * Q) {
+            const int p = e % (Q / 2), rest = e / (Q / 2);
+            const int j = rest % kz_ld, cc = rest / kz_ld;
+            cp_async16(stage + (cc * NH + j) * Q + 2 * p, base + ((int64_t)cc * Kz + j) * plane + 2 * p);
+        }
+    };
+    float2 nxt[ASYNC ? 1 : NH];
+    if constexpr (ASYNC) {
+        issue(0);
+        cp_async_commit();
+    } else {
 #pragma unroll
-    for (int j = 0; j < NH; ++j) nxt[j] = (ok && j < Kz) ? col[(int64_t)j * plane] : zero;
+        for (int j = 0; j < NH; ++j) nxt[j] = (ok && j < Kz) ? col[(int64_t)j * plane] : zero;
+    }
     // the 7 kernel spectra of this CTA's (kz, kx) points, reused by every RHS:
     // dense octant lookup, or Tucker expansion on chip (scratch = the spectra buffer)
     if (sv.spec) {
@@ -408,16 +528,28 @@ __global__ void __launch_bounds__(5 * Q)
     }
     for (int r = 0; r < nrhs; ++r) {
         float2 v[N];
+        if constexpr (ASYNC) {
+            asm volatile("cp.async.wait_group 0;\n" ::);
+            __syncthreads();
 #pragma unroll
-        for (int j = 0; j < N; ++j) v[j] = j < NH ? nxt[j] : zero;
+            for (int j = 0; j < N; ++j) v[j] = (j < NH && j < Kz) ? stage[(c * NH + j) * Q + q] : zero;
+            __syncthreads();
+            if (r + 1 < nrhs) issue(r + 1);
+            cp_async_commit();
+        } else {
+#pragma unroll
+            for (int j = 0; j < N; ++j) v[j] = j < NH ? nxt[j] : zero;
+        }
         reg_fft<N, -1>(v);
 #pragma unroll
         for (int k = 0; k < N; ++k) S[(c * N + k) * Q + q] = v[k];
         __syncthreads();
-        if (r + 1 < nrhs) {
-            const float2* nc = col + (r + 1) * rstride;
+        if constexpr (!ASYNC) {
+            if (r + 1 < nrhs) {
+                const float2* nc = col + (r + 1) * rstride;
 #pragma unroll
-            for (int j = 0; j < NH; ++j) nxt[j] = (ok && j < Kz) ? nc[(int64_t)j * plane] : zero;
+                for (int j = 0; j < NH; ++j) nxt[j] = (ok && j < Kz) ? nc[(int64_t)j * plane] : zero;
+            }
         }
         for (int t = threadIdx.x; t < N * Q; t += 5 * Q) {
             const int k = t / Q, qq = t % Q;
@@ -562,6 +694,23 @@ void run_pass_a(svh_handle* h, const float2* in, bool packed, int nrhs, cudaStre
 template <int N, int DIR>
 void run_pass_y(svh_handle* h, const float2* in, float2* out, int Lin, int Lout, int nrhs, cudaStream_t s) {
     constexpr int Q = col_q<N>();
+    static const bool use_pipe = getenv("SVH_NO_PIPE") == nullptr;
+    if constexpr (DIR > 0 && fft_r2(N) > 1 && Q >= 2 && colpipe_smem<N, Q, DIR>() <= 220 * 1024) {
+        if (use_pipe && h->nx % Q == 0) {
+            const int tiles_x = h->nx / Q;
+            const int ntiles = tiles_x * h->kz * 5 * nrhs;
+            const size_t smem = colpipe_smem<N, Q, DIR>();
+            const int nt = fft_threads_per_pencil(N) * Q;
+            int dev = 0, nsm = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            const int grid = std::min(ntiles, nsm);
+            prep(k_col_pipe<N, Q, DIR>, smem);
+            SVH_LAUNCH((k_col_pipe<N, Q, DIR>), grid, nt, smem, s, in, out, h->d_tw[1], h->nx, h->kz, Lin, Lout,
+                       ntiles, tiles_x);
+            return;
+        }
+    }
     const int nt = fft_threads_per_pencil(N) * Q;
     const size_t smem = fft_r2(N) == 1 ? 0 : (size_t)em_size<N, Q>() * sizeof(float2);
     dim3 grid((h->nx + Q - 1) / Q, h->kz, 5 * nrhs);
@@ -585,11 +734,25 @@ void run_pass_c(svh_handle* h, int nrhs, cudaStream_t s) {
             }
         }
     if constexpr (N <= 64) {
-        constexpr int Q = N >= 64 ? 16 : 32;
-        const size_t smem = (size_t)freq_small_spec_f2<N, Q>() * sizeof(float2) + (size_t)7 * N * Q * sizeof(float);
-        dim3 grid((h->nx + Q - 1) / Q, h->ny);
-        prep(k_freq_small<N, Q>, smem);
-        SVH_LAUNCH((k_freq_small<N, Q>), grid, 5 * Q, smem, s, h->X2, sv, h->nx, h->ny, h->kz, h->gscale, nrhs);
+        static const int cq = getenv("SVH_CQ") ? atoi(getenv("SVH_CQ")) : 32;
+        static const bool casync = getenv("SVH_CASYNC") != nullptr;
+        auto launch = [&](auto Qc, auto Ac) {
+            constexpr int Q = decltype(Qc)::value;
+            constexpr bool A = decltype(Ac)::value;
+            const size_t smem = freq_small_smem<N, Q, A>();
+            dim3 grid((h->nx + Q - 1) / Q, h->ny);
+            prep(k_freq_small<N, Q, A>, smem);
+            SVH_LAUNCH((k_freq_small<N, Q, A>), grid, 5 * Q, smem, s, h->X2, sv, h->nx, h->ny, h->kz, h->gscale,
+                       nrhs);
+        };
+        const bool async_ok = casync && h->nx % 32 == 0;
+        if (N >= 64 || cq == 16) {
+            if (async_ok) launch(std::integral_constant<int, 16>{}, std::true_type{});
+            else launch(std::integral_constant<int, 16>{}, std::false_type{});
+        } else {
+            if (async_ok) launch(std::integral_constant<int, 32>{}, std::true_type{});
+            else launch(std::integral_constant<int, 32>{}, std::false_type{});
+        }
     } else {
         const int tpp = fft_threads_per_pencil(N);
         int Q = std::max(1, fft_max_threads(N) / (tpp * 5));

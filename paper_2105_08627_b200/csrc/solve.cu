@@ -20,6 +20,7 @@
 #include <chrono>
 #include <cmath>
 #include <complex>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <numeric>
@@ -686,7 +687,10 @@ int pairwise(const CsrHost& A, std::vector<int>& agg) {
         for (int p = A.rowptr[i]; p < A.rowptr[i + 1]; ++p) {
             const int j = A.col[p];
             if (j == i) continue;
-            const double s = std::fabs(A.val[p]) / std::sqrt(std::fabs(diag[i] * diag[j]) + 1e-300);
+            static const bool neg = getenv("SVH_AMG_ABS") == nullptr;
+            // strength of connection: negative couplings (AGMG-style), or |a_ij| if SVH_AMG_ABS
+            const double a = neg ? -A.val[p] : std::fabs(A.val[p]);
+            const double s = a / std::sqrt(std::fabs(diag[i] * diag[j]) + 1e-300);
             rowmax = std::max(rowmax, s);
             if (agg[j] < 0 && s > bv) {
                 bv = s;
@@ -906,6 +910,14 @@ static void vcycle(Solve* S, int l, const double* b, double* x, cudaStream_t s) 
     SVH_LAUNCH(k_restrict2, nblk(n), 256, 0, s, n, L.agg, L.tmp, rc);
     vcycle(S, l + 1, rc, ec, s);
     SVH_LAUNCH(k_prolong2, nblk(n), 256, 0, s, n, L.agg, ec, L.x2);
+    static const int wlev = getenv("SVH_AMG_W") ? atoi(getenv("SVH_AMG_W")) : 2;
+    if (l < wlev) {   // W-cycle on the top levels: second coarse-grid correction
+        SVH_LAUNCH(k_resid2, nblk(n), 256, 0, s, n, L.rowptr, L.col, L.val, b, L.x2, L.tmp);
+        SVH_LAUNCH(k_zero, nblk(2 * L.nc), 256, 0, s, rc, (int64_t)2 * L.nc);
+        SVH_LAUNCH(k_restrict2, nblk(n), 256, 0, s, n, L.agg, L.tmp, rc);
+        vcycle(S, l + 1, rc, ec, s);
+        SVH_LAUNCH(k_prolong2, nblk(n), 256, 0, s, n, L.agg, ec, L.x2);
+    }
     SVH_LAUNCH(k_jacobi2, nblk(n), 256, 0, s, n, L.rowptr, L.col, L.val, L.dinv, b, L.x2, x);
     SVH_LAUNCH(k_jacobi2, nblk(n), 256, 0, s, n, L.rowptr, L.col, L.val, L.dinv, b, x, L.x2);
     SVH_CUDA(cudaMemcpyAsync(x, L.x2, 2 * (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, s));

@@ -184,6 +184,7 @@ class Handle:
         self._h = h
         self.device = device
         self.freq = float(freq)
+        self.tucker = tucker_tol > 0
         self.shape = (kz, ky, kx)
         K, M = ctypes.c_int64(), ctypes.c_int64()
         _check(L.svh_unknowns(h, ctypes.byref(K), ctypes.byref(M)))

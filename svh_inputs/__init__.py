@@ -89,14 +89,21 @@ def _holes(g, m, z0, z1, n, lo_side, hi_side, keep):
 
 
 def config3(seed=3, sigma0=NB[0]):
-    """BASELINE configs[2]: 90-degree L strip 8 wide over a holed ground, 512x512x4, dx 0.05 um."""
+    """BASELINE configs[2]: 90-degree L strip 8 wide over a holed ground, 512x512x4, dx 0.05 um.
+
+    Two ports, one at each end of the bend (strip against the ground beneath).  An
+    8x8 via at the inner corner ties the strip to the ground, so each port sees a
+    closed loop and the 2-port Y is non-singular (without a shunt path a series
+    element has no Z-parameters; DESIGN.md input recipe).
+    """
     Kx, Ky, Kz = 512, 512, 4
     g = rng(seed)
     m = np.zeros((Kz, Ky, Kx), dtype=np.uint8)
     _box(m, (0, 0, 0), (Kx, Ky, 1))
-    _holes(g, m, 0, 1, 32, 4, 16, keep=[(0, 256, 8, 264), (256, 504, 264, 512)])
+    _holes(g, m, 0, 1, 32, 4, 16, keep=[(0, 256, 8, 264), (256, 504, 264, 512), (256, 256, 264, 264)])
     _box(m, (0, 256, 2), (264, 264, 4))
     _box(m, (256, 256, 2), (264, 512, 4))
+    _box(m, (256, 256, 1), (264, 264, 2))   # corner via strip -> ground
     p1 = {"plus": [(0, -1, (0, 256, 2), (1, 264, 4))], "minus": [(0, -1, (0, 256, 0), (1, 264, 1))]}
     p2 = {"plus": [(1, +1, (256, 511, 2), (264, 512, 4))], "minus": [(1, +1, (256, 511, 0), (264, 512, 1))]}
     return dict(name="cfg3_bend_512x512x4", mat_id=m, dx=0.05e-6, materials=[(sigma0, NB[1])],
