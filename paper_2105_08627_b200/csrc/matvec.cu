@@ -285,7 +285,7 @@ constexpr size_t colpipe_smem() {
 }
 
 template <int N, int Q, int DIR>
-__global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q, 1)
+__global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
     k_col_pipe(const float2* __restrict__ in, float2* __restrict__ out, const float2* __restrict__ tw, int Nx,
                int Kz, int Lin, int Lout, int ntiles, int tiles_x) {
     constexpr int R1 = fft_r1(N), R2 = fft_r2(N);
@@ -407,6 +407,7 @@ __device__ void tucker_tile(const SpecView& sv, int kx0, int ky, int Nx, int Ny,
     const float sy = ky <= (Ny >> 1) ? 1.f : -1.f;
     float* G = scratch;            // [d3][d1]
     float* H = scratch + 32 * 32;  // [Q][d3]
+#pragma unroll
     for (int m = 0; m < 7; ++m) {
         const int d1 = sv.rk[m][0], d2 = sv.rk[m][1], d3 = sv.rk[m][2];
         const float* C = sv.core[m];
@@ -610,6 +611,7 @@ __global__ void __launch_bounds__(fft_max_threads(N))
             const int kx = kx0 + q;
             const int o3[3] = {kx <= (Nx >> 1) ? kx : Nx - kx, ky <= (Ny >> 1) ? ky : Ny - ky,
                                kz <= (N >> 1) ? kz : N - kz};
+#pragma unroll
             for (int m = 0; m < 7; ++m) {
                 const int d1 = sv.rk[m][0], d2 = sv.rk[m][1], d3 = sv.rk[m][2];
                 const float* f1 = sv.fac[m][0] + (int64_t)o3[0] * d1;
@@ -695,20 +697,37 @@ template <int N, int DIR>
 void run_pass_y(svh_handle* h, const float2* in, float2* out, int Lin, int Lout, int nrhs, cudaStream_t s) {
     constexpr int Q = col_q<N>();
     static const bool use_pipe = getenv("SVH_NO_PIPE") == nullptr;
-    if constexpr (DIR > 0 && fft_r2(N) > 1 && Q >= 2 && colpipe_smem<N, Q, DIR>() <= 220 * 1024) {
-        if (use_pipe && h->nx % Q == 0) {
-            const int tiles_x = h->nx / Q;
+    static const bool pipe_fwd = getenv("SVH_PIPE_B") != nullptr;
+    static const int pipe_q = getenv("SVH_PIPE_Q") ? atoi(getenv("SVH_PIPE_Q")) : 8;
+    if constexpr (fft_r2(N) > 1 && Q >= 4) {
+        auto launch_pipe = [&](auto Qc) {
+            constexpr int QP = decltype(Qc)::value;
+            const int tiles_x = h->nx / QP;
             const int ntiles = tiles_x * h->kz * 5 * nrhs;
-            const size_t smem = colpipe_smem<N, Q, DIR>();
-            const int nt = fft_threads_per_pencil(N) * Q;
+            const size_t smem = colpipe_smem<N, QP, DIR>();
+            const int nt = fft_threads_per_pencil(N) * QP;
             int dev = 0, nsm = 148;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-            const int grid = std::min(ntiles, nsm);
-            prep(k_col_pipe<N, Q, DIR>, smem);
-            SVH_LAUNCH((k_col_pipe<N, Q, DIR>), grid, nt, smem, s, in, out, h->d_tw[1], h->nx, h->kz, Lin, Lout,
+            int per_sm = (int)std::max<size_t>(1, (220 * 1024) / (smem + 1024));
+            per_sm = std::min(per_sm, std::max(1, 1024 / nt));
+            const int grid = std::min(ntiles, nsm * per_sm);
+            prep(k_col_pipe<N, QP, DIR>, smem);
+            SVH_LAUNCH((k_col_pipe<N, QP, DIR>), grid, nt, smem, s, in, out, h->d_tw[1], h->nx, h->kz, Lin, Lout,
                        ntiles, tiles_x);
-            return;
+        };
+        const bool want = use_pipe && (DIR > 0 || pipe_fwd);
+        if (want && h->nx % 8 == 0) {
+            if constexpr (colpipe_smem<N, 8, DIR>() <= 220 * 1024) {
+                if (pipe_q == 8) {
+                    launch_pipe(std::integral_constant<int, 8>{});
+                    return;
+                }
+            }
+            if constexpr (colpipe_smem<N, 4, DIR>() <= 220 * 1024) {
+                launch_pipe(std::integral_constant<int, 4>{});
+                return;
+            }
         }
     }
     const int nt = fft_threads_per_pencil(N) * Q;
