@@ -189,6 +189,59 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def cufft_reference(h, case, R, reps=3):
+    """cuFFT reference pipeline (north star: 'cuFFT timed alongside as a reference point,
+    not the product'): zero-pad each component to the embedding, torch.fft.fftn (cuFFT),
+    5->5 MAC with the 7 full-grid kernel spectra (built from libsvh's kernel tables by
+    embedding + cuFFT, outside the timed region), ifftn, crop.  Grid layout, c64.
+    Returns ms per RHS."""
+    import torch
+    kz, ky, kx = h.shape
+    nx, ny, nz = h.embedding
+    K = torch.from_numpy(h.kernels()).cuda()            # fp64 [7][kz][ky][kx], m >= 0
+    odd = [None, 2, 1, 0, None, None, None]             # K1x odd along x (tensor dim 2), ...
+    spec = []
+    for q in range(7):
+        e = torch.zeros((nz, ny, nx), dtype=torch.float64, device="cuda")
+        for sz in (1, -1):
+            for sy in (1, -1):
+                for sx in (1, -1):
+                    sign = 1.0
+                    if odd[q] is not None and (sx, sy, sz)[2 - odd[q]] < 0:
+                        sign = -1.0
+                    zi = torch.arange(kz, device="cuda") * sz % nz
+                    yi = torch.arange(ky, device="cuda") * sy % ny
+                    xi = torch.arange(kx, device="cuda") * sx % nx
+                    e[zi[:, None, None], yi[None, :, None], xi[None, None, :]] = sign * K[q]
+        spec.append(torch.fft.fftn(e).to(torch.complex64))
+    w = 2 * np.pi * case["freq"]
+    g = 1j * w * 4e-7 * np.pi * case["dx"]
+    occ = torch.from_numpy(case["mat_id"] != 0).cuda()
+    I = torch.randn((5, kz, ky, kx), dtype=torch.complex64, device="cuda") * occ
+
+    def one():
+        Ih = torch.fft.fftn(torch.nn.functional.pad(I, (0, nx - kx, 0, ny - ky, 0, nz - kz)), dim=(1, 2, 3))
+        m1 = [Ih[3] + Ih[4], Ih[4] - Ih[3], -2 * Ih[4]]
+        P0 = [spec[0] * Ih[c] + spec[1 + c] * m1[c] for c in range(3)]
+        P1 = [-spec[1 + c] * Ih[c] + spec[4 + c] * m1[c] for c in range(3)]
+        out = torch.stack(P0 + [P1[0] - P1[1], P1[0] + P1[1] - 2 * P1[2]])
+        return (g * torch.fft.ifftn(out, dim=(1, 2, 3)))[:, :kz, :ky, :kx]
+    ref = one()
+    ours = h.matvec_grid(I[None], green_only=True)[0]
+    rel = float(torch.linalg.norm((ref - ours)[:, occ]) / torch.linalg.norm(ours[:, occ]))
+    del ref, ours
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        one()
+    e1.record()
+    torch.cuda.synchronize()
+    del spec, K
+    torch.cuda.empty_cache()
+    return e0.elapsed_time(e1) / reps, rel
+
+
 def time_to_L(name, device, world, rank):
     """Time to the port L-matrix (BASELINE metric, 3rd part): svh_setup + svh_solve on a
     BASELINE config, wall clock around the public API calls (ports sharded over ranks)."""
@@ -227,6 +280,7 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-solve", action="store_true", help="skip the time-to-L measurement")
+    ap.add_argument("--no-cufft", action="store_true", help="skip the cuFFT reference-pipeline timing")
     ap.add_argument("--solve-workload", default="cfg2")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -345,6 +399,13 @@ def main():
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes},
             "gpu_launches": int(launches),
             "clocks": clk.summary()}
+
+    if not args.no_cufft:
+        ms_cufft, rel_cufft = cufft_reference(h, case, R)
+        line["config"]["cufft_reference"] = {
+            "ms_per_rhs": round(ms_cufft, 4), "ours_ms_per_rhs": round(ms_max / R, 4),
+            "speedup_vs_cufft": round(ms_cufft / (ms_max / R), 3), "rel_l2_vs_ours": rel_cufft,
+            "what": "torch.fft (cuFFT) pad+fftn, 5->5 MAC with full-grid spectra, ifftn, crop; grid layout"}
 
     if not args.no_solve:
         line["time_to_L"] = time_to_L(args.solve_workload, local, world, rank)

@@ -142,6 +142,9 @@ static void destroy(svh_handle* h) {
     for (int a = 0; a < 3; ++a) cudaFree(h->d_tw[a]);
     cudaFree(h->X1);
     cudaFree(h->X2);
+    for (auto st : h->streams) cudaStreamDestroy(st);
+    for (auto ev : h->stream_events) cudaEventDestroy(ev);
+    if (h->fork_event) cudaEventDestroy(h->fork_event);
     delete h;
 }
 

@@ -69,10 +69,10 @@ __device__ __forceinline__ void reg_fft(float2 (&v)[L]) {
                     } else {
                         constexpr float wr = (float)kTwCos64[k * (64 / len)];
                         constexpr float wi = (float)(DIR * kTwSin64[k * (64 / len)]);
-                        t = make_float2(b.x * wr - b.y * wi, b.x * wi + b.y * wr);
+                        t = cmul(b, make_float2(wr, wi));
                     }
-                    v[i + k] = make_float2(a.x + t.x, a.y + t.y);
-                    v[i + k + half] = make_float2(a.x - t.x, a.y - t.y);
+                    v[i + k] = cadd(a, t);
+                    v[i + k + half] = csub(a, t);
                 });
             });
         });

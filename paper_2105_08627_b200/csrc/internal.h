@@ -50,6 +50,9 @@ struct svh_handle {
     float2* X1 = nullptr;                // [chunk][5][kz][ky][nx]
     float2* X2 = nullptr;                // [chunk][5][kz][ny][nx]
     int ws_rhs = 0;
+    std::vector<cudaStream_t> streams;   // internal streams for concurrent RHS sub-batches
+    std::vector<cudaEvent_t> stream_events;
+    cudaEvent_t fork_event = nullptr;
     // solve-side data (built lazily by svh_solve / svh_apply_system)
     svh::Solve* solve = nullptr;
     double t_setup = 0;

@@ -264,6 +264,105 @@ __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
     }
 }
 
+// Three-level variant of the strided pass for N >= 512 (opt-in, SVH_COL3=1|2|3): N =
+// R1*R2*R3 with at most 16 complex values per thread (vs 32 in the two-level kernel),
+// so more warps fit on an SM.  Measured slower than the two-level kernel on B200 for
+// config 4 (the extra shared-memory phase costs more than the occupancy gains).  Phase 1 (R1-point FFTs) reads straight from
+// HBM, phases 2 (R2) and 3 (R3) work through one shared tile, phase 3 stores
+// straight to HBM.  Element e of pencil q lives at S[e*Q + q + 4*(e/R3)] (Q = 8),
+// which keeps every phase at the minimum two shared-memory wavefronts per warp.
+template <int N>
+struct Col3 {
+    static constexpr int R1 = N >= 1024 ? 16 : 8;
+    static constexpr int R3 = N >= 4096 ? 16 : 8;
+    static constexpr int R2 = N / (R1 * R3);
+    static constexpr int M = R2 * R3;
+};
+template <int N, int Q>
+__device__ __forceinline__ int c3idx(int e, int q) {
+    return e * Q + q + (e / Col3<N>::R3) * 4;
+}
+template <int N, int Q>
+constexpr int c3size() {
+    return N * Q + (N / Col3<N>::R3) * 4;
+}
+
+template <int N, int Q, int DIR>
+__global__ void __launch_bounds__(Col3<N>::M * Q)
+    k_col3(const float2* __restrict__ in, float2* __restrict__ out, const float2* __restrict__ tw, int Nx, int Kz,
+           int Lin, int Lout) {
+    constexpr int R1 = Col3<N>::R1, R2 = Col3<N>::R2, R3 = Col3<N>::R3, M = Col3<N>::M;
+    extern __shared__ float2 S[];
+    const int kx0 = blockIdx.x * Q;
+    const int z = blockIdx.y;
+    const int64_t rc = blockIdx.z;
+    const float2* src = in + ((rc * Kz + z) * Lin) * (int64_t)Nx + kx0;
+    float2* dst = out + ((rc * Kz + z) * Lout) * (int64_t)Nx + kx0;
+    const float2 zero = make_float2(0.f, 0.f);
+    const int base = threadIdx.x / Q, q = threadIdx.x % Q;
+    const bool ok = kx0 + q < Nx;
+    {   // phase 1: x[M n1 + m] -> R1-point FFT, twiddle W_N^{m k1}
+        const int m = base;
+        float2 v[R1];
+#pragma unroll
+        for (int n1 = 0; n1 < R1; ++n1) {
+            const int j = M * n1 + m;
+            if (DIR < 0)
+                v[n1] = (n1 < R1 / 2 && j < Lin && ok) ? src[(int64_t)j * Nx + q] : zero;
+            else
+                v[n1] = ok ? src[(int64_t)j * Nx + q] : zero;
+        }
+        reg_fft<R1, DIR>(v);
+#pragma unroll
+        for (int k1 = 1; k1 < R1; ++k1) {
+            float2 w = __ldg(&tw[m * k1]);
+            if (DIR > 0) w.y = -w.y;
+            v[k1] = cmul(v[k1], w);
+        }
+#pragma unroll
+        for (int k1 = 0; k1 < R1; ++k1) S[c3idx<N, Q>(k1 * M + m, q)] = v[k1];
+    }
+    __syncthreads();
+    // phase 2: for each (k1, n3): R2-point FFT over n2, twiddle W_M^{n3 k2}, in place
+#pragma unroll
+    for (int i = 0; i < (R1 * R3) / M; ++i) {
+        const int tau = base + i * M;
+        const int n3 = tau % R3, k1 = tau / R3;
+        float2 u[R2];
+#pragma unroll
+        for (int n2 = 0; n2 < R2; ++n2) u[n2] = S[c3idx<N, Q>(k1 * M + R3 * n2 + n3, q)];
+        reg_fft<R2, DIR>(u);
+#pragma unroll
+        for (int k2 = 1; k2 < R2; ++k2) {
+            float2 w = __ldg(&tw[R1 * n3 * k2]);
+            if (DIR > 0) w.y = -w.y;
+            u[k2] = cmul(u[k2], w);
+        }
+#pragma unroll
+        for (int k2 = 0; k2 < R2; ++k2) S[c3idx<N, Q>(k1 * M + R3 * k2 + n3, q)] = u[k2];
+    }
+    __syncthreads();
+    // phase 3: for each (k1, k2): R3-point FFT over n3 -> X[k1 + R1 (k2 + R2 k3)]
+    if (!ok) return;
+#pragma unroll
+    for (int i = 0; i < (R1 * R2) / M; ++i) {
+        const int tau = base + i * M;
+        const int k2 = tau % R2, k1 = tau / R2;
+        float2 w3[R3];
+#pragma unroll
+        for (int n3 = 0; n3 < R3; ++n3) w3[n3] = S[c3idx<N, Q>(k1 * M + R3 * k2 + n3, q)];
+        reg_fft<R3, DIR>(w3);
+#pragma unroll
+        for (int k3 = 0; k3 < R3; ++k3) {
+            const int j = k1 + R1 * (k2 + R2 * k3);
+            if (DIR < 0)
+                dst[(int64_t)j * Nx + q] = w3[k3];
+            else if (k3 < R3 / 2 && j < Lout)
+                dst[(int64_t)j * Nx + q] = w3[k3];
+        }
+    }
+}
+
 // Persistent, software-pipelined variant of the strided pass for N > 64: every CTA
 // loops over tiles; the input tile of the next iteration is copied HBM -> shared
 // memory with cp.async (16-byte LDGSTS, no register cost) while the current tile is
@@ -285,7 +384,7 @@ constexpr size_t colpipe_smem() {
 }
 
 template <int N, int Q, int DIR>
-__global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
+__global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q, 1)
     k_col_pipe(const float2* __restrict__ in, float2* __restrict__ out, const float2* __restrict__ tw, int Nx,
                int Kz, int Lin, int Lout, int ntiles, int tiles_x) {
     constexpr int R1 = fft_r1(N), R2 = fft_r2(N);
@@ -377,11 +476,11 @@ __device__ __forceinline__ void mac5(float2 (&v)[5], float k0, float s1x, float 
     const float2 P0x = cadd(cscale(Ix, k0), cmul_i(m1x, -s1x));
     const float2 P0y = cadd(cscale(Iy, k0), cmul_i(m1y, -s1y));
     const float2 P0z = cadd(cscale(Iz, k0), cmul_i(m1z, -s1z));
-    const float2 P1x = cadd(cmul_i(Ix, s1x), cscale(m1x, k2x));
-    const float2 P1y = cadd(cmul_i(Iy, s1y), cscale(m1y, k2y));
-    const float2 P1z = cadd(cmul_i(Iz, s1z), cscale(m1z, k2z));
+    const float2 P1x = cfma_s(m1x, k2x, cmul_i(Ix, s1x));
+    const float2 P1y = cfma_s(m1y, k2y, cmul_i(Iy, s1y));
+    const float2 P1z = cfma_s(m1z, k2z, cmul_i(Iz, s1z));
     const float2 C2 = csub(P1x, P1y);
-    const float2 C3 = csub(cadd(P1x, P1y), cscale(P1z, 2.f));
+    const float2 C3 = cfma_s(P1z, -2.f, cadd(P1x, P1y));
     v[0] = cmul_i(P0x, g);
     v[1] = cmul_i(P0y, g);
     v[2] = cmul_i(P0z, g);
@@ -676,7 +775,7 @@ constexpr int col_q() {
 }
 
 template <int N>
-void run_pass_a(svh_handle* h, const float2* in, bool packed, int nrhs, cudaStream_t s) {
+void run_pass_a(svh_handle* h, const float2* in, float2* X1, bool packed, int nrhs, cudaStream_t s) {
     constexpr int Q = row_q<N>();
     const int rows = h->ky * h->kz;
     const int nt = fft_threads_per_pencil(N) * Q;
@@ -684,11 +783,11 @@ void run_pass_a(svh_handle* h, const float2* in, bool packed, int nrhs, cudaStre
     dim3 grid((rows + Q - 1) / Q, 5 * nrhs);
     if (packed) {
         prep(k_row_fwd<N, Q, true>, smem);
-        SVH_LAUNCH((k_row_fwd<N, Q, true>), grid, nt, smem, s, in, h->X1, h->d_rowinfo, h->rowW, h->d_tw[0], h->kx,
+        SVH_LAUNCH((k_row_fwd<N, Q, true>), grid, nt, smem, s, in, X1, h->d_rowinfo, h->rowW, h->d_tw[0], h->kx,
                    rows, h->K, h->Kt);
     } else {
         prep(k_row_fwd<N, Q, false>, smem);
-        SVH_LAUNCH((k_row_fwd<N, Q, false>), grid, nt, smem, s, in, h->X1, h->d_rowinfo, h->rowW, h->d_tw[0], h->kx,
+        SVH_LAUNCH((k_row_fwd<N, Q, false>), grid, nt, smem, s, in, X1, h->d_rowinfo, h->rowW, h->d_tw[0], h->kx,
                    rows, h->K, h->Kt);
     }
 }
@@ -716,7 +815,8 @@ void run_pass_y(svh_handle* h, const float2* in, float2* out, int Lin, int Lout,
             SVH_LAUNCH((k_col_pipe<N, QP, DIR>), grid, nt, smem, s, in, out, h->d_tw[1], h->nx, h->kz, Lin, Lout,
                        ntiles, tiles_x);
         };
-        const bool want = use_pipe && (DIR > 0 || pipe_fwd);
+        static const int col3e = getenv("SVH_COL3") ? atoi(getenv("SVH_COL3")) : 0;
+        const bool want = use_pipe && ((DIR > 0 && !(N >= 512 && (col3e & 2))) || (DIR < 0 && pipe_fwd));
         if (want && h->nx % 8 == 0) {
             if constexpr (colpipe_smem<N, 8, DIR>() <= 220 * 1024) {
                 if (pipe_q == 8) {
@@ -730,6 +830,19 @@ void run_pass_y(svh_handle* h, const float2* in, float2* out, int Lin, int Lout,
             }
         }
     }
+    static const int col3 = getenv("SVH_COL3") ? atoi(getenv("SVH_COL3")) : 0;
+    if constexpr (N >= 512) {
+        const bool use3 = (DIR < 0) ? (col3 & 1) : (col3 & 2);
+        if (use3) {
+            constexpr int Q3 = 8;
+            const int nt = Col3<N>::M * Q3;
+            const size_t smem = (size_t)c3size<N, Q3>() * sizeof(float2);
+            dim3 grid((h->nx + Q3 - 1) / Q3, h->kz, 5 * nrhs);
+            prep(k_col3<N, Q3, DIR>, smem);
+            SVH_LAUNCH((k_col3<N, Q3, DIR>), grid, nt, smem, s, in, out, h->d_tw[1], h->nx, h->kz, Lin, Lout);
+            return;
+        }
+    }
     const int nt = fft_threads_per_pencil(N) * Q;
     const size_t smem = fft_r2(N) == 1 ? 0 : (size_t)em_size<N, Q>() * sizeof(float2);
     dim3 grid((h->nx + Q - 1) / Q, h->kz, 5 * nrhs);
@@ -738,7 +851,7 @@ void run_pass_y(svh_handle* h, const float2* in, float2* out, int Lin, int Lout,
 }
 
 template <int N>
-void run_pass_c(svh_handle* h, int nrhs, cudaStream_t s) {
+void run_pass_c(svh_handle* h, float2* X2, int nrhs, cudaStream_t s) {
     SpecView sv{};
     sv.spec = h->use_tucker ? nullptr : h->d_spec;
     sv.hx = h->hx;
@@ -761,7 +874,7 @@ void run_pass_c(svh_handle* h, int nrhs, cudaStream_t s) {
             const size_t smem = freq_small_smem<N, Q, A>();
             dim3 grid((h->nx + Q - 1) / Q, h->ny);
             prep(k_freq_small<N, Q, A>, smem);
-            SVH_LAUNCH((k_freq_small<N, Q, A>), grid, 5 * Q, smem, s, h->X2, sv, h->nx, h->ny, h->kz, h->gscale,
+            SVH_LAUNCH((k_freq_small<N, Q, A>), grid, 5 * Q, smem, s, X2, sv, h->nx, h->ny, h->kz, h->gscale,
                        nrhs);
         };
         const bool async_ok = casync && h->nx % 32 == 0;
@@ -780,13 +893,13 @@ void run_pass_c(svh_handle* h, int nrhs, cudaStream_t s) {
         const size_t smem = (size_t)N * (5 * Q + 1) * sizeof(float2);
         dim3 grid((h->nx + Q - 1) / Q, h->ny, nrhs);
         prep(k_freq_big<N>, smem);
-        SVH_LAUNCH((k_freq_big<N>), grid, nt, smem, s, h->X2, sv, h->d_tw[2], h->nx, h->ny, h->kz, Q, h->gscale);
+        SVH_LAUNCH((k_freq_big<N>), grid, nt, smem, s, X2, sv, h->d_tw[2], h->nx, h->ny, h->kz, Q, h->gscale);
     }
 }
 
 template <int N>
-void run_pass_e(svh_handle* h, const float2* in, float2* out, bool packed, bool green_only, int nrhs,
-                cudaStream_t s) {
+void run_pass_e(svh_handle* h, const float2* X1, const float2* in, float2* out, bool packed, bool green_only,
+                int nrhs, cudaStream_t s) {
     constexpr int Q = row_q<N>();
     const int rows = h->ky * h->kz;
     const int nt = fft_threads_per_pencil(N) * Q;
@@ -795,11 +908,11 @@ void run_pass_e(svh_handle* h, const float2* in, float2* out, bool packed, bool 
     const int nzl = (int)h->mats.size() + 1;
     if (packed) {
         prep(k_row_inv<N, Q, true>, smem);
-        SVH_LAUNCH((k_row_inv<N, Q, true>), grid, nt, smem, s, h->X1, out, in, h->d_rowinfo, h->rowW, h->d_matp,
+        SVH_LAUNCH((k_row_inv<N, Q, true>), grid, nt, smem, s, X1, out, in, h->d_rowinfo, h->rowW, h->d_matp,
                    h->d_zloc, nzl, h->d_tw[0], h->kx, rows, h->K, h->Kt, (int)green_only);
     } else {
         prep(k_row_inv<N, Q, false>, smem);
-        SVH_LAUNCH((k_row_inv<N, Q, false>), grid, nt, smem, s, h->X1, out, in, h->d_rowinfo, h->rowW, h->d_matp,
+        SVH_LAUNCH((k_row_inv<N, Q, false>), grid, nt, smem, s, X1, out, in, h->d_rowinfo, h->rowW, h->d_matp,
                    h->d_zloc, nzl, h->d_tw[0], h->kx, rows, h->K, h->Kt, (int)green_only);
     }
 }
@@ -851,47 +964,80 @@ int max_chunk(svh_handle* h) {
     return (int)std::max<size_t>(1, std::min<size_t>(64, budget / per));
 }
 
+// one sub-batch of nr RHS on stream s with workspace slices X1, X2
+static void matvec_batch(svh_handle* h, const float2* in, float2* out, float2* X1, float2* X2, int nr,
+                         bool green_only, bool packed, cudaStream_t s) {
+    static const bool dbg = getenv("SVH_SYNC_DEBUG") != nullptr;
+    auto tick = [&](int pass, bool begin) {
+        if (dbg && !begin) {
+            cudaError_t e = cudaStreamSynchronize(s);
+            if (e != cudaSuccess)
+                throw Error{SVH_ECUDA, "pass " + std::to_string(pass) + ": " + cudaGetErrorString(e)};
+        }
+        if (!h->prof_on) return;
+        if (begin) {
+            svh_handle::ProfRec r{pass, nullptr, nullptr};
+            SVH_CUDA(cudaEventCreate(&r.a));
+            SVH_CUDA(cudaEventCreate(&r.b));
+            SVH_CUDA(cudaEventRecord(r.a, s));
+            h->prof.push_back(r);
+        } else {
+            SVH_CUDA(cudaEventRecord(h->prof.back().b, s));
+        }
+    };
+    tick(0, true);
+    SVH_DISPATCH_N(h->nx, run_pass_a<NN>(h, in, X1, packed, nr, s));
+    tick(0, false);
+    tick(1, true);
+    SVH_DISPATCH_N(h->ny, (run_pass_y<NN, -1>(h, X1, X2, h->ky, h->ny, nr, s)));
+    tick(1, false);
+    tick(2, true);
+    SVH_DISPATCH_N(h->nz, run_pass_c<NN>(h, X2, nr, s));
+    tick(2, false);
+    tick(3, true);
+    SVH_DISPATCH_N(h->ny, (run_pass_y<NN, +1>(h, X2, X1, h->ny, h->ky, nr, s)));
+    tick(3, false);
+    tick(4, true);
+    SVH_DISPATCH_N(h->nx, run_pass_e<NN>(h, X1, in, out, packed, green_only, nr, s));
+    tick(4, false);
+}
+
 void matvec(svh_handle* h, const float2* I, float2* CC, int nrhs, bool green_only, bool packed, cudaStream_t s) {
     const int chunk = std::min(nrhs, max_chunk(h));
     ensure_workspace(h, chunk);
     const int64_t per_rhs = 5 * (packed ? h->K : h->Kt);
+    const size_t x1_per = (size_t)5 * h->kz * h->ky * h->nx, x2_per = (size_t)5 * h->kz * h->ny * h->nx;
+    // optional RHS sub-batches on concurrent streams (SVH_STREAMS; measured no gain on B200
+    // for config 4 since every pass already fills the GPU, so the default is 1)
+    static const int nstreams = getenv("SVH_STREAMS") ? std::max(1, atoi(getenv("SVH_STREAMS"))) : 1;
     for (int r0 = 0; r0 < nrhs; r0 += chunk) {
         const int nr = std::min(chunk, nrhs - r0);
-        const float2* in = I + r0 * per_rhs;
-        float2* out = CC + r0 * per_rhs;
-        static const bool dbg = getenv("SVH_SYNC_DEBUG") != nullptr;
-        auto tick = [&](int pass, bool begin) {
-            if (dbg && !begin) {
-                cudaError_t e = cudaStreamSynchronize(s);
-                if (e != cudaSuccess)
-                    throw Error{SVH_ECUDA, "pass " + std::to_string(pass) + ": " + cudaGetErrorString(e)};
-            }
-            if (!h->prof_on) return;
-            if (begin) {
-                svh_handle::ProfRec r{pass, nullptr, nullptr};
-                SVH_CUDA(cudaEventCreate(&r.a));
-                SVH_CUDA(cudaEventCreate(&r.b));
-                SVH_CUDA(cudaEventRecord(r.a, s));
-                h->prof.push_back(r);
-            } else {
-                SVH_CUDA(cudaEventRecord(h->prof.back().b, s));
-            }
-        };
-        tick(0, true);
-        SVH_DISPATCH_N(h->nx, run_pass_a<NN>(h, in, packed, nr, s));
-        tick(0, false);
-        tick(1, true);
-        SVH_DISPATCH_N(h->ny, (run_pass_y<NN, -1>(h, h->X1, h->X2, h->ky, h->ny, nr, s)));
-        tick(1, false);
-        tick(2, true);
-        SVH_DISPATCH_N(h->nz, run_pass_c<NN>(h, nr, s));
-        tick(2, false);
-        tick(3, true);
-        SVH_DISPATCH_N(h->ny, (run_pass_y<NN, +1>(h, h->X2, h->X1, h->ny, h->ky, nr, s)));
-        tick(3, false);
-        tick(4, true);
-        SVH_DISPATCH_N(h->nx, run_pass_e<NN>(h, in, out, packed, green_only, nr, s));
-        tick(4, false);
+        const int ns = std::min(nstreams, nr);
+        if (ns <= 1) {
+            matvec_batch(h, I + r0 * per_rhs, CC + r0 * per_rhs, h->X1, h->X2, nr, green_only, packed, s);
+            continue;
+        }
+        while ((int)h->streams.size() < ns) {
+            cudaStream_t st;
+            SVH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+            cudaEvent_t ev;
+            SVH_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            h->streams.push_back(st);
+            h->stream_events.push_back(ev);
+        }
+        if (!h->fork_event) SVH_CUDA(cudaEventCreateWithFlags(&h->fork_event, cudaEventDisableTiming));
+        SVH_CUDA(cudaEventRecord(h->fork_event, s));
+        int off = 0;
+        for (int k = 0; k < ns; ++k) {
+            const int nk = nr / ns + (k < nr % ns ? 1 : 0);
+            cudaStream_t st = h->streams[k];
+            SVH_CUDA(cudaStreamWaitEvent(st, h->fork_event, 0));
+            matvec_batch(h, I + (r0 + off) * per_rhs, CC + (r0 + off) * per_rhs, h->X1 + off * x1_per,
+                         h->X2 + off * x2_per, nk, green_only, packed, st);
+            SVH_CUDA(cudaEventRecord(h->stream_events[k], st));
+            off += nk;
+        }
+        for (int k = 0; k < ns; ++k) SVH_CUDA(cudaStreamWaitEvent(s, h->stream_events[k], 0));
     }
 }
 
