@@ -112,22 +112,24 @@ class ClockSampler:
 
 
 def pass_bytes(h, R, packed=True):
-    """Algorithmic HBM bytes of each pass per launch (R RHS), DESIGN.md "Roofline".
+    """Algorithmic HBM bytes of each pass per launch (R RHS), DESIGN.md §5.
 
-    pts/comp: A reads K (packed) + writes 2Kt; B 2Kt -> 4Kt; C 4Kt -> 4Kt (+ the 7 fp32
-    octant spectra once, dense mode); D 4Kt -> 2Kt; E 2Kt + K (I again) -> K; maps: the
-    row-occupancy words (8 B per 32 cells) in A and E, the packed material ids (1 B per
-    voxel) in E -- each counted once per launch (compulsory bytes).
+    Rows (y, z) / planes z holding no voxel are zero in every embedded current and the
+    pruned passes never touch them, so with Rn non-empty rows and Pn non-empty planes
+    (pts/comp): A reads K (packed) + writes Rn*Nx; B Rn*Nx -> Pn*Ny*Nx; C Pn*Ny*Nx ->
+    Pn*Ny*Nx (+ the 7 fp32 octant spectra once, dense mode); D Pn*Ny*Nx -> Rn*Nx;
+    E Rn*Nx + K (I again) -> K.  Maps: the row-occupancy words (8 B per 32 cells) and the
+    row list (4 B per row) in A and E, the packed material ids (1 B per voxel) in E,
+    the row mask in B/D -- each counted once per launch (compulsory bytes).
     """
     kz, ky, kx = h.shape
-    Kt = kx * ky * kz
     K = h.K
     nx, ny, nz = h.embedding
     c8 = 5 * 8 * R
-    X1 = kz * ky * nx
-    X2 = kz * ny * nx
+    X1 = h.rows_nonempty * nx
+    X2 = h.planes_nonempty * ny * nx
     spec = 7 * 4 * (nx // 2 + 1) * (ny // 2 + 1) * (nz // 2 + 1)
-    rowinfo = 8 * ky * kz * ((kx + 31) // 32)
+    rowinfo = 8 * h.rows_nonempty * ((kx + 31) // 32) + 4 * h.rows_nonempty
     A = c8 * (K + X1) + rowinfo
     B = c8 * (X1 + X2)
     C = c8 * 2 * X2 + (0 if h.tucker else spec)

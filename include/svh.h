@@ -122,6 +122,12 @@ int svh_unknowns(const svh_handle* h, int64_t* K, int64_t* M);
 /* Embedding extents Nx, Ny, Nz (powers of two >= 2K_i - 1, reading G7). */
 int svh_embedding(const svh_handle* h, int32_t* n3);
 
+/* Matvec plan geometry (for byte accounting of the pruned passes):
+ * info[0] = non-empty (y, z) rows, info[1] = non-empty z planes, info[2] = Ky*Kz rows,
+ * info[3] = Kz.  Rows / planes holding no voxel are zero in every embedded current
+ * and are skipped by the passes (never written or read).  info: host int64[4]. */
+int svh_plan_info(const svh_handle* h, int64_t* info);
+
 /*
  * svh_matvec -- Eq. 9: CC^b = z^b I^b + IFFT{ sum_a Z^{b,a} * FFT(I^a) }, cropped
  * to the non-empty voxels.

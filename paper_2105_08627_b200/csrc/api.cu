@@ -115,6 +115,38 @@ static void build_lattice(svh_handle* h) {
             }
             ri[(size_t)r * h->rowW + w] = make_int2((int)m, (int)first);
         }
+    // non-empty rows / planes (pass pruning)
+    h->rowMW = (ky + 31) / 32;
+    std::vector<uint32_t> rm((size_t)kz * h->rowMW, 0u);
+    std::vector<int32_t> rl;
+    std::vector<uint8_t> pok(kz, 0);
+    std::vector<int32_t> pl;
+    for (int64_t r = 0; r < rows; ++r) {
+        bool any = false;
+        for (int w = 0; w < h->rowW && !any; ++w) any = ri[(size_t)r * h->rowW + w].x != 0;
+        if (!any) continue;
+        const int z = (int)(r / ky), y = (int)(r % ky);
+        rm[(size_t)z * h->rowMW + y / 32] |= 1u << (y % 32);
+        rl.push_back((int32_t)r);
+        pok[z] = 1;
+    }
+    h->planemask = 0;
+    for (int z = 0; z < kz; ++z)
+        if (pok[z]) {
+            pl.push_back(z);
+            if (z < 64) h->planemask |= 1ull << z;
+        }
+    h->n_rows_ne = (int64_t)rl.size();
+    h->nzp = (int)pl.size();
+    SVH_CHECK(h->n_rows_ne > 0, SVH_EINVAL, "no non-empty voxel");
+    SVH_CUDA(cudaMalloc(&h->d_rowmask, rm.size() * sizeof(uint32_t)));
+    SVH_CUDA(cudaMemcpy(h->d_rowmask, rm.data(), rm.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    SVH_CUDA(cudaMalloc(&h->d_rowlist, rl.size() * sizeof(int32_t)));
+    SVH_CUDA(cudaMemcpy(h->d_rowlist, rl.data(), rl.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    SVH_CUDA(cudaMalloc(&h->d_planes, pl.size() * sizeof(int32_t)));
+    SVH_CUDA(cudaMemcpy(h->d_planes, pl.data(), pl.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    SVH_CUDA(cudaMalloc(&h->d_planeok, pok.size()));
+    SVH_CUDA(cudaMemcpy(h->d_planeok, pok.data(), pok.size(), cudaMemcpyHostToDevice));
     SVH_CUDA(cudaMalloc(&h->d_rowinfo, ri.size() * sizeof(int2)));
     SVH_CUDA(cudaMemcpy(h->d_rowinfo, ri.data(), ri.size() * sizeof(int2), cudaMemcpyHostToDevice));
     SVH_CUDA(cudaMalloc(&h->d_matp, matp.size()));
@@ -134,6 +166,10 @@ static void destroy(svh_handle* h) {
     cudaFree(h->d_mat);
     cudaFree(h->d_vmap);
     cudaFree(h->d_rowinfo);
+    cudaFree(h->d_rowmask);
+    cudaFree(h->d_rowlist);
+    cudaFree(h->d_planes);
+    cudaFree(h->d_planeok);
     cudaFree(h->d_matp);
     cudaFree(h->d_vox);
     cudaFree(h->d_kern);
@@ -269,6 +305,16 @@ int svh_embedding(const svh_handle* h, int32_t* n3) {
         n3[0] = h->nx;
         n3[1] = h->ny;
         n3[2] = h->nz;
+    });
+}
+
+int svh_plan_info(const svh_handle* h, int64_t* info) {
+    return guarded([&] {
+        SVH_CHECK(h && info, SVH_EINVAL, "null arg");
+        info[0] = h->n_rows_ne;
+        info[1] = h->nzp;
+        info[2] = (int64_t)h->ky * h->kz;
+        info[3] = h->kz;
     });
 }
 

@@ -38,6 +38,16 @@ struct svh_handle {
     int32_t* d_vox = nullptr;            // [K]
     int2* d_rowinfo = nullptr;           // [Ky*Kz][W]: {occupancy bits of 32 voxels, packed index of the first}
     int rowW = 1;                        // words per row = ceil(Kx/32)
+    // empty-row / empty-plane pruning of the matvec passes (zero rows of the embedded
+    // current never leave HBM untouched: they are neither written nor read)
+    uint32_t* d_rowmask = nullptr;       // [Kz][rowMW] bit y set <=> row (y, z) holds a voxel
+    int rowMW = 1;                       // = ceil(Ky/32)
+    int32_t* d_rowlist = nullptr;        // [n_rows_ne] non-empty rows z*Ky + y, ascending
+    int64_t n_rows_ne = 0;
+    int32_t* d_planes = nullptr;         // [nzp] non-empty z planes, ascending
+    uint8_t* d_planeok = nullptr;        // [Kz] 1 <=> plane z holds a voxel
+    int nzp = 0;
+    uint64_t planemask = 0;              // bit z (z < 64) of d_planeok
     uint8_t* d_matp = nullptr;           // [K] material id in packed order
     double* d_kern = nullptr;            // [7][Kt] unit-voxel kernels, fp64
     float* d_spec = nullptr;             // [7][hz][hy][hx] dense octant spectra (tucker_tol == 0)

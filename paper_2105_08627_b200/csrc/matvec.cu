@@ -59,28 +59,37 @@ __device__ __forceinline__ int packed_index(const int2* __restrict__ rowinfo, in
     return ((bits >> b) & 1u) ? mp.y + __popc(bits & ((1u << b) - 1u)) : -1;
 }
 
+// row_bit: does row (y, z) of the lattice hold a voxel?  (rows that do not are zero in
+// every embedded current; the passes neither write nor read them)
+__device__ __forceinline__ bool row_bit(const uint32_t* __restrict__ rowmask, int rowMW, int z, int y) {
+    return (__ldg(&rowmask[(int64_t)z * rowMW + (y >> 5)]) >> (y & 31)) & 1u;
+}
+
+// Pass A over the non-empty rows only (rowlist[li], li < nlist); X1 keeps the full
+// [rc][rows][N] layout so the strided passes index it by (z, y).
 template <int N, int Q, bool PACKED>
 __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
     k_row_fwd(const float2* __restrict__ in, float2* __restrict__ X1, const int2* __restrict__ rowinfo, int W,
-              const float2* __restrict__ tw, int Kx, int rows, int64_t K, int64_t Kt) {
+              const int32_t* __restrict__ rowlist, int nlist, const float2* __restrict__ tw, int Kx, int rows,
+              int64_t K, int64_t Kt) {
     constexpr int R1 = fft_r1(N), R2 = fft_r2(N);
     const int rc = blockIdx.y;
-    const int row0 = blockIdx.x * Q;
+    const int li0 = blockIdx.x * Q;
     const float2 zero = make_float2(0.f, 0.f);
+    auto row_of = [&](int q) -> int { return li0 + q < nlist ? __ldg(&rowlist[li0 + q]) : -1; };
     auto load = [&](int row, int j) -> float2 {
-        if (row >= rows || j >= Kx) return zero;
+        if (row < 0 || j >= Kx) return zero;
         const int idx = packed_index(rowinfo, W, row, j);
         if (idx < 0) return zero;
         return PACKED ? __ldg(&in[(int64_t)rc * K + idx]) : __ldg(&in[(int64_t)rc * Kt + (int64_t)row * Kx + j]);
     };
     if constexpr (R2 == 1) {
-        const int q = threadIdx.x;
-        const int row = row0 + q;
+        const int row = row_of(threadIdx.x);
         float2 v[N];
 #pragma unroll
         for (int j = 0; j < N; ++j) v[j] = (j < N / 2 || N == 1) ? load(row, j) : zero;
         reg_fft<N, -1>(v);
-        if (row < rows) {
+        if (row >= 0) {
             float2* dst = X1 + ((int64_t)rc * rows + row) * N;
 #pragma unroll
             for (int k = 0; k < N; ++k) dst[k] = v[k];
@@ -89,7 +98,7 @@ __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
         extern __shared__ float2 S[];
         if (threadIdx.x < R2 * Q) {
             const int q = threadIdx.x / R2, n2 = threadIdx.x % R2;
-            const int row = row0 + q;
+            const int row = row_of(q);
             float2 v[R1];
 #pragma unroll
             for (int n1 = 0; n1 < R1; ++n1) v[n1] = (n1 < R1 / 2) ? load(row, R2 * n1 + n2) : zero;
@@ -102,12 +111,12 @@ __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
         __syncthreads();
         if (threadIdx.x < R1 * Q) {
             const int q = threadIdx.x / R1, k1 = threadIdx.x % R1;
-            const int row = row0 + q;
+            const int row = row_of(q);
             float2 u[R2];
 #pragma unroll
             for (int n2 = 0; n2 < R2; ++n2) u[n2] = S[pm_idx<N>(q, n2 * R1 + k1)];
             reg_fft<R2, -1>(u);
-            if (row < rows) {
+            if (row >= 0) {
                 float2* dst = X1 + ((int64_t)rc * rows + row) * N;
 #pragma unroll
                 for (int k2 = 0; k2 < R2; ++k2) dst[k1 + R1 * k2] = u[k2];
@@ -116,25 +125,39 @@ __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
     }
 }
 
+// Pass E over the rows rowlist[li] (packed output: the non-empty rows) or over all
+// rows (rowlist == nullptr, grid output: empty rows are written as zeros without
+// reading X1, which holds no data for them).
 template <int N, int Q, bool PACKED>
 __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
     k_row_inv(const float2* __restrict__ X1, float2* __restrict__ out, const float2* __restrict__ in,
-              const int2* __restrict__ rowinfo, int W, const uint8_t* __restrict__ matp,
+              const int2* __restrict__ rowinfo, int W, const int32_t* __restrict__ rowlist, int nlist,
+              const uint32_t* __restrict__ rowmask, int rowMW, int Ky, const uint8_t* __restrict__ matp,
               const float2* __restrict__ zloc, int nzl, const float2* __restrict__ tw, int Kx, int rows, int64_t K,
               int64_t Kt, int green_only) {
     constexpr int R1 = fft_r1(N), R2 = fft_r2(N);
     const int rc = blockIdx.y;
     const int comp = rc % 5;
-    const int row0 = blockIdx.x * Q;
+    const int li0 = blockIdx.x * Q;
+    const float2 zero = make_float2(0.f, 0.f);
     __shared__ float2 zs[256];   // z^b of this component per material
     for (int m = threadIdx.x; m < nzl; m += blockDim.x) zs[m] = zloc[m * 5 + comp];
     __syncthreads();
+    auto row_of = [&](int q) -> int {
+        const int li = li0 + q;
+        if (li >= nlist) return -1;
+        return rowlist ? __ldg(&rowlist[li]) : li;
+    };
+    // X1 holds data for this row (listed rows are non-empty by construction)
+    auto live = [&](int row) -> bool {
+        return row >= 0 && (rowlist != nullptr || row_bit(rowmask, rowMW, row / Ky, row % Ky));
+    };
     auto store = [&](int row, int j, float2 v) {
-        if (row >= rows || j >= Kx) return;
+        if (row < 0 || j >= Kx) return;
         const int64_t cell = (int64_t)row * Kx + j;
         const int idx = packed_index(rowinfo, W, row, j);
         if (idx < 0) {
-            if (!PACKED) out[(int64_t)rc * Kt + cell] = make_float2(0.f, 0.f);
+            if (!PACKED) out[(int64_t)rc * Kt + cell] = zero;
             return;
         }
         if (!green_only) {
@@ -148,12 +171,12 @@ __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
             out[(int64_t)rc * Kt + cell] = v;
     };
     if constexpr (R2 == 1) {
-        const int q = threadIdx.x;
-        const int row = row0 + q;
+        const int row = row_of(threadIdx.x);
+        const bool ok = live(row);
         float2 v[N];
-        const float2* src = X1 + ((int64_t)rc * rows + min(row, rows - 1)) * N;
+        const float2* src = X1 + ((int64_t)rc * rows + max(row, 0)) * N;
 #pragma unroll
-        for (int k = 0; k < N; ++k) v[k] = src[k];
+        for (int k = 0; k < N; ++k) v[k] = ok ? src[k] : zero;
         reg_fft<N, +1>(v);
 #pragma unroll
         for (int j = 0; j < (N + 1) / 2; ++j) store(row, j, v[j]);
@@ -161,11 +184,12 @@ __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
         extern __shared__ float2 S[];
         if (threadIdx.x < R2 * Q) {
             const int q = threadIdx.x / R2, n2 = threadIdx.x % R2;
-            const int row = min(row0 + q, rows - 1);
-            const float2* src = X1 + ((int64_t)rc * rows + row) * N;
+            const int row = row_of(q);
+            const bool ok = live(row);
+            const float2* src = X1 + ((int64_t)rc * rows + max(row, 0)) * N;
             float2 v[R1];
 #pragma unroll
-            for (int n1 = 0; n1 < R1; ++n1) v[n1] = src[R2 * n1 + n2];
+            for (int n1 = 0; n1 < R1; ++n1) v[n1] = ok ? src[R2 * n1 + n2] : zero;
             reg_fft<R1, +1>(v);
 #pragma unroll
             for (int k1 = 1; k1 < R1; ++k1) {
@@ -179,31 +203,35 @@ __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
         __syncthreads();
         if (threadIdx.x < R1 * Q) {
             const int q = threadIdx.x / R1, k1 = threadIdx.x % R1;
+            const int row = row_of(q);
             float2 u[R2];
 #pragma unroll
             for (int n2 = 0; n2 < R2; ++n2) u[n2] = S[pm_idx<N>(q, n2 * R1 + k1)];
             reg_fft<R2, +1>(u);
 #pragma unroll
-            for (int k2 = 0; k2 < R2 / 2; ++k2) store(row0 + q, k1 + R1 * k2, u[k2]);
+            for (int k2 = 0; k2 < R2 / 2; ++k2) store(row, k1 + R1 * k2, u[k2]);
         }
     }
 }
 
 // ---------------------------------------------------------------------------
-// Strided passes B / D (pencils along y, stride Nx).  Tile = Q consecutive kx at one (z, rc).
-// DIR = -1: input rows j < Lin (<= N/2), zero-padded; all N outputs.
-// DIR = +1: all N inputs; outputs j < Lout (<= N/2).
+// Strided passes B / D (pencils along y, stride Nx).  Tile = Q consecutive kx at one
+// non-empty plane z = planes[blockIdx.y] and one (rhs, component).
+// DIR = -1: input rows j < Lin (<= N/2), zero-padded, and only rows (j, z) holding a
+//           voxel are read (the others are zero and were never written by pass A); all N outputs.
+// DIR = +1: all N inputs; outputs j < Lout (<= N/2) of the rows pass E reads.
 template <int N, int Q, int DIR>
 __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
     k_col(const float2* __restrict__ in, float2* __restrict__ out, const float2* __restrict__ tw, int Nx, int Kz,
-          int Lin, int Lout) {
+          int Lin, int Lout, const int32_t* __restrict__ planes, const uint32_t* __restrict__ rowmask, int rowMW) {
     constexpr int R1 = fft_r1(N), R2 = fft_r2(N);
     const int kx0 = blockIdx.x * Q;
-    const int z = blockIdx.y;
+    const int z = __ldg(&planes[blockIdx.y]);
     const int64_t rc = blockIdx.z;
     const float2* src = in + ((rc * Kz + z) * Lin) * (int64_t)Nx + kx0;
     float2* dst = out + ((rc * Kz + z) * Lout) * (int64_t)Nx + kx0;
     const float2 zero = make_float2(0.f, 0.f);
+    auto live = [&](int j) { return row_bit(rowmask, rowMW, z, j); };
     if constexpr (R2 == 1) {
         const int q = threadIdx.x;
         if (kx0 + q >= Nx) return;
@@ -211,14 +239,14 @@ __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
 #pragma unroll
         for (int j = 0; j < N; ++j) {
             if (DIR < 0)
-                v[j] = ((j < N / 2 || N == 1) && j < Lin) ? src[(int64_t)j * Nx + q] : zero;
+                v[j] = ((j < N / 2 || N == 1) && j < Lin && live(j)) ? src[(int64_t)j * Nx + q] : zero;
             else
                 v[j] = src[(int64_t)j * Nx + q];
         }
         reg_fft<N, DIR>(v);
 #pragma unroll
         for (int j = 0; j < N; ++j) {
-            if (DIR < 0 || (j < (N + 1) / 2 && j < Lout)) dst[(int64_t)j * Nx + q] = v[j];
+            if (DIR < 0 || (j < (N + 1) / 2 && j < Lout && live(j))) dst[(int64_t)j * Nx + q] = v[j];
         }
     } else {
         extern __shared__ float2 S[];
@@ -230,7 +258,7 @@ __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
             for (int n1 = 0; n1 < R1; ++n1) {
                 const int j = R2 * n1 + n2;
                 if (DIR < 0)
-                    v[n1] = (n1 < R1 / 2 && j < Lin && ok) ? src[(int64_t)j * Nx + q] : zero;
+                    v[n1] = (n1 < R1 / 2 && j < Lin && ok && live(j)) ? src[(int64_t)j * Nx + q] : zero;
                 else
                     v[n1] = ok ? src[(int64_t)j * Nx + q] : zero;
             }
@@ -257,108 +285,9 @@ __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
                 const int j = k1 + R1 * k2;
                 if (DIR < 0)
                     dst[(int64_t)j * Nx + q] = u[k2];
-                else if (k2 < R2 / 2 && j < Lout)
+                else if (k2 < R2 / 2 && j < Lout && live(j))
                     dst[(int64_t)j * Nx + q] = u[k2];
             }
-        }
-    }
-}
-
-// Three-level variant of the strided pass for N >= 512 (opt-in, SVH_COL3=1|2|3): N =
-// R1*R2*R3 with at most 16 complex values per thread (vs 32 in the two-level kernel),
-// so more warps fit on an SM.  Measured slower than the two-level kernel on B200 for
-// config 4 (the extra shared-memory phase costs more than the occupancy gains).  Phase 1 (R1-point FFTs) reads straight from
-// HBM, phases 2 (R2) and 3 (R3) work through one shared tile, phase 3 stores
-// straight to HBM.  Element e of pencil q lives at S[e*Q + q + 4*(e/R3)] (Q = 8),
-// which keeps every phase at the minimum two shared-memory wavefronts per warp.
-template <int N>
-struct Col3 {
-    static constexpr int R1 = N >= 1024 ? 16 : 8;
-    static constexpr int R3 = N >= 4096 ? 16 : 8;
-    static constexpr int R2 = N / (R1 * R3);
-    static constexpr int M = R2 * R3;
-};
-template <int N, int Q>
-__device__ __forceinline__ int c3idx(int e, int q) {
-    return e * Q + q + (e / Col3<N>::R3) * 4;
-}
-template <int N, int Q>
-constexpr int c3size() {
-    return N * Q + (N / Col3<N>::R3) * 4;
-}
-
-template <int N, int Q, int DIR>
-__global__ void __launch_bounds__(Col3<N>::M * Q)
-    k_col3(const float2* __restrict__ in, float2* __restrict__ out, const float2* __restrict__ tw, int Nx, int Kz,
-           int Lin, int Lout) {
-    constexpr int R1 = Col3<N>::R1, R2 = Col3<N>::R2, R3 = Col3<N>::R3, M = Col3<N>::M;
-    extern __shared__ float2 S[];
-    const int kx0 = blockIdx.x * Q;
-    const int z = blockIdx.y;
-    const int64_t rc = blockIdx.z;
-    const float2* src = in + ((rc * Kz + z) * Lin) * (int64_t)Nx + kx0;
-    float2* dst = out + ((rc * Kz + z) * Lout) * (int64_t)Nx + kx0;
-    const float2 zero = make_float2(0.f, 0.f);
-    const int base = threadIdx.x / Q, q = threadIdx.x % Q;
-    const bool ok = kx0 + q < Nx;
-    {   // phase 1: x[M n1 + m] -> R1-point FFT, twiddle W_N^{m k1}
-        const int m = base;
-        float2 v[R1];
-#pragma unroll
-        for (int n1 = 0; n1 < R1; ++n1) {
-            const int j = M * n1 + m;
-            if (DIR < 0)
-                v[n1] = (n1 < R1 / 2 && j < Lin && ok) ? src[(int64_t)j * Nx + q] : zero;
-            else
-                v[n1] = ok ? src[(int64_t)j * Nx + q] : zero;
-        }
-        reg_fft<R1, DIR>(v);
-#pragma unroll
-        for (int k1 = 1; k1 < R1; ++k1) {
-            float2 w = __ldg(&tw[m * k1]);
-            if (DIR > 0) w.y = -w.y;
-            v[k1] = cmul(v[k1], w);
-        }
-#pragma unroll
-        for (int k1 = 0; k1 < R1; ++k1) S[c3idx<N, Q>(k1 * M + m, q)] = v[k1];
-    }
-    __syncthreads();
-    // phase 2: for each (k1, n3): R2-point FFT over n2, twiddle W_M^{n3 k2}, in place
-#pragma unroll
-    for (int i = 0; i < (R1 * R3) / M; ++i) {
-        const int tau = base + i * M;
-        const int n3 = tau % R3, k1 = tau / R3;
-        float2 u[R2];
-#pragma unroll
-        for (int n2 = 0; n2 < R2; ++n2) u[n2] = S[c3idx<N, Q>(k1 * M + R3 * n2 + n3, q)];
-        reg_fft<R2, DIR>(u);
-#pragma unroll
-        for (int k2 = 1; k2 < R2; ++k2) {
-            float2 w = __ldg(&tw[R1 * n3 * k2]);
-            if (DIR > 0) w.y = -w.y;
-            u[k2] = cmul(u[k2], w);
-        }
-#pragma unroll
-        for (int k2 = 0; k2 < R2; ++k2) S[c3idx<N, Q>(k1 * M + R3 * k2 + n3, q)] = u[k2];
-    }
-    __syncthreads();
-    // phase 3: for each (k1, k2): R3-point FFT over n3 -> X[k1 + R1 (k2 + R2 k3)]
-    if (!ok) return;
-#pragma unroll
-    for (int i = 0; i < (R1 * R2) / M; ++i) {
-        const int tau = base + i * M;
-        const int k2 = tau % R2, k1 = tau / R2;
-        float2 w3[R3];
-#pragma unroll
-        for (int n3 = 0; n3 < R3; ++n3) w3[n3] = S[c3idx<N, Q>(k1 * M + R3 * k2 + n3, q)];
-        reg_fft<R3, DIR>(w3);
-#pragma unroll
-        for (int k3 = 0; k3 < R3; ++k3) {
-            const int j = k1 + R1 * (k2 + R2 * k3);
-            if (DIR < 0)
-                dst[(int64_t)j * Nx + q] = w3[k3];
-            else if (k3 < R3 / 2 && j < Lout)
-                dst[(int64_t)j * Nx + q] = w3[k3];
         }
     }
 }
@@ -386,7 +315,8 @@ constexpr size_t colpipe_smem() {
 template <int N, int Q, int DIR>
 __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q, 1)
     k_col_pipe(const float2* __restrict__ in, float2* __restrict__ out, const float2* __restrict__ tw, int Nx,
-               int Kz, int Lin, int Lout, int ntiles, int tiles_x) {
+               int Kz, int Lin, int Lout, int ntiles, int tiles_x, const int32_t* __restrict__ planes, int nzp,
+               const uint32_t* __restrict__ rowmask, int rowMW) {
     constexpr int R1 = fft_r1(N), R2 = fft_r2(N);
     constexpr int SR = colpipe_stage_rows<N, Q, DIR>();
     constexpr int NT = fft_threads_per_pencil(N) * Q;
@@ -394,17 +324,16 @@ __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q, 1)
     float2* T = sm + 2 * SR * Q;
     const float2 zero = make_float2(0.f, 0.f);
     const int lin = min(Lin, SR);
-    auto tile_src = [&](int t) {
-        const int xt = t % tiles_x, rest = t / tiles_x;
-        const int z = rest % Kz, rc = rest / Kz;
-        return in + (((int64_t)rc * Kz + z) * Lin) * (int64_t)Nx + (int64_t)xt * Q;
-    };
+    // tile t -> (kx tile, non-empty plane, rhs*component)
+    auto tile_z = [&](int t) { return __ldg(&planes[(t / tiles_x) % nzp]); };
+    auto tile_rc = [&](int t) { return (t / tiles_x) / nzp; };
     auto issue = [&](int t, int buf) {
-        const float2* src = tile_src(t);
+        const int z = tile_z(t), xt = t % tiles_x;
+        const float2* src = in + (((int64_t)tile_rc(t) * Kz + z) * Lin) * (int64_t)Nx + (int64_t)xt * Q;
         float2* st = sm + buf * SR * Q;
         for (int e = threadIdx.x; e < lin * (Q / 2); e += NT) {
             const int j = e / (Q / 2), p = e % (Q / 2);
-            cp_async16(st + j * Q + 2 * p, src + (int64_t)j * Nx + 2 * p);
+            if (DIR > 0 || row_bit(rowmask, rowMW, z, j)) cp_async16(st + j * Q + 2 * p, src + (int64_t)j * Nx + 2 * p);
         }
     };
     int t = blockIdx.x;
@@ -416,6 +345,7 @@ __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q, 1)
         cp_async_commit();
         cp_async_wait1();
         __syncthreads();
+        const int z = tile_z(t);
         const float2* st = sm + buf * SR * Q;
         if (threadIdx.x < R2 * Q) {
             const int n2 = threadIdx.x / Q, q = threadIdx.x % Q;
@@ -424,7 +354,7 @@ __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q, 1)
             for (int n1 = 0; n1 < R1; ++n1) {
                 const int j = R2 * n1 + n2;
                 if (DIR < 0)
-                    v[n1] = (n1 < R1 / 2 && j < lin) ? st[j * Q + q] : zero;
+                    v[n1] = (n1 < R1 / 2 && j < lin && row_bit(rowmask, rowMW, z, j)) ? st[j * Q + q] : zero;
                 else
                     v[n1] = st[j * Q + q];
             }
@@ -441,9 +371,8 @@ __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q, 1)
         __syncthreads();
         if (threadIdx.x < R1 * Q) {
             const int k1 = threadIdx.x / Q, q = threadIdx.x % Q;
-            const int xt = t % tiles_x, rest = t / tiles_x;
-            const int z = rest % Kz, rc = rest / Kz;
-            float2* dst = out + (((int64_t)rc * Kz + z) * Lout) * (int64_t)Nx + (int64_t)xt * Q;
+            const int xt = t % tiles_x;
+            float2* dst = out + (((int64_t)tile_rc(t) * Kz + z) * Lout) * (int64_t)Nx + (int64_t)xt * Q;
             float2 u[R2];
 #pragma unroll
             for (int n2 = 0; n2 < R2; ++n2) u[n2] = T[em_idx<N, Q>(n2 * R1 + k1, q)];
@@ -453,7 +382,7 @@ __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q, 1)
                 const int j = k1 + R1 * k2;
                 if (DIR < 0)
                     dst[(int64_t)j * Nx + q] = u[k2];
-                else if (k2 < R2 / 2 && j < Lout)
+                else if (k2 < R2 / 2 && j < Lout && row_bit(rowmask, rowMW, z, j))
                     dst[(int64_t)j * Nx + q] = u[k2];
             }
         }
@@ -583,7 +512,7 @@ constexpr size_t freq_small_smem() {
 // into a shared staging tile with cp.async (ASYNC = true).
 template <int N, int Q, bool ASYNC>
 __global__ void __launch_bounds__(5 * Q)
-    k_freq_small(float2* __restrict__ X2, SpecView sv, int Nx, int Ny, int Kz, float g, int nrhs) {
+    k_freq_small(float2* __restrict__ X2, SpecView sv, int Nx, int Ny, int Kz, float g, int nrhs, uint64_t pmask) {
     extern __shared__ float2 S[];   // [5][N][Q] spectra (also Tucker scratch), [7][N][Q] kernel values, stage
     float* KV = reinterpret_cast<float*>(S + freq_small_spec_f2<N, Q>());
     constexpr int NH = (N + 1) / 2;
@@ -602,7 +531,8 @@ __global__ void __launch_bounds__(5 * Q)
         for (int e = threadIdx.x; e < 5 * kz_ld * (Q / 2); e += 5 * Q) {
             const int p = e % (Q / 2), rest = e / (Q / 2);
             const int j = rest % kz_ld, cc = rest / kz_ld;
-            cp_async16(stage + (cc * NH + j) * Q + 2 * p, base + ((int64_t)cc * Kz + j) * plane + 2 * p);
+            if ((pmask >> j) & 1u)
+                cp_async16(stage + (cc * NH + j) * Q + 2 * p, base + ((int64_t)cc * Kz + j) * plane + 2 * p);
         }
     };
     float2 nxt[ASYNC ? 1 : NH];
@@ -611,7 +541,7 @@ __global__ void __launch_bounds__(5 * Q)
         cp_async_commit();
     } else {
 #pragma unroll
-        for (int j = 0; j < NH; ++j) nxt[j] = (ok && j < Kz) ? col[(int64_t)j * plane] : zero;
+        for (int j = 0; j < NH; ++j) nxt[j] = (ok && j < Kz && ((pmask >> j) & 1u)) ? col[(int64_t)j * plane] : zero;
     }
     // the 7 kernel spectra of this CTA's (kz, kx) points, reused by every RHS:
     // dense octant lookup, or Tucker expansion on chip (scratch = the spectra buffer)
@@ -632,7 +562,7 @@ __global__ void __launch_bounds__(5 * Q)
             asm volatile("cp.async.wait_group 0;\n" ::);
             __syncthreads();
 #pragma unroll
-            for (int j = 0; j < N; ++j) v[j] = (j < NH && j < Kz) ? stage[(c * NH + j) * Q + q] : zero;
+            for (int j = 0; j < N; ++j) v[j] = (j < NH && j < Kz && ((pmask >> j) & 1u)) ? stage[(c * NH + j) * Q + q] : zero;
             __syncthreads();
             if (r + 1 < nrhs) issue(r + 1);
             cp_async_commit();
@@ -648,7 +578,7 @@ __global__ void __launch_bounds__(5 * Q)
             if (r + 1 < nrhs) {
                 const float2* nc = col + (r + 1) * rstride;
 #pragma unroll
-                for (int j = 0; j < NH; ++j) nxt[j] = (ok && j < Kz) ? nc[(int64_t)j * plane] : zero;
+                for (int j = 0; j < NH; ++j) nxt[j] = (ok && j < Kz && ((pmask >> j) & 1u)) ? nc[(int64_t)j * plane] : zero;
             }
         }
         for (int t = threadIdx.x; t < N * Q; t += 5 * Q) {
@@ -670,7 +600,7 @@ __global__ void __launch_bounds__(5 * Q)
             float2* dst = col + r * rstride;
 #pragma unroll
             for (int j = 0; j < NH; ++j)
-                if (j < Kz) dst[(int64_t)j * plane] = v[j];
+                if (j < Kz && ((pmask >> j) & 1u)) dst[(int64_t)j * plane] = v[j];
         }
     }
 }
@@ -679,7 +609,7 @@ __global__ void __launch_bounds__(5 * Q)
 template <int N>
 __global__ void __launch_bounds__(fft_max_threads(N))
     k_freq_big(float2* __restrict__ X2, SpecView sv, const float2* __restrict__ tw, int Nx, int Ny, int Kz, int Q,
-               float g) {
+               float g, const uint8_t* __restrict__ planeok) {
     extern __shared__ float2 S[];
     const int Q5 = 5 * Q;
     const int PP = Q5 + 1;
@@ -694,7 +624,7 @@ __global__ void __launch_bounds__(fft_max_threads(N))
         const int rest = t / Q;
         const int j = rest % N, c = rest / N;
         float2 v = make_float2(0.f, 0.f);
-        if (j < Kz && q < nq) v = base[((int64_t)c * Kz + j) * plane + q];
+        if (j < Kz && q < nq && __ldg(&planeok[j])) v = base[((int64_t)c * Kz + j) * plane + q];
         S[j * PP + c * Q + q] = v;
     }
     __syncthreads();
@@ -746,7 +676,7 @@ __global__ void __launch_bounds__(fft_max_threads(N))
         const int q = t % Q;
         const int rest = t / Q;
         const int j = rest % Kz, c = rest / Kz;
-        if (q < nq) base[((int64_t)c * Kz + j) * plane + q] = S[j * PP + c * Q + q];
+        if (q < nq && __ldg(&planeok[j])) base[((int64_t)c * Kz + j) * plane + q] = S[j * PP + c * Q + q];
     }
 }
 
@@ -780,29 +710,33 @@ void run_pass_a(svh_handle* h, const float2* in, float2* X1, bool packed, int nr
     const int rows = h->ky * h->kz;
     const int nt = fft_threads_per_pencil(N) * Q;
     const size_t smem = fft_r2(N) == 1 ? 0 : (size_t)Q * (N + N / fft_r1(N)) * sizeof(float2);
-    dim3 grid((rows + Q - 1) / Q, 5 * nrhs);
+    const int nlist = (int)h->n_rows_ne;
+    dim3 grid((nlist + Q - 1) / Q, 5 * nrhs);
     if (packed) {
         prep(k_row_fwd<N, Q, true>, smem);
-        SVH_LAUNCH((k_row_fwd<N, Q, true>), grid, nt, smem, s, in, X1, h->d_rowinfo, h->rowW, h->d_tw[0], h->kx,
-                   rows, h->K, h->Kt);
+        SVH_LAUNCH((k_row_fwd<N, Q, true>), grid, nt, smem, s, in, X1, h->d_rowinfo, h->rowW, h->d_rowlist, nlist,
+                   h->d_tw[0], h->kx, rows, h->K, h->Kt);
     } else {
         prep(k_row_fwd<N, Q, false>, smem);
-        SVH_LAUNCH((k_row_fwd<N, Q, false>), grid, nt, smem, s, in, X1, h->d_rowinfo, h->rowW, h->d_tw[0], h->kx,
-                   rows, h->K, h->Kt);
+        SVH_LAUNCH((k_row_fwd<N, Q, false>), grid, nt, smem, s, in, X1, h->d_rowinfo, h->rowW, h->d_rowlist, nlist,
+                   h->d_tw[0], h->kx, rows, h->K, h->Kt);
     }
 }
 
 template <int N, int DIR>
 void run_pass_y(svh_handle* h, const float2* in, float2* out, int Lin, int Lout, int nrhs, cudaStream_t s) {
     constexpr int Q = col_q<N>();
+    // D (DIR = +1) runs the persistent cp.async-pipelined kernel; B the one-tile-per-CTA
+    // kernel (measured faster for the zero-padded forward direction).  SVH_NO_PIPE /
+    // SVH_PIPE_B flip these for experiments.
     static const bool use_pipe = getenv("SVH_NO_PIPE") == nullptr;
     static const bool pipe_fwd = getenv("SVH_PIPE_B") != nullptr;
-    static const int pipe_q = getenv("SVH_PIPE_Q") ? atoi(getenv("SVH_PIPE_Q")) : 8;
-    if constexpr (fft_r2(N) > 1 && Q >= 4) {
-        auto launch_pipe = [&](auto Qc) {
-            constexpr int QP = decltype(Qc)::value;
+    if constexpr (fft_r2(N) > 1 && Q >= 4 && colpipe_smem<N, 8, DIR>() <= 220 * 1024) {
+        const bool want = use_pipe && (DIR > 0 || pipe_fwd);
+        if (want && h->nx % 8 == 0) {
+            constexpr int QP = 8;
             const int tiles_x = h->nx / QP;
-            const int ntiles = tiles_x * h->kz * 5 * nrhs;
+            const int ntiles = tiles_x * h->nzp * 5 * nrhs;
             const size_t smem = colpipe_smem<N, QP, DIR>();
             const int nt = fft_threads_per_pencil(N) * QP;
             int dev = 0, nsm = 148;
@@ -813,41 +747,16 @@ void run_pass_y(svh_handle* h, const float2* in, float2* out, int Lin, int Lout,
             const int grid = std::min(ntiles, nsm * per_sm);
             prep(k_col_pipe<N, QP, DIR>, smem);
             SVH_LAUNCH((k_col_pipe<N, QP, DIR>), grid, nt, smem, s, in, out, h->d_tw[1], h->nx, h->kz, Lin, Lout,
-                       ntiles, tiles_x);
-        };
-        static const int col3e = getenv("SVH_COL3") ? atoi(getenv("SVH_COL3")) : 0;
-        const bool want = use_pipe && ((DIR > 0 && !(N >= 512 && (col3e & 2))) || (DIR < 0 && pipe_fwd));
-        if (want && h->nx % 8 == 0) {
-            if constexpr (colpipe_smem<N, 8, DIR>() <= 220 * 1024) {
-                if (pipe_q == 8) {
-                    launch_pipe(std::integral_constant<int, 8>{});
-                    return;
-                }
-            }
-            if constexpr (colpipe_smem<N, 4, DIR>() <= 220 * 1024) {
-                launch_pipe(std::integral_constant<int, 4>{});
-                return;
-            }
-        }
-    }
-    static const int col3 = getenv("SVH_COL3") ? atoi(getenv("SVH_COL3")) : 0;
-    if constexpr (N >= 512) {
-        const bool use3 = (DIR < 0) ? (col3 & 1) : (col3 & 2);
-        if (use3) {
-            constexpr int Q3 = 8;
-            const int nt = Col3<N>::M * Q3;
-            const size_t smem = (size_t)c3size<N, Q3>() * sizeof(float2);
-            dim3 grid((h->nx + Q3 - 1) / Q3, h->kz, 5 * nrhs);
-            prep(k_col3<N, Q3, DIR>, smem);
-            SVH_LAUNCH((k_col3<N, Q3, DIR>), grid, nt, smem, s, in, out, h->d_tw[1], h->nx, h->kz, Lin, Lout);
+                       ntiles, tiles_x, h->d_planes, h->nzp, h->d_rowmask, h->rowMW);
             return;
         }
     }
     const int nt = fft_threads_per_pencil(N) * Q;
     const size_t smem = fft_r2(N) == 1 ? 0 : (size_t)em_size<N, Q>() * sizeof(float2);
-    dim3 grid((h->nx + Q - 1) / Q, h->kz, 5 * nrhs);
+    dim3 grid((h->nx + Q - 1) / Q, h->nzp, 5 * nrhs);
     prep(k_col<N, Q, DIR>, smem);
-    SVH_LAUNCH((k_col<N, Q, DIR>), grid, nt, smem, s, in, out, h->d_tw[1], h->nx, h->kz, Lin, Lout);
+    SVH_LAUNCH((k_col<N, Q, DIR>), grid, nt, smem, s, in, out, h->d_tw[1], h->nx, h->kz, Lin, Lout, h->d_planes,
+               h->d_rowmask, h->rowMW);
 }
 
 template <int N>
@@ -875,7 +784,7 @@ void run_pass_c(svh_handle* h, float2* X2, int nrhs, cudaStream_t s) {
             dim3 grid((h->nx + Q - 1) / Q, h->ny);
             prep(k_freq_small<N, Q, A>, smem);
             SVH_LAUNCH((k_freq_small<N, Q, A>), grid, 5 * Q, smem, s, X2, sv, h->nx, h->ny, h->kz, h->gscale,
-                       nrhs);
+                       nrhs, (uint64_t)h->planemask);
         };
         const bool async_ok = casync && h->nx % 32 == 0;
         if (N >= 64 || cq == 16) {
@@ -893,7 +802,8 @@ void run_pass_c(svh_handle* h, float2* X2, int nrhs, cudaStream_t s) {
         const size_t smem = (size_t)N * (5 * Q + 1) * sizeof(float2);
         dim3 grid((h->nx + Q - 1) / Q, h->ny, nrhs);
         prep(k_freq_big<N>, smem);
-        SVH_LAUNCH((k_freq_big<N>), grid, nt, smem, s, X2, sv, h->d_tw[2], h->nx, h->ny, h->kz, Q, h->gscale);
+        SVH_LAUNCH((k_freq_big<N>), grid, nt, smem, s, X2, sv, h->d_tw[2], h->nx, h->ny, h->kz, Q, h->gscale,
+                   h->d_planeok);
     }
 }
 
@@ -904,16 +814,21 @@ void run_pass_e(svh_handle* h, const float2* X1, const float2* in, float2* out, 
     const int rows = h->ky * h->kz;
     const int nt = fft_threads_per_pencil(N) * Q;
     const size_t smem = fft_r2(N) == 1 ? 0 : (size_t)Q * (N + N / fft_r1(N)) * sizeof(float2);
-    dim3 grid((rows + Q - 1) / Q, 5 * nrhs);
     const int nzl = (int)h->mats.size() + 1;
+    // packed output: only the non-empty rows; grid output: every row (empty ones get zeros)
+    const int nlist = packed ? (int)h->n_rows_ne : rows;
+    const int32_t* rl = packed ? h->d_rowlist : nullptr;
+    dim3 grid((nlist + Q - 1) / Q, 5 * nrhs);
     if (packed) {
         prep(k_row_inv<N, Q, true>, smem);
-        SVH_LAUNCH((k_row_inv<N, Q, true>), grid, nt, smem, s, X1, out, in, h->d_rowinfo, h->rowW, h->d_matp,
-                   h->d_zloc, nzl, h->d_tw[0], h->kx, rows, h->K, h->Kt, (int)green_only);
+        SVH_LAUNCH((k_row_inv<N, Q, true>), grid, nt, smem, s, X1, out, in, h->d_rowinfo, h->rowW, rl, nlist,
+                   h->d_rowmask, h->rowMW, h->ky, h->d_matp, h->d_zloc, nzl, h->d_tw[0], h->kx, rows, h->K, h->Kt,
+                   (int)green_only);
     } else {
         prep(k_row_inv<N, Q, false>, smem);
-        SVH_LAUNCH((k_row_inv<N, Q, false>), grid, nt, smem, s, X1, out, in, h->d_rowinfo, h->rowW, h->d_matp,
-                   h->d_zloc, nzl, h->d_tw[0], h->kx, rows, h->K, h->Kt, (int)green_only);
+        SVH_LAUNCH((k_row_inv<N, Q, false>), grid, nt, smem, s, X1, out, in, h->d_rowinfo, h->rowW, rl, nlist,
+                   h->d_rowmask, h->rowMW, h->ky, h->d_matp, h->d_zloc, nzl, h->d_tw[0], h->kx, rows, h->K, h->Kt,
+                   (int)green_only);
     }
 }
 

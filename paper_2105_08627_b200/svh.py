@@ -81,6 +81,7 @@ def lib():
         L.svh_set_frequency.argtypes = [vp, dbl]
         L.svh_unknowns.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]
         L.svh_embedding.argtypes = [vp, ctypes.POINTER(i32)]
+        L.svh_plan_info.argtypes = [vp, ctypes.POINTER(i64)]
         L.svh_matvec.argtypes = [vp, vp, vp, i32, i32, vp]
         L.svh_matvec_grid.argtypes = [vp, vp, vp, i32, i32, vp]
         L.svh_apply_system.argtypes = [vp, vp, vp, i32, vp]
@@ -97,7 +98,7 @@ def lib():
         L.svh_destroy.restype = None
         L.svh_last_error.restype = ctypes.c_char_p
         L.svh_launch_count.restype = i64
-        for name in ("svh_setup", "svh_set_frequency", "svh_unknowns", "svh_embedding", "svh_matvec",
+        for name in ("svh_setup", "svh_set_frequency", "svh_unknowns", "svh_embedding", "svh_plan_info", "svh_matvec",
                      "svh_matvec_grid", "svh_apply_system", "svh_solve", "svh_solve_columns", "svh_get_kernels",
                      "svh_get_stats", "svh_profile_enable", "svh_profile_read", "svh_y_to_zl"):
             getattr(L, name).restype = ctypes.c_int
@@ -105,7 +106,8 @@ def lib():
     return _lib
 
 
-EXPORTED = ("svh_default_opts", "svh_setup", "svh_set_frequency", "svh_unknowns", "svh_embedding", "svh_matvec",
+EXPORTED = ("svh_default_opts", "svh_setup", "svh_set_frequency", "svh_unknowns", "svh_embedding", "svh_plan_info",
+            "svh_matvec",
             "svh_matvec_grid", "svh_apply_system", "svh_solve", "svh_solve_columns", "svh_get_kernels",
             "svh_get_stats", "svh_profile_enable", "svh_profile_read", "svh_y_to_zl", "svh_destroy",
             "svh_last_error", "svh_launch_count")
@@ -193,6 +195,10 @@ class Handle:
         n3 = (ctypes.c_int32 * 3)()
         _check(L.svh_embedding(h, n3))
         self.embedding = tuple(n3)
+        info = (ctypes.c_int64 * 4)()
+        _check(L.svh_plan_info(h, info))
+        # non-empty (y, z) rows and z planes: the pruned passes touch only these
+        self.rows_nonempty, self.planes_nonempty = int(info[0]), int(info[1])
 
     # -- lifetime
     def close(self):

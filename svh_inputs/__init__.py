@@ -170,6 +170,33 @@ def random_fill(shape_xyz, fill=0.5, seed=5, n_mat=1, materials=None, dx=0.1e-6,
                 freq=freq, ports=[])
 
 
+def layered(shape_xyz, seed=9, n_mat=2, dx=0.1e-6, freq=10e9):
+    """Thin-film-like stack with empty rows and empty planes (the structure of configs
+    3-4 at test size): a randomly holed plane at z=0, empty z=1, x-running strips at
+    z=2 (some rows empty), empty z=3, a few via voxels at z=4, and empty planes above;
+    for Kz > 8 the pattern repeats every 8 planes with the top quarter left empty."""
+    Kx, Ky, Kz = shape_xyz
+    g = rng(seed)
+    m = np.zeros((Kz, Ky, Kx), dtype=np.uint8)
+    top = Kz - max(1, Kz // 4) if Kz > 2 else Kz
+    for z in range(top):
+        lz = z % 8
+        if lz == 0:
+            m[z] = (g.random((Ky, Kx)) < 0.7) * g.integers(1, n_mat + 1, (Ky, Kx))
+        elif lz == 2:
+            for y in range(0, Ky, 3):
+                if g.random() < 0.6:
+                    x0 = int(g.integers(0, max(1, Kx // 3)))
+                    m[z, y, x0:Kx - int(g.integers(0, max(1, Kx // 3)))] = int(g.integers(1, n_mat + 1))
+        elif lz == 4:
+            for _ in range(max(1, Kx * Ky // 200)):
+                m[z, int(g.integers(0, Ky)), int(g.integers(0, Kx))] = 1
+    if not m.any():
+        m[0, 0, 0] = 1
+    mats = [NB, (5.8e7, float("inf"))][:n_mat]
+    return dict(name=f"layered_{Kx}x{Ky}x{Kz}_s{seed}", mat_id=m, dx=dx, materials=mats, freq=freq, ports=[])
+
+
 def sweep_shapes():
     """BASELINE configs[4] grid list (cubic + slab)."""
     return [(64, 64, 64), (128, 128, 128), (256, 256, 256), (512, 512, 4), (512, 512, 16),

@@ -143,3 +143,39 @@ def test_launch_count_increments(svh_lib):
         h.matvec(I)
         torch.cuda.synchronize()
         assert svh_lib.launch_count() - n0 == 5
+
+
+# Geometries with empty (y, z) rows and empty z planes: the passes skip them (DESIGN.md
+# §5 "pruning"), so these cover every pass path with skipped data -- row passes with
+# R2 = 1 and R2 > 1 (Nx = 128 / 256), the strided passes incl. the pipelined inverse
+# (Ny = 256), and the z pass with Nz <= 64 and Nz = 256 (k_freq_big).
+LAYERED = [(40, 70, 6), (3, 4, 70), (130, 9, 3)]
+
+
+@pytest.mark.parametrize("shape", LAYERED)
+@pytest.mark.parametrize("grid", [False, True])
+def test_matvec_pruned_layers(svh_lib, shape, grid):
+    case = svh_inputs.layered(shape)
+    lat = Lattice(case["mat_id"])
+    I = svh_inputs.currents(lat.K, nrhs=2, seed=21)
+    w = 2 * np.pi * case["freq"]
+    for go in (True, False):
+        ref = matvec_direct(lat, case["materials"], w, case["dx"], I, green_only=go)
+        got = gpu_matvec(svh_lib, case, I, green_only=go, grid=grid)
+        for r in range(2):
+            assert rel_l2(got[r], ref[r]) < TOL, (go, r, rel_l2(got[r], ref[r]))
+
+
+def test_matvec_grid_zero_outside(svh_lib):
+    """Grid layout: the output is exactly zero at empty voxels (incl. whole empty rows/planes)."""
+    import torch
+    case = svh_inputs.layered((40, 70, 6))
+    occ = case["mat_id"] > 0
+    with svh_lib.setup_case(case) as h:
+        assert h.rows_nonempty == int(occ.any(axis=2).sum())
+        assert h.planes_nonempty == int(occ.any(axis=(1, 2)).sum())
+        g = np.zeros((1, 5) + h.shape, dtype=np.complex64)
+        g[:, :, occ] = svh_inputs.currents(int(occ.sum()), 1, seed=3)[0].astype(np.complex64)
+        out = h.matvec_grid(torch.from_numpy(g).cuda()).cpu().numpy()
+    assert np.all(out[:, :, ~occ] == 0)
+    assert np.all(np.isfinite(out))
