@@ -44,36 +44,62 @@ struct Error {
                                               cudaGetErrorString(e__)};        \
     } while (0)
 
-// Complex arithmetic on float2.  On sm_100a the paired-FP32 instructions
-// (FADD2 / FMUL2 / FFMA2, CUDA 12.9 __fadd2_rn etc.) do the real and imaginary
-// halves in one instruction; a complex multiply is FMUL2 + FFMA2 with scalar
-// broadcast operands.  Measured slower on B200 for these passes (fewer issue
-// slots but extra operand moves), so it is opt-in: -DSVH_USE_F32X2.
-#if defined(SVH_USE_F32X2) && defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
-__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-    return __ffma2_rn(make_float2(a.x, a.x), b, __fmul2_rn(make_float2(a.y, a.y), make_float2(-b.y, b.x)));
+// Complex arithmetic on float2 (re, im).  In device code for sm_100a every helper is
+// one or two paired-FP32 instructions (FADD2 / FMUL2 / FFMA2 act on both halves of a
+// 64-bit register pair): the swap (a.y, a.x) and scalar broadcasts fold into operand
+// modifiers (.LO_HI, .F32), so a complex multiply is FMUL2 + FFMA2 and a butterfly
+// add/sub one FADD2 each -- about 0.55x the FP instructions of the scalar form on the
+// FFT-bound passes (cuobjdump-checked).  -DSVH_SCALAR_COMPLEX
+// restores the scalar forms.
+#if !defined(SVH_SCALAR_COMPLEX) && defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000
+#define SVH_F32X2 1
+#endif
+__host__ __device__ __forceinline__ float2 cswap(float2 a) { return make_float2(a.y, a.x); }
+__host__ __device__ __forceinline__ float2 cadd(float2 a, float2 b) {
+#ifdef SVH_F32X2
+    return __fadd2_rn(a, b);
+#else
+    return make_float2(a.x + b.x, a.y + b.y);
+#endif
 }
-__device__ __forceinline__ float2 cscale(float2 a, float s) { return __fmul2_rn(a, make_float2(s, s)); }
+__host__ __device__ __forceinline__ float2 csub(float2 a, float2 b) {
+#ifdef SVH_F32X2
+    return __fadd2_rn(a, make_float2(-b.x, -b.y));
+#else
+    return make_float2(a.x - b.x, a.y - b.y);
+#endif
+}
+__host__ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+#ifdef SVH_F32X2
+    // (a.x b.x - a.y b.y, a.y b.x + a.x b.y) = a*(b.x, b.x) + swap(a)*(-b.y, b.y)
+    return __ffma2_rn(cswap(a), make_float2(-b.y, b.y), __fmul2_rn(a, make_float2(b.x, b.x)));
+#else
+    return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+#endif
+}
+__host__ __device__ __forceinline__ float2 cscale(float2 a, float s) {
+#ifdef SVH_F32X2
+    return __fmul2_rn(a, make_float2(s, s));
+#else
+    return make_float2(a.x * s, a.y * s);
+#endif
+}
 // a * (i s), s real
-__device__ __forceinline__ float2 cmul_i(float2 a, float s) {
-    return __fmul2_rn(make_float2(a.y, a.x), make_float2(-s, s));
+__host__ __device__ __forceinline__ float2 cmul_i(float2 a, float s) {
+#ifdef SVH_F32X2
+    return __fmul2_rn(cswap(a), make_float2(-s, s));
+#else
+    return make_float2(-a.y * s, a.x * s);
+#endif
 }
 // a + b * s (s real)
-__device__ __forceinline__ float2 cfma_s(float2 b, float s, float2 a) { return __ffma2_rn(b, make_float2(s, s), a); }
-#else
-__host__ __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__host__ __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
-__host__ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-    return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
-}
-__host__ __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
-__host__ __device__ __forceinline__ float2 cmul_i(float2 a, float s) { return make_float2(-a.y * s, a.x * s); }
 __host__ __device__ __forceinline__ float2 cfma_s(float2 b, float s, float2 a) {
+#ifdef SVH_F32X2
+    return __ffma2_rn(b, make_float2(s, s), a);
+#else
     return make_float2(a.x + b.x * s, a.y + b.y * s);
-}
 #endif
+}
 
 inline int ilog2(int64_t n) {
     int l = 0;

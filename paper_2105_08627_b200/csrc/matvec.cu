@@ -390,6 +390,128 @@ __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q, 1)
     cp_async_commit();
 }
 
+// Staged strided pass (B / D), the default for 128 <= N <= 1024.  One persistent CTA per
+// SM; tiles (Q consecutive kx of one non-empty plane of one (rhs, component)) stream
+// HBM -> shared memory through an S-deep cp.async ring (16-byte LDGSTS, no register
+// cost), so loads of the next S-1 tiles are in flight while the current one is
+// transformed.  Phase 1 (R1-point FFTs) reads the staged tile, phase 2 (R2-point FFTs)
+// stores straight to HBM.  The phase-1 twiddles W_N^(n2 k1) are loop-invariant per
+// thread and live in registers; rows holding no voxel are zero-filled in shared memory
+// (forward) or not stored (inverse) -- the pruning of k_col.
+template <int N, int Q, int DIR, int S>
+struct YStage {
+    static constexpr int R1 = fft_r1(N), R2 = fft_r2(N);
+    static constexpr int NT = R1 * Q;
+    static constexpr int SR = DIR < 0 ? N / 2 : N;
+    static constexpr int MW = (N / 2 + 31) / 32;
+    static constexpr size_t smem = (size_t)(S * SR * Q + em_size<N, Q>()) * sizeof(float2) + (size_t)S * MW * 4;
+};
+
+template <int N, int Q, int DIR, int S>
+__global__ void __launch_bounds__(fft_r1(N) * Q, 1)
+    k_ystage(const float2* __restrict__ in, float2* __restrict__ out, const float2* __restrict__ tw, int Nx,
+             int Kz, int Lin, int Lout, int ntiles, int tiles_x, const int32_t* __restrict__ planes, int nzp,
+             const uint32_t* __restrict__ rowmask, int rowMW) {
+    using P = YStage<N, Q, DIR, S>;
+    constexpr int R1 = P::R1, R2 = P::R2, NT = P::NT, SR = P::SR, MW = P::MW;
+    constexpr int NL = DIR < 0 ? R1 / 2 : R1;
+    extern __shared__ __align__(16) float2 sm[];
+    float2* stage = sm;
+    float2* T = sm + S * SR * Q;
+    uint32_t* M = reinterpret_cast<uint32_t*>(T + em_size<N, Q>());
+    const int tid = threadIdx.x;
+    const float2 zero = make_float2(0.f, 0.f);
+    const int lin = min(Lin, SR);
+    // rows lin..SR-1 of every stage are never copied: zero them once
+    for (int e = tid; e < S * (SR - lin) * Q; e += NT) {
+        const int st = e / ((SR - lin) * Q), r = e % ((SR - lin) * Q);
+        stage[st * SR * Q + lin * Q + r] = zero;
+    }
+    auto decode = [&](int t, int& z, int64_t& bin, int64_t& bout) {
+        const int xt = t % tiles_x, pr = t / tiles_x;
+        const int rc = pr / nzp;
+        z = __ldg(&planes[pr - rc * nzp]);
+        bin = ((int64_t)rc * Kz + z) * Lin * (int64_t)Nx + (int64_t)xt * Q;
+        bout = ((int64_t)rc * Kz + z) * Lout * (int64_t)Nx + (int64_t)xt * Q;
+    };
+    auto issue = [&](int t, int st) {
+        if (t < ntiles) {
+            int z;
+            int64_t bin, bout;
+            decode(t, z, bin, bout);
+            const uint32_t* pm = rowmask + (int64_t)z * rowMW;
+            if (tid < MW) M[st * MW + tid] = tid < rowMW ? __ldg(&pm[tid]) : 0u;
+            const float2* src = in + bin;
+            float2* dst = stage + st * SR * Q;
+            for (int e = tid; e < lin * (Q / 2); e += NT) {
+                const int j = e / (Q / 2), p2 = 2 * (e % (Q / 2));
+                if (DIR > 0 || ((__ldg(&pm[j >> 5]) >> (j & 31)) & 1u))
+                    cp_async16(dst + j * Q + p2, src + (int64_t)j * Nx + p2);
+                else
+                    *reinterpret_cast<float4*>(dst + j * Q + p2) = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+        cp_async_commit();
+    };
+    // phase-1 role (n2, q1): twiddles W_N^(n2 k1), k1 = 1..R1-1, held in registers
+    const int n2 = tid / Q, q1 = tid % Q;
+    const bool ph1 = n2 < R2;
+    float2 tw1[R1];
+#pragma unroll
+    for (int kk = 1; kk < R1; ++kk) {
+        float2 w = ph1 ? __ldg(&tw[n2 * kk]) : zero;
+        if (DIR > 0) w.y = -w.y;
+        tw1[kk] = w;
+    }
+    const int k1 = tid / Q, q2 = tid % Q;   // phase-2 role
+    int t = blockIdx.x;
+#pragma unroll
+    for (int s = 0; s < S - 1; ++s) issue(t + s * (int)gridDim.x, s);
+    for (int i = 0; t < ntiles; ++i, t += gridDim.x) {
+        issue(t + (S - 1) * (int)gridDim.x, (i + S - 1) % S);
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(S - 1));
+        __syncthreads();
+        const int st = i % S;
+        int z;
+        int64_t bin, bout;
+        decode(t, z, bin, bout);
+        if (ph1) {
+            const float2* src = stage + st * SR * Q;
+            float2 v[R1];
+#pragma unroll
+            for (int n1 = 0; n1 < R1; ++n1) v[n1] = n1 < NL ? src[(R2 * n1 + n2) * Q + q1] : zero;
+            reg_fft<R1, DIR>(v);
+#pragma unroll
+            for (int kk = 1; kk < R1; ++kk) v[kk] = cmul(v[kk], tw1[kk]);
+#pragma unroll
+            for (int kk = 0; kk < R1; ++kk) T[em_idx<N, Q>(n2 * R1 + kk, q1)] = v[kk];
+        }
+        uint32_t keep = 0;   // inverse: which of this thread's output rows hold a voxel
+        if (DIR > 0) {
+#pragma unroll
+            for (int k2 = 0; k2 < R2 / 2; ++k2) {
+                const int j = k1 + R1 * k2;
+                if (j < Lout && ((M[st * MW + (j >> 5)] >> (j & 31)) & 1u)) keep |= 1u << k2;
+            }
+        }
+        __syncthreads();
+        float2 u[R2];
+#pragma unroll
+        for (int m = 0; m < R2; ++m) u[m] = T[em_idx<N, Q>(m * R1 + k1, q2)];
+        reg_fft<R2, DIR>(u);
+        float2* dst = out + bout + q2;
+#pragma unroll
+        for (int k2 = 0; k2 < R2; ++k2) {
+            const int off = (k1 + R1 * k2) * Nx;
+            if (DIR < 0)
+                dst[off] = u[k2];
+            else if (k2 < R2 / 2 && ((keep >> k2) & 1u))
+                dst[off] = u[k2];
+        }
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::);
+}
+
 // ---------------------------------------------------------------------------
 // Moment-form 5->5 multiply-accumulate at one frequency point:
 //   m1x = I2D + I3D, m1y = I3D - I2D, m1z = -2 I3D
@@ -731,6 +853,22 @@ void run_pass_y(svh_handle* h, const float2* in, float2* out, int Lin, int Lout,
     // SVH_PIPE_B flip these for experiments.
     static const bool use_pipe = getenv("SVH_NO_PIPE") == nullptr;
     static const bool pipe_fwd = getenv("SVH_PIPE_B") != nullptr;
+    static const int ystage = getenv("SVH_YSTAGE") ? atoi(getenv("SVH_YSTAGE")) : 3;  // 0 = off; bit0 fwd, bit1 inv
+    if constexpr (N >= 128 && N <= 1024) {
+        if (((DIR < 0 && (ystage & 1)) || (DIR > 0 && (ystage & 2))) && h->nx % 8 == 0) {
+            constexpr int QS = 8, SS = DIR < 0 ? 3 : 2;
+            using P = YStage<N, QS, DIR, SS>;
+            const int tiles_x = h->nx / QS;
+            const int ntiles = tiles_x * h->nzp * 5 * nrhs;
+            int dev = 0, nsm = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            prep(k_ystage<N, QS, DIR, SS>, P::smem);
+            SVH_LAUNCH((k_ystage<N, QS, DIR, SS>), std::min(ntiles, nsm), P::NT, P::smem, s, in, out, h->d_tw[1],
+                       h->nx, h->kz, Lin, Lout, ntiles, tiles_x, h->d_planes, h->nzp, h->d_rowmask, h->rowMW);
+            return;
+        }
+    }
     if constexpr (fft_r2(N) > 1 && Q >= 4 && colpipe_smem<N, 8, DIR>() <= 220 * 1024) {
         const bool want = use_pipe && (DIR > 0 || pipe_fwd);
         if (want && h->nx % 8 == 0) {
