@@ -39,7 +39,11 @@ __device__ __forceinline__ void static_for(F&& f) {
 
 __host__ __device__ constexpr int ilog2_c(int n) { return n <= 1 ? 0 : 1 + ilog2_c(n >> 1); }
 
-template <int L, int DIR>
+// HALF_IN: inputs L/2..L-1 are known zero (the zero-padded half of a circulant
+// embedding).  After the bit reversal they sit at the odd positions, so the
+// first radix-2 stage reduces to copies (x + 0 is not folded by the compiler under
+// IEEE semantics, so the pruning is explicit).
+template <int L, int DIR, bool HALF_IN = false>
 __device__ __forceinline__ void reg_fft(float2 (&v)[L]) {
     if constexpr (L > 1) {
         static_for<L>([&](auto I) {
@@ -60,6 +64,10 @@ __device__ __forceinline__ void reg_fft(float2 (&v)[L]) {
                     constexpr int k = decltype(Kc)::value;
                     const float2 a = v[i + k];
                     const float2 b = v[i + k + half];
+                    if constexpr (HALF_IN && len == 2) {
+                        v[i + k + half] = a;
+                        return;
+                    }
                     float2 t;
                     if constexpr (k == 0) {
                         t = b;

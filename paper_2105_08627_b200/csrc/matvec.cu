@@ -24,6 +24,7 @@
 
 #include "fft.cuh"
 #include "internal.h"
+#include "tma.cuh"
 
 namespace svh {
 
@@ -88,7 +89,7 @@ __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
         float2 v[N];
 #pragma unroll
         for (int j = 0; j < N; ++j) v[j] = (j < N / 2 || N == 1) ? load(row, j) : zero;
-        reg_fft<N, -1>(v);
+        reg_fft<N, -1, (N > 1)>(v);
         if (row >= 0) {
             float2* dst = X1 + ((int64_t)rc * rows + row) * N;
 #pragma unroll
@@ -102,7 +103,7 @@ __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
             float2 v[R1];
 #pragma unroll
             for (int n1 = 0; n1 < R1; ++n1) v[n1] = (n1 < R1 / 2) ? load(row, R2 * n1 + n2) : zero;
-            reg_fft<R1, -1>(v);
+            reg_fft<R1, -1, true>(v);
 #pragma unroll
             for (int k1 = 1; k1 < R1; ++k1) v[k1] = cmul(v[k1], __ldg(&tw[n2 * k1]));
 #pragma unroll
@@ -480,7 +481,7 @@ __global__ void __launch_bounds__(fft_r1(N) * Q, 1)
             float2 v[R1];
 #pragma unroll
             for (int n1 = 0; n1 < R1; ++n1) v[n1] = n1 < NL ? src[(R2 * n1 + n2) * Q + q1] : zero;
-            reg_fft<R1, DIR>(v);
+            reg_fft<R1, DIR, (DIR < 0)>(v);
 #pragma unroll
             for (int kk = 1; kk < R1; ++kk) v[kk] = cmul(v[kk], tw1[kk]);
 #pragma unroll
@@ -510,6 +511,176 @@ __global__ void __launch_bounds__(fft_r1(N) * Q, 1)
         }
     }
     asm volatile("cp.async.wait_group 0;\n" ::);
+}
+
+// TMA variant of the staged strided pass (default when the tensor map encodes).  X2 =
+// [plane p = rc*Kz + z][ky < Ny][kx < Nx] is described by ONE 3-D tensor map (box 8 kx x
+// 256 rows): the forward pass (B) stores its output tile with it, the inverse pass (D)
+// loads its input tile with it, one cp.async.bulk.tensor per 256-row box into an
+// mbarrier-tracked ring.  The other side keeps the pruned row traffic of k_ystage: B
+// loads only the rows holding a voxel (cp.async), D stores only those rows.
+template <int N, int DIR, int S, int QQ>
+struct YTma {
+    static constexpr int Q = QQ;
+    static constexpr int R1 = fft_r1(N), R2 = fft_r2(N);
+    static constexpr int NT = R1 * Q;
+    static constexpr int SR = DIR < 0 ? N / 2 : N;
+    static constexpr int MW = (N / 2 + 31) / 32;
+    static constexpr int BOX = N < 256 ? N : 256;
+    static constexpr size_t stage_b = (size_t)SR * Q * sizeof(float2);
+    static constexpr size_t T_b = ((size_t)em_size<N, Q>() * sizeof(float2) + 127) / 128 * 128;
+    static constexpr size_t O_b = DIR < 0 ? (size_t)N * Q * sizeof(float2) : 0;
+    static constexpr size_t smem = S * stage_b + T_b + O_b + (size_t)S * MW * 4 + S * 8 + 128;
+};
+
+template <int N, int DIR, int S, int QQ>
+__global__ void __launch_bounds__(fft_r1(N) * QQ, QQ == 4 ? 2 : 1)
+    k_ytma(const float2* __restrict__ in, float2* __restrict__ out, const __grid_constant__ CUtensorMap tmap,
+           const float2* __restrict__ tw, int Nx, int Kz, int Lin, int Lout, int ntiles, int tiles_x,
+           const int32_t* __restrict__ planes, int nzp, const uint32_t* __restrict__ rowmask, int rowMW) {
+    using P = YTma<N, DIR, S, QQ>;
+    constexpr int Q = P::Q, R1 = P::R1, R2 = P::R2, NT = P::NT, SR = P::SR, MW = P::MW, BOX = P::BOX;
+    constexpr int NL = DIR < 0 ? R1 / 2 : R1;
+    extern __shared__ __align__(128) unsigned char smraw[];
+    float2* stage = reinterpret_cast<float2*>(smraw);
+    float2* T = reinterpret_cast<float2*>(smraw + S * P::stage_b);
+    float2* O = reinterpret_cast<float2*>(smraw + S * P::stage_b + P::T_b);
+    uint32_t* M = reinterpret_cast<uint32_t*>(smraw + S * P::stage_b + P::T_b + P::O_b);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + ((S * P::stage_b + P::T_b + P::O_b + S * MW * 4 + 7) / 8) * 8);
+    const int tid = threadIdx.x;
+    const float2 zero = make_float2(0.f, 0.f);
+    const int lin = min(Lin, SR);
+    if (DIR < 0) {
+        for (int e = tid; e < S * (SR - lin) * Q; e += NT) {
+            const int st = e / ((SR - lin) * Q), r = e % ((SR - lin) * Q);
+            stage[st * SR * Q + lin * Q + r] = zero;
+        }
+    } else if (tid == 0) {
+        for (int st = 0; st < S; ++st) mbar_init(&bar[st], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    auto decode = [&](int t, int& z, int& p, int64_t& bin, int64_t& bout) {
+        const int xt = t % tiles_x, pr = t / tiles_x;
+        const int rc = pr / nzp;
+        z = __ldg(&planes[pr - rc * nzp]);
+        p = rc * Kz + z;
+        bin = (int64_t)p * Lin * Nx + (int64_t)xt * Q;
+        bout = (int64_t)p * Lout * Nx + (int64_t)xt * Q;
+    };
+    auto issue = [&](int t, int st) {
+        if (DIR < 0) {
+            if (t < ntiles) {
+                int z, p;
+                int64_t bin, bout;
+                decode(t, z, p, bin, bout);
+                const uint32_t* pm = rowmask + (int64_t)z * rowMW;
+                const float2* src = in + bin;
+                float2* dst = stage + st * SR * Q;
+                constexpr int NE = (SR * (Q / 2) + NT - 1) / NT;   // 16-byte chunks per thread
+                uint32_t wd[NE];
+#pragma unroll
+                for (int k = 0; k < NE; ++k) {   // all mask words first: one load latency, not NE
+                    const int j = (tid + k * NT) / (Q / 2);
+                    wd[k] = j < lin ? __ldg(&pm[j >> 5]) : 0u;
+                }
+#pragma unroll
+                for (int k = 0; k < NE; ++k) {
+                    const int e = tid + k * NT;
+                    const int j = e / (Q / 2), p2 = 2 * (e % (Q / 2));
+                    if (j < lin) {
+                        if ((wd[k] >> (j & 31)) & 1u)
+                            cp_async16(dst + j * Q + p2, src + (int64_t)j * Nx + p2);
+                        else
+                            *reinterpret_cast<float4*>(dst + j * Q + p2) = make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+                }
+            }
+            cp_async_commit();
+        } else if (t < ntiles) {
+            int z, p;
+            int64_t bin, bout;
+            decode(t, z, p, bin, bout);
+            if (tid < MW) M[st * MW + tid] = tid < rowMW ? __ldg(&rowmask[(int64_t)z * rowMW + tid]) : 0u;
+            if (tid == 0) {
+                mbar_arrive_expect_tx(&bar[st], (uint32_t)P::stage_b);
+#pragma unroll
+                for (int b = 0; b < N / BOX; ++b)
+                    tma_load_3d(stage + st * SR * Q + b * BOX * Q, &tmap, (t % tiles_x) * Q, b * BOX, p, &bar[st]);
+            }
+        }
+    };
+    const int n2 = tid / Q, q1 = tid % Q;
+    const bool ph1 = n2 < R2;
+    float2 tw1[R1];
+#pragma unroll
+    for (int kk = 1; kk < R1; ++kk) {
+        float2 w = ph1 ? __ldg(&tw[n2 * kk]) : zero;
+        if (DIR > 0) w.y = -w.y;
+        tw1[kk] = w;
+    }
+    const int k1 = tid / Q, q2 = tid % Q;
+    int t = blockIdx.x;
+#pragma unroll
+    for (int s2 = 0; s2 < S - 1; ++s2) issue(t + s2 * (int)gridDim.x, s2);
+    for (int i = 0; t < ntiles; ++i, t += gridDim.x) {
+        issue(t + (S - 1) * (int)gridDim.x, (i + S - 1) % S);
+        const int st = i % S;
+        if (DIR < 0) {
+            asm volatile("cp.async.wait_group %0;\n" ::"n"(S - 1));
+        } else {
+            mbar_wait(&bar[st], (uint32_t)((i / S) & 1));
+        }
+        __syncthreads();
+        int z, p;
+        int64_t bin, bout;
+        decode(t, z, p, bin, bout);
+        if (ph1) {
+            const float2* src = stage + st * SR * Q;
+            float2 v[R1];
+#pragma unroll
+            for (int n1 = 0; n1 < R1; ++n1) v[n1] = n1 < NL ? src[(R2 * n1 + n2) * Q + q1] : zero;
+            reg_fft<R1, DIR, (DIR < 0)>(v);
+#pragma unroll
+            for (int kk = 1; kk < R1; ++kk) v[kk] = cmul(v[kk], tw1[kk]);
+#pragma unroll
+            for (int kk = 0; kk < R1; ++kk) T[em_idx<N, Q>(n2 * R1 + kk, q1)] = v[kk];
+        }
+        uint32_t keep = 0;
+        if (DIR > 0) {
+#pragma unroll
+            for (int k2 = 0; k2 < R2 / 2; ++k2) {
+                const int j = k1 + R1 * k2;
+                if (j < Lout && ((M[st * MW + (j >> 5)] >> (j & 31)) & 1u)) keep |= 1u << k2;
+            }
+        }
+        if (DIR < 0 && tid == 0) tma_store_wait_read0();   // O of the previous tile has been read out
+        __syncthreads();
+        float2 u[R2];
+#pragma unroll
+        for (int m = 0; m < R2; ++m) u[m] = T[em_idx<N, Q>(m * R1 + k1, q2)];
+        reg_fft<R2, DIR>(u);
+        if (DIR < 0) {
+#pragma unroll
+            for (int k2 = 0; k2 < R2; ++k2) O[(k1 + R1 * k2) * Q + q2] = u[k2];
+            fence_proxy_async_smem();
+            __syncthreads();
+            if (tid == 0) {
+#pragma unroll
+                for (int b = 0; b < N / BOX; ++b) tma_store_3d(&tmap, (t % tiles_x) * Q, b * BOX, p, O + b * BOX * Q);
+                tma_store_commit();
+            }
+        } else {
+            float2* dst = out + bout + q2;
+#pragma unroll
+            for (int k2 = 0; k2 < R2 / 2; ++k2)
+                if ((keep >> k2) & 1u) dst[(k1 + R1 * k2) * Nx] = u[k2];
+        }
+    }
+    if (DIR < 0) {
+        asm volatile("cp.async.wait_group 0;\n" ::);
+        if (tid == 0) tma_store_wait0();
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -727,6 +898,110 @@ __global__ void __launch_bounds__(5 * Q)
     }
 }
 
+// Pass C, default for 2 <= Nz <= 32: 32 pencils (kx) x 5 components per CTA, one
+// thread per (component, pencil) for the z-FFTs in registers, the CTA loops over all
+// RHS (register prefetch of the next one).  Compared with k_freq_small:
+//  * the prefactor j*omega*mu0*dx/(Nx Ny Nz) and the constants of the moment form are
+//    folded into the 7 kernel values once per CTA, so the MAC is 19 paired-FP32 ops;
+//  * the MAC points are split warp-uniformly (warp w takes kz = w, w+5, ...; lane = kx),
+//    all shared-memory offsets are compile-time;
+//  * the forward z-FFT skips its zero-padded half (reg_fft HALF_IN).
+// Folded values per point (K1 = -i s1):
+//   f0 = g K0, f1 = g s1x, f2 = g s1y, f3 = -2 g s1z, f4 = g K2x, f5 = g K2y, f6 = 4 g K2z
+//   CCx = i f0 Ix + f1 m1x,  CCy = i f0 Iy + f2 m1y,  CCz = i f0 Iz + f3 I3
+//   Qx = -f1 Ix + i f4 m1x,  Qy = -f2 Iy + i f5 m1y,  Qz' = -2 Qz = -f3 Iz + i f6 I3
+//   CC2D = Qx - Qy,  CC3D = Qx + Qy + Qz'          (m1x = I2D + I3D, m1y = I3D - I2D)
+template <int N>
+constexpr int zmac_s_f2() {   // spectra buffer, also >= the 2048-float Tucker scratch
+    return 5 * N * 32 > 1024 ? 5 * N * 32 : 1024;
+}
+template <int N>
+constexpr size_t zmac_smem() {
+    return (size_t)zmac_s_f2<N>() * sizeof(float2) + (size_t)7 * N * 32 * sizeof(float);
+}
+
+template <int N>
+__global__ void __launch_bounds__(160, 3)
+    k_zmac(float2* __restrict__ X2, SpecView sv, int Nx, int Ny, int Kz, float g, int nrhs, uint64_t pmask) {
+    constexpr int Q = 32, NH = N / 2;
+    extern __shared__ float2 S[];                       // [5][N][Q] spectra; Tucker scratch
+    float* KV = reinterpret_cast<float*>(S + zmac_s_f2<N>());   // [7][N][Q] folded kernel values
+    const int tid = threadIdx.x;
+    const int c = tid >> 5, q = tid & 31;               // FFT role: component c, pencil q
+    const int kx0 = blockIdx.x * Q;
+    const int ky = blockIdx.y;
+    const int64_t plane = (int64_t)Nx * Ny;
+    const bool ok = kx0 + q < Nx;
+    const float2 zero = make_float2(0.f, 0.f);
+    float2* col = X2 + (int64_t)c * Kz * plane + (int64_t)ky * Nx + kx0 + q;
+    const int64_t rstride = 5 * Kz * plane;
+    // rows z < min(Kz, N/2) of non-empty planes are loaded / stored; the rest are zero / dropped
+    const uint32_t lm = ok ? (uint32_t)(pmask & ((1ull << min(Kz, NH)) - 1ull)) : 0u;
+    float2 nxt[NH];
+#pragma unroll
+    for (int j = 0; j < NH; ++j) nxt[j] = ((lm >> j) & 1u) ? col[(int64_t)j * plane] : zero;
+    if (sv.spec) {
+        for (int t = tid; t < N * Q; t += 5 * Q) {
+            const int k = t / Q, qq = t % Q;
+            float kv[7];
+            kernel_values(sv, min(kx0 + qq, Nx - 1), ky, k, Nx, Ny, N, kv);
+#pragma unroll
+            for (int m = 0; m < 7; ++m) KV[(m * N + k) * Q + qq] = kv[m];
+        }
+    } else {
+        tucker_tile<N, Q>(sv, kx0, ky, Nx, Ny, KV, reinterpret_cast<float*>(S));
+    }
+    __syncthreads();
+    for (int t = tid; t < 7 * N * Q; t += 5 * Q) {
+        const int m = t / (N * Q);
+        KV[t] *= m == 3 ? -2.f * g : (m == 6 ? 4.f * g : g);
+    }
+    // MAC role: warp w = c takes kz = w + 5 i; lane = pencil
+    const int w = c;
+    for (int r = 0; r < nrhs; ++r) {
+        float2 v[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) v[j] = j < NH ? nxt[j] : zero;
+        reg_fft<N, -1, true>(v);
+#pragma unroll
+        for (int k = 0; k < N; ++k) S[(c * N + k) * Q + q] = v[k];
+        __syncthreads();
+        if (r + 1 < nrhs) {
+            const float2* nc = col + (r + 1) * rstride;
+#pragma unroll
+            for (int j = 0; j < NH; ++j) nxt[j] = ((lm >> j) & 1u) ? nc[(int64_t)j * plane] : zero;
+        }
+        float2* sp = S + w * Q + q;
+        const float* kp = KV + w * Q + q;
+#pragma unroll 1
+        for (int k = w; k < N; k += 5, sp += 5 * Q, kp += 5 * Q) {
+            {
+                const float2 Ix = sp[0 * N * Q], Iy = sp[1 * N * Q], Iz = sp[2 * N * Q];
+                const float2 I2 = sp[3 * N * Q], I3 = sp[4 * N * Q];
+                const float f0 = kp[0 * N * Q], f1 = kp[1 * N * Q], f2 = kp[2 * N * Q], f3 = kp[3 * N * Q];
+                const float f4 = kp[4 * N * Q], f5 = kp[5 * N * Q], f6 = kp[6 * N * Q];
+                const float2 m1x = cadd(I2, I3), m1y = csub(I3, I2);
+                const float2 Qx = cfma_s(Ix, -f1, cmul_i(m1x, f4));
+                const float2 Qy = cfma_s(Iy, -f2, cmul_i(m1y, f5));
+                const float2 Qz = cfma_s(Iz, -f3, cmul_i(I3, f6));
+                sp[0 * N * Q] = cfma_s(m1x, f1, cmul_i(Ix, f0));
+                sp[1 * N * Q] = cfma_s(m1y, f2, cmul_i(Iy, f0));
+                sp[2 * N * Q] = cfma_s(I3, f3, cmul_i(Iz, f0));
+                sp[3 * N * Q] = csub(Qx, Qy);
+                sp[4 * N * Q] = cadd(cadd(Qx, Qy), Qz);
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < N; ++k) v[k] = S[(c * N + k) * Q + q];   // own column: no barrier before reuse
+        reg_fft<N, +1>(v);
+        float2* dst = col + r * rstride;
+#pragma unroll
+        for (int j = 0; j < NH; ++j)
+            if ((lm >> j) & 1u) dst[(int64_t)j * plane] = v[j];
+    }
+}
+
 // Pass C for Nz > 64: generic shared-memory FFT over 5Q pencils (smem_fft).
 template <int N>
 __global__ void __launch_bounds__(fft_max_threads(N))
@@ -854,6 +1129,34 @@ void run_pass_y(svh_handle* h, const float2* in, float2* out, int Lin, int Lout,
     static const bool use_pipe = getenv("SVH_NO_PIPE") == nullptr;
     static const bool pipe_fwd = getenv("SVH_PIPE_B") != nullptr;
     static const int ystage = getenv("SVH_YSTAGE") ? atoi(getenv("SVH_YSTAGE")) : 3;  // 0 = off; bit0 fwd, bit1 inv
+    static const bool ytma = getenv("SVH_YTMA") == nullptr || atoi(getenv("SVH_YTMA")) != 0;
+    if constexpr (N >= 128 && N <= 1024) {
+        CUtensorMap tmap;
+        const float2* x2 = DIR < 0 ? out : in;   // the X2 side of the pass
+        static const int yq = getenv("SVH_YQ") ? atoi(getenv("SVH_YQ")) : 8;
+        auto launch = [&](auto Qc) -> bool {
+            constexpr int QQ = decltype(Qc)::value;
+            using P = YTma<N, DIR, 2, QQ>;
+            if (h->nx % QQ != 0 ||
+                !encode_tmap_c64_3d(&tmap, x2, (uint64_t)h->nx, (uint64_t)h->ny, (uint64_t)5 * nrhs * h->kz,
+                                    (uint64_t)h->nx, (uint64_t)h->nx * h->ny, QQ, P::BOX))
+                return false;
+            const int tiles_x = h->nx / QQ;
+            const int ntiles = tiles_x * h->nzp * 5 * nrhs;
+            int dev = 0, nsm = 148, occ = 1;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            prep(k_ytma<N, DIR, 2, QQ>, P::smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ytma<N, DIR, 2, QQ>, P::NT, P::smem);
+            SVH_LAUNCH((k_ytma<N, DIR, 2, QQ>), std::min(ntiles, nsm * std::max(occ, 1)), P::NT, P::smem, s, in,
+                       out, tmap, h->d_tw[1], h->nx, h->kz, Lin, Lout, ntiles, tiles_x, h->d_planes, h->nzp,
+                       h->d_rowmask, h->rowMW);
+            return true;
+        };
+        if (ytma && ((yq == 4 && launch(std::integral_constant<int, 4>{})) ||
+                     (yq != 4 && launch(std::integral_constant<int, 8>{}))))
+            return;
+    }
     if constexpr (N >= 128 && N <= 1024) {
         if (((DIR < 0 && (ystage & 1)) || (DIR > 0 && (ystage & 2))) && h->nx % 8 == 0) {
             constexpr int QS = 8, SS = DIR < 0 ? 3 : 2;
@@ -912,6 +1215,17 @@ void run_pass_c(svh_handle* h, float2* X2, int nrhs, cudaStream_t s) {
                 sv.rk[m][a] = h->tucker.ranks[m][a];
             }
         }
+    static const bool zmac = getenv("SVH_ZMAC") == nullptr || atoi(getenv("SVH_ZMAC")) != 0;
+    if constexpr (N >= 2 && N <= 32) {
+        if (zmac) {
+            const size_t smem = zmac_smem<N>();
+            dim3 grid((h->nx + 31) / 32, h->ny);
+            prep(k_zmac<N>, smem);
+            SVH_LAUNCH((k_zmac<N>), grid, 160, smem, s, X2, sv, h->nx, h->ny, h->kz, h->gscale, nrhs,
+                       (uint64_t)h->planemask);
+            return;
+        }
+    }
     if constexpr (N <= 64) {
         static const int cq = getenv("SVH_CQ") ? atoi(getenv("SVH_CQ")) : 32;
         static const bool casync = getenv("SVH_CASYNC") != nullptr;
