@@ -1133,7 +1133,7 @@ void run_pass_y(svh_handle* h, const float2* in, float2* out, int Lin, int Lout,
     if constexpr (N >= 128 && N <= 1024) {
         CUtensorMap tmap;
         const float2* x2 = DIR < 0 ? out : in;   // the X2 side of the pass
-        static const int yq = getenv("SVH_YQ") ? atoi(getenv("SVH_YQ")) : 8;
+        static const int yq = getenv("SVH_YQ") ? atoi(getenv("SVH_YQ")) : 4;
         auto launch = [&](auto Qc) -> bool {
             constexpr int QQ = decltype(Qc)::value;
             using P = YTma<N, DIR, 2, QQ>;
