@@ -144,6 +144,33 @@ int svh_matvec(svh_handle* h, const void* I, void* CC, int32_t nrhs, int32_t gre
 int svh_matvec_grid(svh_handle* h, const void* I, void* CC, int32_t nrhs, int32_t green_only, svh_stream stream);
 
 /*
+ * Slab-decomposed matvec (the operator is Eq. 9 as in svh_matvec_grid,
+ * P:79-83).  P ranks, each holding the same handle (replicated setup); rank r owns the
+ * y-slab r*Kyl <= y < (r+1)*Kyl of every plane, Kyl = Ky/P (requires Ky % P == 0 and
+ * Nx % P == 0).  One product is three calls with two all-to-alls between them, done by
+ * the caller (NCCL all_to_all_single over NVLink, equal chunks):
+ *   svh_slab_forward  (I_slab -> send)        pass A on the slab, packed by destination kx-slab
+ *   all-to-all        (send -> recv)
+ *   svh_slab_middle   (recv -> send)          passes B, C, D on kx-slab r (Nxl = Nx/P columns)
+ *   all-to-all        (send -> recv)
+ *   svh_slab_backward (recv, I_slab -> CC)    pass E on the slab (+ local term unless green_only)
+ * I_slab, CC_slab : device complex64 [nrhs][5][Kz][Kyl][Kx] (lattice layout of the slab, zero
+ *                   at empty voxels; CC is written zero there).
+ * send, recv      : device complex64, nrhs * sizes[3] elements, chunk for peer p at
+ *                   p * nrhs * sizes[2] (layout [p][nrhs][5][Kz][Kyl][Nxl]); caller-owned.
+ * svh_slab_sizes  : sizes[0] = Kyl, [1] = Nxl, [2] = elements per peer chunk per RHS,
+ *                   [3] = send/recv elements per RHS.  Errors: SVH_EINVAL (bad P / rank).
+ * The calls use the handle's matvec workspace: one slab product per handle at a time.
+ */
+int svh_slab_sizes(const svh_handle* h, int32_t P, int64_t* sizes);
+int svh_slab_forward(svh_handle* h, int32_t rank, int32_t P, const void* I_slab, void* send, int32_t nrhs,
+                     svh_stream stream);
+int svh_slab_middle(svh_handle* h, int32_t rank, int32_t P, const void* recv, void* send, int32_t nrhs,
+                    svh_stream stream);
+int svh_slab_backward(svh_handle* h, int32_t rank, int32_t P, const void* recv, const void* I_slab, void* CC_slab,
+                      int32_t nrhs, int32_t green_only, svh_stream stream);
+
+/*
  * svh_apply_system -- Eq. 7 saddle operator (reading G12 sign convention):
  *   y_I   = Z.x_I + A^T x_Phi,   y_Phi = A x_I
  * x, y : device complex64 [nrhs][5K + M].  Errors: SVH_EINVAL, SVH_ECUDA.

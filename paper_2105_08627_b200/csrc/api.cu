@@ -137,6 +137,7 @@ static void build_lattice(svh_handle* h) {
             if (z < 64) h->planemask |= 1ull << z;
         }
     h->n_rows_ne = (int64_t)rl.size();
+    h->h_rowlist = rl;
     h->nzp = (int)pl.size();
     SVH_CHECK(h->n_rows_ne > 0, SVH_EINVAL, "no non-empty voxel");
     SVH_CUDA(cudaMalloc(&h->d_rowmask, rm.size() * sizeof(uint32_t)));
@@ -166,6 +167,7 @@ static void destroy(svh_handle* h) {
     cudaFree(h->d_mat);
     cudaFree(h->d_vmap);
     cudaFree(h->d_rowinfo);
+    for (auto& sr : h->slab_rows) cudaFree(sr.d);
     cudaFree(h->d_rowmask);
     cudaFree(h->d_rowlist);
     cudaFree(h->d_planes);
@@ -315,6 +317,41 @@ int svh_plan_info(const svh_handle* h, int64_t* info) {
         info[1] = h->nzp;
         info[2] = (int64_t)h->ky * h->kz;
         info[3] = h->kz;
+    });
+}
+
+int svh_slab_sizes(const svh_handle* h, int32_t P, int64_t* sizes) {
+    return guarded([&] {
+        SVH_CHECK(h && sizes, SVH_EINVAL, "null arg");
+        slab_sizes(h, P, sizes);
+    });
+}
+
+int svh_slab_forward(svh_handle* h, int32_t rank, int32_t P, const void* I_slab, void* send, int32_t nrhs,
+                     svh_stream stream) {
+    return guarded([&] {
+        SVH_CHECK(h && I_slab && send && nrhs >= 1, SVH_EINVAL, "bad slab args");
+        SVH_CUDA(cudaSetDevice(h->device));
+        slab_forward(h, rank, P, (const float2*)I_slab, (float2*)send, nrhs, (cudaStream_t)stream);
+    });
+}
+
+int svh_slab_middle(svh_handle* h, int32_t rank, int32_t P, const void* recv, void* send, int32_t nrhs,
+                    svh_stream stream) {
+    return guarded([&] {
+        SVH_CHECK(h && recv && send && recv != send && nrhs >= 1, SVH_EINVAL, "bad slab args");
+        SVH_CUDA(cudaSetDevice(h->device));
+        slab_middle(h, rank, P, (const float2*)recv, (float2*)send, nrhs, (cudaStream_t)stream);
+    });
+}
+
+int svh_slab_backward(svh_handle* h, int32_t rank, int32_t P, const void* recv, const void* I_slab, void* CC_slab,
+                      int32_t nrhs, int32_t green_only, svh_stream stream) {
+    return guarded([&] {
+        SVH_CHECK(h && recv && I_slab && CC_slab && I_slab != CC_slab && nrhs >= 1, SVH_EINVAL, "bad slab args");
+        SVH_CUDA(cudaSetDevice(h->device));
+        slab_backward(h, rank, P, (const float2*)recv, (const float2*)I_slab, (float2*)CC_slab, nrhs,
+                      green_only != 0, (cudaStream_t)stream);
     });
 }
 

@@ -73,6 +73,15 @@ struct svh_handle {
         cudaEvent_t a, b;
     };
     std::vector<ProfRec> prof;
+    // slab-decomposed matvec: host copy of the non-empty row list and the
+    // per-(P, rank) slab row lists on the device (built on first use)
+    std::vector<int32_t> h_rowlist;
+    struct SlabRows {
+        int P, rank;
+        int32_t* d = nullptr;
+        int n = 0;
+    };
+    std::vector<SlabRows> slab_rows;
 };
 
 namespace svh {
@@ -80,6 +89,11 @@ namespace svh {
 void matvec(svh_handle* h, const float2* I, float2* CC, int nrhs, bool green_only, bool packed,
             cudaStream_t s);
 void ensure_workspace(svh_handle* h, int nrhs);
+void slab_sizes(const svh_handle* h, int P, int64_t* out4);
+void slab_forward(svh_handle* h, int rank, int P, const float2* I, float2* send, int nrhs, cudaStream_t s);
+void slab_middle(svh_handle* h, int rank, int P, const float2* recv, float2* send, int nrhs, cudaStream_t s);
+void slab_backward(svh_handle* h, int rank, int P, const float2* recv, const float2* I, float2* CC, int nrhs,
+                   bool green_only, cudaStream_t s);
 // quad.cu
 void compute_kernels(svh_handle* h);
 // spectra.cu

@@ -66,23 +66,27 @@ __device__ __forceinline__ bool row_bit(const uint32_t* __restrict__ rowmask, in
     return (__ldg(&rowmask[(int64_t)z * rowMW + (y >> 5)]) >> (y & 31)) & 1u;
 }
 
-// Pass A over the non-empty rows only (rowlist[li], li < nlist); X1 keeps the full
-// [rc][rows][N] layout so the strided passes index it by (z, y).
+// Pass A over the non-empty rows only (rowlist[li], li < nlist, global row z*Ky + y); X1
+// keeps the [rc][rows][N] layout so the strided passes index it by (z, y).  A y-slab
+// (rows y0 <= y < y0 + Kyl of every plane) uses the local row
+// z*Kyl + y - y0 for X1 and for a grid-layout input; the whole grid is Kyl = Ky, y0 = 0.
 template <int N, int Q, bool PACKED>
 __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
     k_row_fwd(const float2* __restrict__ in, float2* __restrict__ X1, const int2* __restrict__ rowinfo, int W,
               const int32_t* __restrict__ rowlist, int nlist, const float2* __restrict__ tw, int Kx, int rows,
-              int64_t K, int64_t Kt) {
+              int64_t K, int64_t Kt, int Ky, int Kyl, int y0) {
     constexpr int R1 = fft_r1(N), R2 = fft_r2(N);
     const int rc = blockIdx.y;
     const int li0 = blockIdx.x * Q;
     const float2 zero = make_float2(0.f, 0.f);
     auto row_of = [&](int q) -> int { return li0 + q < nlist ? __ldg(&rowlist[li0 + q]) : -1; };
+    auto local = [&](int row) -> int { return (row / Ky) * Kyl + row % Ky - y0; };
     auto load = [&](int row, int j) -> float2 {
         if (row < 0 || j >= Kx) return zero;
         const int idx = packed_index(rowinfo, W, row, j);
         if (idx < 0) return zero;
-        return PACKED ? __ldg(&in[(int64_t)rc * K + idx]) : __ldg(&in[(int64_t)rc * Kt + (int64_t)row * Kx + j]);
+        return PACKED ? __ldg(&in[(int64_t)rc * K + idx])
+                      : __ldg(&in[(int64_t)rc * Kt + (int64_t)local(row) * Kx + j]);
     };
     if constexpr (R2 == 1) {
         const int row = row_of(threadIdx.x);
@@ -91,7 +95,7 @@ __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
         for (int j = 0; j < N; ++j) v[j] = (j < N / 2 || N == 1) ? load(row, j) : zero;
         reg_fft<N, -1, (N > 1)>(v);
         if (row >= 0) {
-            float2* dst = X1 + ((int64_t)rc * rows + row) * N;
+            float2* dst = X1 + ((int64_t)rc * rows + local(row)) * N;
 #pragma unroll
             for (int k = 0; k < N; ++k) dst[k] = v[k];
         }
@@ -118,7 +122,7 @@ __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
             for (int n2 = 0; n2 < R2; ++n2) u[n2] = S[pm_idx<N>(q, n2 * R1 + k1)];
             reg_fft<R2, -1>(u);
             if (row >= 0) {
-                float2* dst = X1 + ((int64_t)rc * rows + row) * N;
+                float2* dst = X1 + ((int64_t)rc * rows + local(row)) * N;
 #pragma unroll
                 for (int k2 = 0; k2 < R2; ++k2) dst[k1 + R1 * k2] = u[k2];
             }
@@ -135,7 +139,7 @@ __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
               const int2* __restrict__ rowinfo, int W, const int32_t* __restrict__ rowlist, int nlist,
               const uint32_t* __restrict__ rowmask, int rowMW, int Ky, const uint8_t* __restrict__ matp,
               const float2* __restrict__ zloc, int nzl, const float2* __restrict__ tw, int Kx, int rows, int64_t K,
-              int64_t Kt, int green_only) {
+              int64_t Kt, int green_only, int Kyl, int y0) {
     constexpr int R1 = fft_r1(N), R2 = fft_r2(N);
     const int rc = blockIdx.y;
     const int comp = rc % 5;
@@ -144,18 +148,21 @@ __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
     __shared__ float2 zs[256];   // z^b of this component per material
     for (int m = threadIdx.x; m < nzl; m += blockDim.x) zs[m] = zloc[m * 5 + comp];
     __syncthreads();
+    // global row z*Ky + y of slot q (rowlist: packed output over the non-empty rows;
+    // nullptr: every row of the (slab) grid, local slot z*Kyl + y - y0)
     auto row_of = [&](int q) -> int {
         const int li = li0 + q;
         if (li >= nlist) return -1;
-        return rowlist ? __ldg(&rowlist[li]) : li;
+        return rowlist ? __ldg(&rowlist[li]) : (li / Kyl) * Ky + y0 + li % Kyl;
     };
+    auto local = [&](int row) -> int { return (row / Ky) * Kyl + row % Ky - y0; };
     // X1 holds data for this row (listed rows are non-empty by construction)
     auto live = [&](int row) -> bool {
         return row >= 0 && (rowlist != nullptr || row_bit(rowmask, rowMW, row / Ky, row % Ky));
     };
     auto store = [&](int row, int j, float2 v) {
         if (row < 0 || j >= Kx) return;
-        const int64_t cell = (int64_t)row * Kx + j;
+        const int64_t cell = (int64_t)local(row) * Kx + j;
         const int idx = packed_index(rowinfo, W, row, j);
         if (idx < 0) {
             if (!PACKED) out[(int64_t)rc * Kt + cell] = zero;
@@ -175,7 +182,7 @@ __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
         const int row = row_of(threadIdx.x);
         const bool ok = live(row);
         float2 v[N];
-        const float2* src = X1 + ((int64_t)rc * rows + max(row, 0)) * N;
+        const float2* src = X1 + ((int64_t)rc * rows + (ok ? local(row) : 0)) * N;
 #pragma unroll
         for (int k = 0; k < N; ++k) v[k] = ok ? src[k] : zero;
         reg_fft<N, +1>(v);
@@ -187,7 +194,7 @@ __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
             const int q = threadIdx.x / R2, n2 = threadIdx.x % R2;
             const int row = row_of(q);
             const bool ok = live(row);
-            const float2* src = X1 + ((int64_t)rc * rows + max(row, 0)) * N;
+            const float2* src = X1 + ((int64_t)rc * rows + (ok ? local(row) : 0)) * N;
             float2 v[R1];
 #pragma unroll
             for (int n1 = 0; n1 < R1; ++n1) v[n1] = ok ? src[R2 * n1 + n2] : zero;
@@ -805,7 +812,8 @@ constexpr size_t freq_small_smem() {
 // into a shared staging tile with cp.async (ASYNC = true).
 template <int N, int Q, bool ASYNC>
 __global__ void __launch_bounds__(5 * Q)
-    k_freq_small(float2* __restrict__ X2, SpecView sv, int Nx, int Ny, int Kz, float g, int nrhs, uint64_t pmask) {
+    k_freq_small(float2* __restrict__ X2, SpecView sv, int Nx, int Ny, int Kz, float g, int nrhs, uint64_t pmask,
+                 int Nxs, int kxg) {
     extern __shared__ float2 S[];   // [5][N][Q] spectra (also Tucker scratch), [7][N][Q] kernel values, stage
     float* KV = reinterpret_cast<float*>(S + freq_small_spec_f2<N, Q>());
     constexpr int NH = (N + 1) / 2;
@@ -813,14 +821,14 @@ __global__ void __launch_bounds__(5 * Q)
     const int c = threadIdx.x / Q, q = threadIdx.x % Q;
     const int kx0 = blockIdx.x * Q;
     const int ky = blockIdx.y;
-    const int64_t plane = (int64_t)Nx * Ny;
-    const bool ok = kx0 + q < Nx;
+    const int64_t plane = (int64_t)Nxs * Ny;   // array x-extent (a kx-slab: Nx/P)
+    const bool ok = kx0 + q < Nxs;
     const float2 zero = make_float2(0.f, 0.f);
-    float2* col = X2 + (int64_t)c * Kz * plane + (int64_t)ky * Nx + kx0 + q;
+    float2* col = X2 + (int64_t)c * Kz * plane + (int64_t)ky * Nxs + kx0 + q;
     const int64_t rstride = 5 * Kz * plane;
     const int kz_ld = min(Kz, NH);
     auto issue = [&](int r) {   // cp.async the RHS r tile: 5 comps x kz_ld rows x Q columns (16-byte chunks)
-        const float2* base = X2 + r * rstride + (int64_t)ky * Nx + kx0;
+        const float2* base = X2 + r * rstride + (int64_t)ky * Nxs + kx0;
         for (int e = threadIdx.x; e < 5 * kz_ld * (Q / 2); e += 5 * Q) {
             const int p = e % (Q / 2), rest = e / (Q / 2);
             const int j = rest % kz_ld, cc = rest / kz_ld;
@@ -842,12 +850,12 @@ __global__ void __launch_bounds__(5 * Q)
         for (int t = threadIdx.x; t < N * Q; t += 5 * Q) {
             const int k = t / Q, qq = t % Q;
             float kv[7];
-            kernel_values(sv, min(kx0 + qq, Nx - 1), ky, k, Nx, Ny, N, kv);
+            kernel_values(sv, min(kxg + kx0 + qq, Nx - 1), ky, k, Nx, Ny, N, kv);
 #pragma unroll
             for (int m = 0; m < 7; ++m) KV[(m * N + k) * Q + qq] = kv[m];
         }
     } else {
-        tucker_tile<N, Q>(sv, kx0, ky, Nx, Ny, KV, reinterpret_cast<float*>(S));
+        tucker_tile<N, Q>(sv, kxg + kx0, ky, Nx, Ny, KV, reinterpret_cast<float*>(S));
     }
     for (int r = 0; r < nrhs; ++r) {
         float2 v[N];
@@ -922,7 +930,8 @@ constexpr size_t zmac_smem() {
 
 template <int N>
 __global__ void __launch_bounds__(160, 3)
-    k_zmac(float2* __restrict__ X2, SpecView sv, int Nx, int Ny, int Kz, float g, int nrhs, uint64_t pmask) {
+    k_zmac(float2* __restrict__ X2, SpecView sv, int Nx, int Ny, int Kz, float g, int nrhs, uint64_t pmask, int Nxs,
+           int kxg) {
     constexpr int Q = 32, NH = N / 2;
     extern __shared__ float2 S[];                       // [5][N][Q] spectra; Tucker scratch
     float* KV = reinterpret_cast<float*>(S + zmac_s_f2<N>());   // [7][N][Q] folded kernel values
@@ -930,10 +939,10 @@ __global__ void __launch_bounds__(160, 3)
     const int c = tid >> 5, q = tid & 31;               // FFT role: component c, pencil q
     const int kx0 = blockIdx.x * Q;
     const int ky = blockIdx.y;
-    const int64_t plane = (int64_t)Nx * Ny;
-    const bool ok = kx0 + q < Nx;
+    const int64_t plane = (int64_t)Nxs * Ny;   // array x-extent (a kx-slab: Nx/P)
+    const bool ok = kx0 + q < Nxs;
     const float2 zero = make_float2(0.f, 0.f);
-    float2* col = X2 + (int64_t)c * Kz * plane + (int64_t)ky * Nx + kx0 + q;
+    float2* col = X2 + (int64_t)c * Kz * plane + (int64_t)ky * Nxs + kx0 + q;
     const int64_t rstride = 5 * Kz * plane;
     // rows z < min(Kz, N/2) of non-empty planes are loaded / stored; the rest are zero / dropped
     const uint32_t lm = ok ? (uint32_t)(pmask & ((1ull << min(Kz, NH)) - 1ull)) : 0u;
@@ -944,12 +953,12 @@ __global__ void __launch_bounds__(160, 3)
         for (int t = tid; t < N * Q; t += 5 * Q) {
             const int k = t / Q, qq = t % Q;
             float kv[7];
-            kernel_values(sv, min(kx0 + qq, Nx - 1), ky, k, Nx, Ny, N, kv);
+            kernel_values(sv, min(kxg + kx0 + qq, Nx - 1), ky, k, Nx, Ny, N, kv);
 #pragma unroll
             for (int m = 0; m < 7; ++m) KV[(m * N + k) * Q + qq] = kv[m];
         }
     } else {
-        tucker_tile<N, Q>(sv, kx0, ky, Nx, Ny, KV, reinterpret_cast<float*>(S));
+        tucker_tile<N, Q>(sv, kxg + kx0, ky, Nx, Ny, KV, reinterpret_cast<float*>(S));
     }
     __syncthreads();
     for (int t = tid; t < 7 * N * Q; t += 5 * Q) {
@@ -1006,16 +1015,16 @@ __global__ void __launch_bounds__(160, 3)
 template <int N>
 __global__ void __launch_bounds__(fft_max_threads(N))
     k_freq_big(float2* __restrict__ X2, SpecView sv, const float2* __restrict__ tw, int Nx, int Ny, int Kz, int Q,
-               float g, const uint8_t* __restrict__ planeok) {
+               float g, const uint8_t* __restrict__ planeok, int Nxs, int kxg) {
     extern __shared__ float2 S[];
     const int Q5 = 5 * Q;
     const int PP = Q5 + 1;
     const int kx0 = blockIdx.x * Q;
     const int ky = blockIdx.y;
     const int64_t r = blockIdx.z;
-    const int64_t plane = (int64_t)Nx * Ny;
-    float2* base = X2 + r * 5 * Kz * plane + (int64_t)ky * Nx + kx0;
-    const int nq = min(Q, Nx - kx0);
+    const int64_t plane = (int64_t)Nxs * Ny;
+    float2* base = X2 + r * 5 * Kz * plane + (int64_t)ky * Nxs + kx0;
+    const int nq = min(Q, Nxs - kx0);
     for (int t = threadIdx.x; t < Q * N * 5; t += blockDim.x) {
         const int q = t % Q;
         const int rest = t / Q;
@@ -1031,10 +1040,10 @@ __global__ void __launch_bounds__(fft_max_threads(N))
         if (q >= nq) continue;
         float kv[7];
         if (sv.spec) {
-            kernel_values(sv, kx0 + q, ky, kz, Nx, Ny, N, kv);
+            kernel_values(sv, kxg + kx0 + q, ky, kz, Nx, Ny, N, kv);
         } else {
             // Tucker: direct contraction per point (Eq. 10)
-            const int kx = kx0 + q;
+            const int kx = kxg + kx0 + q;
             const int o3[3] = {kx <= (Nx >> 1) ? kx : Nx - kx, ky <= (Ny >> 1) ? ky : Ny - ky,
                                kz <= (N >> 1) ? kz : N - kz};
 #pragma unroll
@@ -1101,27 +1110,47 @@ constexpr int col_q() {
     return fft_r2(N) == 1 ? 128 : (fft_r1(N) >= 64 ? 4 : 8);
 }
 
+}  // namespace
+// Geometry of one pass invocation: the whole grid, or one slab of the slab-decomposed
+// matvec: x-slab passes B-D see the array columns kx0 .. kx0+nx-1 of the
+// global embedding; row passes A/E see the y rows y0 .. y0+kyl-1 of every plane.
+struct Geom {
+    int nx;                   // x extent of the X1 / X2 arrays
+    int kx0;                  // global kx of array column 0
+    int kyl, y0;              // rows of the row passes
+    const int32_t* rowlist;   // pass A: non-empty global rows z*Ky + y (ascending)
+    int nrows;
+};
+static Geom whole_grid(const svh_handle* h) {
+    return Geom{h->nx, 0, h->ky, 0, h->d_rowlist, (int)h->n_rows_ne};
+}
+namespace {
+
 template <int N>
-void run_pass_a(svh_handle* h, const float2* in, float2* X1, bool packed, int nrhs, cudaStream_t s) {
+void run_pass_a(svh_handle* h, const Geom& g, const float2* in, float2* X1, bool packed, int nrhs, cudaStream_t s) {
     constexpr int Q = row_q<N>();
-    const int rows = h->ky * h->kz;
+    const int rows = g.kyl * h->kz;
+    const int64_t Ktl = (int64_t)g.kyl * h->kz * h->kx;
     const int nt = fft_threads_per_pencil(N) * Q;
     const size_t smem = fft_r2(N) == 1 ? 0 : (size_t)Q * (N + N / fft_r1(N)) * sizeof(float2);
-    const int nlist = (int)h->n_rows_ne;
+    const int nlist = g.nrows;
+    if (nlist == 0) return;
     dim3 grid((nlist + Q - 1) / Q, 5 * nrhs);
     if (packed) {
         prep(k_row_fwd<N, Q, true>, smem);
-        SVH_LAUNCH((k_row_fwd<N, Q, true>), grid, nt, smem, s, in, X1, h->d_rowinfo, h->rowW, h->d_rowlist, nlist,
-                   h->d_tw[0], h->kx, rows, h->K, h->Kt);
+        SVH_LAUNCH((k_row_fwd<N, Q, true>), grid, nt, smem, s, in, X1, h->d_rowinfo, h->rowW, g.rowlist, nlist,
+                   h->d_tw[0], h->kx, rows, h->K, Ktl, h->ky, g.kyl, g.y0);
     } else {
         prep(k_row_fwd<N, Q, false>, smem);
-        SVH_LAUNCH((k_row_fwd<N, Q, false>), grid, nt, smem, s, in, X1, h->d_rowinfo, h->rowW, h->d_rowlist, nlist,
-                   h->d_tw[0], h->kx, rows, h->K, h->Kt);
+        SVH_LAUNCH((k_row_fwd<N, Q, false>), grid, nt, smem, s, in, X1, h->d_rowinfo, h->rowW, g.rowlist, nlist,
+                   h->d_tw[0], h->kx, rows, h->K, Ktl, h->ky, g.kyl, g.y0);
     }
 }
 
 template <int N, int DIR>
-void run_pass_y(svh_handle* h, const float2* in, float2* out, int Lin, int Lout, int nrhs, cudaStream_t s) {
+void run_pass_y(svh_handle* h, const Geom& g, const float2* in, float2* out, int Lin, int Lout, int nrhs,
+                cudaStream_t s) {
+    const int nx = g.nx;
     constexpr int Q = col_q<N>();
     // D (DIR = +1) runs the persistent cp.async-pipelined kernel; B the one-tile-per-CTA
     // kernel (measured faster for the zero-padded forward direction).  SVH_NO_PIPE /
@@ -1137,11 +1166,11 @@ void run_pass_y(svh_handle* h, const float2* in, float2* out, int Lin, int Lout,
         auto launch = [&](auto Qc) -> bool {
             constexpr int QQ = decltype(Qc)::value;
             using P = YTma<N, DIR, 2, QQ>;
-            if (h->nx % QQ != 0 ||
-                !encode_tmap_c64_3d(&tmap, x2, (uint64_t)h->nx, (uint64_t)h->ny, (uint64_t)5 * nrhs * h->kz,
-                                    (uint64_t)h->nx, (uint64_t)h->nx * h->ny, QQ, P::BOX))
+            if (nx % QQ != 0 ||
+                !encode_tmap_c64_3d(&tmap, x2, (uint64_t)nx, (uint64_t)h->ny, (uint64_t)5 * nrhs * h->kz,
+                                    (uint64_t)nx, (uint64_t)nx * h->ny, QQ, P::BOX))
                 return false;
-            const int tiles_x = h->nx / QQ;
+            const int tiles_x = nx / QQ;
             const int ntiles = tiles_x * h->nzp * 5 * nrhs;
             int dev = 0, nsm = 148, occ = 1;
             cudaGetDevice(&dev);
@@ -1149,7 +1178,7 @@ void run_pass_y(svh_handle* h, const float2* in, float2* out, int Lin, int Lout,
             prep(k_ytma<N, DIR, 2, QQ>, P::smem);
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ytma<N, DIR, 2, QQ>, P::NT, P::smem);
             SVH_LAUNCH((k_ytma<N, DIR, 2, QQ>), std::min(ntiles, nsm * std::max(occ, 1)), P::NT, P::smem, s, in,
-                       out, tmap, h->d_tw[1], h->nx, h->kz, Lin, Lout, ntiles, tiles_x, h->d_planes, h->nzp,
+                       out, tmap, h->d_tw[1], nx, h->kz, Lin, Lout, ntiles, tiles_x, h->d_planes, h->nzp,
                        h->d_rowmask, h->rowMW);
             return true;
         };
@@ -1158,25 +1187,25 @@ void run_pass_y(svh_handle* h, const float2* in, float2* out, int Lin, int Lout,
             return;
     }
     if constexpr (N >= 128 && N <= 1024) {
-        if (((DIR < 0 && (ystage & 1)) || (DIR > 0 && (ystage & 2))) && h->nx % 8 == 0) {
+        if (((DIR < 0 && (ystage & 1)) || (DIR > 0 && (ystage & 2))) && nx % 8 == 0) {
             constexpr int QS = 8, SS = DIR < 0 ? 3 : 2;
             using P = YStage<N, QS, DIR, SS>;
-            const int tiles_x = h->nx / QS;
+            const int tiles_x = nx / QS;
             const int ntiles = tiles_x * h->nzp * 5 * nrhs;
             int dev = 0, nsm = 148;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
             prep(k_ystage<N, QS, DIR, SS>, P::smem);
             SVH_LAUNCH((k_ystage<N, QS, DIR, SS>), std::min(ntiles, nsm), P::NT, P::smem, s, in, out, h->d_tw[1],
-                       h->nx, h->kz, Lin, Lout, ntiles, tiles_x, h->d_planes, h->nzp, h->d_rowmask, h->rowMW);
+                       nx, h->kz, Lin, Lout, ntiles, tiles_x, h->d_planes, h->nzp, h->d_rowmask, h->rowMW);
             return;
         }
     }
     if constexpr (fft_r2(N) > 1 && Q >= 4 && colpipe_smem<N, 8, DIR>() <= 220 * 1024) {
         const bool want = use_pipe && (DIR > 0 || pipe_fwd);
-        if (want && h->nx % 8 == 0) {
+        if (want && nx % 8 == 0) {
             constexpr int QP = 8;
-            const int tiles_x = h->nx / QP;
+            const int tiles_x = nx / QP;
             const int ntiles = tiles_x * h->nzp * 5 * nrhs;
             const size_t smem = colpipe_smem<N, QP, DIR>();
             const int nt = fft_threads_per_pencil(N) * QP;
@@ -1187,21 +1216,21 @@ void run_pass_y(svh_handle* h, const float2* in, float2* out, int Lin, int Lout,
             per_sm = std::min(per_sm, std::max(1, 1024 / nt));
             const int grid = std::min(ntiles, nsm * per_sm);
             prep(k_col_pipe<N, QP, DIR>, smem);
-            SVH_LAUNCH((k_col_pipe<N, QP, DIR>), grid, nt, smem, s, in, out, h->d_tw[1], h->nx, h->kz, Lin, Lout,
+            SVH_LAUNCH((k_col_pipe<N, QP, DIR>), grid, nt, smem, s, in, out, h->d_tw[1], nx, h->kz, Lin, Lout,
                        ntiles, tiles_x, h->d_planes, h->nzp, h->d_rowmask, h->rowMW);
             return;
         }
     }
     const int nt = fft_threads_per_pencil(N) * Q;
     const size_t smem = fft_r2(N) == 1 ? 0 : (size_t)em_size<N, Q>() * sizeof(float2);
-    dim3 grid((h->nx + Q - 1) / Q, h->nzp, 5 * nrhs);
+    dim3 grid((nx + Q - 1) / Q, h->nzp, 5 * nrhs);
     prep(k_col<N, Q, DIR>, smem);
-    SVH_LAUNCH((k_col<N, Q, DIR>), grid, nt, smem, s, in, out, h->d_tw[1], h->nx, h->kz, Lin, Lout, h->d_planes,
+    SVH_LAUNCH((k_col<N, Q, DIR>), grid, nt, smem, s, in, out, h->d_tw[1], nx, h->kz, Lin, Lout, h->d_planes,
                h->d_rowmask, h->rowMW);
 }
 
 template <int N>
-void run_pass_c(svh_handle* h, float2* X2, int nrhs, cudaStream_t s) {
+void run_pass_c(svh_handle* h, const Geom& g, float2* X2, int nrhs, cudaStream_t s) {
     SpecView sv{};
     sv.spec = h->use_tucker ? nullptr : h->d_spec;
     sv.hx = h->hx;
@@ -1219,10 +1248,10 @@ void run_pass_c(svh_handle* h, float2* X2, int nrhs, cudaStream_t s) {
     if constexpr (N >= 2 && N <= 32) {
         if (zmac) {
             const size_t smem = zmac_smem<N>();
-            dim3 grid((h->nx + 31) / 32, h->ny);
+            dim3 grid((g.nx + 31) / 32, h->ny);
             prep(k_zmac<N>, smem);
             SVH_LAUNCH((k_zmac<N>), grid, 160, smem, s, X2, sv, h->nx, h->ny, h->kz, h->gscale, nrhs,
-                       (uint64_t)h->planemask);
+                       (uint64_t)h->planemask, g.nx, g.kx0);
             return;
         }
     }
@@ -1233,12 +1262,12 @@ void run_pass_c(svh_handle* h, float2* X2, int nrhs, cudaStream_t s) {
             constexpr int Q = decltype(Qc)::value;
             constexpr bool A = decltype(Ac)::value;
             const size_t smem = freq_small_smem<N, Q, A>();
-            dim3 grid((h->nx + Q - 1) / Q, h->ny);
+            dim3 grid((g.nx + Q - 1) / Q, h->ny);
             prep(k_freq_small<N, Q, A>, smem);
             SVH_LAUNCH((k_freq_small<N, Q, A>), grid, 5 * Q, smem, s, X2, sv, h->nx, h->ny, h->kz, h->gscale,
-                       nrhs, (uint64_t)h->planemask);
+                       nrhs, (uint64_t)h->planemask, g.nx, g.kx0);
         };
-        const bool async_ok = casync && h->nx % 32 == 0;
+        const bool async_ok = casync && g.nx % 32 == 0;
         if (N >= 64 || cq == 16) {
             if (async_ok) launch(std::integral_constant<int, 16>{}, std::true_type{});
             else launch(std::integral_constant<int, 16>{}, std::false_type{});
@@ -1252,18 +1281,20 @@ void run_pass_c(svh_handle* h, float2* X2, int nrhs, cudaStream_t s) {
         while (Q > 1 && (size_t)N * (5 * Q + 1) * sizeof(float2) > 160 * 1024) Q >>= 1;
         const int nt = std::max(32, tpp * 5 * Q);
         const size_t smem = (size_t)N * (5 * Q + 1) * sizeof(float2);
-        dim3 grid((h->nx + Q - 1) / Q, h->ny, nrhs);
+        dim3 grid((g.nx + Q - 1) / Q, h->ny, nrhs);
         prep(k_freq_big<N>, smem);
         SVH_LAUNCH((k_freq_big<N>), grid, nt, smem, s, X2, sv, h->d_tw[2], h->nx, h->ny, h->kz, Q, h->gscale,
-                   h->d_planeok);
+                   h->d_planeok, g.nx, g.kx0);
     }
 }
 
 template <int N>
-void run_pass_e(svh_handle* h, const float2* X1, const float2* in, float2* out, bool packed, bool green_only,
+void run_pass_e(svh_handle* h, const Geom& g, const float2* X1, const float2* in, float2* out, bool packed,
+                bool green_only,
                 int nrhs, cudaStream_t s) {
     constexpr int Q = row_q<N>();
-    const int rows = h->ky * h->kz;
+    const int rows = g.kyl * h->kz;
+    const int64_t Ktl = (int64_t)g.kyl * h->kz * h->kx;
     const int nt = fft_threads_per_pencil(N) * Q;
     const size_t smem = fft_r2(N) == 1 ? 0 : (size_t)Q * (N + N / fft_r1(N)) * sizeof(float2);
     const int nzl = (int)h->mats.size() + 1;
@@ -1274,13 +1305,13 @@ void run_pass_e(svh_handle* h, const float2* X1, const float2* in, float2* out, 
     if (packed) {
         prep(k_row_inv<N, Q, true>, smem);
         SVH_LAUNCH((k_row_inv<N, Q, true>), grid, nt, smem, s, X1, out, in, h->d_rowinfo, h->rowW, rl, nlist,
-                   h->d_rowmask, h->rowMW, h->ky, h->d_matp, h->d_zloc, nzl, h->d_tw[0], h->kx, rows, h->K, h->Kt,
-                   (int)green_only);
+                   h->d_rowmask, h->rowMW, h->ky, h->d_matp, h->d_zloc, nzl, h->d_tw[0], h->kx, rows, h->K, Ktl,
+                   (int)green_only, g.kyl, g.y0);
     } else {
         prep(k_row_inv<N, Q, false>, smem);
         SVH_LAUNCH((k_row_inv<N, Q, false>), grid, nt, smem, s, X1, out, in, h->d_rowinfo, h->rowW, rl, nlist,
-                   h->d_rowmask, h->rowMW, h->ky, h->d_matp, h->d_zloc, nzl, h->d_tw[0], h->kx, rows, h->K, h->Kt,
-                   (int)green_only);
+                   h->d_rowmask, h->rowMW, h->ky, h->d_matp, h->d_zloc, nzl, h->d_tw[0], h->kx, rows, h->K, Ktl,
+                   (int)green_only, g.kyl, g.y0);
     }
 }
 
@@ -1352,20 +1383,21 @@ static void matvec_batch(svh_handle* h, const float2* in, float2* out, float2* X
             SVH_CUDA(cudaEventRecord(h->prof.back().b, s));
         }
     };
+    const Geom g = whole_grid(h);
     tick(0, true);
-    SVH_DISPATCH_N(h->nx, run_pass_a<NN>(h, in, X1, packed, nr, s));
+    SVH_DISPATCH_N(h->nx, run_pass_a<NN>(h, g, in, X1, packed, nr, s));
     tick(0, false);
     tick(1, true);
-    SVH_DISPATCH_N(h->ny, (run_pass_y<NN, -1>(h, X1, X2, h->ky, h->ny, nr, s)));
+    SVH_DISPATCH_N(h->ny, (run_pass_y<NN, -1>(h, g, X1, X2, h->ky, h->ny, nr, s)));
     tick(1, false);
     tick(2, true);
-    SVH_DISPATCH_N(h->nz, run_pass_c<NN>(h, X2, nr, s));
+    SVH_DISPATCH_N(h->nz, run_pass_c<NN>(h, g, X2, nr, s));
     tick(2, false);
     tick(3, true);
-    SVH_DISPATCH_N(h->ny, (run_pass_y<NN, +1>(h, X2, X1, h->ny, h->ky, nr, s)));
+    SVH_DISPATCH_N(h->ny, (run_pass_y<NN, +1>(h, g, X2, X1, h->ny, h->ky, nr, s)));
     tick(3, false);
     tick(4, true);
-    SVH_DISPATCH_N(h->nx, run_pass_e<NN>(h, X1, in, out, packed, green_only, nr, s));
+    SVH_DISPATCH_N(h->nx, run_pass_e<NN>(h, g, X1, in, out, packed, green_only, nr, s));
     tick(4, false);
 }
 
@@ -1406,6 +1438,118 @@ void matvec(svh_handle* h, const float2* I, float2* CC, int nrhs, bool green_onl
         }
         for (int k = 0; k < ns; ++k) SVH_CUDA(cudaStreamWaitEvent(s, h->stream_events[k], 0));
     }
+}
+
+// ---------------------------------------------------------------------------
+// Slab-decomposed matvec: P ranks; rank r holds the y-slab
+// y in [r Kyl, (r+1) Kyl) of every plane (grid layout), Kyl = Ky/P.
+//   forward : pass A on the slab's rows, pack X1 by destination kx-slab        -> send
+//   (all-to-all #1: every rank now has kx in [r Nxl, (r+1) Nxl) for all y, Nxl = Nx/P)
+//   middle  : unpack, passes B, C, D on the kx-slab (global kx offset for the kernels),
+//             pack by destination y-slab                                         -> send
+//   (all-to-all #2)
+//   backward: unpack, pass E on the slab's rows (+ local term)                   -> CC
+// All-to-all buffers: [peer p][5 nrhs Kz][Kyl][Nxl] complex64 (equal chunks).  Only the
+// minimum volume is exchanged: the x-FFT'd current, 2 Kt points/comp per direction.
+namespace {
+// element (p, b, y, k) of the buffer [p][b][y][k] <-> array element b*SB + y*SY + p*SP + k
+__global__ void k_slab_copy(float2* __restrict__ buf, float2* __restrict__ arr, int P, int64_t Bt, int Kyl, int Nxl,
+                            int64_t SB, int64_t SY, int64_t SP, int to_array) {
+    const int64_t total = (int64_t)P * Bt * Kyl * Nxl;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int k = (int)(i % Nxl);
+        int64_t r = i / Nxl;
+        const int y = (int)(r % Kyl);
+        r /= Kyl;
+        const int64_t b = r % Bt;
+        const int p = (int)(r / Bt);
+        const int64_t a = b * SB + (int64_t)y * SY + (int64_t)p * SP + k;
+        if (to_array)
+            arr[a] = buf[i];
+        else
+            buf[i] = arr[a];
+    }
+}
+
+void slab_copy(float2* buf, float2* arr, int P, int64_t Bt, int Kyl, int Nxl, int64_t SB, int64_t SY, int64_t SP,
+               bool to_array, cudaStream_t s) {
+    const int64_t total = (int64_t)P * Bt * Kyl * Nxl;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)nsm * 8);
+    SVH_LAUNCH(k_slab_copy, std::max(grid, 1), 256, 0, s, buf, arr, P, Bt, Kyl, Nxl, SB, SY, SP, (int)to_array);
+}
+
+void check_slab(const svh_handle* h, int rank, int P) {
+    SVH_CHECK(P >= 1 && rank >= 0 && rank < P, SVH_EINVAL, "bad slab rank / count");
+    SVH_CHECK(h->ky % P == 0 && h->nx % P == 0, SVH_EINVAL, "slab decomposition needs Ky % P == 0 and Nx % P == 0");
+}
+
+const svh_handle::SlabRows& slab_rows(svh_handle* h, int rank, int P) {
+    for (auto& sr : h->slab_rows)
+        if (sr.P == P && sr.rank == rank) return sr;
+    const int Kyl = h->ky / P, y0 = rank * Kyl;
+    std::vector<int32_t> rl;
+    for (int32_t row : h->h_rowlist) {
+        const int y = row % h->ky;
+        if (y >= y0 && y < y0 + Kyl) rl.push_back(row);
+    }
+    svh_handle::SlabRows sr{P, rank, nullptr, (int)rl.size()};
+    if (!rl.empty()) {
+        SVH_CUDA(cudaMalloc(&sr.d, rl.size() * sizeof(int32_t)));
+        SVH_CUDA(cudaMemcpy(sr.d, rl.data(), rl.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+    h->slab_rows.push_back(sr);
+    return h->slab_rows.back();
+}
+}  // namespace
+
+void slab_sizes(const svh_handle* h, int P, int64_t* out4) {
+    check_slab(h, 0, P);
+    const int64_t Kyl = h->ky / P, Nxl = h->nx / P;
+    out4[0] = Kyl;
+    out4[1] = Nxl;
+    out4[2] = 5 * (int64_t)h->kz * Kyl * Nxl;       // complex elements per peer chunk per RHS
+    out4[3] = out4[2] * P;                          // send / recv buffer elements per RHS
+}
+
+void slab_forward(svh_handle* h, int rank, int P, const float2* I, float2* send, int nrhs, cudaStream_t s) {
+    check_slab(h, rank, P);
+    ensure_workspace(h, nrhs);
+    const int Kyl = h->ky / P, Nxl = h->nx / P;
+    const auto& sr = slab_rows(h, rank, P);
+    const Geom g{h->nx, 0, Kyl, rank * Kyl, sr.d, sr.n};
+    SVH_DISPATCH_N(h->nx, run_pass_a<NN>(h, g, I, h->X1, false, nrhs, s));
+    const int64_t Bt = 5LL * nrhs * h->kz;
+    slab_copy(send, h->X1, P, Bt, Kyl, Nxl, (int64_t)Kyl * h->nx, h->nx, Nxl, false, s);
+}
+
+void slab_middle(svh_handle* h, int rank, int P, const float2* recv, float2* send, int nrhs, cudaStream_t s) {
+    check_slab(h, rank, P);
+    ensure_workspace(h, nrhs);
+    const int Kyl = h->ky / P, Nxl = h->nx / P;
+    const int64_t Bt = 5LL * nrhs * h->kz;
+    // [s][b][y][k] -> X1 [b][s Kyl + y][k]
+    slab_copy(const_cast<float2*>(recv), h->X1, P, Bt, Kyl, Nxl, (int64_t)h->ky * Nxl, Nxl, (int64_t)Kyl * Nxl, true,
+              s);
+    const Geom g{Nxl, rank * Nxl, h->ky, 0, nullptr, 0};
+    SVH_DISPATCH_N(h->ny, (run_pass_y<NN, -1>(h, g, h->X1, h->X2, h->ky, h->ny, nrhs, s)));
+    SVH_DISPATCH_N(h->nz, run_pass_c<NN>(h, g, h->X2, nrhs, s));
+    SVH_DISPATCH_N(h->ny, (run_pass_y<NN, +1>(h, g, h->X2, h->X1, h->ny, h->ky, nrhs, s)));
+    slab_copy(send, h->X1, P, Bt, Kyl, Nxl, (int64_t)h->ky * Nxl, Nxl, (int64_t)Kyl * Nxl, false, s);
+}
+
+void slab_backward(svh_handle* h, int rank, int P, const float2* recv, const float2* I, float2* CC, int nrhs,
+                   bool green_only, cudaStream_t s) {
+    check_slab(h, rank, P);
+    ensure_workspace(h, nrhs);
+    const int Kyl = h->ky / P, Nxl = h->nx / P;
+    const int64_t Bt = 5LL * nrhs * h->kz;
+    // [s][b][y][k] -> X1 [b][y][s Nxl + k]
+    slab_copy(const_cast<float2*>(recv), h->X1, P, Bt, Kyl, Nxl, (int64_t)Kyl * h->nx, h->nx, Nxl, true, s);
+    const Geom g{h->nx, 0, Kyl, rank * Kyl, nullptr, 0};
+    SVH_DISPATCH_N(h->nx, run_pass_e<NN>(h, g, h->X1, I, CC, false, green_only, nrhs, s));
 }
 
 }  // namespace svh

@@ -1,10 +1,21 @@
-"""Multi-GPU port sharding: one RHS per port, ports p = rank (mod world).
+"""Multi-GPU paths of SURVEY 8(e).
+
+(1) Port sharding: one RHS per port, ports p = rank (mod world).
 
 Each rank owns a replicated libsvh handle on its GPU, solves its ports through
 ``svh_solve_columns`` (C-ABI) and the admittance columns are all-gathered over
 the process group -- the only collective of the solve.  Y -> Z -> L/R is done
 by ``svh_y_to_zl`` in libsvh.  The partition / gather / assembly logic is
 independent of the solver so it can be exercised with gloo on CPU.
+
+(2) Slab-decomposed matvec (``SlabMatvec``): for a grid too large for one GPU or
+strong scaling, rank r holds the y-slab r*Kyl <= y < (r+1)*Kyl; one product is
+svh_slab_forward -> all-to-all -> svh_slab_middle -> all-to-all ->
+svh_slab_backward (C-ABI; every FFT pass runs in libsvh).  The all-to-all moves
+the x-transformed current once per direction (2 Kt points per component in
+total, the minimum for a 3-D FFT transpose).  ``virtual_ranks`` runs all P slabs
+in one process on one GPU with the exchange done by device copies (the path the
+single-GPU tests exercise; NCCL cannot place two ranks on one GPU).
 """
 from __future__ import annotations
 
@@ -67,3 +78,75 @@ def solve_sharded(handle, ports, group=None):
     Y = gather_columns(cols, sel, P, group)
     Z, L, R = svh.y_to_zl(Y, handle.freq)
     return dict(Y=Y, Z=Z, L=L, R=R, stats=stats, code=code, ports_local=sel)
+
+
+def slab_exchange(send, recv, P, group=None):
+    """The all-to-all of the slab matvec: chunk p of ``send`` goes to rank p, chunk s of
+    ``recv`` comes from rank s (equal chunks; NCCL over NVLink on GPUs, gloo on CPU)."""
+    import torch.distributed as dist
+    assert send.numel() % P == 0 and recv.numel() == send.numel()
+    dist.all_to_all_single(recv, send, group=group)
+
+
+def virtual_exchange(sends, recvs):
+    """In-process all-to-all between P virtual ranks: recv[r] chunk s = send[s] chunk r."""
+    P = len(sends)
+    for r in range(P):
+        rc = recvs[r].view(P, -1)
+        for s_ in range(P):
+            rc[s_].copy_(sends[s_].view(P, -1)[r])
+
+
+class SlabMatvec:
+    """Slab-decomposed Eq. 9 product on lattice-layout slabs [nrhs][5][Kz][Kyl][Kx].
+
+    ``rank``/``P`` with a process group: one slab per process (torch.distributed).
+    ``virtual_ranks`` (P > 1, no group): all slabs of one process, exchange by copies.
+    """
+
+    def __init__(self, handle, P, rank=0, group=None):
+        self.h, self.P, self.rank, self.group = handle, int(P), int(rank), group
+        self.Kyl, self.Nxl, self.chunk, self.per_rhs = handle.slab_sizes(self.P)
+
+    def _buffers(self, nrhs, device):
+        import torch
+        n = nrhs * self.per_rhs
+        return (torch.empty(n, dtype=torch.complex64, device=device),
+                torch.empty(n, dtype=torch.complex64, device=device))
+
+    def matvec(self, I_slab, green_only=False):
+        """This rank's slab of Z.I (collective over the group)."""
+        import torch
+        I_slab = I_slab.contiguous()
+        nrhs = I_slab.shape[0]
+        send, recv = self._buffers(nrhs, I_slab.device)
+        out = torch.empty_like(I_slab)
+        self.h.slab_forward(self.rank, self.P, I_slab, send)
+        torch.cuda.current_stream().synchronize()
+        slab_exchange(send, recv, self.P, self.group)
+        self.h.slab_middle(self.rank, self.P, recv, send, nrhs)
+        torch.cuda.current_stream().synchronize()
+        slab_exchange(send, recv, self.P, self.group)
+        self.h.slab_backward(self.rank, self.P, recv, I_slab, out, green_only)
+        return out
+
+    def matvec_virtual(self, I_grid, green_only=False):
+        """All P slabs in this process: I_grid [nrhs][5][Kz][Ky][Kx] -> Z.I (same layout)."""
+        import torch
+        P, Kyl = self.P, self.Kyl
+        nrhs = I_grid.shape[0]
+        slabs = [I_grid[:, :, :, r * Kyl:(r + 1) * Kyl, :].contiguous() for r in range(P)]
+        bufs = [self._buffers(nrhs, I_grid.device) for _ in range(P)]
+        sends, recvs = [b[0] for b in bufs], [b[1] for b in bufs]
+        for r in range(P):
+            self.h.slab_forward(r, P, slabs[r], sends[r])
+        virtual_exchange(sends, recvs)
+        for r in range(P):
+            self.h.slab_middle(r, P, recvs[r], sends[r], nrhs)
+        virtual_exchange(sends, recvs)
+        out = torch.empty_like(I_grid)
+        for r in range(P):
+            o = torch.empty_like(slabs[r])
+            self.h.slab_backward(r, P, recvs[r], slabs[r], o, green_only)
+            out[:, :, :, r * Kyl:(r + 1) * Kyl, :] = o
+        return out

@@ -82,6 +82,10 @@ def lib():
         L.svh_unknowns.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]
         L.svh_embedding.argtypes = [vp, ctypes.POINTER(i32)]
         L.svh_plan_info.argtypes = [vp, ctypes.POINTER(i64)]
+        L.svh_slab_sizes.argtypes = [vp, i32, ctypes.POINTER(i64)]
+        L.svh_slab_forward.argtypes = [vp, i32, i32, vp, vp, i32, vp]
+        L.svh_slab_middle.argtypes = [vp, i32, i32, vp, vp, i32, vp]
+        L.svh_slab_backward.argtypes = [vp, i32, i32, vp, vp, vp, i32, i32, vp]
         L.svh_matvec.argtypes = [vp, vp, vp, i32, i32, vp]
         L.svh_matvec_grid.argtypes = [vp, vp, vp, i32, i32, vp]
         L.svh_apply_system.argtypes = [vp, vp, vp, i32, vp]
@@ -98,7 +102,8 @@ def lib():
         L.svh_destroy.restype = None
         L.svh_last_error.restype = ctypes.c_char_p
         L.svh_launch_count.restype = i64
-        for name in ("svh_setup", "svh_set_frequency", "svh_unknowns", "svh_embedding", "svh_plan_info", "svh_matvec",
+        for name in ("svh_slab_sizes", "svh_slab_forward", "svh_slab_middle", "svh_slab_backward",
+                     "svh_setup", "svh_set_frequency", "svh_unknowns", "svh_embedding", "svh_plan_info", "svh_matvec",
                      "svh_matvec_grid", "svh_apply_system", "svh_solve", "svh_solve_columns", "svh_get_kernels",
                      "svh_get_stats", "svh_profile_enable", "svh_profile_read", "svh_y_to_zl"):
             getattr(L, name).restype = ctypes.c_int
@@ -107,6 +112,7 @@ def lib():
 
 
 EXPORTED = ("svh_default_opts", "svh_setup", "svh_set_frequency", "svh_unknowns", "svh_embedding", "svh_plan_info",
+            "svh_slab_sizes", "svh_slab_forward", "svh_slab_middle", "svh_slab_backward",
             "svh_matvec",
             "svh_matvec_grid", "svh_apply_system", "svh_solve", "svh_solve_columns", "svh_get_kernels",
             "svh_get_stats", "svh_profile_enable", "svh_profile_read", "svh_y_to_zl", "svh_destroy",
@@ -244,6 +250,26 @@ class Handle:
         _check(lib().svh_matvec_grid(self._h, ctypes.c_void_p(I.data_ptr()), ctypes.c_void_p(o.data_ptr()),
                                      I.shape[0], int(green_only), _stream_ptr(stream)))
         return o
+
+    # -- slab-decomposed matvec; orchestration in parallel.SlabMatvec
+    def slab_sizes(self, P):
+        """(Kyl, Nxl, elements per peer chunk per RHS, send/recv elements per RHS)."""
+        out = (ctypes.c_int64 * 4)()
+        _check(lib().svh_slab_sizes(self._h, int(P), out))
+        return tuple(int(v) for v in out)
+
+    def slab_forward(self, rank, P, I_slab, send, stream=None):
+        _check(lib().svh_slab_forward(self._h, int(rank), int(P), ctypes.c_void_p(I_slab.data_ptr()),
+                                      ctypes.c_void_p(send.data_ptr()), I_slab.shape[0], _stream_ptr(stream)))
+
+    def slab_middle(self, rank, P, recv, send, nrhs, stream=None):
+        _check(lib().svh_slab_middle(self._h, int(rank), int(P), ctypes.c_void_p(recv.data_ptr()),
+                                     ctypes.c_void_p(send.data_ptr()), int(nrhs), _stream_ptr(stream)))
+
+    def slab_backward(self, rank, P, recv, I_slab, out, green_only=False, stream=None):
+        _check(lib().svh_slab_backward(self._h, int(rank), int(P), ctypes.c_void_p(recv.data_ptr()),
+                                       ctypes.c_void_p(I_slab.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                       I_slab.shape[0], int(green_only), _stream_ptr(stream)))
 
     def apply_system(self, x, out=None, stream=None):
         import torch

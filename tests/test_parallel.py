@@ -67,3 +67,52 @@ def test_y_to_zl_host():
     assert np.allclose(L, Z.imag / (2 * np.pi * f)) and np.allclose(R, Z.real)
     with pytest.raises(svh.SvhError):
         svh.y_to_zl(np.zeros((2, 2)), f)
+
+
+def _slab_worker(rank, world, port, q):
+    """Each rank fills its send buffer with (src rank, dest chunk, index) tags; after the
+    all-to-all chunk s of recv must hold rank s's chunk addressed to this rank."""
+    import torch
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    chunk = 6
+    send = torch.zeros(world * chunk, dtype=torch.complex64)
+    for p in range(world):
+        for i in range(chunk):
+            send[p * chunk + i] = complex(100 * rank + p, i)
+    recv = torch.empty_like(send)
+    parallel.slab_exchange(send, recv, world)
+    ok = all(recv[s * chunk + i] == complex(100 * s + rank, i) for s in range(world) for i in range(chunk))
+    q.put((rank, bool(ok)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_slab_exchange_gloo(world):
+    """SURVEY 8(e)(2) slab transpose: the NCCL/gloo all-to-all routes chunk p of rank r's
+    send buffer to chunk r of rank p's recv buffer, as svh_slab_* lay them out."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_slab_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res), res
+
+
+def test_virtual_exchange_matches_all_to_all():
+    """The single-process exchange used by the virtual-slab GPU tests is the same routing."""
+    import torch
+    P, chunk = 4, 3
+    sends = [torch.tensor([complex(100 * r + p, i) for p in range(P) for i in range(chunk)], dtype=torch.complex64)
+             for r in range(P)]
+    recvs = [torch.empty_like(s) for s in sends]
+    parallel.virtual_exchange(sends, recvs)
+    for r in range(P):
+        for s in range(P):
+            for i in range(chunk):
+                assert recvs[r][s * chunk + i] == complex(100 * s + r, i)
