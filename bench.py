@@ -270,6 +270,53 @@ def time_to_L(name, device, world, rank):
             "rre": st.get("final_rre"), "converged": st.get("converged")}
 
 
+def run_slab(args, case, R, world, rank, local):
+    """--slab: the slab-decomposed matvec, strong scaling (total grid fixed; value = 5 Kt R / t)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2105_08627_b200 import svh
+    from paper_2105_08627_b200.parallel import SlabMatvec
+    h = svh.setup_case(case, device=local)
+    kz, ky, kx = h.shape
+    Kt = kx * ky * kz
+    P = world if world > 1 else args.slab
+    sm = SlabMatvec(h, P, rank=rank if world > 1 else 0)
+    g = torch.Generator(device="cuda").manual_seed(100)
+    occ = torch.from_numpy(case["mat_id"] != 0).cuda()
+    I = (torch.randn((R, 5, kz, ky, kx), dtype=torch.complex64, device="cuda", generator=g) * occ)
+    if world > 1:
+        I = I[:, :, :, rank * sm.Kyl:(rank + 1) * sm.Kyl, :].contiguous()
+    step = (lambda: sm.matvec(I)) if world > 1 else (lambda: sm.matvec_virtual(I))
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    line = {"metric": METRIC, "value": 5.0 * Kt * R / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "c64", "data": "synthetic",
+            "config": {"workload": case["name"], "grid": [kx, ky, kz], "nrhs": R, "slabs": P,
+                       "mode": "NCCL all_to_all" if world > 1 else "virtual slabs on one GPU (exchange by copies)",
+                       "layout": "grid [nrhs][5][Kz][Ky/P][Kx] per slab"},
+            "clocks": clk.summary()}
+    h.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -284,6 +331,9 @@ def main():
     ap.add_argument("--no-solve", action="store_true", help="skip the time-to-L measurement")
     ap.add_argument("--no-cufft", action="store_true", help="skip the cuFFT reference-pipeline timing")
     ap.add_argument("--solve-workload", default="cfg2")
+    ap.add_argument("--slab", type=int, default=0,
+                    help="slab-decomposed matvec (SURVEY 8(e)(2), strong scaling): under torchrun one y-slab per "
+                         "rank with NCCL all-to-alls; with --gpus 1, P virtual slabs on one GPU (exchange by copies)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -302,6 +352,8 @@ def main():
     case, R = workload(args.workload)
     if args.nrhs:
         R = args.nrhs
+    if args.slab:
+        return run_slab(args, case, R, world, rank, local)
     t0 = time.perf_counter()
     h = svh.setup_case(case, tucker_tol=args.tucker, device=local)
     torch.cuda.synchronize()

@@ -949,21 +949,41 @@ __global__ void __launch_bounds__(160, 3)
     float2 nxt[NH];
 #pragma unroll
     for (int j = 0; j < NH; ++j) nxt[j] = ((lm >> j) & 1u) ? col[(int64_t)j * plane] : zero;
+    const float fold[7] = {g, g, g, -2.f * g, g, g, 4.f * g};
     if (sv.spec) {
-        for (int t = tid; t < N * Q; t += 5 * Q) {
-            const int k = t / Q, qq = t % Q;
-            float kv[7];
-            kernel_values(sv, min(kxg + kx0 + qq, Nx - 1), ky, k, Nx, Ny, N, kv);
+        // dense octant lookup, folded: warp c takes kz = c + 5 i, lane = kx (coalesced along
+        // the octant's x rows); all 7 x ceil(N/5) loads are independent and issued together
+        const int kx = min(kxg + kx0 + q, Nx - 1);
+        const int ox = kx <= (Nx >> 1) ? kx : Nx - kx;
+        const int oy = ky <= (Ny >> 1) ? ky : Ny - ky;
+        const float sx = kx <= (Nx >> 1) ? 1.f : -1.f, sy = ky <= (Ny >> 1) ? 1.f : -1.f;
+        const int64_t pl = (int64_t)sv.hx * sv.hy * sv.hz;
+        float kv[(N + 4) / 5][7];
 #pragma unroll
-            for (int m = 0; m < 7; ++m) KV[(m * N + k) * Q + qq] = kv[m];
+        for (int i = 0; i < (N + 4) / 5; ++i) {
+            const int k = c + 5 * i;
+            const int oz = (k < N ? (k <= (N >> 1) ? k : N - k) : 0);
+            const int64_t o = ((int64_t)oz * sv.hy + oy) * sv.hx + ox;
+#pragma unroll
+            for (int m = 0; m < 7; ++m) kv[i][m] = __ldg(&sv.spec[m * pl + o]);
+        }
+#pragma unroll
+        for (int i = 0; i < (N + 4) / 5; ++i) {
+            const int k = c + 5 * i;
+            if (k < N) {
+                const float sz = k <= (N >> 1) ? 1.f : -1.f;
+                const float sgn[7] = {1.f, sx, sy, sz, 1.f, 1.f, 1.f};
+#pragma unroll
+                for (int m = 0; m < 7; ++m) KV[(m * N + k) * Q + q] = kv[i][m] * sgn[m] * fold[m];
+            }
         }
     } else {
         tucker_tile<N, Q>(sv, kxg + kx0, ky, Nx, Ny, KV, reinterpret_cast<float*>(S));
-    }
-    __syncthreads();
-    for (int t = tid; t < 7 * N * Q; t += 5 * Q) {
-        const int m = t / (N * Q);
-        KV[t] *= m == 3 ? -2.f * g : (m == 6 ? 4.f * g : g);
+        __syncthreads();
+        for (int t = tid; t < 7 * N * Q; t += 5 * Q) {
+            const int m = t / (N * Q);
+            KV[t] *= m == 3 ? -2.f * g : (m == 6 ? 4.f * g : g);
+        }
     }
     // MAC role: warp w = c takes kz = w + 5 i; lane = pencil
     const int w = c;
