@@ -84,6 +84,12 @@ struct Solve {
     float2* c64_out = nullptr;
     double* d_red = nullptr;         // reduction scratch
     int inner_its = 0;
+    // PCG with device-side scalars, one CUDA graph per iteration (V-cycle included); the
+    // graph is rebuilt whenever the AMG hierarchy is (port set change)
+    cudaStream_t stream = nullptr;
+    cudaGraphExec_t pcg_graph = nullptr;
+    double* d_pcg = nullptr;         // [16]: rz, pq, rr, thr, alpha, beta, rz2, done (2 each)
+    double t_matvec = 0, t_precond = 0;
 };
 
 // ---------------------------------------------------------------------------
@@ -383,6 +389,24 @@ __global__ void k_xpby2(int64_t n, const double* __restrict__ z, const double* _
     p[2 * i + 1] = z[2 * i + 1] + beta[1] * p[2 * i + 1];
 }
 
+// PCG scalars on the device (pc = Solve::d_pcg): 0 rz, 2 pq, 4 rr, 6 thr, 8 alpha, 10 beta,
+// 12 rz2, 14 done -- two independent real systems (re / im parts)
+__global__ void k_pcg_alpha(double* pc) {
+    const int c = threadIdx.x;
+    if (c < 2) pc[8 + c] = (pc[14 + c] != 0 || pc[2 + c] == 0) ? 0.0 : pc[0 + c] / pc[2 + c];
+}
+__global__ void k_pcg_check(double* pc) {
+    const int c = threadIdx.x;
+    if (c < 2 && pc[4 + c] <= pc[6 + c]) pc[14 + c] = 1.0;
+}
+__global__ void k_pcg_beta(double* pc) {
+    const int c = threadIdx.x;
+    if (c < 2) {
+        pc[10 + c] = (pc[14 + c] != 0 || pc[0 + c] == 0) ? 0.0 : pc[12 + c] / pc[0 + c];
+        pc[0 + c] = pc[12 + c];
+    }
+}
+
 // ---- complex Krylov helpers (double2 vectors of length n)
 // out[i] += sum_e conj(V_i[e]) w[e], i < m ; grid (blocks, m)
 __global__ void k_cdots(int64_t n, const double2* __restrict__ V, int64_t ldv, const double2* __restrict__ w,
@@ -572,7 +596,12 @@ static void build_structure(svh_handle* h) {
     S->N = 5 * h->K + S->M;
 }
 
+static void drop_pcg_graph(Solve* S) {
+    if (S->pcg_graph) cudaGraphExecDestroy(S->pcg_graph);
+    S->pcg_graph = nullptr;
+}
 static void free_levels(Solve* S) {
+    drop_pcg_graph(S);
     for (auto& L : S->levels) {
         cudaFree(L.vb);
         cudaFree(L.vx);
@@ -608,6 +637,8 @@ void free_solve(svh_handle* h) {
     cudaFree(S->c64_in);
     cudaFree(S->c64_out);
     cudaFree(S->d_red);
+    cudaFree(S->d_pcg);
+    if (S->stream) cudaStreamDestroy(S->stream);
     delete S;
     h->solve = nullptr;
 }
@@ -862,6 +893,7 @@ static void ensure_work(svh_handle* h, int restart) {
     Solve* S = h->solve;
     const size_t need = (size_t)2 * std::max<int64_t>(S->nf, 1);
     if (S->wsize < need) {
+        drop_pcg_graph(S);
         for (auto& b : S->wbuf) cudaFree(b);
         for (auto& b : S->wbuf) SVH_CUDA(cudaMalloc(&b, need * sizeof(double) * 1));
         S->wsize = need;
@@ -923,7 +955,11 @@ static void vcycle(Solve* S, int l, const double* b, double* x, cudaStream_t s) 
     SVH_CUDA(cudaMemcpyAsync(x, L.x2, 2 * (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, s));
 }
 
-// PCG on S (level 0) for 2 real RHS: x = S^-1 b to relative tol
+// PCG on S (level 0) for 2 real RHS: x = S^-1 b to relative tol.  All scalars stay on the
+// device; one iteration (SpMV, 3 dot products, the scalar updates and the whole AMG cycle,
+// ~250 kernels) is a CUDA graph captured once per hierarchy and replayed, and the host
+// reads the convergence flags every kCheck iterations -- the solve is launch-latency
+// bound otherwise (P:166 AGMG-CG; reading G15).
 static int pcg2(svh_handle* h, const double* b, double* x, double tol, int maxit, cudaStream_t s) {
     Solve* S = h->solve;
     const CsrDev& A = S->levels[0];
@@ -932,48 +968,64 @@ static int pcg2(svh_handle* h, const double* b, double* x, double tol, int maxit
     double* z = S->wbuf[1];
     double* p = S->wbuf[2];
     double* q = S->wbuf[3];
-    double* red = S->d_red;
+    double* pc = S->d_pcg;
     auto dot = [&](const double* a, const double* bb, double* out2) {
-        SVH_CUDA(cudaMemsetAsync(red, 0, 2 * sizeof(double), s));
-        SVH_LAUNCH(k_dot2, 296, 256, 0, s, (int64_t)n, a, bb, red);
-        SVH_CUDA(cudaMemcpyAsync(out2, red, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
-        SVH_CUDA(cudaStreamSynchronize(s));
+        SVH_CUDA(cudaMemsetAsync(out2, 0, 2 * sizeof(double), s));
+        SVH_LAUNCH(k_dot2, 296, 256, 0, s, (int64_t)n, a, bb, out2);
     };
+    auto iteration = [&] {
+        SVH_LAUNCH(k_spmv2, nblk(n), 256, 0, s, n, A.rowptr, A.col, A.val, p, q);
+        dot(p, q, pc + 2);
+        SVH_LAUNCH(k_pcg_alpha, 1, 32, 0, s, pc);
+        SVH_LAUNCH(k_axpy2, nblk(n), 256, 0, s, (int64_t)n, pc + 8, +1, p, x);
+        SVH_LAUNCH(k_axpy2, nblk(n), 256, 0, s, (int64_t)n, pc + 8, -1, q, r);
+        dot(r, r, pc + 4);
+        SVH_LAUNCH(k_pcg_check, 1, 32, 0, s, pc);
+        vcycle(S, 0, r, z, s);
+        dot(r, z, pc + 12);
+        SVH_LAUNCH(k_pcg_beta, 1, 32, 0, s, pc);
+        SVH_LAUNCH(k_xpby2, nblk(n), 256, 0, s, (int64_t)n, z, pc + 10, p);
+    };
+    // b.b -> thresholds thr = tol^2 b.b; done if b = 0
+    dot(b, b, pc + 4);
     double bn[2];
-    dot(b, b, bn);
+    SVH_CUDA(cudaMemcpyAsync(bn, pc + 4, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    SVH_CUDA(cudaStreamSynchronize(s));
     SVH_LAUNCH(k_zero, nblk(2 * n), 256, 0, s, x, (int64_t)2 * n);
     if (bn[0] == 0 && bn[1] == 0) return 0;
+    const double init[16] = {0, 0, 0, 0, 0, 0, tol * tol * bn[0], tol * tol * bn[1],
+                             0, 0, 0, 0, 0, 0, bn[0] == 0 ? 1.0 : 0.0, bn[1] == 0 ? 1.0 : 0.0};
+    SVH_CUDA(cudaMemcpyAsync(pc, init, sizeof(init), cudaMemcpyHostToDevice, s));
     SVH_CUDA(cudaMemcpyAsync(r, b, 2 * n * sizeof(double), cudaMemcpyDeviceToDevice, s));
     vcycle(S, 0, r, z, s);
     SVH_CUDA(cudaMemcpyAsync(p, z, 2 * n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    double rz[2];
-    dot(r, z, rz);
-    double* dscal = red + 8;
-    int it = 0;
-    bool done[2] = {bn[0] == 0, bn[1] == 0};
-    for (it = 1; it <= maxit; ++it) {
-        SVH_LAUNCH(k_spmv2, nblk(n), 256, 0, s, n, A.rowptr, A.col, A.val, p, q);
-        double pq[2];
-        dot(p, q, pq);
-        double alpha[2] = {done[0] || pq[0] == 0 ? 0 : rz[0] / pq[0], done[1] || pq[1] == 0 ? 0 : rz[1] / pq[1]};
-        SVH_CUDA(cudaMemcpyAsync(dscal, alpha, 2 * sizeof(double), cudaMemcpyHostToDevice, s));
-        SVH_LAUNCH(k_axpy2, nblk(n), 256, 0, s, (int64_t)n, dscal, +1, p, x);
-        SVH_LAUNCH(k_axpy2, nblk(n), 256, 0, s, (int64_t)n, dscal, -1, q, r);
-        double rr[2];
-        dot(r, r, rr);
-        for (int c = 0; c < 2; ++c)
-            if (!done[c] && std::sqrt(rr[c]) <= tol * std::sqrt(bn[c])) done[c] = true;
-        if (done[0] && done[1]) break;
-        vcycle(S, 0, r, z, s);
-        double rz2[2];
-        dot(r, z, rz2);
-        double beta[2] = {done[0] || rz[0] == 0 ? 0 : rz2[0] / rz[0], done[1] || rz[1] == 0 ? 0 : rz2[1] / rz[1]};
-        rz[0] = rz2[0];
-        rz[1] = rz2[1];
-        SVH_CUDA(cudaMemcpyAsync(dscal, beta, 2 * sizeof(double), cudaMemcpyHostToDevice, s));
-        SVH_LAUNCH(k_xpby2, nblk(n), 256, 0, s, (int64_t)n, z, dscal, p);
+    dot(r, z, pc + 0);
+    static const bool use_graph = getenv("SVH_NO_PCG_GRAPH") == nullptr;
+    if (use_graph && !S->pcg_graph && s != nullptr) {
+        cudaGraph_t g = nullptr;
+        SVH_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        iteration();
+        SVH_CUDA(cudaStreamEndCapture(s, &g));
+        SVH_CUDA(cudaGraphInstantiate(&S->pcg_graph, g, 0));
+        cudaGraphDestroy(g);
     }
-    return std::min(it, maxit);
+    constexpr int kCheck = 8;
+    int it = 0;
+    double done[2];
+    while (it < maxit) {
+        const int nb = std::min(kCheck, maxit - it);
+        for (int k = 0; k < nb; ++k) {
+            if (S->pcg_graph)
+                SVH_CUDA(cudaGraphLaunch(S->pcg_graph, s));
+            else
+                iteration();
+        }
+        it += nb;
+        SVH_CUDA(cudaMemcpyAsync(done, pc + 14, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+        SVH_CUDA(cudaStreamSynchronize(s));
+        if (done[0] != 0 && done[1] != 0) break;
+    }
+    return it;
 }
 
 // out = Q^-1 in  (right preconditioner)
@@ -1035,8 +1087,15 @@ static int fgmres(svh_handle* h, const double2* b, double2* x, double rre, int m
         g[0] = beta;
         int j = 0;
         for (; j < m && total < maxit; ++j, ++total) {
+            auto c0 = std::chrono::steady_clock::now();
             precond(h, V + (size_t)j * N, Zp + (size_t)j * N, tol_inner, inner_max, s);
+            SVH_CUDA(cudaStreamSynchronize(s));
+            auto c1 = std::chrono::steady_clock::now();
             apply_sys(h, Zp + (size_t)j * N, w, true, s);
+            SVH_CUDA(cudaStreamSynchronize(s));
+            auto c2 = std::chrono::steady_clock::now();
+            S->t_precond += std::chrono::duration<double>(c1 - c0).count();
+            S->t_matvec += std::chrono::duration<double>(c2 - c1).count();
             // CGS2
             std::vector<cd> hj(j + 2, 0.0);
             for (int pass = 0; pass < 2; ++pass) {
@@ -1176,7 +1235,10 @@ static void solve_columns(svh_handle* h, const svh_port* ports, int P, const int
     build_amg(h, ps.fixed);
     const int m = std::max(1, h->opts.restart);
     ensure_work(h, m);
-    cudaStream_t s = 0;
+    if (!S->stream) SVH_CUDA(cudaStreamCreateWithFlags(&S->stream, cudaStreamNonBlocking));
+    if (!S->d_pcg) SVH_CUDA(cudaMalloc(&S->d_pcg, 16 * sizeof(double)));
+    cudaStream_t s = S->stream;
+    SVH_CUDA(cudaDeviceSynchronize());   // setup copies (legacy stream) before the non-blocking stream
     const int64_t N = S->N;
     double2* b = S->d_krylov + (size_t)(2 * m + 3) * N;   // scratch slot (also used by precond -> copy out first)
     double2* x = nullptr;
@@ -1195,13 +1257,16 @@ static void solve_columns(svh_handle* h, const svh_port* ports, int P, const int
     double worst = 0;
     int tot_it = 0;
     S->inner_its = 0;
+    S->t_matvec = S->t_precond = 0;
     (void)b;
     for (int si = 0; si < nsel; ++si) {
         const int p = sel[si];
         SVH_CHECK(p >= 0 && p < P, SVH_EINVAL, "bad port index");
         std::vector<uint8_t> mask(S->M, 0);
         for (int32_t r : ps.plus[p]) mask[r] = 1;
-        SVH_CUDA(cudaMemcpy(pm, mask.data(), S->M, cudaMemcpyHostToDevice));
+        // stream-ordered H2D (a pageable cudaMemcpy may return before its DMA lands, and
+        // the solve stream does not wait for the legacy stream)
+        SVH_CUDA(cudaMemcpyAsync(pm, mask.data(), S->M, cudaMemcpyHostToDevice, s));
         SVH_LAUNCH(k_rhs, nblk(h->K + S->M), 256, 0, s, bb, pm, S->d_fnode, h->K, S->M);
         double rre_out = 0;
         const int its = fgmres(h, bb, x, h->opts.rre, m, h->opts.max_iters, rre_out, s);
@@ -1210,15 +1275,18 @@ static void solve_columns(svh_handle* h, const svh_port* ports, int P, const int
         if (!(rre_out <= h->opts.rre * 1.0001)) all_conv = false;
         if (st) st->iterations = its;
         for (int q = 0; q < P; ++q) {
-            SVH_CUDA(cudaMemcpy(dnodes, ps.plus[q].data(), ps.plus[q].size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+            SVH_CUDA(cudaMemcpyAsync(dnodes, ps.plus[q].data(), ps.plus[q].size() * sizeof(int32_t),
+                                     cudaMemcpyHostToDevice, s));
             SVH_LAUNCH(k_port_current, 1, 256, 0, s, x, dnodes, (int)ps.plus[q].size(), S->d_node_vox, S->d_node_axis,
                        h->K, cur);
             double c2[2];
-            SVH_CUDA(cudaMemcpy(c2, cur, 2 * sizeof(double), cudaMemcpyDeviceToHost));
+            SVH_CUDA(cudaMemcpyAsync(c2, cur, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+            SVH_CUDA(cudaStreamSynchronize(s));
             Ycols[2 * ((size_t)si * P + q)] = c2[0];
             Ycols[2 * ((size_t)si * P + q) + 1] = c2[1];
         }
     }
+    SVH_CUDA(cudaStreamSynchronize(s));
     cudaFree(x);
     cudaFree(bb);
     cudaFree(pm);
@@ -1227,6 +1295,8 @@ static void solve_columns(svh_handle* h, const svh_port* ports, int P, const int
     if (st) {
         st->total_iterations += tot_it;
         st->inner_iterations += S->inner_its;
+        st->t_matvec_s += S->t_matvec;
+        st->t_precond_s += S->t_precond;
         st->converged = all_conv ? 1 : 0;
         st->final_rre = std::max(st->final_rre, worst);
         st->t_solve_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
