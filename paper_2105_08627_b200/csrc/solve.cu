@@ -39,6 +39,11 @@ struct CsrDev {
     int* col = nullptr;
     double* val = nullptr;
     double* dinv = nullptr;   // l1-Jacobi: 1 / sum_j |a_ij|
+    // ELL copy used by the SpMV-type kernels: column-major [ellw][n] (entry k of row i at
+    // k*n + i, so a warp's loads of one k are coalesced); padding col = i, val = 0
+    int ellw = 0;
+    int* ecol = nullptr;
+    double* eval = nullptr;
     int* agg = nullptr;       // fine -> coarse aggregate (except coarsest level)
     int nc = 0;
     double* vb = nullptr;     // level right-hand side (levels >= 1) [n][2]
@@ -253,54 +258,49 @@ __global__ void k_pre_a(const double2* __restrict__ c, const double2* __restrict
 
 // ---- AMG / PCG on [n][2] interleaved real vectors
 // y = A x (2 vectors)
-__global__ void k_spmv2(int n, const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ v,
+__device__ __forceinline__ double2 ell_row2(int n, int w, const int* __restrict__ ec, const double* __restrict__ ev,
+                                            const double2* __restrict__ x, int i) {
+    double a0 = 0, a1 = 0;
+    for (int k = 0; k < w; ++k) {
+        const double v = __ldg(&ev[(int64_t)k * n + i]);
+        const double2 xj = __ldg(&x[__ldg(&ec[(int64_t)k * n + i])]);
+        a0 = fma(v, xj.x, a0);
+        a1 = fma(v, xj.y, a1);
+    }
+    return make_double2(a0, a1);
+}
+__global__ void k_spmv2(int n, int w, const int* __restrict__ ec, const double* __restrict__ ev,
                         const double* __restrict__ x, double* __restrict__ y) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    double a0 = 0, a1 = 0;
-    for (int p = rp[i]; p < rp[i + 1]; ++p) {
-        const double w = v[p];
-        const int j = ci[p];
-        a0 += w * x[2 * j];
-        a1 += w * x[2 * j + 1];
-    }
-    y[2 * i] = a0;
-    y[2 * i + 1] = a1;
+    reinterpret_cast<double2*>(y)[i] = ell_row2(n, w, ec, ev, reinterpret_cast<const double2*>(x), i);
 }
 // l1-Jacobi sweep: xo = x + D^-1 (b - A x); x may be null (= zero initial guess)
-__global__ void k_jacobi2(int n, const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ v,
+__global__ void k_jacobi2(int n, int w, const int* __restrict__ ec, const double* __restrict__ ev,
                           const double* __restrict__ dinv, const double* __restrict__ b, const double* __restrict__ x,
                           double* __restrict__ xo) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    double a0 = 0, a1 = 0, x0 = 0, x1 = 0;
+    const double2 bi = reinterpret_cast<const double2*>(b)[i];
+    const double d = dinv[i];
+    double2 o;
     if (x) {
-        for (int p = rp[i]; p < rp[i + 1]; ++p) {
-            const double w = v[p];
-            const int j = ci[p];
-            a0 += w * x[2 * j];
-            a1 += w * x[2 * j + 1];
-        }
-        x0 = x[2 * i];
-        x1 = x[2 * i + 1];
+        const double2 ax = ell_row2(n, w, ec, ev, reinterpret_cast<const double2*>(x), i);
+        const double2 xi = reinterpret_cast<const double2*>(x)[i];
+        o = make_double2(xi.x + d * (bi.x - ax.x), xi.y + d * (bi.y - ax.y));
+    } else {
+        o = make_double2(d * bi.x, d * bi.y);
     }
-    xo[2 * i] = x0 + dinv[i] * (b[2 * i] - a0);
-    xo[2 * i + 1] = x1 + dinv[i] * (b[2 * i + 1] - a1);
+    reinterpret_cast<double2*>(xo)[i] = o;
 }
 // r = b - A x
-__global__ void k_resid2(int n, const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ v,
+__global__ void k_resid2(int n, int w, const int* __restrict__ ec, const double* __restrict__ ev,
                          const double* __restrict__ b, const double* __restrict__ x, double* __restrict__ r) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    double a0 = 0, a1 = 0;
-    for (int p = rp[i]; p < rp[i + 1]; ++p) {
-        const double w = v[p];
-        const int j = ci[p];
-        a0 += w * x[2 * j];
-        a1 += w * x[2 * j + 1];
-    }
-    r[2 * i] = b[2 * i] - a0;
-    r[2 * i + 1] = b[2 * i + 1] - a1;
+    const double2 ax = ell_row2(n, w, ec, ev, reinterpret_cast<const double2*>(x), i);
+    const double2 bi = reinterpret_cast<const double2*>(b)[i];
+    reinterpret_cast<double2*>(r)[i] = make_double2(bi.x - ax.x, bi.y - ax.y);
 }
 __global__ void k_zero(double* __restrict__ x, int64_t n) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -612,6 +612,8 @@ static void free_levels(Solve* S) {
         cudaFree(L.val);
         cudaFree(L.dinv);
         cudaFree(L.agg);
+        cudaFree(L.ecol);
+        cudaFree(L.eval);
     }
     S->levels.clear();
     cudaFree(S->d_cinv);
@@ -784,6 +786,23 @@ CsrDev upload(const CsrHost& A) {
     SVH_CUDA(cudaMemcpy(d.col, A.col.data(), A.col.size() * sizeof(int), cudaMemcpyHostToDevice));
     SVH_CUDA(cudaMemcpy(d.val, A.val.data(), A.val.size() * sizeof(double), cudaMemcpyHostToDevice));
     SVH_CUDA(cudaMemcpy(d.dinv, dinv.data(), A.n * sizeof(double), cudaMemcpyHostToDevice));
+    int w = 1;
+    for (int i = 0; i < A.n; ++i) w = std::max(w, A.rowptr[i + 1] - A.rowptr[i]);
+    std::vector<int> ec((size_t)w * std::max(1, A.n));
+    std::vector<double> ev((size_t)w * std::max(1, A.n), 0.0);
+    for (int i = 0; i < A.n; ++i) {
+        int k = 0;
+        for (int p = A.rowptr[i]; p < A.rowptr[i + 1]; ++p, ++k) {
+            ec[(size_t)k * A.n + i] = A.col[p];
+            ev[(size_t)k * A.n + i] = A.val[p];
+        }
+        for (; k < w; ++k) ec[(size_t)k * A.n + i] = i;
+    }
+    d.ellw = w;
+    SVH_CUDA(cudaMalloc(&d.ecol, ec.size() * sizeof(int)));
+    SVH_CUDA(cudaMalloc(&d.eval, ev.size() * sizeof(double)));
+    SVH_CUDA(cudaMemcpy(d.ecol, ec.data(), ec.size() * sizeof(int), cudaMemcpyHostToDevice));
+    SVH_CUDA(cudaMemcpy(d.eval, ev.data(), ev.size() * sizeof(double), cudaMemcpyHostToDevice));
     const size_t vb = (size_t)2 * std::max(1, A.n) * sizeof(double);
     SVH_CUDA(cudaMalloc(&d.vb, vb));
     SVH_CUDA(cudaMalloc(&d.vx, vb));
@@ -935,23 +954,23 @@ static void vcycle(Solve* S, int l, const double* b, double* x, cudaStream_t s) 
     const CsrDev& C = S->levels[l + 1];
     double* rc = C.vb;
     double* ec = C.vx;
-    SVH_LAUNCH(k_jacobi2, nblk(n), 256, 0, s, n, L.rowptr, L.col, L.val, L.dinv, b, (const double*)nullptr, x);
-    SVH_LAUNCH(k_jacobi2, nblk(n), 256, 0, s, n, L.rowptr, L.col, L.val, L.dinv, b, x, L.x2);
-    SVH_LAUNCH(k_resid2, nblk(n), 256, 0, s, n, L.rowptr, L.col, L.val, b, L.x2, L.tmp);
+    SVH_LAUNCH(k_jacobi2, nblk(n), 256, 0, s, n, L.ellw, L.ecol, L.eval, L.dinv, b, (const double*)nullptr, x);
+    SVH_LAUNCH(k_jacobi2, nblk(n), 256, 0, s, n, L.ellw, L.ecol, L.eval, L.dinv, b, x, L.x2);
+    SVH_LAUNCH(k_resid2, nblk(n), 256, 0, s, n, L.ellw, L.ecol, L.eval, b, L.x2, L.tmp);
     SVH_LAUNCH(k_zero, nblk(2 * L.nc), 256, 0, s, rc, (int64_t)2 * L.nc);
     SVH_LAUNCH(k_restrict2, nblk(n), 256, 0, s, n, L.agg, L.tmp, rc);
     vcycle(S, l + 1, rc, ec, s);
     SVH_LAUNCH(k_prolong2, nblk(n), 256, 0, s, n, L.agg, ec, L.x2);
     static const int wlev = getenv("SVH_AMG_W") ? atoi(getenv("SVH_AMG_W")) : 2;
     if (l < wlev) {   // W-cycle on the top levels: second coarse-grid correction
-        SVH_LAUNCH(k_resid2, nblk(n), 256, 0, s, n, L.rowptr, L.col, L.val, b, L.x2, L.tmp);
+        SVH_LAUNCH(k_resid2, nblk(n), 256, 0, s, n, L.ellw, L.ecol, L.eval, b, L.x2, L.tmp);
         SVH_LAUNCH(k_zero, nblk(2 * L.nc), 256, 0, s, rc, (int64_t)2 * L.nc);
         SVH_LAUNCH(k_restrict2, nblk(n), 256, 0, s, n, L.agg, L.tmp, rc);
         vcycle(S, l + 1, rc, ec, s);
         SVH_LAUNCH(k_prolong2, nblk(n), 256, 0, s, n, L.agg, ec, L.x2);
     }
-    SVH_LAUNCH(k_jacobi2, nblk(n), 256, 0, s, n, L.rowptr, L.col, L.val, L.dinv, b, L.x2, x);
-    SVH_LAUNCH(k_jacobi2, nblk(n), 256, 0, s, n, L.rowptr, L.col, L.val, L.dinv, b, x, L.x2);
+    SVH_LAUNCH(k_jacobi2, nblk(n), 256, 0, s, n, L.ellw, L.ecol, L.eval, L.dinv, b, L.x2, x);
+    SVH_LAUNCH(k_jacobi2, nblk(n), 256, 0, s, n, L.ellw, L.ecol, L.eval, L.dinv, b, x, L.x2);
     SVH_CUDA(cudaMemcpyAsync(x, L.x2, 2 * (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, s));
 }
 
@@ -974,7 +993,7 @@ static int pcg2(svh_handle* h, const double* b, double* x, double tol, int maxit
         SVH_LAUNCH(k_dot2, 296, 256, 0, s, (int64_t)n, a, bb, out2);
     };
     auto iteration = [&] {
-        SVH_LAUNCH(k_spmv2, nblk(n), 256, 0, s, n, A.rowptr, A.col, A.val, p, q);
+        SVH_LAUNCH(k_spmv2, nblk(n), 256, 0, s, n, A.ellw, A.ecol, A.eval, p, q);
         dot(p, q, pc + 2);
         SVH_LAUNCH(k_pcg_alpha, 1, 32, 0, s, pc);
         SVH_LAUNCH(k_axpy2, nblk(n), 256, 0, s, (int64_t)n, pc + 8, +1, p, x);
