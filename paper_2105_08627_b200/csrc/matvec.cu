@@ -630,6 +630,7 @@ __global__ void __launch_bounds__(fft_r1(N) * QQ, QQ == 4 ? 2 : 1)
     int t = blockIdx.x;
 #pragma unroll
     for (int s2 = 0; s2 < S - 1; ++s2) issue(t + s2 * (int)gridDim.x, s2);
+    int pend_xt = 0, pend_p = -1;   // forward: output tile staged in O, store not yet issued
     for (int i = 0; t < ntiles; ++i, t += gridDim.x) {
         issue(t + (S - 1) * (int)gridDim.x, (i + S - 1) % S);
         const int st = i % S;
@@ -639,6 +640,11 @@ __global__ void __launch_bounds__(fft_r1(N) * QQ, QQ == 4 ? 2 : 1)
             mbar_wait(&bar[st], (uint32_t)((i / S) & 1));
         }
         __syncthreads();
+        if (DIR < 0 && tid == 0 && pend_p >= 0) {
+#pragma unroll
+            for (int b = 0; b < N / BOX; ++b) tma_store_3d(&tmap, pend_xt, b * BOX, pend_p, O + b * BOX * Q);
+            tma_store_commit();
+        }
         int z, p;
         int64_t bin, bout;
         decode(t, z, p, bin, bout);
@@ -668,15 +674,13 @@ __global__ void __launch_bounds__(fft_r1(N) * QQ, QQ == 4 ? 2 : 1)
         for (int m = 0; m < R2; ++m) u[m] = T[em_idx<N, Q>(m * R1 + k1, q2)];
         reg_fft<R2, DIR>(u);
         if (DIR < 0) {
+            // staged for the TMA store, which thread 0 issues after the NEXT tile's top barrier
+            // (that barrier orders these writes; no extra barrier per tile)
 #pragma unroll
             for (int k2 = 0; k2 < R2; ++k2) O[(k1 + R1 * k2) * Q + q2] = u[k2];
             fence_proxy_async_smem();
-            __syncthreads();
-            if (tid == 0) {
-#pragma unroll
-                for (int b = 0; b < N / BOX; ++b) tma_store_3d(&tmap, (t % tiles_x) * Q, b * BOX, p, O + b * BOX * Q);
-                tma_store_commit();
-            }
+            pend_xt = (t % tiles_x) * Q;
+            pend_p = p;
         } else {
             float2* dst = out + bout + q2;
 #pragma unroll
@@ -686,7 +690,15 @@ __global__ void __launch_bounds__(fft_r1(N) * QQ, QQ == 4 ? 2 : 1)
     }
     if (DIR < 0) {
         asm volatile("cp.async.wait_group 0;\n" ::);
-        if (tid == 0) tma_store_wait0();
+        __syncthreads();
+        if (tid == 0) {
+            if (pend_p >= 0) {
+#pragma unroll
+                for (int b = 0; b < N / BOX; ++b) tma_store_3d(&tmap, pend_xt, b * BOX, pend_p, O + b * BOX * Q);
+                tma_store_commit();
+            }
+            tma_store_wait0();
+        }
     }
 }
 
