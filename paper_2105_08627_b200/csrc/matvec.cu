@@ -940,10 +940,10 @@ constexpr size_t zmac_smem() {
     return (size_t)zmac_s_f2<N>() * sizeof(float2) + (size_t)7 * N * 32 * sizeof(float);
 }
 
-template <int N>
+template <int N, int PROBE = 0>
 __global__ void __launch_bounds__(160, 3)
     k_zmac(float2* __restrict__ X2, SpecView sv, int Nx, int Ny, int Kz, float g, int nrhs, uint64_t pmask, int Nxs,
-           int kxg) {
+           int kxg, int zpre) {
     constexpr int Q = 32, NH = N / 2;
     extern __shared__ float2 S[];                       // [5][N][Q] spectra; Tucker scratch
     float* KV = reinterpret_cast<float*>(S + zmac_s_f2<N>());   // [7][N][Q] folded kernel values
@@ -1003,7 +1003,7 @@ __global__ void __launch_bounds__(160, 3)
         float2 v[N];
 #pragma unroll
         for (int j = 0; j < N; ++j) v[j] = j < NH ? nxt[j] : zero;
-        reg_fft<N, -1, true>(v);
+        if (PROBE != 2) reg_fft<N, -1, true>(v);
 #pragma unroll
         for (int k = 0; k < N; ++k) S[(c * N + k) * Q + q] = v[k];
         __syncthreads();
@@ -1012,10 +1012,21 @@ __global__ void __launch_bounds__(160, 3)
 #pragma unroll
             for (int j = 0; j < NH; ++j) nxt[j] = ((lm >> j) & 1u) ? nc[(int64_t)j * plane] : zero;
         }
+        // the RHS after next: its rows of this tile are bulk-prefetched into L2 (one
+        // 256-byte cp.async.bulk.prefetch per (component, z) row, no registers), so the
+        // register prefetch above hits L2 one iteration later
+        if (zpre && r + 2 < nrhs && tid < 5 * NH) {
+            const int cc = tid / NH, j = tid % NH;
+            const int nb = min(Q, Nxs - kx0) * 8 / 16 * 16;
+            if (j < Kz && ((pmask >> j) & 1u) && nb > 0) {
+                const float2* a = X2 + (r + 2) * rstride + ((int64_t)cc * Kz + j) * plane + (int64_t)ky * Nxs + kx0;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a), "r"(nb) : "memory");
+            }
+        }
         float2* sp = S + w * Q + q;
         const float* kp = KV + w * Q + q;
 #pragma unroll 1
-        for (int k = w; k < N; k += 5, sp += 5 * Q, kp += 5 * Q) {
+        for (int k = w; k < N && PROBE != 1; k += 5, sp += 5 * Q, kp += 5 * Q) {
             {
                 const float2 Ix = sp[0 * N * Q], Iy = sp[1 * N * Q], Iz = sp[2 * N * Q];
                 const float2 I2 = sp[3 * N * Q], I3 = sp[4 * N * Q];
@@ -1035,7 +1046,7 @@ __global__ void __launch_bounds__(160, 3)
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < N; ++k) v[k] = S[(c * N + k) * Q + q];   // own column: no barrier before reuse
-        reg_fft<N, +1>(v);
+        if (PROBE != 2) reg_fft<N, +1>(v);
         float2* dst = col + r * rstride;
 #pragma unroll
         for (int j = 0; j < NH; ++j)
@@ -1281,9 +1292,18 @@ void run_pass_c(svh_handle* h, const Geom& g, float2* X2, int nrhs, cudaStream_t
         if (zmac) {
             const size_t smem = zmac_smem<N>();
             dim3 grid((g.nx + 31) / 32, h->ny);
+            static const int probe = getenv("SVH_ZPROBE") ? atoi(getenv("SVH_ZPROBE")) : 0;   // perf probes only
+            if (probe == 1 || probe == 2) {
+                auto kp = probe == 1 ? k_zmac<N, 1> : k_zmac<N, 2>;
+                prep(kp, smem);
+                SVH_LAUNCH(kp, grid, 160, smem, s, X2, sv, h->nx, h->ny, h->kz, h->gscale, nrhs, (uint64_t)h->planemask,
+                           g.nx, g.kx0, 1);
+                return;
+            }
+            static const int zpre = getenv("SVH_ZPRE") ? atoi(getenv("SVH_ZPRE")) : 1;
             prep(k_zmac<N>, smem);
             SVH_LAUNCH((k_zmac<N>), grid, 160, smem, s, X2, sv, h->nx, h->ny, h->kz, h->gscale, nrhs,
-                       (uint64_t)h->planemask, g.nx, g.kx0);
+                       (uint64_t)h->planemask, g.nx, g.kx0, zpre);
             return;
         }
     }
