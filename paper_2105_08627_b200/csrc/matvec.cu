@@ -540,14 +540,19 @@ struct YTma {
     static constexpr size_t smem = S * stage_b + T_b + O_b + (size_t)S * MW * 4 + S * 8 + 128;
 };
 
-template <int N, int DIR, int S, int QQ>
+// TIN (forward only): load whole input tiles by TMA through tmap_in (X1 [plane][y][x]) and
+// zero the rows without voxels in registers, instead of the pruned cp.async row loads.
+template <int N, int DIR, int S, int QQ, bool TIN = false>
 __global__ void __launch_bounds__(fft_r1(N) * QQ, QQ == 4 ? 2 : 1)
     k_ytma(const float2* __restrict__ in, float2* __restrict__ out, const __grid_constant__ CUtensorMap tmap,
-           const float2* __restrict__ tw, int Nx, int Kz, int Lin, int Lout, int ntiles, int tiles_x,
-           const int32_t* __restrict__ planes, int nzp, const uint32_t* __restrict__ rowmask, int rowMW) {
+           const __grid_constant__ CUtensorMap tmap_in, const float2* __restrict__ tw, int Nx, int Kz, int Lin,
+           int Lout, int ntiles, int tiles_x, const int32_t* __restrict__ planes, int nzp,
+           const uint32_t* __restrict__ rowmask, int rowMW) {
     using P = YTma<N, DIR, S, QQ>;
     constexpr int Q = P::Q, R1 = P::R1, R2 = P::R2, NT = P::NT, SR = P::SR, MW = P::MW, BOX = P::BOX;
     constexpr int NL = DIR < 0 ? R1 / 2 : R1;
+    constexpr bool TMA_IN = DIR > 0 || TIN;
+    constexpr int BOXI = SR < 256 ? SR : 256;
     extern __shared__ __align__(128) unsigned char smraw[];
     float2* stage = reinterpret_cast<float2*>(smraw);
     float2* T = reinterpret_cast<float2*>(smraw + S * P::stage_b);
@@ -557,7 +562,7 @@ __global__ void __launch_bounds__(fft_r1(N) * QQ, QQ == 4 ? 2 : 1)
     const int tid = threadIdx.x;
     const float2 zero = make_float2(0.f, 0.f);
     const int lin = min(Lin, SR);
-    if (DIR < 0) {
+    if (DIR < 0 && !TIN) {
         for (int e = tid; e < S * (SR - lin) * Q; e += NT) {
             const int st = e / ((SR - lin) * Q), r = e % ((SR - lin) * Q);
             stage[st * SR * Q + lin * Q + r] = zero;
@@ -576,7 +581,7 @@ __global__ void __launch_bounds__(fft_r1(N) * QQ, QQ == 4 ? 2 : 1)
         bout = (int64_t)p * Lout * Nx + (int64_t)xt * Q;
     };
     auto issue = [&](int t, int st) {
-        if (DIR < 0) {
+        if (!TMA_IN) {
             if (t < ntiles) {
                 int z, p;
                 int64_t bin, bout;
@@ -612,8 +617,9 @@ __global__ void __launch_bounds__(fft_r1(N) * QQ, QQ == 4 ? 2 : 1)
             if (tid == 0) {
                 mbar_arrive_expect_tx(&bar[st], (uint32_t)P::stage_b);
 #pragma unroll
-                for (int b = 0; b < N / BOX; ++b)
-                    tma_load_3d(stage + st * SR * Q + b * BOX * Q, &tmap, (t % tiles_x) * Q, b * BOX, p, &bar[st]);
+                for (int b = 0; b < SR / BOXI; ++b)
+                    tma_load_3d(stage + st * SR * Q + b * BOXI * Q, DIR > 0 ? &tmap : &tmap_in, (t % tiles_x) * Q,
+                                b * BOXI, p, &bar[st]);
             }
         }
     };
@@ -634,7 +640,7 @@ __global__ void __launch_bounds__(fft_r1(N) * QQ, QQ == 4 ? 2 : 1)
     for (int i = 0; t < ntiles; ++i, t += gridDim.x) {
         issue(t + (S - 1) * (int)gridDim.x, (i + S - 1) % S);
         const int st = i % S;
-        if (DIR < 0) {
+        if (!TMA_IN) {
             asm volatile("cp.async.wait_group %0;\n" ::"n"(S - 1));
         } else {
             mbar_wait(&bar[st], (uint32_t)((i / S) & 1));
@@ -652,7 +658,12 @@ __global__ void __launch_bounds__(fft_r1(N) * QQ, QQ == 4 ? 2 : 1)
             const float2* src = stage + st * SR * Q;
             float2 v[R1];
 #pragma unroll
-            for (int n1 = 0; n1 < R1; ++n1) v[n1] = n1 < NL ? src[(R2 * n1 + n2) * Q + q1] : zero;
+            for (int n1 = 0; n1 < R1; ++n1) {
+                const int j = R2 * n1 + n2;
+                bool live = n1 < NL;
+                if (TIN) live = live && ((M[st * MW + (j >> 5)] >> (j & 31)) & 1u);
+                v[n1] = live ? src[j * Q + q1] : zero;
+            }
             reg_fft<R1, DIR, (DIR < 0)>(v);
 #pragma unroll
             for (int kk = 1; kk < R1; ++kk) v[kk] = cmul(v[kk], tw1[kk]);
@@ -689,7 +700,7 @@ __global__ void __launch_bounds__(fft_r1(N) * QQ, QQ == 4 ? 2 : 1)
         }
     }
     if (DIR < 0) {
-        asm volatile("cp.async.wait_group 0;\n" ::);
+        if (!TIN) asm volatile("cp.async.wait_group 0;\n" ::);
         __syncthreads();
         if (tid == 0) {
             if (pend_p >= 0) {
@@ -1206,6 +1217,7 @@ void run_pass_y(svh_handle* h, const Geom& g, const float2* in, float2* out, int
         CUtensorMap tmap;
         const float2* x2 = DIR < 0 ? out : in;   // the X2 side of the pass
         static const int yq = getenv("SVH_YQ") ? atoi(getenv("SVH_YQ")) : 4;
+        static const bool btma = getenv("SVH_BTMA") ? atoi(getenv("SVH_BTMA")) != 0 : false;   // measured slower (more bytes)
         auto launch = [&](auto Qc) -> bool {
             constexpr int QQ = decltype(Qc)::value;
             using P = YTma<N, DIR, 2, QQ>;
@@ -1213,16 +1225,29 @@ void run_pass_y(svh_handle* h, const Geom& g, const float2* in, float2* out, int
                 !encode_tmap_c64_3d(&tmap, x2, (uint64_t)nx, (uint64_t)h->ny, (uint64_t)5 * nrhs * h->kz,
                                     (uint64_t)nx, (uint64_t)nx * h->ny, QQ, P::BOX))
                 return false;
+            CUtensorMap tmap_in = tmap;
+            bool tin = false;
+            if (DIR < 0 && btma) {   // X1 [plane][y < Ky][x], box QQ x min(N/2, 256)
+                constexpr uint32_t BI = (N / 2) < 256 ? (N / 2) : 256;
+                tin = encode_tmap_c64_3d(&tmap_in, in, (uint64_t)nx, (uint64_t)h->ky, (uint64_t)5 * nrhs * h->kz,
+                                         (uint64_t)nx, (uint64_t)nx * h->ky, QQ, BI);
+            }
             const int tiles_x = nx / QQ;
             const int ntiles = tiles_x * h->nzp * 5 * nrhs;
             int dev = 0, nsm = 148, occ = 1;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-            prep(k_ytma<N, DIR, 2, QQ>, P::smem);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ytma<N, DIR, 2, QQ>, P::NT, P::smem);
-            SVH_LAUNCH((k_ytma<N, DIR, 2, QQ>), std::min(ntiles, nsm * std::max(occ, 1)), P::NT, P::smem, s, in,
-                       out, tmap, h->d_tw[1], nx, h->kz, Lin, Lout, ntiles, tiles_x, h->d_planes, h->nzp,
-                       h->d_rowmask, h->rowMW);
+            auto go = [&](auto kern) {
+                prep(kern, P::smem);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, P::NT, P::smem);
+                SVH_LAUNCH(kern, std::min(ntiles, nsm * std::max(occ, 1)), P::NT, P::smem, s, in, out, tmap, tmap_in,
+                           h->d_tw[1], nx, h->kz, Lin, Lout, ntiles, tiles_x, h->d_planes, h->nzp, h->d_rowmask,
+                           h->rowMW);
+            };
+            if (tin)
+                go(k_ytma<N, DIR, 2, QQ, true>);
+            else
+                go(k_ytma<N, DIR, 2, QQ, false>);
             return true;
         };
         if (ytma && ((yq == 4 && launch(std::integral_constant<int, 4>{})) ||
