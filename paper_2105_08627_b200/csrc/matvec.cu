@@ -1087,6 +1087,36 @@ __global__ void __launch_bounds__(fft_max_threads(N))
         if (j < Kz && q < nq && __ldg(&planeok[j])) v = base[((int64_t)c * Kz + j) * plane + q];
         S[j * PP + c * Q + q] = v;
     }
+    // Tucker mode (Eq. 10): separable on-chip expansion, as tucker_tile: per CTA
+    // G_m = core_m x2 F2[oy] (d3 x d1), H_m[q] = G_m x1 F1[ox_q] (d3); per point one d3-term
+    // dot product with the F3 row of its kz (the dense circulant never exists in HBM)
+    __shared__ float Gs[32 * 32];
+    __shared__ float Hs[7][8][32];
+    if (!sv.spec) {
+        const int oy = ky <= (Ny >> 1) ? ky : Ny - ky;
+        for (int m = 0; m < 7; ++m) {
+            const int d1 = sv.rk[m][0], d2 = sv.rk[m][1], d3 = sv.rk[m][2];
+            const float* C = sv.core[m];
+            const float* F2 = sv.fac[m][1] + (int64_t)oy * d2;
+            for (int t = threadIdx.x; t < d3 * d1; t += blockDim.x) {
+                const int c3 = t / d1, c1 = t % d1;
+                float acc = 0.f;
+                for (int c2 = 0; c2 < d2; ++c2) acc = fmaf(__ldg(&C[((int64_t)c3 * d2 + c2) * d1 + c1]), __ldg(&F2[c2]), acc);
+                Gs[t] = acc;
+            }
+            __syncthreads();
+            for (int t = threadIdx.x; t < Q * d3; t += blockDim.x) {
+                const int q = t / d3, c3 = t % d3;
+                const int kx = min(kxg + kx0 + q, Nx - 1);
+                const int ox = kx <= (Nx >> 1) ? kx : Nx - kx;
+                const float* f1 = sv.fac[m][0] + (int64_t)ox * d1;
+                float acc = 0.f;
+                for (int c1 = 0; c1 < d1; ++c1) acc = fmaf(Gs[c3 * d1 + c1], __ldg(&f1[c1]), acc);
+                Hs[m][q][c3] = acc;
+            }
+            __syncthreads();
+        }
+    }
     __syncthreads();
     smem_fft<N, -1>(S, PP, Q5, tw);
     for (int t = threadIdx.x; t < Q * N; t += blockDim.x) {
@@ -1096,27 +1126,14 @@ __global__ void __launch_bounds__(fft_max_threads(N))
         if (sv.spec) {
             kernel_values(sv, kxg + kx0 + q, ky, kz, Nx, Ny, N, kv);
         } else {
-            // Tucker: direct contraction per point (Eq. 10)
             const int kx = kxg + kx0 + q;
-            const int o3[3] = {kx <= (Nx >> 1) ? kx : Nx - kx, ky <= (Ny >> 1) ? ky : Ny - ky,
-                               kz <= (N >> 1) ? kz : N - kz};
+            const int oz = kz <= (N >> 1) ? kz : N - kz;
 #pragma unroll
             for (int m = 0; m < 7; ++m) {
-                const int d1 = sv.rk[m][0], d2 = sv.rk[m][1], d3 = sv.rk[m][2];
-                const float* f1 = sv.fac[m][0] + (int64_t)o3[0] * d1;
-                const float* f2 = sv.fac[m][1] + (int64_t)o3[1] * d2;
-                const float* f3 = sv.fac[m][2] + (int64_t)o3[2] * d3;
+                const int d3 = sv.rk[m][2];
+                const float* f3 = sv.fac[m][2] + (int64_t)oz * d3;
                 float acc = 0.f;
-                for (int c3 = 0; c3 < d3; ++c3) {
-                    float a2 = 0.f;
-                    for (int c2 = 0; c2 < d2; ++c2) {
-                        float a1 = 0.f;
-                        const float* Cr = sv.core[m] + ((int64_t)c3 * d2 + c2) * d1;
-                        for (int c1 = 0; c1 < d1; ++c1) a1 = fmaf(__ldg(&Cr[c1]), __ldg(&f1[c1]), a1);
-                        a2 = fmaf(a1, __ldg(&f2[c2]), a2);
-                    }
-                    acc = fmaf(a2, __ldg(&f3[c3]), acc);
-                }
+                for (int c3 = 0; c3 < d3; ++c3) acc = fmaf(Hs[m][q][c3], __ldg(&f3[c3]), acc);
                 kv[m] = acc;
             }
             kv[1] *= kx <= (Nx >> 1) ? 1.f : -1.f;
@@ -1354,7 +1371,7 @@ void run_pass_c(svh_handle* h, const Geom& g, float2* X2, int nrhs, cudaStream_t
         }
     } else {
         const int tpp = fft_threads_per_pencil(N);
-        int Q = std::max(1, fft_max_threads(N) / (tpp * 5));
+        int Q = std::min(8, std::max(1, fft_max_threads(N) / (tpp * 5)));   // <= 8: Tucker H tile
         while (Q > 1 && (size_t)N * (5 * Q + 1) * sizeof(float2) > 160 * 1024) Q >>= 1;
         const int nt = std::max(32, tpp * 5 * Q);
         const size_t smem = (size_t)N * (5 * Q + 1) * sizeof(float2);

@@ -21,7 +21,10 @@
 // the ranks then match a direct SVD's.
 #include <algorithm>
 #include <cmath>
+#include <mutex>
 #include <vector>
+
+#include <cusolverDn.h>
 
 #include "internal.h"
 
@@ -220,6 +223,46 @@ void sym_eig(std::vector<double> G, int n, std::vector<double>& lam, std::vector
     }
 }
 
+// Same contract as sym_eig for a symmetric n x n matrix already on the device (dG is
+// overwritten): cuSOLVER syevd, used for the large unfoldings (setup only -- the O(n^3) host
+// tridiagonalisation would dominate time-to-setup for n ~ 1000).
+void sym_eig_dev(double* dG, int n, std::vector<double>& lam, std::vector<double>& U) {
+    static cusolverDnHandle_t hs = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] { cusolverDnCreate(&hs); });
+    SVH_CHECK(hs != nullptr, SVH_ECUDA, "cusolverDnCreate failed");
+    int lwork = 0;
+    double* dW = nullptr;
+    SVH_CUDA(cudaMalloc(&dW, n * sizeof(double)));
+    SVH_CHECK(cusolverDnDsyevd_bufferSize(hs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, dG, n, dW, &lwork) ==
+                  CUSOLVER_STATUS_SUCCESS,
+              SVH_ECUDA, "syevd buffer");
+    double* work = nullptr;
+    int* info = nullptr;
+    SVH_CUDA(cudaMalloc(&work, std::max(1, lwork) * sizeof(double)));
+    SVH_CUDA(cudaMalloc(&info, sizeof(int)));
+    SVH_CHECK(cusolverDnDsyevd(hs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, dG, n, dW, work, lwork, info) ==
+                  CUSOLVER_STATUS_SUCCESS,
+              SVH_ECUDA, "syevd");
+    std::vector<double> w(n), V((size_t)n * n);
+    int hinfo = 0;
+    SVH_CUDA(cudaMemcpy(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost));
+    SVH_CUDA(cudaMemcpy(w.data(), dW, n * sizeof(double), cudaMemcpyDeviceToHost));
+    SVH_CUDA(cudaMemcpy(V.data(), dG, V.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    cudaFree(dW);
+    cudaFree(work);
+    cudaFree(info);
+    SVH_CHECK(hinfo == 0, SVH_ECUDA, "syevd did not converge");
+    lam.resize(n);
+    U.resize((size_t)n * n);
+    for (int j = 0; j < n; ++j) {   // ascending -> descending
+        lam[j] = w[n - 1 - j];
+        std::copy(V.begin() + (size_t)(n - 1 - j) * n, V.begin() + (size_t)(n - j) * n, U.begin() + (size_t)j * n);
+    }
+}
+
+constexpr int kDevEig = 256;   // matrices at least this large go to the device eigensolver
+
 }  // namespace
 
 void free_tucker(svh_handle* h) {
@@ -270,7 +313,10 @@ void compute_tucker(svh_handle* h) {
             SVH_CUDA(cudaMemcpy(G.data(), dG, G.size() * sizeof(double), cudaMemcpyDeviceToHost));
             trace = 0;
             for (int i = 0; i < n; ++i) trace += G[(size_t)i * n + i];
-            sym_eig(G, n, lam[a], U[a]);
+            if (n >= kDevEig)
+                sym_eig_dev(dG, n, lam[a], U[a]);
+            else
+                sym_eig(G, n, lam[a], U[a]);
             // Deflated refinement (reading G9): a Gram eigensolve resolves eigenvalues only down
             // to ~eps*lam_1 (singular values to sqrt(eps)*s_1), too coarse for tol < ~1e-7.  The
             // unreliable tail block U_t is re-resolved from the unfolding itself: C = U_t^T A,
@@ -279,7 +325,7 @@ void compute_tucker(svh_handle* h) {
             int d0 = 1;
             while (d0 < n && lam[a][d0] > 1e-11 * lam[a][0]) ++d0;
             const int nt = n - d0;
-            if (nt > 1 && lam[a][0] > 0) {
+            if (tol < 1e-6 && nt > 1 && lam[a][0] > 0) {
                 double *dX, *dC, *dG2;
                 SVH_CUDA(cudaMalloc(&dX, (size_t)n * nt * sizeof(double)));
                 SVH_CUDA(cudaMalloc(&dC, (size_t)nt * rest * sizeof(double)));
@@ -290,11 +336,15 @@ void compute_tucker(svh_handle* h) {
                 SVH_LAUNCH(k_proj, (unsigned)((tot + 255) / 256), 256, 0, 0, dX, dU, dC, n, nt, (int64_t)rest);
                 dgemm_nt(nt, nt, rest, dC, nt, dC, nt, dG2, nt);
                 std::vector<double> G2((size_t)nt * nt), lam2, W;
-                SVH_CUDA(cudaMemcpy(G2.data(), dG2, G2.size() * sizeof(double), cudaMemcpyDeviceToHost));
+                if (nt >= kDevEig) {
+                    sym_eig_dev(dG2, nt, lam2, W);
+                } else {
+                    SVH_CUDA(cudaMemcpy(G2.data(), dG2, G2.size() * sizeof(double), cudaMemcpyDeviceToHost));
+                    sym_eig(G2, nt, lam2, W);
+                }
                 cudaFree(dX);
                 cudaFree(dC);
                 cudaFree(dG2);
-                sym_eig(G2, nt, lam2, W);
                 std::vector<double> Ut((size_t)n * nt, 0.0);
                 for (int j = 0; j < nt; ++j)
                     for (int i = 0; i < nt; ++i) {
