@@ -139,6 +139,14 @@ int svh_plan_info(const svh_handle* h, int64_t* info);
  */
 int svh_matvec(svh_handle* h, const void* I, void* CC, int32_t nrhs, int32_t green_only, svh_stream stream);
 
+/* svh_matvec_host -- svh_matvec on HOST buffers (the end-to-end call): I_host, CC_host are
+ * host complex64 [nrhs][5][K] (pinned memory for copy/compute overlap; pageable works but
+ * serialises).  The RHS stream through the GPU in chunks of `chunk` (0 = 4): the H2D copy of
+ * the next chunk and the D2H copy of the previous one overlap the passes of the current one.
+ * Returns after CC_host is complete (synchronises `stream`).  Errors as svh_matvec. */
+int svh_matvec_host(svh_handle* h, const void* I_host, void* CC_host, int32_t nrhs, int32_t green_only,
+                    int32_t chunk, svh_stream stream);
+
 /* Same operator on the lattice layout: complex64 [nrhs][5][kz][ky][kx]; input
  * values at empty voxels are ignored (treated as 0); output is 0 there. */
 int svh_matvec_grid(svh_handle* h, const void* I, void* CC, int32_t nrhs, int32_t green_only, svh_stream stream);

@@ -180,6 +180,7 @@ static void destroy(svh_handle* h) {
     for (int a = 0; a < 3; ++a) cudaFree(h->d_tw[a]);
     cudaFree(h->X1);
     cudaFree(h->X2);
+    free_host_pipe(h);
     for (auto st : h->streams) cudaStreamDestroy(st);
     for (auto ev : h->stream_events) cudaEventDestroy(ev);
     if (h->fork_event) cudaEventDestroy(h->fork_event);
@@ -360,6 +361,15 @@ int svh_matvec(svh_handle* h, const void* I, void* CC, int32_t nrhs, int32_t gre
         SVH_CHECK(h && I && CC && nrhs >= 1 && I != CC, SVH_EINVAL, "bad matvec args");
         SVH_CUDA(cudaSetDevice(h->device));
         matvec(h, (const float2*)I, (float2*)CC, nrhs, green_only != 0, true, (cudaStream_t)stream);
+    });
+}
+
+int svh_matvec_host(svh_handle* h, const void* I_host, void* CC_host, int32_t nrhs, int32_t green_only,
+                    int32_t chunk, svh_stream stream) {
+    return guarded([&] {
+        SVH_CHECK(h && I_host && CC_host && nrhs >= 1 && I_host != CC_host, SVH_EINVAL, "bad matvec args");
+        SVH_CUDA(cudaSetDevice(h->device));
+        matvec_host(h, (const float2*)I_host, (float2*)CC_host, nrhs, green_only != 0, chunk, (cudaStream_t)stream);
     });
 }
 

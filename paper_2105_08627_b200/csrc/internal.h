@@ -63,6 +63,15 @@ struct svh_handle {
     std::vector<cudaStream_t> streams;   // internal streams for concurrent RHS sub-batches
     std::vector<cudaEvent_t> stream_events;
     cudaEvent_t fork_event = nullptr;
+    // host-buffer matvec pipeline (svh_matvec_host): double-buffered device slots, copy streams
+    struct HostPipe {
+        size_t cap = 0;                       // RHS per slot
+        float2* din[2] = {nullptr, nullptr};
+        float2* dout[2] = {nullptr, nullptr};
+        cudaStream_t h2d = nullptr, d2h = nullptr;
+        cudaEvent_t in_ready[2] = {}, mv_done[2] = {}, out_done[2] = {};
+    };
+    HostPipe* pipe = nullptr;
     // solve-side data (built lazily by svh_solve / svh_apply_system)
     svh::Solve* solve = nullptr;
     double t_setup = 0;
@@ -89,6 +98,9 @@ namespace svh {
 void matvec(svh_handle* h, const float2* I, float2* CC, int nrhs, bool green_only, bool packed,
             cudaStream_t s);
 void ensure_workspace(svh_handle* h, int nrhs);
+void matvec_host(svh_handle* h, const float2* I_host, float2* CC_host, int nrhs, bool green_only, int chunk,
+                 cudaStream_t s);
+void free_host_pipe(svh_handle* h);
 void slab_sizes(const svh_handle* h, int P, int64_t* out4);
 void slab_forward(svh_handle* h, int rank, int P, const float2* I, float2* send, int nrhs, cudaStream_t s);
 void slab_middle(svh_handle* h, int rank, int P, const float2* recv, float2* send, int nrhs, cudaStream_t s);

@@ -1646,4 +1646,68 @@ void slab_backward(svh_handle* h, int rank, int P, const float2* recv, const flo
     SVH_DISPATCH_N(h->nx, run_pass_e<NN>(h, g, h->X1, I, CC, false, green_only, nrhs, s));
 }
 
+// ---------------------------------------------------------------------------
+// Host-buffer matvec (svh_matvec_host): the RHS stream through the GPU in chunks; the H2D
+// copy of chunk c+1 and the D2H copy of chunk c-1 run on their own streams while chunk c is
+// multiplied, so the host<->device traffic hides behind the passes (pinned host memory).
+void free_host_pipe(svh_handle* h) {
+    auto* P = h->pipe;
+    if (!P) return;
+    for (int k = 0; k < 2; ++k) {
+        cudaFree(P->din[k]);
+        cudaFree(P->dout[k]);
+        if (P->in_ready[k]) cudaEventDestroy(P->in_ready[k]);
+        if (P->mv_done[k]) cudaEventDestroy(P->mv_done[k]);
+        if (P->out_done[k]) cudaEventDestroy(P->out_done[k]);
+    }
+    if (P->h2d) cudaStreamDestroy(P->h2d);
+    if (P->d2h) cudaStreamDestroy(P->d2h);
+    delete P;
+    h->pipe = nullptr;
+}
+
+void matvec_host(svh_handle* h, const float2* I_host, float2* CC_host, int nrhs, bool green_only, int chunk,
+                 cudaStream_t s) {
+    const size_t per = (size_t)5 * h->K;
+    const int cr = std::max(1, std::min(nrhs, chunk > 0 ? chunk : 4));
+    if (!h->pipe || h->pipe->cap < (size_t)cr) {
+        free_host_pipe(h);
+        auto* P = new svh_handle::HostPipe();
+        h->pipe = P;
+        P->cap = cr;
+        for (int k = 0; k < 2; ++k) {
+            SVH_CUDA(cudaMalloc(&P->din[k], cr * per * sizeof(float2)));
+            SVH_CUDA(cudaMalloc(&P->dout[k], cr * per * sizeof(float2)));
+            SVH_CUDA(cudaEventCreateWithFlags(&P->in_ready[k], cudaEventDisableTiming));
+            SVH_CUDA(cudaEventCreateWithFlags(&P->mv_done[k], cudaEventDisableTiming));
+            SVH_CUDA(cudaEventCreateWithFlags(&P->out_done[k], cudaEventDisableTiming));
+        }
+        SVH_CUDA(cudaStreamCreateWithFlags(&P->h2d, cudaStreamNonBlocking));
+        SVH_CUDA(cudaStreamCreateWithFlags(&P->d2h, cudaStreamNonBlocking));
+    }
+    auto* P = h->pipe;
+    // order the pipeline after earlier work on the caller's stream
+    SVH_CUDA(cudaEventRecord(P->mv_done[0], s));
+    SVH_CUDA(cudaStreamWaitEvent(P->h2d, P->mv_done[0], 0));
+    SVH_CUDA(cudaEventRecord(P->mv_done[1], s));
+    const int nch = (nrhs + cr - 1) / cr;
+    for (int c = 0; c < nch; ++c) {
+        const int k = c & 1, r0 = c * cr, nr = std::min(cr, nrhs - r0);
+        const size_t bytes = (size_t)nr * per * sizeof(float2);
+        // slot k: its input was last read by the matvec of chunk c-2, its output by the D2H of c-2
+        SVH_CUDA(cudaStreamWaitEvent(P->h2d, P->mv_done[k], 0));
+        SVH_CUDA(cudaMemcpyAsync(P->din[k], I_host + r0 * per, bytes, cudaMemcpyHostToDevice, P->h2d));
+        SVH_CUDA(cudaEventRecord(P->in_ready[k], P->h2d));
+        SVH_CUDA(cudaStreamWaitEvent(s, P->in_ready[k], 0));
+        if (c >= 2) SVH_CUDA(cudaStreamWaitEvent(s, P->out_done[k], 0));
+        matvec(h, P->din[k], P->dout[k], nr, green_only, true, s);
+        SVH_CUDA(cudaEventRecord(P->mv_done[k], s));
+        SVH_CUDA(cudaStreamWaitEvent(P->d2h, P->mv_done[k], 0));
+        SVH_CUDA(cudaMemcpyAsync(CC_host + r0 * per, P->dout[k], bytes, cudaMemcpyDeviceToHost, P->d2h));
+        SVH_CUDA(cudaEventRecord(P->out_done[k], P->d2h));
+    }
+    for (int k = 0; k < 2 && k < nch; ++k) SVH_CUDA(cudaStreamWaitEvent(s, P->out_done[k], 0));
+    SVH_CUDA(cudaStreamSynchronize(s));
+}
+
 }  // namespace svh

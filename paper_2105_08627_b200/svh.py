@@ -83,6 +83,7 @@ def lib():
         L.svh_embedding.argtypes = [vp, ctypes.POINTER(i32)]
         L.svh_plan_info.argtypes = [vp, ctypes.POINTER(i64)]
         L.svh_slab_sizes.argtypes = [vp, i32, ctypes.POINTER(i64)]
+        L.svh_matvec_host.argtypes = [vp, vp, vp, i32, i32, i32, vp]
         L.svh_slab_forward.argtypes = [vp, i32, i32, vp, vp, i32, vp]
         L.svh_slab_middle.argtypes = [vp, i32, i32, vp, vp, i32, vp]
         L.svh_slab_backward.argtypes = [vp, i32, i32, vp, vp, vp, i32, i32, vp]
@@ -102,7 +103,7 @@ def lib():
         L.svh_destroy.restype = None
         L.svh_last_error.restype = ctypes.c_char_p
         L.svh_launch_count.restype = i64
-        for name in ("svh_slab_sizes", "svh_slab_forward", "svh_slab_middle", "svh_slab_backward",
+        for name in ("svh_matvec_host", "svh_slab_sizes", "svh_slab_forward", "svh_slab_middle", "svh_slab_backward",
                      "svh_setup", "svh_set_frequency", "svh_unknowns", "svh_embedding", "svh_plan_info", "svh_matvec",
                      "svh_matvec_grid", "svh_apply_system", "svh_solve", "svh_solve_columns", "svh_get_kernels",
                      "svh_get_stats", "svh_profile_enable", "svh_profile_read", "svh_y_to_zl"):
@@ -112,7 +113,7 @@ def lib():
 
 
 EXPORTED = ("svh_default_opts", "svh_setup", "svh_set_frequency", "svh_unknowns", "svh_embedding", "svh_plan_info",
-            "svh_slab_sizes", "svh_slab_forward", "svh_slab_middle", "svh_slab_backward",
+            "svh_matvec_host", "svh_slab_sizes", "svh_slab_forward", "svh_slab_middle", "svh_slab_backward",
             "svh_matvec",
             "svh_matvec_grid", "svh_apply_system", "svh_solve", "svh_solve_columns", "svh_get_kernels",
             "svh_get_stats", "svh_profile_enable", "svh_profile_read", "svh_y_to_zl", "svh_destroy",
@@ -240,6 +241,16 @@ class Handle:
         _check(lib().svh_matvec(self._h, ctypes.c_void_p(Ib.data_ptr()), ctypes.c_void_p(o.data_ptr()),
                                 Ib.shape[0], int(green_only), _stream_ptr(stream)))
         return o[0] if squeeze and out is None else o
+
+    def matvec_host(self, I_host, out_host, green_only=False, chunk=0, stream=None):
+        """End-to-end product on host tensors (complex64 [nrhs, 5, K], pinned for overlap):
+        H2D / passes / D2H pipelined by libsvh; returns when out_host is filled."""
+        import torch
+        assert I_host.dtype == torch.complex64 and not I_host.is_cuda and I_host.is_contiguous()
+        assert out_host.shape == I_host.shape and out_host.dtype == torch.complex64 and not out_host.is_cuda
+        _check(lib().svh_matvec_host(self._h, ctypes.c_void_p(I_host.data_ptr()), ctypes.c_void_p(out_host.data_ptr()),
+                                     I_host.shape[0], int(green_only), int(chunk), _stream_ptr(stream)))
+        return out_host
 
     def matvec_grid(self, I, out=None, green_only=False, stream=None):
         """I: torch complex64 cuda tensor [nrhs, 5, kz, ky, kx]."""
