@@ -80,6 +80,8 @@ typedef struct {
     int32_t max_iters;    /* total GMRES iteration cap */
     int32_t rhs_chunk;    /* max RHS per internal matvec batch (workspace sizing); 0 = auto */
     int32_t verbose;      /* 0 quiet */
+    const char* kernel_cache;  /* NULL: kernels by quadrature; else an SVXT file (svh_kernel_cache_build):
+                                  the grid's Toeplitz tensors are restored from it (Alg. 2) */
 } svh_opts;
 
 typedef struct {
@@ -92,6 +94,13 @@ typedef struct {
     int32_t ranks[7][3];       /* Tucker multilinear ranks per kernel (0 if dense) */
     double  compression_ratio; /* dense octant spectra bytes / Tucker bytes (P:202 CR) */
 } svh_stats;
+
+/* svh_kernel_cache_build -- Algorithm 2, install stage: Tucker-compress the 7
+ * unit-voxel Toeplitz kernels on the offset domain nmax[0] x nmax[1] x nmax[2] (tolerance tol,
+ * Algorithm 1) and write them to `path` (format in csrc/cache.cu).  Any grid with K_i <=
+ * nmax[i] can then be set up with svh_opts.kernel_cache = path (no 6-D quadrature; restored
+ * kernels carry relative error <= tol).  Errors: SVH_EINVAL, SVH_ECACHE (I/O), SVH_ECUDA. */
+int svh_kernel_cache_build(const char* path, const int32_t* nmax, double tol, int32_t device);
 
 /* Default options (P:95 tol 1e-8 when Tucker is on, P:174 restart 50, RRE 1e-8, P:166 inner 1e-8). */
 void svh_default_opts(svh_opts* o);

@@ -266,7 +266,11 @@ int svh_setup(const svh_grid* grid, const uint8_t* mat_id, const svh_material* m
             h->omega = 2.0 * M_PI * freq_hz;
             update_local_terms(h);
             make_twiddles(h);
-            compute_kernels(h);
+            if (h->opts.kernel_cache)
+                kernel_cache_restore(h, h->opts.kernel_cache);   // Algorithm 2
+            else
+                compute_kernels(h);
+            h->opts.kernel_cache = nullptr;   // the caller's string is not kept
             if (h->opts.tucker_tol > 0) {
                 h->use_tucker = true;
                 compute_tucker(h);
@@ -281,6 +285,10 @@ int svh_setup(const svh_grid* grid, const uint8_t* mat_id, const svh_material* m
         h->t_setup = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         *out = h;
     });
+}
+
+int svh_kernel_cache_build(const char* path, const int32_t* nmax, double tol, int32_t device) {
+    return guarded([&] { kernel_cache_build(path, nmax, tol, device); });
 }
 
 int svh_set_frequency(svh_handle* h, double freq_hz) {

@@ -108,6 +108,9 @@ void slab_backward(svh_handle* h, int rank, int P, const float2* recv, const flo
                    bool green_only, cudaStream_t s);
 // quad.cu
 void compute_kernels(svh_handle* h);
+// cache.cu (Algorithm 2)
+void kernel_cache_build(const char* path, const int* nmax, double tol, int device);
+void kernel_cache_restore(svh_handle* h, const char* path);
 // spectra.cu
 void compute_spectra(svh_handle* h);
 void compute_tucker(svh_handle* h);

@@ -21,6 +21,7 @@
 // the ranks then match a direct SVD's.
 #include <algorithm>
 #include <cmath>
+#include <functional>
 #include <mutex>
 #include <vector>
 
@@ -276,8 +277,19 @@ void free_tucker(svh_handle* h) {
     }
 }
 
-void compute_tucker(svh_handle* h) {
-    const double tol = h->opts.tucker_tol;
+// Algorithm 1 on the 7 kernels of h->d_kern.  With a sink, each kernel's raw HOSVD
+// (ranks, all eigenvectors U_a column-major n_a x n_a of which the first d_a are kept, the
+// device fp64 core [d3][d2][d1], the measured error) goes to the sink (the install-time
+// cache of Algorithm 2) instead of becoming spectral factors.
+using TuckerSink = std::function<void(int q, const int* d, const std::vector<double>* U, const double* dCore,
+                                      double err)>;
+static void compute_tucker_impl(svh_handle* h, double tol, const TuckerSink& sink);
+
+void compute_tucker(svh_handle* h) { compute_tucker_impl(h, h->opts.tucker_tol, nullptr); }
+
+void tucker_hosvd_raw(svh_handle* h, double tol, const TuckerSink& sink) { compute_tucker_impl(h, tol, sink); }
+
+static void compute_tucker_impl(svh_handle* h, double tol, const TuckerSink& sink) {
     const int K3[3] = {h->kx, h->ky, h->kz};
     const int N3[3] = {h->nx, h->ny, h->nz};
     const int H3[3] = {h->hx, h->hy, h->hz};
@@ -400,6 +412,10 @@ void compute_tucker(svh_handle* h) {
                     grown = true;
                 }
             if (!grown) break;
+        }
+        if (sink) {
+            sink(q, d, U, dCore, err);
+            continue;
         }
         h->tucker.rel_err[q] = err;
         SVH_CHECK(d[0] <= 32 && d[2] <= 32, SVH_EINVAL,

@@ -47,7 +47,7 @@ class Port(ctypes.Structure):
 class Opts(ctypes.Structure):
     _fields_ = [("tucker_tol", ctypes.c_double), ("restart", ctypes.c_int32), ("rre", ctypes.c_double),
                 ("inner_tol", ctypes.c_double), ("inner_maxit", ctypes.c_int32), ("max_iters", ctypes.c_int32),
-                ("rhs_chunk", ctypes.c_int32), ("verbose", ctypes.c_int32)]
+                ("rhs_chunk", ctypes.c_int32), ("verbose", ctypes.c_int32), ("kernel_cache", ctypes.c_char_p)]
 
 
 class Stats(ctypes.Structure):
@@ -84,6 +84,7 @@ def lib():
         L.svh_plan_info.argtypes = [vp, ctypes.POINTER(i64)]
         L.svh_slab_sizes.argtypes = [vp, i32, ctypes.POINTER(i64)]
         L.svh_matvec_host.argtypes = [vp, vp, vp, i32, i32, i32, vp]
+        L.svh_kernel_cache_build.argtypes = [ctypes.c_char_p, ctypes.POINTER(i32), dbl, i32]
         L.svh_slab_forward.argtypes = [vp, i32, i32, vp, vp, i32, vp]
         L.svh_slab_middle.argtypes = [vp, i32, i32, vp, vp, i32, vp]
         L.svh_slab_backward.argtypes = [vp, i32, i32, vp, vp, vp, i32, i32, vp]
@@ -103,7 +104,7 @@ def lib():
         L.svh_destroy.restype = None
         L.svh_last_error.restype = ctypes.c_char_p
         L.svh_launch_count.restype = i64
-        for name in ("svh_matvec_host", "svh_slab_sizes", "svh_slab_forward", "svh_slab_middle", "svh_slab_backward",
+        for name in ("svh_kernel_cache_build", "svh_matvec_host", "svh_slab_sizes", "svh_slab_forward", "svh_slab_middle", "svh_slab_backward",
                      "svh_setup", "svh_set_frequency", "svh_unknowns", "svh_embedding", "svh_plan_info", "svh_matvec",
                      "svh_matvec_grid", "svh_apply_system", "svh_solve", "svh_solve_columns", "svh_get_kernels",
                      "svh_get_stats", "svh_profile_enable", "svh_profile_read", "svh_y_to_zl"):
@@ -113,7 +114,8 @@ def lib():
 
 
 EXPORTED = ("svh_default_opts", "svh_setup", "svh_set_frequency", "svh_unknowns", "svh_embedding", "svh_plan_info",
-            "svh_matvec_host", "svh_slab_sizes", "svh_slab_forward", "svh_slab_middle", "svh_slab_backward",
+            "svh_kernel_cache_build", "svh_matvec_host", "svh_slab_sizes", "svh_slab_forward", "svh_slab_middle",
+            "svh_slab_backward",
             "svh_matvec",
             "svh_matvec_grid", "svh_apply_system", "svh_solve", "svh_solve_columns", "svh_get_kernels",
             "svh_get_stats", "svh_profile_enable", "svh_profile_read", "svh_y_to_zl", "svh_destroy",
@@ -186,7 +188,7 @@ class Handle:
         L.svh_default_opts(ctypes.byref(o))
         o.tucker_tol = float(tucker_tol)
         for k, v in opts.items():
-            setattr(o, k, v)
+            setattr(o, k, v.encode() if isinstance(v, str) else v)
         h = ctypes.c_void_p()
         _check(L.svh_setup(ctypes.byref(g), mat.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), mats,
                            len(materials), float(freq), ctypes.byref(o), int(device), ctypes.byref(h)))
@@ -343,6 +345,13 @@ class Handle:
         st = Stats()
         _check(lib().svh_get_stats(self._h, ctypes.byref(st)))
         return st.as_dict()
+
+
+def kernel_cache_build(path, nmax, tol=1e-10, device=0):
+    """Algorithm 2 install stage (svh_kernel_cache_build): Tucker-compressed unit-voxel kernels on
+    the offset domain nmax = (Nx, Ny, Nz), written to `path`; use with setup(kernel_cache=path)."""
+    n = (ctypes.c_int32 * 3)(*[int(v) for v in nmax])
+    _check(lib().svh_kernel_cache_build(str(path).encode(), n, float(tol), int(device)))
 
 
 def setup_case(case, tucker_tol=None, device=0, **opts):
