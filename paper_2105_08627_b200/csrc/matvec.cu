@@ -1065,6 +1065,104 @@ __global__ void __launch_bounds__(160, 3)
     }
 }
 
+// Pass C, occupancy variant (dense octant spectra, Nz <= 32): the kernel values are kept for
+// kz <= Nz/2 only (K0, K1x, K1y, K2 are even in kz, K1z odd: 15 KB instead of 28 KB) and the
+// next RHS is not staged in registers but bulk-prefetched into L2 (cp.async.bulk.prefetch), so
+// a CTA needs <= 96 registers / thread and ~55 KB of shared memory: 4 CTAs (20 warps) per SM
+// instead of 3.  Same arithmetic as k_zmac.
+template <int N>
+constexpr size_t zmac2_smem() {
+    return (size_t)zmac_s_f2<N>() * sizeof(float2) + (size_t)7 * (N / 2 + 1) * 32 * sizeof(float);
+}
+
+template <int N>
+__global__ void __launch_bounds__(160, 4)
+    k_zmac2(float2* __restrict__ X2, SpecView sv, int Nx, int Ny, int Kz, float g, int nrhs, uint64_t pmask, int Nxs,
+            int kxg) {
+    constexpr int Q = 32, NH = N / 2, NK = N / 2 + 1;
+    extern __shared__ float2 S[];
+    float* KV = reinterpret_cast<float*>(S + zmac_s_f2<N>());   // [7][NK][Q]
+    const int tid = threadIdx.x;
+    const int c = tid >> 5, q = tid & 31;
+    const int kx0 = blockIdx.x * Q;
+    const int ky = blockIdx.y;
+    const int64_t plane = (int64_t)Nxs * Ny;
+    const bool ok = kx0 + q < Nxs;
+    const float2 zero = make_float2(0.f, 0.f);
+    float2* col = X2 + (int64_t)c * Kz * plane + (int64_t)ky * Nxs + kx0 + q;
+    const int64_t rstride = 5 * Kz * plane;
+    const uint32_t lm = ok ? (uint32_t)(pmask & ((1ull << min(Kz, NH)) - 1ull)) : 0u;
+    const int nb = min(Q, Nxs - kx0) * 8 / 16 * 16;
+    auto prefetch = [&](int r) {   // this tile's rows of RHS r -> L2
+        if (r < nrhs && tid < 5 * NH) {
+            const int cc = tid / NH, j = tid % NH;
+            if (j < Kz && ((pmask >> j) & 1u) && nb > 0) {
+                const float2* a = X2 + r * rstride + ((int64_t)cc * Kz + j) * plane + (int64_t)ky * Nxs + kx0;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a), "r"(nb) : "memory");
+            }
+        }
+    };
+    prefetch(0);
+    prefetch(1);
+    {
+        const int kx = min(kxg + kx0 + q, Nx - 1);
+        const int ox = kx <= (Nx >> 1) ? kx : Nx - kx;
+        const int oy = ky <= (Ny >> 1) ? ky : Ny - ky;
+        const float sx = kx <= (Nx >> 1) ? 1.f : -1.f, sy = ky <= (Ny >> 1) ? 1.f : -1.f;
+        const float fold[7] = {g, g * sx, g * sy, -2.f * g, g, g, 4.f * g};
+        const int64_t pl = (int64_t)sv.hx * sv.hy * sv.hz;
+#pragma unroll
+        for (int i = 0; i < (NK + 4) / 5; ++i) {
+            const int k = c + 5 * i;
+            if (k < NK) {
+                const int64_t o = ((int64_t)k * sv.hy + oy) * sv.hx + ox;
+#pragma unroll
+                for (int m = 0; m < 7; ++m) KV[(m * NK + k) * Q + q] = __ldg(&sv.spec[m * pl + o]) * fold[m];
+            }
+        }
+    }
+    const int w = c;
+    for (int r = 0; r < nrhs; ++r) {
+        float2 v[N];
+        const float2* src = col + r * rstride;
+#pragma unroll
+        for (int j = 0; j < N; ++j) v[j] = (j < NH && ((lm >> j) & 1u)) ? src[(int64_t)j * plane] : zero;
+        prefetch(r + 2);
+        reg_fft<N, -1, true>(v);
+#pragma unroll
+        for (int k = 0; k < N; ++k) S[(c * N + k) * Q + q] = v[k];
+        __syncthreads();
+#pragma unroll 1
+        for (int k = w; k < N; k += 5) {
+            const int kh = k <= NH ? k : N - k;
+            const float s3 = k <= NH ? 1.f : -1.f;   // K1z is odd in kz
+            float2* sp = S + k * Q + q;
+            const float* kp = KV + kh * Q + q;
+            const float2 Ix = sp[0 * N * Q], Iy = sp[1 * N * Q], Iz = sp[2 * N * Q];
+            const float2 I2 = sp[3 * N * Q], I3 = sp[4 * N * Q];
+            const float f0 = kp[0 * NK * Q], f1 = kp[1 * NK * Q], f2 = kp[2 * NK * Q], f3 = s3 * kp[3 * NK * Q];
+            const float f4 = kp[4 * NK * Q], f5 = kp[5 * NK * Q], f6 = kp[6 * NK * Q];
+            const float2 m1x = cadd(I2, I3), m1y = csub(I3, I2);
+            const float2 Qx = cfma_s(Ix, -f1, cmul_i(m1x, f4));
+            const float2 Qy = cfma_s(Iy, -f2, cmul_i(m1y, f5));
+            const float2 Qz = cfma_s(Iz, -f3, cmul_i(I3, f6));
+            sp[0 * N * Q] = cfma_s(m1x, f1, cmul_i(Ix, f0));
+            sp[1 * N * Q] = cfma_s(m1y, f2, cmul_i(Iy, f0));
+            sp[2 * N * Q] = cfma_s(I3, f3, cmul_i(Iz, f0));
+            sp[3 * N * Q] = csub(Qx, Qy);
+            sp[4 * N * Q] = cadd(cadd(Qx, Qy), Qz);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < N; ++k) v[k] = S[(c * N + k) * Q + q];
+        reg_fft<N, +1>(v);
+        float2* dst = col + r * rstride;
+#pragma unroll
+        for (int j = 0; j < NH; ++j)
+            if ((lm >> j) & 1u) dst[(int64_t)j * plane] = v[j];
+    }
+}
+
 // Pass C for Nz > 64: generic shared-memory FFT over 5Q pencils (smem_fft).
 template <int N>
 __global__ void __launch_bounds__(fft_max_threads(N))
@@ -1340,6 +1438,14 @@ void run_pass_c(svh_handle* h, const Geom& g, float2* X2, int nrhs, cudaStream_t
                 prep(kp, smem);
                 SVH_LAUNCH(kp, grid, 160, smem, s, X2, sv, h->nx, h->ny, h->kz, h->gscale, nrhs, (uint64_t)h->planemask,
                            g.nx, g.kx0, 1);
+                return;
+            }
+            static const int zmac2 = getenv("SVH_ZMAC2") ? atoi(getenv("SVH_ZMAC2")) : 1;
+            if (zmac2 && sv.spec) {
+                const size_t smem2 = zmac2_smem<N>();
+                prep(k_zmac2<N>, smem2);
+                SVH_LAUNCH((k_zmac2<N>), grid, 160, smem2, s, X2, sv, h->nx, h->ny, h->kz, h->gscale, nrhs,
+                           (uint64_t)h->planemask, g.nx, g.kx0);
                 return;
             }
             static const int zpre = getenv("SVH_ZPRE") ? atoi(getenv("SVH_ZPRE")) : 1;
