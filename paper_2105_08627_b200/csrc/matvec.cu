@@ -1070,18 +1070,22 @@ __global__ void __launch_bounds__(160, 3)
 // next RHS is not staged in registers but bulk-prefetched into L2 (cp.async.bulk.prefetch), so
 // a CTA needs <= 96 registers / thread and ~55 KB of shared memory: 4 CTAs (20 warps) per SM
 // instead of 3.  Same arithmetic as k_zmac.
-template <int N>
+template <int N, bool HALF = false>
 constexpr size_t zmac2_smem() {
-    return (size_t)zmac_s_f2<N>() * sizeof(float2) + (size_t)7 * (N / 2 + 1) * 32 * sizeof(float);
+    return (size_t)(HALF ? 5 * (N / 2) * 32 : zmac_s_f2<N>()) * sizeof(float2) +
+           (size_t)7 * (N / 2 + 1) * 32 * sizeof(float);
 }
 
-template <int N>
-__global__ void __launch_bounds__(160, 4)
+// HALF: the spectra buffer holds kz < N/2 and then kz >= N/2 (MAC in two rounds, 4 barriers
+// per RHS instead of 2) -- 35 KB of shared memory, 5 CTAs (25 warps) per SM.
+template <int N, bool HALF = false>
+__global__ void __launch_bounds__(160, HALF ? 5 : 4)
     k_zmac2(float2* __restrict__ X2, SpecView sv, int Nx, int Ny, int Kz, float g, int nrhs, uint64_t pmask, int Nxs,
             int kxg) {
     constexpr int Q = 32, NH = N / 2, NK = N / 2 + 1;
+    constexpr int NS = HALF ? N / 2 : N;                 // kz rows held in S at a time
     extern __shared__ float2 S[];
-    float* KV = reinterpret_cast<float*>(S + zmac_s_f2<N>());   // [7][NK][Q]
+    float* KV = reinterpret_cast<float*>(S + (HALF ? 5 * NS * Q : zmac_s_f2<N>()));   // [7][NK][Q]
     const int tid = threadIdx.x;
     const int c = tid >> 5, q = tid & 31;
     const int kx0 = blockIdx.x * Q;
@@ -1130,31 +1134,36 @@ __global__ void __launch_bounds__(160, 4)
         prefetch(r + 2);
         reg_fft<N, -1, true>(v);
 #pragma unroll
-        for (int k = 0; k < N; ++k) S[(c * N + k) * Q + q] = v[k];
-        __syncthreads();
-#pragma unroll 1
-        for (int k = w; k < N; k += 5) {
-            const int kh = k <= NH ? k : N - k;
-            const float s3 = k <= NH ? 1.f : -1.f;   // K1z is odd in kz
-            float2* sp = S + k * Q + q;
-            const float* kp = KV + kh * Q + q;
-            const float2 Ix = sp[0 * N * Q], Iy = sp[1 * N * Q], Iz = sp[2 * N * Q];
-            const float2 I2 = sp[3 * N * Q], I3 = sp[4 * N * Q];
-            const float f0 = kp[0 * NK * Q], f1 = kp[1 * NK * Q], f2 = kp[2 * NK * Q], f3 = s3 * kp[3 * NK * Q];
-            const float f4 = kp[4 * NK * Q], f5 = kp[5 * NK * Q], f6 = kp[6 * NK * Q];
-            const float2 m1x = cadd(I2, I3), m1y = csub(I3, I2);
-            const float2 Qx = cfma_s(Ix, -f1, cmul_i(m1x, f4));
-            const float2 Qy = cfma_s(Iy, -f2, cmul_i(m1y, f5));
-            const float2 Qz = cfma_s(Iz, -f3, cmul_i(I3, f6));
-            sp[0 * N * Q] = cfma_s(m1x, f1, cmul_i(Ix, f0));
-            sp[1 * N * Q] = cfma_s(m1y, f2, cmul_i(Iy, f0));
-            sp[2 * N * Q] = cfma_s(I3, f3, cmul_i(Iz, f0));
-            sp[3 * N * Q] = csub(Qx, Qy);
-            sp[4 * N * Q] = cadd(cadd(Qx, Qy), Qz);
-        }
-        __syncthreads();
+        for (int hh = 0; hh < (HALF ? 2 : 1); ++hh) {
+            const int k0 = hh * NS;   // kz rows [k0, k0 + NS) in S
 #pragma unroll
-        for (int k = 0; k < N; ++k) v[k] = S[(c * N + k) * Q + q];
+            for (int k = 0; k < NS; ++k) S[(c * NS + k) * Q + q] = v[k0 + k];
+            __syncthreads();
+#pragma unroll 1
+            for (int kk = w; kk < NS; kk += 5) {
+                const int k = k0 + kk;
+                const int kh = k <= NH ? k : N - k;
+                const float s3 = k <= NH ? 1.f : -1.f;   // K1z is odd in kz
+                float2* sp = S + kk * Q + q;
+                const float* kp = KV + kh * Q + q;
+                const float2 Ix = sp[0 * NS * Q], Iy = sp[1 * NS * Q], Iz = sp[2 * NS * Q];
+                const float2 I2 = sp[3 * NS * Q], I3 = sp[4 * NS * Q];
+                const float f0 = kp[0 * NK * Q], f1 = kp[1 * NK * Q], f2 = kp[2 * NK * Q], f3 = s3 * kp[3 * NK * Q];
+                const float f4 = kp[4 * NK * Q], f5 = kp[5 * NK * Q], f6 = kp[6 * NK * Q];
+                const float2 m1x = cadd(I2, I3), m1y = csub(I3, I2);
+                const float2 Qx = cfma_s(Ix, -f1, cmul_i(m1x, f4));
+                const float2 Qy = cfma_s(Iy, -f2, cmul_i(m1y, f5));
+                const float2 Qz = cfma_s(Iz, -f3, cmul_i(I3, f6));
+                sp[0 * NS * Q] = cfma_s(m1x, f1, cmul_i(Ix, f0));
+                sp[1 * NS * Q] = cfma_s(m1y, f2, cmul_i(Iy, f0));
+                sp[2 * NS * Q] = cfma_s(I3, f3, cmul_i(Iz, f0));
+                sp[3 * NS * Q] = csub(Qx, Qy);
+                sp[4 * NS * Q] = cadd(cadd(Qx, Qy), Qz);
+            }
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < NS; ++k) v[k0 + k] = S[(c * NS + k) * Q + q];   // own column
+        }
         reg_fft<N, +1>(v);
         float2* dst = col + r * rstride;
 #pragma unroll
@@ -1441,6 +1450,13 @@ void run_pass_c(svh_handle* h, const Geom& g, float2* X2, int nrhs, cudaStream_t
                 return;
             }
             static const int zmac2 = getenv("SVH_ZMAC2") ? atoi(getenv("SVH_ZMAC2")) : 1;
+            if (zmac2 == 2 && sv.spec && N >= 4) {
+                const size_t smem2 = zmac2_smem<N, true>();
+                prep(k_zmac2<N, true>, smem2);
+                SVH_LAUNCH((k_zmac2<N, true>), grid, 160, smem2, s, X2, sv, h->nx, h->ny, h->kz, h->gscale, nrhs,
+                           (uint64_t)h->planemask, g.nx, g.kx0);
+                return;
+            }
             if (zmac2 && sv.spec) {
                 const size_t smem2 = zmac2_smem<N>();
                 prep(k_zmac2<N>, smem2);
