@@ -1173,8 +1173,15 @@ __global__ void __launch_bounds__(160, HALF ? 5 : 4)
 }
 
 // Pass C for Nz > 64: generic shared-memory FFT over 5Q pencils (smem_fft).
+// CTA size: smem_fft needs >= 5 Q x max(R1, R2) threads; with Q = 1 and R1 = 64 (N >= 2048)
+// that is 320, above fft_max_threads(N)
 template <int N>
-__global__ void __launch_bounds__(fft_max_threads(N))
+constexpr int freq_big_threads() {
+    return fft_max_threads(N) > 5 * fft_threads_per_pencil(N) ? fft_max_threads(N) : 5 * fft_threads_per_pencil(N);
+}
+
+template <int N>
+__global__ void __launch_bounds__(freq_big_threads<N>())
     k_freq_big(float2* __restrict__ X2, SpecView sv, const float2* __restrict__ tw, int Nx, int Ny, int Kz, int Q,
                float g, const uint8_t* __restrict__ planeok, int Nxs, int kxg) {
     extern __shared__ float2 S[];

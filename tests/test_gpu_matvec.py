@@ -193,3 +193,33 @@ def test_matvec_host_pipeline(svh_lib):
             out = torch.empty_like(I).pin_memory()
             h.matvec_host(I.pin_memory(), out, chunk=chunk)
             assert torch.equal(out, dev), chunk
+
+
+# Maximum extents (svh_setup accepts K_i <= 2048 -> embeddings up to 4096 per axis): the
+# 4096-point row passes, the 4096-point strided fallback passes and the generic z pass
+# (k_freq_big) -- compared with the oracle on sampled output voxels.
+MAXES = [(2048, 3, 2), (2, 2048, 2), (3, 2, 1100)]
+
+
+@pytest.mark.parametrize("shape", MAXES)
+def test_matvec_max_extents_sampled(svh_lib, shape):
+    case = svh_inputs.random_fill(shape, fill=0.5, seed=sum(shape), n_mat=2)
+    lat = Lattice(case["mat_id"])
+    rows = np.sort(np.random.default_rng(5).choice(lat.K, 24, replace=False))
+    I = svh_inputs.currents(lat.K, 1, seed=17)
+    w = 2 * np.pi * case["freq"]
+    for go in (True, False):
+        ref = matvec_direct(lat, case["materials"], w, case["dx"], I, green_only=go, rows=rows)
+        got = gpu_matvec(svh_lib, case, I, green_only=go)[:, :, rows]
+        assert rel_l2(got, ref) < TOL, (go, rel_l2(got, ref))
+
+
+def test_setup_rejects_bad_grids(svh_lib):
+    """Degenerate / out-of-range inputs fail loudly through the C-ABI (no silent fallback)."""
+    ok = svh_inputs.random_fill((4, 4, 2), fill=0.5, seed=1)
+    empty = dict(ok, mat_id=np.zeros_like(ok["mat_id"]))
+    with pytest.raises(svh_lib.SvhError):
+        svh_lib.setup_case(empty)
+    big = dict(ok, mat_id=np.ones((1, 1, 2049), dtype=np.uint8))
+    with pytest.raises(svh_lib.SvhError):
+        svh_lib.setup_case(big)
