@@ -92,8 +92,10 @@ struct Solve {
     // PCG with device-side scalars, one CUDA graph per iteration (V-cycle included); the
     // graph is rebuilt whenever the AMG hierarchy is (port set change)
     cudaStream_t stream = nullptr;
-    cudaGraphExec_t pcg_graph = nullptr;
-    double* d_pcg = nullptr;         // [16]: rz, pq, rr, thr, alpha, beta, rz2, done (2 each)
+    std::vector<std::pair<int, cudaGraphExec_t>> pcg_graphs;   // per vector-pair count NVP
+    double* d_pcg = nullptr;         // [8][2 nvp_cap]: rz, pq, rr, thr, alpha, beta, rz2, done
+    int nvp_cap = 1;                 // vector pairs (ports) the level / work buffers hold
+    int pcg_cap = 0;
     double t_matvec = 0, t_precond = 0;
 };
 
@@ -256,154 +258,160 @@ __global__ void k_pre_a(const double2* __restrict__ c, const double2* __restrict
     }
 }
 
-// ---- AMG / PCG on [n][2] interleaved real vectors
-// y = A x (2 vectors)
-__device__ __forceinline__ double2 ell_row2(int n, int w, const int* __restrict__ ec, const double* __restrict__ ev,
-                                            const double2* __restrict__ x, int i) {
+// ---- AMG / PCG on NV = 2*NVP real vectors stored row-major [n][NV] (pairs as double2): one
+// pair per port (re, im of the Schur right-hand side); NVP = 1 is the single-port solve, NVP = B
+// the batched multi-port solve (the matrix and the cycle are shared by all B ports).
+// thread t -> row t / NVP, pair t % NVP (threads of a row share its ELL loads through L1)
+__global__ void k_spmvV(int n, int w, const int* __restrict__ ec, const double* __restrict__ ev,
+                        const double* __restrict__ x, double* __restrict__ y, int sh) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (n << sh)) return;
+    const int i = t >> sh, p = t & ((1 << sh) - 1);
+    const int NVP = 1 << sh;
+    const double2* x2 = reinterpret_cast<const double2*>(x);
     double a0 = 0, a1 = 0;
     for (int k = 0; k < w; ++k) {
         const double v = __ldg(&ev[(int64_t)k * n + i]);
-        const double2 xj = __ldg(&x[__ldg(&ec[(int64_t)k * n + i])]);
+        const double2 xj = __ldg(&x2[(int64_t)__ldg(&ec[(int64_t)k * n + i]) * NVP + p]);
         a0 = fma(v, xj.x, a0);
         a1 = fma(v, xj.y, a1);
     }
-    return make_double2(a0, a1);
-}
-__global__ void k_spmv2(int n, int w, const int* __restrict__ ec, const double* __restrict__ ev,
-                        const double* __restrict__ x, double* __restrict__ y) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    reinterpret_cast<double2*>(y)[i] = ell_row2(n, w, ec, ev, reinterpret_cast<const double2*>(x), i);
+    reinterpret_cast<double2*>(y)[t] = make_double2(a0, a1);
 }
 // l1-Jacobi sweep: xo = x + D^-1 (b - A x); x may be null (= zero initial guess)
-__global__ void k_jacobi2(int n, int w, const int* __restrict__ ec, const double* __restrict__ ev,
+__global__ void k_jacobiV(int n, int w, const int* __restrict__ ec, const double* __restrict__ ev,
                           const double* __restrict__ dinv, const double* __restrict__ b, const double* __restrict__ x,
-                          double* __restrict__ xo) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const double2 bi = reinterpret_cast<const double2*>(b)[i];
+                          double* __restrict__ xo, int sh) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (n << sh)) return;
+    const int i = t >> sh, p = t & ((1 << sh) - 1);
+    const int NVP = 1 << sh;
+    const double2 bi = reinterpret_cast<const double2*>(b)[t];
     const double d = dinv[i];
     double2 o;
     if (x) {
-        const double2 ax = ell_row2(n, w, ec, ev, reinterpret_cast<const double2*>(x), i);
-        const double2 xi = reinterpret_cast<const double2*>(x)[i];
-        o = make_double2(xi.x + d * (bi.x - ax.x), xi.y + d * (bi.y - ax.y));
+        const double2* x2 = reinterpret_cast<const double2*>(x);
+        double a0 = 0, a1 = 0;
+        for (int k = 0; k < w; ++k) {
+            const double v = __ldg(&ev[(int64_t)k * n + i]);
+            const double2 xj = x2[(int64_t)__ldg(&ec[(int64_t)k * n + i]) * NVP + p];
+            a0 = fma(v, xj.x, a0);
+            a1 = fma(v, xj.y, a1);
+        }
+        const double2 xi = x2[t];
+        o = make_double2(xi.x + d * (bi.x - a0), xi.y + d * (bi.y - a1));
     } else {
         o = make_double2(d * bi.x, d * bi.y);
     }
-    reinterpret_cast<double2*>(xo)[i] = o;
+    reinterpret_cast<double2*>(xo)[t] = o;
 }
 // r = b - A x
-__global__ void k_resid2(int n, int w, const int* __restrict__ ec, const double* __restrict__ ev,
-                         const double* __restrict__ b, const double* __restrict__ x, double* __restrict__ r) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const double2 ax = ell_row2(n, w, ec, ev, reinterpret_cast<const double2*>(x), i);
-    const double2 bi = reinterpret_cast<const double2*>(b)[i];
-    reinterpret_cast<double2*>(r)[i] = make_double2(bi.x - ax.x, bi.y - ax.y);
+__global__ void k_residV(int n, int w, const int* __restrict__ ec, const double* __restrict__ ev,
+                         const double* __restrict__ b, const double* __restrict__ x, double* __restrict__ r, int sh) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (n << sh)) return;
+    const int i = t >> sh, p = t & ((1 << sh) - 1);
+    const int NVP = 1 << sh;
+    const double2* x2 = reinterpret_cast<const double2*>(x);
+    double a0 = 0, a1 = 0;
+    for (int k = 0; k < w; ++k) {
+        const double v = __ldg(&ev[(int64_t)k * n + i]);
+        const double2 xj = x2[(int64_t)__ldg(&ec[(int64_t)k * n + i]) * NVP + p];
+        a0 = fma(v, xj.x, a0);
+        a1 = fma(v, xj.y, a1);
+    }
+    const double2 bi = reinterpret_cast<const double2*>(b)[t];
+    reinterpret_cast<double2*>(r)[t] = make_double2(bi.x - a0, bi.y - a1);
 }
 __global__ void k_zero(double* __restrict__ x, int64_t n) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) x[i] = 0.0;
 }
 // restriction: rc[agg[i]] += r[i]
-__global__ void k_restrict2(int n, const int* __restrict__ agg, const double* __restrict__ r, double* __restrict__ rc) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const int I = agg[i];
-    atomicAdd(&rc[2 * I], r[2 * i]);
-    atomicAdd(&rc[2 * I + 1], r[2 * i + 1]);
+__global__ void k_restrictV(int n, const int* __restrict__ agg, const double* __restrict__ r, double* __restrict__ rc,
+                            int sh) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (n << sh)) return;
+    const int i = t >> sh, p = t & ((1 << sh) - 1);
+    const int NVP = 1 << sh;
+    const int I = (agg[i] << sh) + p;
+    atomicAdd(&rc[2 * I], r[2 * t]);
+    atomicAdd(&rc[2 * I + 1], r[2 * t + 1]);
 }
 // prolongation: x[i] += ec[agg[i]]
-__global__ void k_prolong2(int n, const int* __restrict__ agg, const double* __restrict__ ec, double* __restrict__ x) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const int I = agg[i];
-    x[2 * i] += ec[2 * I];
-    x[2 * i + 1] += ec[2 * I + 1];
+__global__ void k_prolongV(int n, const int* __restrict__ agg, const double* __restrict__ ec, double* __restrict__ x,
+                           int sh) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (n << sh)) return;
+    const int i = t >> sh, p = t & ((1 << sh) - 1);
+    const int NVP = 1 << sh;
+    const int I = (agg[i] << sh) + p;
+    x[2 * t] += ec[2 * I];
+    x[2 * t + 1] += ec[2 * I + 1];
 }
-// dense coarse solve: x = Cinv b (2 vectors), one warp per row
-__global__ void k_dense2(int n, const double* __restrict__ Ci, const double* __restrict__ b, double* __restrict__ x) {
-    const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+// dense coarse solve: x = Cinv b, one warp per (row, pair)
+__global__ void k_denseV(int n, const double* __restrict__ Ci, const double* __restrict__ b, double* __restrict__ x,
+                         int sh) {
+    const int wid = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
     const int lane = threadIdx.x & 31;
-    if (row >= n) return;
+    if (wid >= (n << sh)) return;
+    const int row = wid >> sh, p = wid & ((1 << sh) - 1), NVP = 1 << sh;
     double a0 = 0, a1 = 0;
     for (int j = lane; j < n; j += 32) {
         const double w = Ci[(int64_t)row * n + j];
-        a0 += w * b[2 * j];
-        a1 += w * b[2 * j + 1];
+        a0 += w * b[2 * ((int64_t)j * NVP + p)];
+        a1 += w * b[2 * ((int64_t)j * NVP + p) + 1];
     }
     for (int o = 16; o > 0; o >>= 1) {
         a0 += __shfl_xor_sync(0xffffffff, a0, o);
         a1 += __shfl_xor_sync(0xffffffff, a1, o);
     }
     if (lane == 0) {
-        x[2 * row] = a0;
-        x[2 * row + 1] = a1;
+        x[2 * wid] = a0;
+        x[2 * wid + 1] = a1;
     }
 }
-// out[0..3] += (a . b) per component pair: out[0] = sum a0 b0, out[1] = sum a1 b1
-__global__ void k_dot2(int64_t n, const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ out) {
-    double s0 = 0, s1 = 0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        s0 += a[2 * i] * b[2 * i];
-        s1 += a[2 * i + 1] * b[2 * i + 1];
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        s0 += __shfl_xor_sync(0xffffffff, s0, o);
-        s1 += __shfl_xor_sync(0xffffffff, s1, o);
-    }
-    __shared__ double sh[2][32];
-    const int w = threadIdx.x / 32, l = threadIdx.x & 31;
-    if (l == 0) {
-        sh[0][w] = s0;
-        sh[1][w] = s1;
-    }
-    __syncthreads();
-    if (w == 0) {
-        s0 = l < blockDim.x / 32 ? sh[0][l] : 0;
-        s1 = l < blockDim.x / 32 ? sh[1][l] : 0;
-        for (int o = 16; o > 0; o >>= 1) {
-            s0 += __shfl_xor_sync(0xffffffff, s0, o);
-            s1 += __shfl_xor_sync(0xffffffff, s1, o);
-        }
-        if (l == 0) {
-            atomicAdd(&out[0], s0);
-            atomicAdd(&out[1], s1);
-        }
-    }
+// out[v] += sum_i a[i][v] b[i][v], v < NV = 2^(sh+1): with the grid stride a multiple of NV,
+// every thread keeps one fixed vector v = t & (NV-1); lanes of equal v reduce by shuffles
+__global__ void k_dotV(int n, const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ out,
+                       int sh) {
+    const int NV = 2 << sh;
+    const int tot = n * NV;
+    const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
+    double acc = 0;
+    for (int t = t0; t < tot; t += gridDim.x * blockDim.x) acc = fma(a[t], b[t], acc);
+    for (int o = 16; o >= NV; o >>= 1) acc += __shfl_xor_sync(0xffffffff, acc, o);
+    if ((threadIdx.x & 31) < NV && (threadIdx.x & 31) < 32) atomicAdd(&out[t0 & (NV - 1)], acc);
 }
-// x += alpha_c y (per component alpha[c]); y2 = ...
-__global__ void k_axpy2(int64_t n, const double* __restrict__ alpha, int sign, const double* __restrict__ y,
-                        double* __restrict__ x) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    x[2 * i] += sign * alpha[0] * y[2 * i];
-    x[2 * i + 1] += sign * alpha[1] * y[2 * i + 1];
+// x += sign alpha_v y (per vector v)
+__global__ void k_axpyV(int n, const double* __restrict__ alpha, int sign, const double* __restrict__ y,
+                        double* __restrict__ x, int sh) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (n << (sh + 1))) return;
+    x[i] += sign * alpha[i & ((2 << sh) - 1)] * y[i];
 }
-// p = z + beta p
-__global__ void k_xpby2(int64_t n, const double* __restrict__ z, const double* __restrict__ beta, double* __restrict__ p) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    p[2 * i] = z[2 * i] + beta[0] * p[2 * i];
-    p[2 * i + 1] = z[2 * i + 1] + beta[1] * p[2 * i + 1];
+// p = z + beta_v p
+__global__ void k_xpbyV(int n, const double* __restrict__ z, const double* __restrict__ beta,
+                        double* __restrict__ p, int sh) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (n << (sh + 1))) return;
+    p[i] = z[i] + beta[i & ((2 << sh) - 1)] * p[i];
 }
-
-// PCG scalars on the device (pc = Solve::d_pcg): 0 rz, 2 pq, 4 rr, 6 thr, 8 alpha, 10 beta,
-// 12 rz2, 14 done -- two independent real systems (re / im parts)
-__global__ void k_pcg_alpha(double* pc) {
-    const int c = threadIdx.x;
-    if (c < 2) pc[8 + c] = (pc[14 + c] != 0 || pc[2 + c] == 0) ? 0.0 : pc[0 + c] / pc[2 + c];
+// PCG scalars on the device, pc = Solve::d_pcg laid out [slot][NV]: slots 0 rz, 1 pq, 2 rr,
+// 3 thr, 4 alpha, 5 beta, 6 rz2, 7 done -- NV independent real systems
+__global__ void k_pcg_alpha(double* pc, int NV) {
+    const int v = threadIdx.x;
+    if (v < NV) pc[4 * NV + v] = (pc[7 * NV + v] != 0 || pc[NV + v] == 0) ? 0.0 : pc[v] / pc[NV + v];
 }
-__global__ void k_pcg_check(double* pc) {
-    const int c = threadIdx.x;
-    if (c < 2 && pc[4 + c] <= pc[6 + c]) pc[14 + c] = 1.0;
+__global__ void k_pcg_check(double* pc, int NV) {
+    const int v = threadIdx.x;
+    if (v < NV && pc[2 * NV + v] <= pc[3 * NV + v]) pc[7 * NV + v] = 1.0;
 }
-__global__ void k_pcg_beta(double* pc) {
-    const int c = threadIdx.x;
-    if (c < 2) {
-        pc[10 + c] = (pc[14 + c] != 0 || pc[0 + c] == 0) ? 0.0 : pc[12 + c] / pc[0 + c];
-        pc[0 + c] = pc[12 + c];
+__global__ void k_pcg_beta(double* pc, int NV) {
+    const int v = threadIdx.x;
+    if (v < NV) {
+        pc[5 * NV + v] = (pc[7 * NV + v] != 0 || pc[v] == 0) ? 0.0 : pc[6 * NV + v] / pc[v];
+        pc[v] = pc[6 * NV + v];
     }
 }
 
@@ -597,8 +605,8 @@ static void build_structure(svh_handle* h) {
 }
 
 static void drop_pcg_graph(Solve* S) {
-    if (S->pcg_graph) cudaGraphExecDestroy(S->pcg_graph);
-    S->pcg_graph = nullptr;
+    for (auto& g : S->pcg_graphs) cudaGraphExecDestroy(g.second);
+    S->pcg_graphs.clear();
 }
 static void free_levels(Solve* S) {
     drop_pcg_graph(S);
@@ -768,6 +776,7 @@ CsrHost galerkin(const CsrHost& A, const std::vector<int>& agg, int nc) {
     return C;
 }
 
+int g_upload_nvp = 1;   // vector pairs the level buffers are sized for (set by build_amg)
 CsrDev upload(const CsrHost& A) {
     CsrDev d;
     d.n = A.n;
@@ -803,7 +812,7 @@ CsrDev upload(const CsrHost& A) {
     SVH_CUDA(cudaMalloc(&d.eval, ev.size() * sizeof(double)));
     SVH_CUDA(cudaMemcpy(d.ecol, ec.data(), ec.size() * sizeof(int), cudaMemcpyHostToDevice));
     SVH_CUDA(cudaMemcpy(d.eval, ev.data(), ev.size() * sizeof(double), cudaMemcpyHostToDevice));
-    const size_t vb = (size_t)2 * std::max(1, A.n) * sizeof(double);
+    const size_t vb = (size_t)2 * std::max(1, A.n) * sizeof(double) * g_upload_nvp;
     SVH_CUDA(cudaMalloc(&d.vb, vb));
     SVH_CUDA(cudaMalloc(&d.vx, vb));
     SVH_CUDA(cudaMalloc(&d.tmp, vb));
@@ -851,10 +860,12 @@ std::vector<double> dense_inverse(const CsrHost& A) {
 
 }  // namespace
 
-static void build_amg(svh_handle* h, const std::vector<int32_t>& fixed) {
+static void build_amg(svh_handle* h, const std::vector<int32_t>& fixed, int nvp) {
     Solve* S = h->solve;
-    if (!S->levels.empty() && fixed == S->fixed_nodes) return;
+    if (!S->levels.empty() && fixed == S->fixed_nodes && nvp <= S->nvp_cap) return;
     free_levels(S);
+    S->nvp_cap = std::max(1, nvp);
+    g_upload_nvp = S->nvp_cap;
     S->fixed_nodes = fixed;
     std::vector<uint8_t> fr(S->M, 1);
     for (int32_t r : fixed) fr[r] = 0;
@@ -910,7 +921,7 @@ static void build_amg(svh_handle* h, const std::vector<int32_t>& fixed) {
 // host: solver workspace and operators
 static void ensure_work(svh_handle* h, int restart) {
     Solve* S = h->solve;
-    const size_t need = (size_t)2 * std::max<int64_t>(S->nf, 1);
+    const size_t need = (size_t)2 * std::max<int64_t>(S->nf, 1) * S->nvp_cap;
     if (S->wsize < need) {
         drop_pcg_graph(S);
         for (auto& b : S->wbuf) cudaFree(b);
@@ -943,106 +954,125 @@ static void apply_sys(svh_handle* h, const double2* x, double2* y, bool masked, 
                S->M);
 }
 
-// AMG V-cycle on level l: x = B^-1 b (x overwritten), 2 vectors, V(2,2) l1-Jacobi
-static void vcycle(Solve* S, int l, const double* b, double* x, cudaStream_t s) {
+// AMG cycle on level l: x = B^-1 b (x overwritten) for NVP vector pairs, V(2,2) l1-Jacobi,
+// W-cycle on the top levels
+static void vcycle(Solve* S, int l, const double* b, double* x, cudaStream_t s, int NVP) {
+    const int sh = __builtin_ctz(NVP);
     const CsrDev& L = S->levels[l];
     const int n = L.n;
+    const int64_t nt = (int64_t)n * NVP;
     if (l == (int)S->levels.size() - 1) {
-        SVH_LAUNCH(k_dense2, nblk(n, 8), 256, 0, s, n, S->d_cinv, b, x);
+        SVH_LAUNCH(k_denseV, nblk(nt, 8), 256, 0, s, n, S->d_cinv, b, x, sh);
         return;
     }
     const CsrDev& C = S->levels[l + 1];
     double* rc = C.vb;
     double* ec = C.vx;
-    SVH_LAUNCH(k_jacobi2, nblk(n), 256, 0, s, n, L.ellw, L.ecol, L.eval, L.dinv, b, (const double*)nullptr, x);
-    SVH_LAUNCH(k_jacobi2, nblk(n), 256, 0, s, n, L.ellw, L.ecol, L.eval, L.dinv, b, x, L.x2);
-    SVH_LAUNCH(k_resid2, nblk(n), 256, 0, s, n, L.ellw, L.ecol, L.eval, b, L.x2, L.tmp);
-    SVH_LAUNCH(k_zero, nblk(2 * L.nc), 256, 0, s, rc, (int64_t)2 * L.nc);
-    SVH_LAUNCH(k_restrict2, nblk(n), 256, 0, s, n, L.agg, L.tmp, rc);
-    vcycle(S, l + 1, rc, ec, s);
-    SVH_LAUNCH(k_prolong2, nblk(n), 256, 0, s, n, L.agg, ec, L.x2);
+    const int64_t ncv = 2LL * L.nc * NVP;
+    SVH_LAUNCH(k_jacobiV, nblk(nt), 256, 0, s, n, L.ellw, L.ecol, L.eval, L.dinv, b, (const double*)nullptr, x, sh);
+    SVH_LAUNCH(k_jacobiV, nblk(nt), 256, 0, s, n, L.ellw, L.ecol, L.eval, L.dinv, b, x, L.x2, sh);
+    SVH_LAUNCH(k_residV, nblk(nt), 256, 0, s, n, L.ellw, L.ecol, L.eval, b, L.x2, L.tmp, sh);
+    SVH_LAUNCH(k_zero, nblk(ncv), 256, 0, s, rc, ncv);
+    SVH_LAUNCH(k_restrictV, nblk(nt), 256, 0, s, n, L.agg, L.tmp, rc, sh);
+    vcycle(S, l + 1, rc, ec, s, NVP);
+    SVH_LAUNCH(k_prolongV, nblk(nt), 256, 0, s, n, L.agg, ec, L.x2, sh);
     static const int wlev = getenv("SVH_AMG_W") ? atoi(getenv("SVH_AMG_W")) : 2;
     if (l < wlev) {   // W-cycle on the top levels: second coarse-grid correction
-        SVH_LAUNCH(k_resid2, nblk(n), 256, 0, s, n, L.ellw, L.ecol, L.eval, b, L.x2, L.tmp);
-        SVH_LAUNCH(k_zero, nblk(2 * L.nc), 256, 0, s, rc, (int64_t)2 * L.nc);
-        SVH_LAUNCH(k_restrict2, nblk(n), 256, 0, s, n, L.agg, L.tmp, rc);
-        vcycle(S, l + 1, rc, ec, s);
-        SVH_LAUNCH(k_prolong2, nblk(n), 256, 0, s, n, L.agg, ec, L.x2);
+        SVH_LAUNCH(k_residV, nblk(nt), 256, 0, s, n, L.ellw, L.ecol, L.eval, b, L.x2, L.tmp, sh);
+        SVH_LAUNCH(k_zero, nblk(ncv), 256, 0, s, rc, ncv);
+        SVH_LAUNCH(k_restrictV, nblk(nt), 256, 0, s, n, L.agg, L.tmp, rc, sh);
+        vcycle(S, l + 1, rc, ec, s, NVP);
+        SVH_LAUNCH(k_prolongV, nblk(nt), 256, 0, s, n, L.agg, ec, L.x2, sh);
     }
-    SVH_LAUNCH(k_jacobi2, nblk(n), 256, 0, s, n, L.ellw, L.ecol, L.eval, L.dinv, b, L.x2, x);
-    SVH_LAUNCH(k_jacobi2, nblk(n), 256, 0, s, n, L.ellw, L.ecol, L.eval, L.dinv, b, x, L.x2);
-    SVH_CUDA(cudaMemcpyAsync(x, L.x2, 2 * (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    SVH_LAUNCH(k_jacobiV, nblk(nt), 256, 0, s, n, L.ellw, L.ecol, L.eval, L.dinv, b, L.x2, x, sh);
+    SVH_LAUNCH(k_jacobiV, nblk(nt), 256, 0, s, n, L.ellw, L.ecol, L.eval, L.dinv, b, x, L.x2, sh);
+    SVH_CUDA(cudaMemcpyAsync(x, L.x2, 2 * (size_t)nt * sizeof(double), cudaMemcpyDeviceToDevice, s));
 }
 
-// PCG on S (level 0) for 2 real RHS: x = S^-1 b to relative tol.  All scalars stay on the
-// device; one iteration (SpMV, 3 dot products, the scalar updates and the whole AMG cycle,
-// ~250 kernels) is a CUDA graph captured once per hierarchy and replayed, and the host
-// reads the convergence flags every kCheck iterations -- the solve is launch-latency
-// bound otherwise (P:166 AGMG-CG; reading G15).
-static int pcg2(svh_handle* h, const double* b, double* x, double tol, int maxit, cudaStream_t s) {
+// PCG on S (level 0) for NV = 2 NVP real right-hand sides (re / im of NVP ports): x = S^-1 b
+// to relative tol per vector.  All scalars stay on the device; one iteration (SpMV, 3 dot
+// products, the scalar updates and the whole AMG cycle, ~250 kernels) is a CUDA graph captured
+// once per hierarchy and NVP and replayed, and the host reads the convergence flags every
+// kCheck iterations -- the solve is launch-latency bound otherwise (P:166 AGMG-CG; G15).
+static int pcgV(svh_handle* h, const double* b, double* x, double tol, int maxit, cudaStream_t s, int NVP) {
     Solve* S = h->solve;
     const CsrDev& A = S->levels[0];
     const int n = A.n;
+    const int NV = 2 * NVP;
+    const int sh = __builtin_ctz(NVP);
+    SVH_CHECK((NVP & (NVP - 1)) == 0 && NVP <= 16, SVH_EINVAL, "pcg: vector pairs must be a power of two <= 16");
+    const int64_t nt = (int64_t)n * NVP, nd = 2 * nt;
     double* r = S->wbuf[0];
     double* z = S->wbuf[1];
     double* p = S->wbuf[2];
     double* q = S->wbuf[3];
     double* pc = S->d_pcg;
-    auto dot = [&](const double* a, const double* bb, double* out2) {
-        SVH_CUDA(cudaMemsetAsync(out2, 0, 2 * sizeof(double), s));
-        SVH_LAUNCH(k_dot2, 296, 256, 0, s, (int64_t)n, a, bb, out2);
+    auto dot = [&](const double* a, const double* bb, double* out) {
+        SVH_CUDA(cudaMemsetAsync(out, 0, NV * sizeof(double), s));
+        SVH_LAUNCH(k_dotV, 296, 256, 0, s, n, a, bb, out, sh);
     };
     auto iteration = [&] {
-        SVH_LAUNCH(k_spmv2, nblk(n), 256, 0, s, n, A.ellw, A.ecol, A.eval, p, q);
-        dot(p, q, pc + 2);
-        SVH_LAUNCH(k_pcg_alpha, 1, 32, 0, s, pc);
-        SVH_LAUNCH(k_axpy2, nblk(n), 256, 0, s, (int64_t)n, pc + 8, +1, p, x);
-        SVH_LAUNCH(k_axpy2, nblk(n), 256, 0, s, (int64_t)n, pc + 8, -1, q, r);
-        dot(r, r, pc + 4);
-        SVH_LAUNCH(k_pcg_check, 1, 32, 0, s, pc);
-        vcycle(S, 0, r, z, s);
-        dot(r, z, pc + 12);
-        SVH_LAUNCH(k_pcg_beta, 1, 32, 0, s, pc);
-        SVH_LAUNCH(k_xpby2, nblk(n), 256, 0, s, (int64_t)n, z, pc + 10, p);
+        SVH_LAUNCH(k_spmvV, nblk(nt), 256, 0, s, n, A.ellw, A.ecol, A.eval, p, q, sh);
+        dot(p, q, pc + 1 * NV);
+        SVH_LAUNCH(k_pcg_alpha, 1, 64, 0, s, pc, NV);
+        SVH_LAUNCH(k_axpyV, nblk(nd), 256, 0, s, n, pc + 4 * NV, +1, p, x, sh);
+        SVH_LAUNCH(k_axpyV, nblk(nd), 256, 0, s, n, pc + 4 * NV, -1, q, r, sh);
+        dot(r, r, pc + 2 * NV);
+        SVH_LAUNCH(k_pcg_check, 1, 64, 0, s, pc, NV);
+        vcycle(S, 0, r, z, s, NVP);
+        dot(r, z, pc + 6 * NV);
+        SVH_LAUNCH(k_pcg_beta, 1, 64, 0, s, pc, NV);
+        SVH_LAUNCH(k_xpbyV, nblk(nd), 256, 0, s, n, z, pc + 5 * NV, p, sh);
     };
-    // b.b -> thresholds thr = tol^2 b.b; done if b = 0
-    dot(b, b, pc + 4);
-    double bn[2];
-    SVH_CUDA(cudaMemcpyAsync(bn, pc + 4, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    // b.b -> thresholds thr = tol^2 b.b; vectors with b = 0 are done from the start
+    dot(b, b, pc + 2 * NV);
+    std::vector<double> bn(NV);
+    SVH_CUDA(cudaMemcpyAsync(bn.data(), pc + 2 * NV, NV * sizeof(double), cudaMemcpyDeviceToHost, s));
     SVH_CUDA(cudaStreamSynchronize(s));
-    SVH_LAUNCH(k_zero, nblk(2 * n), 256, 0, s, x, (int64_t)2 * n);
-    if (bn[0] == 0 && bn[1] == 0) return 0;
-    const double init[16] = {0, 0, 0, 0, 0, 0, tol * tol * bn[0], tol * tol * bn[1],
-                             0, 0, 0, 0, 0, 0, bn[0] == 0 ? 1.0 : 0.0, bn[1] == 0 ? 1.0 : 0.0};
-    SVH_CUDA(cudaMemcpyAsync(pc, init, sizeof(init), cudaMemcpyHostToDevice, s));
-    SVH_CUDA(cudaMemcpyAsync(r, b, 2 * n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    vcycle(S, 0, r, z, s);
-    SVH_CUDA(cudaMemcpyAsync(p, z, 2 * n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    dot(r, z, pc + 0);
+    SVH_LAUNCH(k_zero, nblk(nd), 256, 0, s, x, nd);
+    bool any = false;
+    std::vector<double> init(8 * NV, 0.0);
+    for (int v = 0; v < NV; ++v) {
+        init[3 * NV + v] = tol * tol * bn[v];
+        init[7 * NV + v] = bn[v] == 0 ? 1.0 : 0.0;
+        any = any || bn[v] != 0;
+    }
+    if (!any) return 0;
+    SVH_CUDA(cudaMemcpyAsync(pc, init.data(), init.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+    SVH_CUDA(cudaMemcpyAsync(r, b, nd * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    vcycle(S, 0, r, z, s, NVP);
+    SVH_CUDA(cudaMemcpyAsync(p, z, nd * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    dot(r, z, pc + 0 * NV);
     static const bool use_graph = getenv("SVH_NO_PCG_GRAPH") == nullptr;
-    if (use_graph && !S->pcg_graph && s != nullptr) {
+    cudaGraphExec_t gx = nullptr;
+    for (auto& gg : S->pcg_graphs)
+        if (gg.first == NVP) gx = gg.second;
+    if (use_graph && !gx && s != nullptr) {
         cudaGraph_t g = nullptr;
         SVH_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
         iteration();
         SVH_CUDA(cudaStreamEndCapture(s, &g));
-        SVH_CUDA(cudaGraphInstantiate(&S->pcg_graph, g, 0));
+        SVH_CUDA(cudaGraphInstantiate(&gx, g, 0));
         cudaGraphDestroy(g);
+        S->pcg_graphs.push_back({NVP, gx});
     }
     constexpr int kCheck = 8;
     int it = 0;
-    double done[2];
+    std::vector<double> done(NV);
     while (it < maxit) {
         const int nb = std::min(kCheck, maxit - it);
         for (int k = 0; k < nb; ++k) {
-            if (S->pcg_graph)
-                SVH_CUDA(cudaGraphLaunch(S->pcg_graph, s));
+            if (gx)
+                SVH_CUDA(cudaGraphLaunch(gx, s));
             else
                 iteration();
         }
         it += nb;
-        SVH_CUDA(cudaMemcpyAsync(done, pc + 14, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+        SVH_CUDA(cudaMemcpyAsync(done.data(), pc + 7 * NV, NV * sizeof(double), cudaMemcpyDeviceToHost, s));
         SVH_CUDA(cudaStreamSynchronize(s));
-        if (done[0] != 0 && done[1] != 0) break;
+        bool all = true;
+        for (int v = 0; v < NV; ++v) all = all && done[v] != 0;
+        if (all) break;
     }
     return it;
 }
@@ -1058,7 +1088,7 @@ static void precond(svh_handle* h, const double2* in, double2* out, double tol, 
     if (S->nf > 0) {
         SVH_LAUNCH(k_pre_e2, nblk(S->nf), 256, 0, s, tt, in + n5, e2, S->d_free_list, S->d_node_vox, S->d_node_axis, K,
                    S->nf);
-        S->inner_its += pcg2(h, e2, b2, tol, maxit, s);
+        S->inner_its += pcgV(h, e2, b2, tol, maxit, s, 1);
     }
     SVH_LAUNCH(k_pre_b, nblk(S->M), 256, 0, s, b2, in + n5, out + n5, S->d_node2free, S->M);
     SVH_LAUNCH(k_pre_a, nblk(K), 256, 0, s, in, out + n5, S->d_yinv, out, S->d_fnode, S->d_free, K);
@@ -1251,11 +1281,16 @@ static void solve_columns(svh_handle* h, const svh_port* ports, int P, const int
     Solve* S = h->solve;
     auto t0 = std::chrono::steady_clock::now();
     PortSets ps = port_sets(h, ports, P);
-    build_amg(h, ps.fixed);
+    build_amg(h, ps.fixed, 1);
     const int m = std::max(1, h->opts.restart);
     ensure_work(h, m);
     if (!S->stream) SVH_CUDA(cudaStreamCreateWithFlags(&S->stream, cudaStreamNonBlocking));
-    if (!S->d_pcg) SVH_CUDA(cudaMalloc(&S->d_pcg, 16 * sizeof(double)));
+    if (!S->d_pcg || S->pcg_cap < S->nvp_cap) {
+        drop_pcg_graph(S);
+        cudaFree(S->d_pcg);
+        SVH_CUDA(cudaMalloc(&S->d_pcg, 16 * (size_t)S->nvp_cap * sizeof(double)));
+        S->pcg_cap = S->nvp_cap;
+    }
     cudaStream_t s = S->stream;
     SVH_CUDA(cudaDeviceSynchronize());   // setup copies (legacy stream) before the non-blocking stream
     const int64_t N = S->N;
