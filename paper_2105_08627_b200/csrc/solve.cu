@@ -235,6 +235,23 @@ __global__ void k_pre_e2(const double2* __restrict__ t, const double2* __restric
     e2[2 * f] = at.x - d[r].x;
     e2[2 * f + 1] = at.y - d[r].y;
 }
+// batched variants: the Schur right-hand side / solution of port slot p is pair p of [nf][NVP]
+__global__ void k_pre_e2V(const double2* __restrict__ t, const double2* __restrict__ d, double* __restrict__ e2,
+                          const int32_t* __restrict__ free_list, const int32_t* __restrict__ nv,
+                          const int8_t* __restrict__ na, int64_t K, int nf, int NVP, int p) {
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= nf) return;
+    const int r = free_list[f];
+    const double2 at = apply_A_node(t, K, r, nv, na);
+    reinterpret_cast<double2*>(e2)[(int64_t)f * NVP + p] = make_double2(at.x - d[r].x, at.y - d[r].y);
+}
+__global__ void k_pre_bV(const double* __restrict__ b2, const double2* __restrict__ d, double2* __restrict__ outphi,
+                         const int32_t* __restrict__ node2free, int64_t M, int NVP, int p) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= M) return;
+    const int f = node2free[r];
+    outphi[r] = f >= 0 ? reinterpret_cast<const double2*>(b2)[(int64_t)f * NVP + p] : d[r];
+}
 // b[node] = b2 (free) or d (fixed); stored into out Phi part
 __global__ void k_pre_b(const double* __restrict__ b2, const double2* __restrict__ d, double2* __restrict__ outphi,
                         const int32_t* __restrict__ node2free, int64_t M) {
@@ -1203,6 +1220,189 @@ static int fgmres(svh_handle* h, const double2* b, double2* x, double rre, int m
     return total;
 }
 
+// Batched FGMRES over B ports in lockstep (time to the L-matrix): every port keeps its own
+// Krylov space, Hessenberg and restart cycle, but each iteration applies the preconditioner to
+// all active ports with ONE PCG on 2 NVP real right-hand sides (the AMG hierarchy, its matrices
+// and the ~250-kernel cycle are shared, so the matrix traffic and launch latency are paid once
+// per iteration instead of once per port) and the operator with ONE B-RHS matvec.
+struct BatchWork {
+    int B = 0, m = 0;
+    int64_t N = 0;
+    double2* kry = nullptr;   // per port: V (m+1), Z (m), w, r   -> (2m+3) N
+    float2* cin = nullptr;    // [B][5K] complex64 operator input / output
+    float2* cout = nullptr;
+    double2* base(int p) const { return kry + (size_t)p * (2 * m + 3) * N; }
+    double2* V(int p, int j) const { return base(p) + (size_t)j * N; }
+    double2* Z(int p, int j) const { return base(p) + (size_t)(m + 1 + j) * N; }
+    double2* w(int p) const { return base(p) + (size_t)(2 * m + 1) * N; }
+    double2* r(int p) const { return base(p) + (size_t)(2 * m + 2) * N; }
+    void release() {
+        cudaFree(kry);
+        cudaFree(cin);
+        cudaFree(cout);
+        kry = nullptr;
+        cin = cout = nullptr;
+    }
+};
+
+static void fgmres_batch(svh_handle* h, BatchWork& W, int nb, double2* const* bb, double2* const* xx, double rre,
+                         int maxit, int NVP, std::vector<double>& final_rre, std::vector<int>& its, cudaStream_t s) {
+    Solve* S = h->solve;
+    const int64_t N = S->N, K = h->K, n5 = 5 * K;
+    const int m = W.m;
+    const double tol_inner = h->opts.inner_tol;
+    const int inner_max = h->opts.inner_maxit;
+    double* hcol = S->d_red + 16;
+    struct St {
+        double bnorm = 0;
+        bool done = false;     // converged (or zero right-hand side)
+        bool incycle = false;  // taking part in the current restart cycle
+        int j = 0;             // Krylov vectors of the current cycle
+        std::vector<cd> H, cs, sn, g;
+    };
+    std::vector<St> st(nb);
+    final_rre.assign(nb, 1.0);
+    its.assign(nb, 0);
+    for (int p = 0; p < nb; ++p) {
+        st[p].bnorm = cnorm(h, bb[p], s);
+        SVH_CUDA(cudaMemsetAsync(xx[p], 0, N * sizeof(double2), s));
+        if (st[p].bnorm == 0) {
+            st[p].done = true;
+            final_rre[p] = 0;
+        }
+    }
+    double* e2 = S->wbuf[4];
+    double* b2 = S->wbuf[5];
+    while (true) {
+        // cycle start: true residual of every unconverged port
+        int nin = 0;
+        for (int p = 0; p < nb; ++p) {
+            St& P = st[p];
+            P.incycle = false;
+            if (P.done || its[p] >= maxit) continue;
+            apply_sys(h, xx[p], W.w(p), true, s);
+            SVH_LAUNCH(k_csub, nblk(N), 256, 0, s, N, bb[p], W.w(p), W.r(p));
+            const double beta = cnorm(h, W.r(p), s);
+            final_rre[p] = beta / P.bnorm;
+            if (final_rre[p] <= rre) {
+                P.done = true;
+                continue;
+            }
+            SVH_LAUNCH(k_cscale, nblk(N), 256, 0, s, N, W.r(p), 1.0 / beta, W.V(p, 0));
+            P.H.assign((size_t)(m + 1) * m, 0.0);
+            P.cs.assign(m, 0.0);
+            P.sn.assign(m, 0.0);
+            P.g.assign(m + 1, 0.0);
+            P.g[0] = beta;
+            P.j = 0;
+            P.incycle = true;
+            ++nin;
+        }
+        if (nin == 0) break;
+        for (int j = 0; j < m; ++j) {
+            std::vector<int> act;
+            for (int p = 0; p < nb; ++p)
+                if (st[p].incycle && st[p].j == j && its[p] < maxit) act.push_back(p);
+            if (act.empty()) break;
+            // ---- preconditioner, all active ports at once
+            SVH_CUDA(cudaMemsetAsync(e2, 0, 2 * (size_t)std::max(S->nf, 1) * NVP * sizeof(double), s));
+            for (int p : act) {
+                SVH_LAUNCH(k_pre_e, nblk(n5), 256, 0, s, W.V(p, j), S->d_yinv, W.w(p), n5);
+                if (S->nf > 0)
+                    SVH_LAUNCH(k_pre_e2V, nblk(S->nf), 256, 0, s, W.w(p), W.V(p, j) + n5, e2, S->d_free_list,
+                               S->d_node_vox, S->d_node_axis, K, S->nf, NVP, p);
+            }
+            auto c0 = std::chrono::steady_clock::now();
+            if (S->nf > 0) S->inner_its += pcgV(h, e2, b2, tol_inner, inner_max, s, NVP);
+            for (int p : act) {
+                SVH_LAUNCH(k_pre_bV, nblk(S->M), 256, 0, s, b2, W.V(p, j) + n5, W.Z(p, j) + n5, S->d_node2free, S->M,
+                           NVP, p);
+                SVH_LAUNCH(k_pre_a, nblk(K), 256, 0, s, W.V(p, j), W.Z(p, j) + n5, S->d_yinv, W.Z(p, j), S->d_fnode,
+                           S->d_free, K);
+            }
+            SVH_CUDA(cudaStreamSynchronize(s));
+            auto c1 = std::chrono::steady_clock::now();
+            // ---- operator, one matvec over the batch: w = A Z_j
+            for (int p : act) SVH_LAUNCH(k_to_c64, nblk(n5), 256, 0, s, W.Z(p, j), W.cin + (size_t)p * n5, n5);
+            matvec(h, W.cin, W.cout, nb, false, true, s);
+            for (int p : act) {
+                SVH_LAUNCH(k_sys_I, nblk(K), 256, 0, s, W.cout + (size_t)p * n5, W.Z(p, j), W.w(p), S->d_fnode,
+                           S->d_free, K);
+                SVH_LAUNCH(k_sys_Phi, nblk(S->M), 256, 0, s, W.Z(p, j), W.w(p), S->d_node_vox, S->d_node_axis,
+                           S->d_free, K, S->M);
+            }
+            SVH_CUDA(cudaStreamSynchronize(s));
+            auto c2 = std::chrono::steady_clock::now();
+            S->t_precond += std::chrono::duration<double>(c1 - c0).count();
+            S->t_matvec += std::chrono::duration<double>(c2 - c1).count();
+            // ---- per port: CGS2 and the Givens update (host)
+            for (int p : act) {
+                St& P = st[p];
+                double2* V = W.V(p, 0);
+                double2* w = W.w(p);
+                std::vector<cd> hj(j + 2, 0.0);
+                for (int pass = 0; pass < 2; ++pass) {
+                    SVH_CUDA(cudaMemsetAsync(hcol, 0, 2 * (j + 1) * sizeof(double), s));
+                    SVH_LAUNCH(k_cdots, dim3(148, j + 1), 256, 0, s, N, V, N, w, hcol);
+                    SVH_LAUNCH(k_cupdate, nblk(N), 256, 0, s, N, V, N, hcol, j + 1, w, 1.0);
+                    std::vector<double> hv(2 * (j + 1));
+                    SVH_CUDA(cudaMemcpyAsync(hv.data(), hcol, hv.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+                    SVH_CUDA(cudaStreamSynchronize(s));
+                    for (int i = 0; i <= j; ++i) hj[i] += cd(hv[2 * i], hv[2 * i + 1]);
+                }
+                const double hn = cnorm(h, w, s);
+                hj[j + 1] = hn;
+                if (hn > 0) SVH_LAUNCH(k_cscale, nblk(N), 256, 0, s, N, w, 1.0 / hn, W.V(p, j + 1));
+                for (int i = 0; i < j; ++i) {
+                    const cd t0 = std::conj(P.cs[i]) * hj[i] + std::conj(P.sn[i]) * hj[i + 1];
+                    const cd t1 = -P.sn[i] * hj[i] + P.cs[i] * hj[i + 1];
+                    hj[i] = t0;
+                    hj[i + 1] = t1;
+                }
+                const double den = std::sqrt(std::norm(hj[j]) + std::norm(hj[j + 1]));
+                P.cs[j] = den > 0 ? hj[j] / den : cd(1.0);
+                P.sn[j] = den > 0 ? hj[j + 1] / den : cd(0.0);
+                hj[j] = den;
+                hj[j + 1] = 0.0;
+                P.g[j + 1] = -P.sn[j] * P.g[j];
+                P.g[j] = std::conj(P.cs[j]) * P.g[j];
+                for (int i = 0; i <= j; ++i) P.H[(size_t)i * m + j] = hj[i];
+                P.j = j + 1;
+                ++its[p];
+                if (std::abs(P.g[j + 1]) / P.bnorm <= rre * 0.5 || hn == 0) P.incycle = false;   // cycle ends
+            }
+        }
+        // ---- cycle end: x_p += Z_p y_p
+        for (int p = 0; p < nb; ++p) {
+            St& P = st[p];
+            if (P.done || P.j == 0) continue;
+            const int jj = P.j;
+            std::vector<cd> y(jj);
+            for (int i = jj - 1; i >= 0; --i) {
+                cd acc = P.g[i];
+                for (int k = i + 1; k < jj; ++k) acc -= P.H[(size_t)i * m + k] * y[k];
+                y[i] = acc / P.H[(size_t)i * m + i];
+            }
+            std::vector<double> yv(2 * jj);
+            for (int i = 0; i < jj; ++i) {
+                yv[2 * i] = y[i].real();
+                yv[2 * i + 1] = y[i].imag();
+            }
+            SVH_CUDA(cudaMemcpyAsync(hcol, yv.data(), yv.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+            SVH_LAUNCH(k_cupdate, nblk(N), 256, 0, s, N, W.Z(p, 0), N, hcol, jj, xx[p], -1.0);
+            SVH_CUDA(cudaStreamSynchronize(s));
+            P.j = 0;
+        }
+    }
+    // final true residuals
+    for (int p = 0; p < nb; ++p) {
+        if (st[p].bnorm == 0) continue;
+        apply_sys(h, xx[p], W.w(p), true, s);
+        SVH_LAUNCH(k_csub, nblk(N), 256, 0, s, N, bb[p], W.w(p), W.r(p));
+        final_rre[p] = cnorm(h, W.r(p), s) / st[p].bnorm;
+    }
+}
+
 // ---------------------------------------------------------------------------
 struct PortSets {
     std::vector<std::vector<int32_t>> plus, minus;
@@ -1281,8 +1481,20 @@ static void solve_columns(svh_handle* h, const svh_port* ports, int P, const int
     Solve* S = h->solve;
     auto t0 = std::chrono::steady_clock::now();
     PortSets ps = port_sets(h, ports, P);
-    build_amg(h, ps.fixed, 1);
     const int m = std::max(1, h->opts.restart);
+    // batched multi-port solve (lockstep FGMRES, one shared PCG): batch size by memory, <= 16
+    static const int batch_env = getenv("SVH_SOLVE_BATCH") ? atoi(getenv("SVH_SOLVE_BATCH")) : 16;
+    int Bmax = std::min(nsel, std::max(1, std::min(16, batch_env)));
+    if (Bmax > 1) {
+        ensure_structure(h);
+        size_t fr = 0, tt = 0;
+        cudaMemGetInfo(&fr, &tt);
+        const size_t per = (size_t)(2 * m + 5) * S->N * sizeof(double2) + (size_t)10 * h->K * sizeof(float2);
+        Bmax = std::max(1, std::min(Bmax, (int)(0.5 * (double)fr / (double)per)));
+    }
+    int NVP = 1;
+    while (NVP < Bmax) NVP <<= 1;
+    build_amg(h, ps.fixed, NVP);
     ensure_work(h, m);
     if (!S->stream) SVH_CUDA(cudaStreamCreateWithFlags(&S->stream, cudaStreamNonBlocking));
     if (!S->d_pcg || S->pcg_cap < S->nvp_cap) {
@@ -1313,6 +1525,73 @@ static void solve_columns(svh_handle* h, const svh_port* ports, int P, const int
     S->inner_its = 0;
     S->t_matvec = S->t_precond = 0;
     (void)b;
+    auto port_currents = [&](const double2* xs, int si) {
+        for (int q = 0; q < P; ++q) {
+            SVH_CUDA(cudaMemcpyAsync(dnodes, ps.plus[q].data(), ps.plus[q].size() * sizeof(int32_t),
+                                     cudaMemcpyHostToDevice, s));
+            SVH_LAUNCH(k_port_current, 1, 256, 0, s, xs, dnodes, (int)ps.plus[q].size(), S->d_node_vox,
+                       S->d_node_axis, h->K, cur);
+            double c2[2];
+            SVH_CUDA(cudaMemcpyAsync(c2, cur, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+            SVH_CUDA(cudaStreamSynchronize(s));
+            Ycols[2 * ((size_t)si * P + q)] = c2[0];
+            Ycols[2 * ((size_t)si * P + q) + 1] = c2[1];
+        }
+    };
+    if (Bmax > 1) {
+        BatchWork W;
+        W.B = Bmax;
+        W.m = m;
+        W.N = N;
+        std::vector<double2*> bbs(Bmax, nullptr), xs(Bmax, nullptr);
+        auto release = [&] {
+            W.release();
+            for (auto q : bbs) cudaFree(q);
+            for (auto q : xs) cudaFree(q);
+        };
+        try {
+            SVH_CUDA(cudaMalloc(&W.kry, (size_t)Bmax * (2 * m + 3) * N * sizeof(double2)));
+            SVH_CUDA(cudaMalloc(&W.cin, (size_t)Bmax * 5 * h->K * sizeof(float2)));
+            SVH_CUDA(cudaMalloc(&W.cout, (size_t)Bmax * 5 * h->K * sizeof(float2)));
+            SVH_CUDA(cudaMemsetAsync(W.cin, 0, (size_t)Bmax * 5 * h->K * sizeof(float2), s));
+            for (int p = 0; p < Bmax; ++p) {
+                SVH_CUDA(cudaMalloc(&bbs[p], N * sizeof(double2)));
+                SVH_CUDA(cudaMalloc(&xs[p], N * sizeof(double2)));
+            }
+            for (int s0 = 0; s0 < nsel; s0 += Bmax) {
+                const int nb = std::min(Bmax, nsel - s0);
+                for (int k = 0; k < nb; ++k) {
+                    const int p = sel[s0 + k];
+                    SVH_CHECK(p >= 0 && p < P, SVH_EINVAL, "bad port index");
+                    std::vector<uint8_t> mask(S->M, 0);
+                    for (int32_t r : ps.plus[p]) mask[r] = 1;
+                    SVH_CUDA(cudaMemcpyAsync(pm, mask.data(), S->M, cudaMemcpyHostToDevice, s));
+                    SVH_LAUNCH(k_rhs, nblk(h->K + S->M), 256, 0, s, bbs[k], pm, S->d_fnode, h->K, S->M);
+                    SVH_CUDA(cudaStreamSynchronize(s));   // pm is reused by the next port
+                }
+                std::vector<double> rres;
+                std::vector<int> itv;
+                fgmres_batch(h, W, nb, bbs.data(), xs.data(), h->opts.rre, h->opts.max_iters, NVP, rres, itv, s);
+                for (int k = 0; k < nb; ++k) {
+                    tot_it += itv[k];
+                    worst = std::max(worst, rres[k]);
+                    if (!(rres[k] <= h->opts.rre * 1.0001)) all_conv = false;
+                    if (st) st->iterations = itv[k];
+                    port_currents(xs[k], s0 + k);
+                }
+            }
+        } catch (...) {
+            release();
+            cudaFree(x);
+            cudaFree(bb);
+            cudaFree(pm);
+            cudaFree(dnodes);
+            cudaFree(cur);
+            throw;
+        }
+        release();
+        nsel = 0;   // done
+    }
     for (int si = 0; si < nsel; ++si) {
         const int p = sel[si];
         SVH_CHECK(p >= 0 && p < P, SVH_EINVAL, "bad port index");
@@ -1328,17 +1607,7 @@ static void solve_columns(svh_handle* h, const svh_port* ports, int P, const int
         worst = std::max(worst, rre_out);
         if (!(rre_out <= h->opts.rre * 1.0001)) all_conv = false;
         if (st) st->iterations = its;
-        for (int q = 0; q < P; ++q) {
-            SVH_CUDA(cudaMemcpyAsync(dnodes, ps.plus[q].data(), ps.plus[q].size() * sizeof(int32_t),
-                                     cudaMemcpyHostToDevice, s));
-            SVH_LAUNCH(k_port_current, 1, 256, 0, s, x, dnodes, (int)ps.plus[q].size(), S->d_node_vox, S->d_node_axis,
-                       h->K, cur);
-            double c2[2];
-            SVH_CUDA(cudaMemcpyAsync(c2, cur, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
-            SVH_CUDA(cudaStreamSynchronize(s));
-            Ycols[2 * ((size_t)si * P + q)] = c2[0];
-            Ycols[2 * ((size_t)si * P + q) + 1] = c2[1];
-        }
+        port_currents(x, si);
     }
     SVH_CUDA(cudaStreamSynchronize(s));
     cudaFree(x);
