@@ -353,7 +353,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-solve", action="store_true", help="skip the time-to-L measurement")
     ap.add_argument("--no-cufft", action="store_true", help="skip the cuFFT reference-pipeline timing")
-    ap.add_argument("--solve-workload", default="cfg2")
+    ap.add_argument("--solve-workload", default="cfg3")
     ap.add_argument("--slab", type=int, default=0,
                     help="slab-decomposed matvec (SURVEY 8(e)(2), strong scaling): under torchrun one y-slab per "
                          "rank with NCCL all-to-alls; with --gpus 1, P virtual slabs on one GPU (exchange by copies)")
