@@ -93,3 +93,48 @@ def test_preconditioner_reduces_iterations(svh_lib):
     case = svh_inputs.bar(12, 3, 3, dx=0.25e-6, material=(0.0, 90e-9))
     res = gpu_solve(svh_lib, case, rre=1e-7)
     assert res["stats"]["total_iterations"] < 40
+
+
+def test_three_port_batched_vs_oracle(svh_lib):
+    """3 ports (the batched lockstep FGMRES pads to 4 right-hand-side pairs): L vs the oracle's
+    dense solve, reciprocity of Y (P12)."""
+    mat = np.zeros((3, 8, 16), np.uint8)
+    mat[0, :, :] = 1
+    mat[2, 1:3, 1:15] = 1
+    mat[2, 5:7, 1:15] = 1
+    mat[1, 1:3, 14:15] = 1
+    mat[1, 5:7, 14:15] = 1
+    g = [(0, -1, (0, 0, 0), (1, 8, 1))]
+    ports = [{"plus": [(0, -1, (1, 1, 2), (2, 3, 3))], "minus": g},
+             {"plus": [(0, -1, (1, 5, 2), (2, 7, 3))], "minus": g},
+             {"plus": [(0, +1, (15, 0, 0), (16, 8, 1))], "minus": g}]
+    case = dict(mat_id=mat, dx=0.25e-6, materials=[(1.7e7, 90e-9)], freq=10e9, ports=ports)
+    res = gpu_solve(svh_lib, case, rre=1e-7)
+    ref = oracle_L(case)
+    assert res["code"] == 0, res
+    assert np.max(np.abs(res["L"] - ref["L"])) < L_TOL * np.max(np.abs(ref["L"]))
+    assert np.allclose(res["Y"], res["Y"].T, rtol=1e-4, atol=1e-4 * np.abs(res["Y"]).max())
+
+
+def test_config2_frequency_sweep(svh_lib):
+    """BASELINE configs[1]: 256x32x4 meander, f = 1-50 GHz over 5 points through
+    svh_set_frequency (kernels are f-independent, only z^b and the Green prefactor change):
+    equals a fresh setup at each frequency; with sigma0 = 0 the inductance is f-independent
+    (P11, SPEC acceptance #7)."""
+    case = svh_inputs.config2()
+    freqs = np.geomspace(1e9, 50e9, 5)
+    with svh_lib.setup_case(case, tucker_tol=0.0, rre=1e-7) as h:
+        Ls = []
+        for f in freqs:
+            h.set_frequency(f)
+            Ls.append(float(h.solve(case["ports"])["L"][0, 0]))
+    with svh_lib.setup_case(dict(case, freq=freqs[-1]), tucker_tol=0.0, rre=1e-7) as h:
+        fresh = float(h.solve(case["ports"])["L"][0, 0])
+    assert abs(Ls[-1] - fresh) <= 1e-5 * abs(fresh)
+    sc = dict(case, materials=[(0.0, m[1]) for m in case["materials"]])
+    with svh_lib.setup_case(sc, tucker_tol=0.0, rre=1e-7) as h:
+        L0 = []
+        for f in (freqs[0], freqs[-1]):
+            h.set_frequency(f)
+            L0.append(float(h.solve(sc["ports"])["L"][0, 0]))
+    assert abs(L0[0] - L0[1]) <= 1e-4 * abs(L0[0]), L0
