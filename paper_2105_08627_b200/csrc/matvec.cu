@@ -1271,6 +1271,341 @@ __global__ void __launch_bounds__(freq_big_threads<N>())
     }
 }
 
+// Pass C for 128 <= Nz <= 512 (TMA-staged): a persistent CTA per SM walks tiles of one RHS x
+// Q consecutive kx x one ky.  The tile's 5 x Kz x Q input block arrives by five
+// cp.async.bulk.tensor loads (box Q x 1 x Kz, one per component) into a double-buffered
+// mbarrier ring, so the load of the next tile overlaps this tile's transforms; the result
+// leaves the same way (five TMA stores from the consumed input slot).  The z-FFT is the
+// two-level R1 x R2 register/shared-memory transform of the strided passes (first level
+// pruned to the Kz <= N/2 live inputs), the 5 spectra meet in shared memory in natural kz
+// order for the moment-form MAC (mac5), and the inverse runs the transposed two-level
+// transform, cropped to z < Kz.  Rows of planes without voxels are read as zero (X2 there is
+// never written by pass B); their results are written but never read (pass D skips them).
+template <int N, int Q>
+struct ZTma {
+    static constexpr int R1 = fft_r1(N), R2 = fft_r2(N), R = R1 > R2 ? R1 : R2;
+    static constexpr int NT = 5 * R * Q, NH = N / 2, EM = em_size<N, Q>();
+    static constexpr int SLOT = 5 * NH * Q;   // float2 per ring slot (= spectrum rows kz < N/2)
+    static constexpr size_t stage_b = (size_t)SLOT * sizeof(float2);
+    static constexpr size_t T_b = ((size_t)5 * EM * sizeof(float2) + 127) / 128 * 128;
+    // ring slot x2, the upper-half spectrum rows, the transpose buffer, twiddles, plane flags
+    static constexpr size_t smem = 3 * stage_b + T_b + (size_t)N * sizeof(float2) + NH + 16 + 128;
+};
+
+template <int N, int Q>
+__global__ void __launch_bounds__(ZTma<N, Q>::NT, 1)
+    k_ztma(const __grid_constant__ CUtensorMap tmap, SpecView sv, const float2* __restrict__ tw, int Nx, int Ny,
+           int Kz, float g, int nrhs, int ntiles, int tiles_x, const uint8_t* __restrict__ planeok, int kxg) {
+    using P = ZTma<N, Q>;
+    constexpr int R1 = P::R1, R2 = P::R2, R = P::R, NT = P::NT, NH = P::NH, EM = P::EM, SLOT = P::SLOT;
+    extern __shared__ __align__(128) unsigned char smraw[];
+    float2* stage = reinterpret_cast<float2*>(smraw);                        // [2][5][NH][Q]
+    float2* hi = reinterpret_cast<float2*>(smraw + 2 * P::stage_b);          // [5][NH][Q], kz >= N/2
+    float2* T = reinterpret_cast<float2*>(smraw + 3 * P::stage_b);           // [5][EM]
+    float2* tws = reinterpret_cast<float2*>(smraw + 3 * P::stage_b + P::T_b);
+    uint8_t* pok = reinterpret_cast<uint8_t*>(tws + N);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + ((3 * P::stage_b + P::T_b + N * sizeof(float2) + NH + 7) / 8) * 8);
+    const int tid = threadIdx.x;
+    const float2 zero = make_float2(0.f, 0.f);
+    for (int j = tid; j < N; j += NT) tws[j] = __ldg(&tw[j]);
+    for (int j = tid; j < NH; j += NT) pok[j] = (j < Kz && __ldg(&planeok[j])) ? 1 : 0;
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    auto issue = [&](int t, int st) {
+        if (t >= ntiles) return;
+        const int r = t % nrhs, rest = t / nrhs;
+        const int xt = rest % tiles_x, ky = rest / tiles_x;
+        mbar_arrive_expect_tx(&bar[st], (uint32_t)(5 * Kz * Q * sizeof(float2)));
+#pragma unroll
+        for (int c = 0; c < 5; ++c)
+            tma_load_3d(stage + st * SLOT + c * NH * Q, &tmap, xt * Q, ky, (r * 5 + c) * Kz, &bar[st]);
+    };
+    const int c = tid / (R * Q), j = (tid % (R * Q)) / Q, q = tid % Q;
+    float2* Tc = T + c * EM;
+    int t = blockIdx.x;
+    if (tid == 0) issue(t, 0);
+    for (int i = 0; t < ntiles; ++i, t += gridDim.x) {
+        const int st = i & 1;
+        float2* slot = stage + st * SLOT;
+        mbar_wait(&bar[st], (uint32_t)((i >> 1) & 1));
+        // forward, level 1 (thread n2 = j): FFT_R1 over n1 of x[R2 n1 + n2], twiddle W_N^{n2 k1}
+        if (j < R2) {
+            float2 v[R1];
+#pragma unroll
+            for (int n1 = 0; n1 < R1; ++n1) {
+                const int z = R2 * n1 + j;
+                v[n1] = (n1 < R1 / 2 && pok[z]) ? slot[(c * NH + z) * Q + q] : zero;
+            }
+            reg_fft<R1, -1, true>(v);
+#pragma unroll
+            for (int k1 = 1; k1 < R1; ++k1) v[k1] = cmul(v[k1], tws[j * k1]);
+#pragma unroll
+            for (int k1 = 0; k1 < R1; ++k1) Tc[em_idx<N, Q>(j * R1 + k1, q)] = v[k1];
+        }
+        __syncthreads();
+        if (tid == 0) {   // the other slot: its output store (tile i-1) must have left smem
+            tma_store_wait_read0();
+            issue(t + (int)gridDim.x, st ^ 1);
+        }
+        // forward, level 2 (thread k1 = j): FFT_R2 over n2 -> spectrum at kz = k1 + R1 k2,
+        // stored in natural order: kz < N/2 into the consumed slot, kz >= N/2 into hi
+        float2 u[R2];
+        if (j < R1) {
+#pragma unroll
+            for (int m = 0; m < R2; ++m) u[m] = Tc[em_idx<N, Q>(m * R1 + j, q)];
+            reg_fft<R2, -1>(u);
+#pragma unroll
+            for (int k2 = 0; k2 < R2; ++k2) {
+                const int kz = j + R1 * k2;
+                (kz < NH ? slot : hi)[(c * NH + (kz & (NH - 1))) * Q + q] = u[k2];
+            }
+        }
+        __syncthreads();
+        {
+            const int r = t % nrhs, rest = t / nrhs;
+            const int xt = rest % tiles_x, ky = rest / tiles_x;
+            for (int e = tid; e < N * Q; e += NT) {
+                const int kz = e / Q, qq = e % Q;
+                float kv[7];
+                kernel_values(sv, kxg + xt * Q + qq, ky, kz, Nx, Ny, N, kv);
+                float2* b = (kz < NH ? slot : hi) + (kz & (NH - 1)) * Q + qq;
+                float2 v5[5];
+#pragma unroll
+                for (int cc = 0; cc < 5; ++cc) v5[cc] = b[cc * NH * Q];
+                mac5(v5, kv[0], kv[1], kv[2], kv[3], kv[4], kv[5], kv[6], g);
+#pragma unroll
+                for (int cc = 0; cc < 5; ++cc) b[cc * NH * Q] = v5[cc];
+            }
+            (void)r;
+        }
+        __syncthreads();
+        // inverse, level 1 (thread k1 = j): IFFT_R2 over k2, twiddle W_N^{-n2 k1}
+        if (j < R1) {
+#pragma unroll
+            for (int k2 = 0; k2 < R2; ++k2) {
+                const int kz = j + R1 * k2;
+                u[k2] = (kz < NH ? slot : hi)[(c * NH + (kz & (NH - 1))) * Q + q];
+            }
+            reg_fft<R2, +1>(u);
+#pragma unroll
+            for (int n2 = 0; n2 < R2; ++n2) {
+                float2 w = tws[n2 * j];
+                w.y = -w.y;
+                Tc[em_idx<N, Q>(n2 * R1 + j, q)] = n2 ? cmul(u[n2], w) : u[n2];
+            }
+        }
+        __syncthreads();
+        // inverse, level 2 (thread n2 = j): IFFT_R1 over k1 -> z = n2 + R2 n1, cropped to z < Kz
+        if (j < R2) {
+            float2 v[R1];
+#pragma unroll
+            for (int k1 = 0; k1 < R1; ++k1) v[k1] = Tc[em_idx<N, Q>(j * R1 + k1, q)];
+            reg_fft<R1, +1>(v);
+#pragma unroll
+            for (int n1 = 0; n1 < R1 / 2; ++n1) {
+                const int z = j + R2 * n1;
+                if (z < Kz) slot[(c * NH + z) * Q + q] = v[n1];
+            }
+        }
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+            const int r = t % nrhs, rest = t / nrhs;
+            const int xt = rest % tiles_x, ky = rest / tiles_x;
+#pragma unroll
+            for (int cc = 0; cc < 5; ++cc) tma_store_3d(&tmap, xt * Q, ky, (r * 5 + cc) * Kz, slot + cc * NH * Q);
+            tma_store_commit();
+        }
+    }
+    if (tid == 0) tma_store_wait0();
+}
+
+// Pass C, second form (default for Nz = 128 .. 512): the same TMA ring and tiles as k_ztma,
+// but the z-FFT is split N = R1 x R2 with a SHORT second level (R2 = 4 / 8) so that one
+// thread holds all 5 components of its (k1, q) column after the forward second level: the
+// moment-form MAC then runs in registers (no spectrum round trip through shared memory),
+// followed directly by the inverse first level, written back over the very elements the
+// thread read (no barrier).  Per tile: 2 shared-memory transposes instead of 4 plus the MAC
+// exchange.  The 7 kernel spectra of a (kx tile, ky) column are folded into shared memory
+// once per group of nrhs tiles (the CTA walks all RHS of a column back to back).
+template <int N, int Q, int R2_>
+struct ZTma2 {
+    static constexpr int R2 = R2_, R1 = N / R2_, NH = N / 2, NK = N / 2 + 1;
+    static constexpr int NT1 = 5 * R2 * Q, NT2 = R1 * Q, NT = NT1 > NT2 ? NT1 : NT2;
+    static constexpr int PADQ = Q < 16 ? Q : 0;
+    static constexpr int EM = N * Q + R2 * PADQ;   // per component
+    static constexpr int SLOT = 5 * NH * Q;
+    static constexpr size_t stage_b = (size_t)SLOT * sizeof(float2);
+    static constexpr size_t T_b = ((size_t)5 * EM * sizeof(float2) + 127) / 128 * 128;
+    static constexpr size_t KV_b = ((size_t)7 * NK * Q * sizeof(float) + 127) / 128 * 128;
+    static constexpr size_t smem = 2 * stage_b + T_b + 2 * KV_b + (size_t)N * sizeof(float2) + NH + 16 + 128;
+    // transpose-buffer index of element (n2, k1) of pencil q (padded per n2 block)
+    static __device__ __forceinline__ int ti(int n2, int k1, int q) { return (n2 * R1 + k1) * Q + q + n2 * PADQ; }
+};
+
+template <int N, int Q, int R2_>
+__global__ void __launch_bounds__(ZTma2<N, Q, R2_>::NT, (N < 512 && Q == 4) ? 2 : 1)
+    k_ztma2(const __grid_constant__ CUtensorMap tmap, SpecView sv, const float2* __restrict__ tw, int Nx, int Ny,
+            int Kz, float g, int nrhs, int ngroups, int tiles_x, const uint8_t* __restrict__ planeok, int kxg) {
+    using P = ZTma2<N, Q, R2_>;
+    constexpr int R1 = P::R1, R2 = P::R2, NH = P::NH, NK = P::NK, NT = P::NT, NT1 = P::NT1, NT2 = P::NT2;
+    constexpr int EM = P::EM, SLOT = P::SLOT;
+    extern __shared__ __align__(128) unsigned char smraw[];
+    float2* stage = reinterpret_cast<float2*>(smraw);                                  // [2][5][NH][Q]
+    float2* T = reinterpret_cast<float2*>(smraw + 2 * P::stage_b);                     // [5][EM]
+    float* KV0 = reinterpret_cast<float*>(smraw + 2 * P::stage_b + P::T_b);            // [2][7][NK][Q]
+    float2* tws = reinterpret_cast<float2*>(smraw + 2 * P::stage_b + P::T_b + 2 * P::KV_b);
+    uint8_t* pok = reinterpret_cast<uint8_t*>(tws + N);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(
+        smraw + ((2 * P::stage_b + P::T_b + 2 * P::KV_b + N * sizeof(float2) + NH + 7) / 8) * 8);
+    const int tid = threadIdx.x;
+    const float2 zero = make_float2(0.f, 0.f);
+    for (int j = tid; j < N; j += NT) tws[j] = __ldg(&tw[j]);
+    for (int j = tid; j < NH; j += NT) pok[j] = (j < Kz && __ldg(&planeok[j])) ? 1 : 0;
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    // this CTA's tile sequence: column groups blockIdx.x, +gridDim.x, ...; all RHS of a group
+    auto group_of = [&](int s) { return (int)blockIdx.x + (s / nrhs) * (int)gridDim.x; };
+    auto issue = [&](int s, int st) {
+        const int grp = group_of(s), r = s % nrhs;
+        if (grp >= ngroups) return;
+        const int xt = grp % tiles_x, ky = grp / tiles_x;
+        mbar_arrive_expect_tx(&bar[st], (uint32_t)(5 * Kz * Q * sizeof(float2)));
+#pragma unroll
+        for (int c = 0; c < 5; ++c)
+            tma_load_3d(stage + st * SLOT + c * NH * Q, &tmap, xt * Q, ky, (r * 5 + c) * Kz, &bar[st]);
+    };
+    const int c1 = tid / (R2 * Q), n2 = (tid / Q) % R2, q1 = tid % Q;   // level-1 roles
+    const int k1 = tid / Q, q2 = tid % Q;                               // level-2 roles
+    // the 7 kernel spectra of a column group (raw octant values; the folding factors are
+    // applied in the MAC), fetched by cp.async one group ahead into a double buffer
+    auto fetch_kv = [&](int gi) {
+        const int grp = (int)blockIdx.x + gi * (int)gridDim.x;
+        if (grp < ngroups) {
+            const int xt = grp % tiles_x, ky = grp / tiles_x;
+            const int oy = ky <= (Ny >> 1) ? ky : Ny - ky;
+            const int64_t pl = (int64_t)sv.hx * sv.hy * sv.hz;
+            float* dst = KV0 + (gi & 1) * (P::KV_b / sizeof(float));
+            for (int e = tid; e < 7 * NK * Q; e += NT) {
+                const int q = e % Q, rest = e / Q;
+                const int kh = rest % NK, m = rest / NK;
+                const int kx = min(kxg + xt * Q + q, Nx - 1);
+                const int ox = kx <= (Nx >> 1) ? kx : Nx - kx;
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(dst + e)),
+                             "l"(sv.spec + m * pl + ((int64_t)kh * sv.hy + oy) * sv.hx + ox)
+                             : "memory");
+            }
+        }
+        cp_async_commit();
+    };
+    fetch_kv(0);
+    if (tid == 0) issue(0, 0);
+    for (int s = 0;; ++s) {
+        const int grp = group_of(s), r = s % nrhs;
+        if (grp >= ngroups) break;
+        const int xt = grp % tiles_x, ky = grp / tiles_x;
+        const int st = s & 1;
+        float2* slot = stage + st * SLOT;
+        if (r == 0) {   // next group's spectra; this group's (fetched one group ago) must have landed
+            fetch_kv(s / nrhs + 1);
+            cp_async_wait1();   // published by the barrier after level 1
+        }
+        const float* KV = KV0 + ((s / nrhs) & 1) * (P::KV_b / sizeof(float));
+        mbar_wait(&bar[st], (uint32_t)((s >> 1) & 1));
+        // forward level 1 (thread (c, n2, q)): FFT_R1 over n1 of x[R2 n1 + n2], twiddle W_N^{n2 k1}
+        if (tid < NT1) {
+            float2 v[R1];
+#pragma unroll
+            for (int n1 = 0; n1 < R1; ++n1) {
+                const int z = R2 * n1 + n2;
+                v[n1] = (n1 < R1 / 2 && pok[z]) ? slot[(c1 * NH + z) * Q + q1] : zero;
+            }
+            reg_fft<R1, -1, true>(v);
+#pragma unroll
+            for (int k = 1; k < R1; ++k) v[k] = cmul(v[k], tws[n2 * k]);
+#pragma unroll
+            for (int k = 0; k < R1; ++k) T[c1 * EM + P::ti(n2, k, q1)] = v[k];
+        }
+        __syncthreads();
+        if (tid == 0) {   // the other slot: its output store (previous tile) must have left smem
+            tma_store_wait_read0();
+            issue(s + 1, st ^ 1);
+        }
+        // level 2 (thread (k1, q)): forward FFT_R2 of all 5 components -> kz = k1 + R1 k2,
+        // MAC in registers, inverse FFT_R2, twiddle W_N^{-n2 k1}, back to the same elements
+        if (tid < NT2) {
+            const int kx = kxg + xt * Q + q2;
+            const float gx = kx <= (Nx >> 1) ? g : -g, gy = ky <= (Ny >> 1) ? g : -g;
+            float2 u[5][R2];
+#pragma unroll
+            for (int c = 0; c < 5; ++c) {
+#pragma unroll
+                for (int m = 0; m < R2; ++m) u[c][m] = T[c * EM + P::ti(m, k1, q2)];
+                reg_fft<R2, -1>(u[c]);
+            }
+#pragma unroll
+            for (int k2 = 0; k2 < R2; ++k2) {
+                const int kz = k1 + R1 * k2;
+                const int kh = kz <= NH ? kz : N - kz;
+                const float s3 = kz <= NH ? 1.f : -1.f;   // K1z is odd in kz
+                const float* kp = KV + kh * Q + q2;
+                const float f0 = g * kp[0 * NK * Q], f1 = gx * kp[1 * NK * Q], f2 = gy * kp[2 * NK * Q];
+                const float f3 = (-2.f * g) * s3 * kp[3 * NK * Q];
+                const float f4 = g * kp[4 * NK * Q], f5 = g * kp[5 * NK * Q], f6 = (4.f * g) * kp[6 * NK * Q];
+                const float2 Ix = u[0][k2], Iy = u[1][k2], Iz = u[2][k2], I2 = u[3][k2], I3 = u[4][k2];
+                const float2 m1x = cadd(I2, I3), m1y = csub(I3, I2);
+                const float2 Qx = cfma_s(Ix, -f1, cmul_i(m1x, f4));
+                const float2 Qy = cfma_s(Iy, -f2, cmul_i(m1y, f5));
+                const float2 Qz = cfma_s(Iz, -f3, cmul_i(I3, f6));
+                u[0][k2] = cfma_s(m1x, f1, cmul_i(Ix, f0));
+                u[1][k2] = cfma_s(m1y, f2, cmul_i(Iy, f0));
+                u[2][k2] = cfma_s(I3, f3, cmul_i(Iz, f0));
+                u[3][k2] = csub(Qx, Qy);
+                u[4][k2] = cadd(cadd(Qx, Qy), Qz);
+            }
+#pragma unroll
+            for (int c = 0; c < 5; ++c) {
+                reg_fft<R2, +1>(u[c]);
+#pragma unroll
+                for (int m = 0; m < R2; ++m) {
+                    float2 w = tws[m * k1];
+                    w.y = -w.y;
+                    T[c * EM + P::ti(m, k1, q2)] = m ? cmul(u[c][m], w) : u[c][m];
+                }
+            }
+        }
+        __syncthreads();
+        // inverse level 2 (thread (c, n2, q)): IFFT_R1 over k1 -> z = n2 + R2 n1, cropped to z < Kz
+        if (tid < NT1) {
+            float2 v[R1];
+#pragma unroll
+            for (int k = 0; k < R1; ++k) v[k] = T[c1 * EM + P::ti(n2, k, q1)];
+            reg_fft<R1, +1>(v);
+#pragma unroll
+            for (int n1 = 0; n1 < R1 / 2; ++n1) {
+                const int z = n2 + R2 * n1;
+                if (z < Kz) slot[(c1 * NH + z) * Q + q1] = v[n1];
+            }
+        }
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+#pragma unroll
+            for (int c = 0; c < 5; ++c) tma_store_3d(&tmap, xt * Q, ky, (r * 5 + c) * Kz, slot + c * NH * Q);
+            tma_store_commit();
+        }
+    }
+    if (tid == 0) tma_store_wait0();
+}
+
 // ---------------------------------------------------------------------------
 // host-side dispatch
 namespace {
@@ -1499,6 +1834,56 @@ void run_pass_c(svh_handle* h, const Geom& g, float2* X2, int nrhs, cudaStream_t
             else launch(std::integral_constant<int, 32>{}, std::false_type{});
         }
     } else {
+        static const bool ztma = getenv("SVH_ZTMA") == nullptr || atoi(getenv("SVH_ZTMA")) != 0;
+        static const int zform = getenv("SVH_ZTMA") ? atoi(getenv("SVH_ZTMA")) : 2;
+        if constexpr (N >= 128 && N <= 512) {
+            static const int zq = getenv("SVH_ZQ") ? atoi(getenv("SVH_ZQ")) : 8;
+            auto launch2 = [&](auto Qc) -> bool {
+                constexpr int Q2 = decltype(Qc)::value, R2 = N == 128 ? 4 : 8;
+                using P2 = ZTma2<N, Q2, R2>;
+                CUtensorMap tm2;
+                if (!(zform == 2 && sv.spec && g.nx % Q2 == 0 &&
+                      encode_tmap_c64_3d_box(&tm2, X2, (uint64_t)g.nx, (uint64_t)h->ny, (uint64_t)5 * nrhs * h->kz,
+                                             (uint64_t)g.nx, (uint64_t)g.nx * h->ny, Q2, 1, (uint32_t)h->kz)))
+                    return false;
+                const int tiles_x = g.nx / Q2;
+                const int ngroups = tiles_x * h->ny;
+                int dev = 0, nsm = 148, occ = 1;
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+                prep(k_ztma2<N, Q2, R2>, P2::smem);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ztma2<N, Q2, R2>, P2::NT, P2::smem);
+                SVH_LAUNCH((k_ztma2<N, Q2, R2>), std::min(ngroups, nsm * std::max(occ, 1)), P2::NT, P2::smem, s, tm2,
+                           sv, h->d_tw[2], h->nx, h->ny, h->kz, h->gscale, nrhs, ngroups, tiles_x, h->d_planeok,
+                           g.kx0);
+                return true;
+            };
+            if constexpr (N == 512) {
+                if (launch2(std::integral_constant<int, 4>{})) return;
+            } else {
+                if (zq == 8 ? launch2(std::integral_constant<int, 8>{}) : launch2(std::integral_constant<int, 4>{}))
+                    return;
+            }
+        }
+        if constexpr (N >= 128 && N <= 512) {
+            constexpr int QZ = N >= 512 ? 4 : 8;
+            using P = ZTma<N, QZ>;
+            CUtensorMap tmap;
+            if (ztma && sv.spec && g.nx % QZ == 0 &&
+                encode_tmap_c64_3d_box(&tmap, X2, (uint64_t)g.nx, (uint64_t)h->ny, (uint64_t)5 * nrhs * h->kz,
+                                       (uint64_t)g.nx, (uint64_t)g.nx * h->ny, QZ, 1, (uint32_t)h->kz)) {
+                const int tiles_x = g.nx / QZ;
+                const int ntiles = tiles_x * h->ny * nrhs;
+                int dev = 0, nsm = 148, occ = 1;
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+                prep(k_ztma<N, QZ>, P::smem);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ztma<N, QZ>, P::NT, P::smem);
+                SVH_LAUNCH((k_ztma<N, QZ>), std::min(ntiles, nsm * std::max(occ, 1)), P::NT, P::smem, s, tmap, sv,
+                           h->d_tw[2], h->nx, h->ny, h->kz, h->gscale, nrhs, ntiles, tiles_x, h->d_planeok, g.kx0);
+                return;
+            }
+        }
         const int tpp = fft_threads_per_pencil(N);
         int Q = std::min(8, std::max(1, fft_max_threads(N) / (tpp * 5)));   // <= 8: Tucker H tile
         while (Q > 1 && (size_t)N * (5 * Q + 1) * sizeof(float2) > 160 * 1024) Q >>= 1;

@@ -68,5 +68,9 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // dims/strides in elements; returns false if the driver entry point is unavailable.
 bool encode_tmap_c64_3d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
                         uint64_t stride1_elems, uint64_t stride2_elems, uint32_t box0, uint32_t box1);
+// the same with a [box0, box1, box2] box (each <= 256)
+bool encode_tmap_c64_3d_box(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+                            uint64_t stride1_elems, uint64_t stride2_elems, uint32_t box0, uint32_t box1,
+                            uint32_t box2);
 
 }  // namespace svh

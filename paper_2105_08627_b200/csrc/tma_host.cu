@@ -27,11 +27,17 @@ EncodeFn encode_fn() {
 
 bool encode_tmap_c64_3d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
                         uint64_t stride1_elems, uint64_t stride2_elems, uint32_t box0, uint32_t box1) {
+    return encode_tmap_c64_3d_box(map, base, d0, d1, d2, stride1_elems, stride2_elems, box0, box1, 1);
+}
+
+bool encode_tmap_c64_3d_box(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+                            uint64_t stride1_elems, uint64_t stride2_elems, uint32_t box0, uint32_t box1,
+                            uint32_t box2) {
     EncodeFn fn = encode_fn();
     if (!fn) return false;
     const cuuint64_t dims[3] = {d0, d1, d2};
     const cuuint64_t strides[2] = {stride1_elems * 8, stride2_elems * 8};   // bytes, dims 1..2
-    const cuuint32_t box[3] = {box0, box1, 1};
+    const cuuint32_t box[3] = {box0, box1, box2};
     const cuuint32_t estr[3] = {1, 1, 1};
     const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, estr,
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,

@@ -29,6 +29,12 @@ def bench_point(shape, nrhs, tucker, reps=5):
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
+        h.profile(True)
+        h.matvec(I, out=out)
+        torch.cuda.synchronize()
+        pms, pn = h.profile_read(reset=True)
+        h.profile(False)
+        passes = {n: round(float(x), 3) for n, x in zip("ABCDE", pms[:5])}
         st = h.stats()
         nx, ny, nz = h.embedding
         kt = int(np.prod(shape))
@@ -37,18 +43,21 @@ def bench_point(shape, nrhs, tucker, reps=5):
         return {"grid": "x".join(map(str, shape)), "embedding": f"{nx}x{ny}x{nz}", "nrhs": nrhs,
                 "kernels": f"tucker {tucker:g} (max rank {max(max(r) for r in st['ranks'])})" if tucker else "dense",
                 "ms": round(ms, 3), "Gvu_s": round(5 * kt * nrhs / (ms / 1e3) / 1e9, 2),
-                "P5_equiv_TBs": round(p5 / (ms / 1e3) / 1e12, 2)}
+                "P5_equiv_TBs": round(p5 / (ms / 1e3) / 1e12, 2), "passes_ms": passes}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
+    ap.add_argument("--min-kz", type=int, default=0, help="only the points with K_z >= this")
+    ap.add_argument("--dense-only", action="store_true")
     args = ap.parse_args()
     pts = [((64, 64, 64), 16, 0.0), ((128, 128, 128), 8, 0.0), ((256, 256, 256), 2, 0.0),
            ((512, 512, 4), 16, 0.0), ((512, 512, 16), 16, 0.0), ((512, 512, 64), 4, 0.0),
            ((1024, 1024, 16), 4, 0.0), ((1024, 1024, 64), 2, 0.0),
            ((512, 512, 16), 1, 0.0), ((512, 512, 16), 4, 0.0), ((512, 512, 16), 64, 0.0),
            ((512, 512, 16), 16, 1e-4), ((512, 512, 16), 16, 1e-8), ((128, 128, 128), 8, 1e-6)]
+    pts = [p for p in pts if p[0][2] >= args.min_kz and not (args.dense_only and p[2])]
     rows = []
     for shape, nrhs, tol in pts:
         try:

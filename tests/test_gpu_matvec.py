@@ -223,3 +223,34 @@ def test_setup_rejects_bad_grids(svh_lib):
     big = dict(ok, mat_id=np.ones((1, 1, 2049), dtype=np.uint8))
     with pytest.raises(svh_lib.SvhError):
         svh_lib.setup_case(big)
+
+
+# Pass C for 128 <= Nz <= 512 (k_ztma, TMA-staged z pass): Kz = 33..64 -> Nz = 128,
+# Kz = 65..128 -> 256, Kz = 129..256 -> 512, incl. Kz = N/2 exactly, a ragged kx tile edge
+# in the embedding and 3 RHS (the tile order is RHS-fastest); plus empty planes.
+ZSHAPES = [((9, 5, 40), 0.5), ((20, 3, 64), 0.5), ((5, 3, 128), 0.6), ((6, 4, 150), 0.5)]
+
+
+@pytest.mark.parametrize("shape,fill", ZSHAPES)
+def test_matvec_ztma_shapes(svh_lib, shape, fill):
+    case = svh_inputs.random_fill(shape, fill=fill, seed=31 + sum(shape), n_mat=2)
+    lat = Lattice(case["mat_id"])
+    I = svh_inputs.currents(lat.K, nrhs=3, seed=5)
+    w = 2 * np.pi * case["freq"]
+    for go in (True, False):
+        ref = matvec_direct(lat, case["materials"], w, case["dx"], I, green_only=go)
+        got = gpu_matvec(svh_lib, case, I, green_only=go)
+        for r in range(3):
+            assert rel_l2(got[r], ref[r]) < TOL, (go, r, rel_l2(got[r], ref[r]))
+
+
+def test_matvec_ztma_empty_planes(svh_lib):
+    """k_ztma over a stack with empty z planes (read as zero, never read back)."""
+    case = svh_inputs.layered((8, 6, 100))
+    lat = Lattice(case["mat_id"])
+    I = svh_inputs.currents(lat.K, nrhs=2, seed=23)
+    w = 2 * np.pi * case["freq"]
+    ref = matvec_direct(lat, case["materials"], w, case["dx"], I, green_only=True)
+    got = gpu_matvec(svh_lib, case, I, green_only=True)
+    for r in range(2):
+        assert rel_l2(got[r], ref[r]) < TOL, (r, rel_l2(got[r], ref[r]))
