@@ -1448,7 +1448,7 @@ struct ZTma2 {
 };
 
 template <int N, int Q, int R2_>
-__global__ void __launch_bounds__(ZTma2<N, Q, R2_>::NT, (N < 512 && Q == 4) ? 2 : 1)
+__global__ void __launch_bounds__(ZTma2<N, Q, R2_>::NT, (N == 128 || (N < 512 && Q == 4)) ? 2 : 1)
     k_ztma2(const __grid_constant__ CUtensorMap tmap, SpecView sv, const float2* __restrict__ tw, int Nx, int Ny,
             int Kz, float g, int nrhs, int ngroups, int tiles_x, const uint8_t* __restrict__ planeok, int kxg) {
     using P = ZTma2<N, Q, R2_>;
@@ -1474,10 +1474,19 @@ __global__ void __launch_bounds__(ZTma2<N, Q, R2_>::NT, (N < 512 && Q == 4) ? 2 
     __syncthreads();
     // this CTA's tile sequence: column groups blockIdx.x, +gridDim.x, ...; all RHS of a group
     auto group_of = [&](int s) { return (int)blockIdx.x + (s / nrhs) * (int)gridDim.x; };
+    // group -> (kx tile, ky), ordered so that the mirror images of a column (kx -> Nx - kx,
+    // ky -> Ny - ky), which read the same octant rows of the kernel spectra, run close together
+    // in time (consecutive groups for x, one tile row apart for y): those rows are then L2 hits
+    auto column = [&](int grp, int& xt, int& ky) {
+        const int xi = grp % tiles_x, yi = grp / tiles_x;
+        xt = (xi & 1) ? tiles_x - 1 - (xi >> 1) : (xi >> 1);
+        ky = yi == 0 ? 0 : yi == 1 ? (Ny >> 1) : ((yi & 1) ? Ny - (yi >> 1) : (yi >> 1));
+    };
     auto issue = [&](int s, int st) {
         const int grp = group_of(s), r = s % nrhs;
         if (grp >= ngroups) return;
-        const int xt = grp % tiles_x, ky = grp / tiles_x;
+        int xt, ky;
+        column(grp, xt, ky);
         mbar_arrive_expect_tx(&bar[st], (uint32_t)(5 * Kz * Q * sizeof(float2)));
 #pragma unroll
         for (int c = 0; c < 5; ++c)
@@ -1490,7 +1499,8 @@ __global__ void __launch_bounds__(ZTma2<N, Q, R2_>::NT, (N < 512 && Q == 4) ? 2 
     auto fetch_kv = [&](int gi) {
         const int grp = (int)blockIdx.x + gi * (int)gridDim.x;
         if (grp < ngroups) {
-            const int xt = grp % tiles_x, ky = grp / tiles_x;
+            int xt, ky;
+        column(grp, xt, ky);
             const int oy = ky <= (Ny >> 1) ? ky : Ny - ky;
             const int64_t pl = (int64_t)sv.hx * sv.hy * sv.hz;
             float* dst = KV0 + (gi & 1) * (P::KV_b / sizeof(float));
@@ -1511,7 +1521,8 @@ __global__ void __launch_bounds__(ZTma2<N, Q, R2_>::NT, (N < 512 && Q == 4) ? 2 
     for (int s = 0;; ++s) {
         const int grp = group_of(s), r = s % nrhs;
         if (grp >= ngroups) break;
-        const int xt = grp % tiles_x, ky = grp / tiles_x;
+        int xt, ky;
+        column(grp, xt, ky);
         const int st = s & 1;
         float2* slot = stage + st * SLOT;
         if (r == 0) {   // next group's spectra; this group's (fetched one group ago) must have landed
