@@ -20,7 +20,9 @@ def _grid_currents(case, lat, I):
     return g
 
 
-@pytest.mark.parametrize("shape,P", [((40, 64, 6), 2), ((40, 64, 6), 4), ((24, 16, 5), 4), ((130, 8, 3), 8)])
+# (40, 8, 40): Nz = 128, the TMA-staged z pass (k_ztma2) on kx-slabs (global kx offset)
+@pytest.mark.parametrize("shape,P", [((40, 64, 6), 2), ((40, 64, 6), 4), ((24, 16, 5), 4), ((130, 8, 3), 8),
+                                     ((40, 8, 40), 2), ((40, 8, 40), 4)])
 @pytest.mark.parametrize("green_only", [False, True])
 def test_slab_matvec_virtual(svh_lib, shape, P, green_only):
     import torch
