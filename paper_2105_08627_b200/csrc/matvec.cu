@@ -1443,6 +1443,7 @@ struct ZTma2 {
     static constexpr size_t T_b = ((size_t)5 * EM * sizeof(float2) + 127) / 128 * 128;
     static constexpr size_t KV_b = ((size_t)7 * NK * Q * sizeof(float) + 127) / 128 * 128;
     static constexpr size_t smem = 2 * stage_b + T_b + 2 * KV_b + (size_t)N * sizeof(float2) + NH + 16 + 128;
+    static_assert(KV_b >= (32 * 32 + 32 * Q) * sizeof(float), "Tucker scratch must fit one KV buffer");
     // transpose-buffer index of element (n2, k1) of pencil q (padded per n2 block)
     static __device__ __forceinline__ int ti(int n2, int k1, int q) { return (n2 * R1 + k1) * Q + q + n2 * PADQ; }
 };
@@ -1496,9 +1497,10 @@ __global__ void __launch_bounds__(ZTma2<N, Q, R2_>::NT, (N == 128 || (N < 512 &&
     const int k1 = tid / Q, q2 = tid % Q;                               // level-2 roles
     // the 7 kernel spectra of a column group (raw octant values; the folding factors are
     // applied in the MAC), fetched by cp.async one group ahead into a double buffer
+    const bool tucker = sv.spec == nullptr;
     auto fetch_kv = [&](int gi) {
         const int grp = (int)blockIdx.x + gi * (int)gridDim.x;
-        if (grp < ngroups) {
+        if (!tucker && grp < ngroups) {
             int xt, ky;
         column(grp, xt, ky);
             const int oy = ky <= (Ny >> 1) ? ky : Ny - ky;
@@ -1528,8 +1530,46 @@ __global__ void __launch_bounds__(ZTma2<N, Q, R2_>::NT, (N == 128 || (N < 512 &&
         if (r == 0) {   // next group's spectra; this group's (fetched one group ago) must have landed
             fetch_kv(s / nrhs + 1);
             cp_async_wait1();   // published by the barrier after level 1
+            if (tucker) {
+                // Tucker mode (Eq. 10): the column's octant rows from the factors, on
+                // chip: G_m = core_m x2 F2[oy] (d3 x d1), H_m[q] = G_m x1 F1[ox_q] (d3), row kh =
+                // H_m[q] . F3[kh] -- into buffer 0, buffer 1 is the scratch
+                float* G = KV0 + P::KV_b / sizeof(float);
+                float* H = G + 32 * 32;
+                const int oy = ky <= (Ny >> 1) ? ky : Ny - ky;
+                for (int m = 0; m < 7; ++m) {
+                    const int d1 = sv.rk[m][0], d2 = sv.rk[m][1], d3 = sv.rk[m][2];
+                    const float* C = sv.core[m];
+                    const float* F2 = sv.fac[m][1] + (int64_t)oy * d2;
+                    for (int t = tid; t < d3 * d1; t += NT) {
+                        const int c3 = t / d1, cc1 = t % d1;
+                        float acc = 0.f;
+                        for (int cc2 = 0; cc2 < d2; ++cc2)
+                            acc = fmaf(__ldg(&C[((int64_t)c3 * d2 + cc2) * d1 + cc1]), __ldg(&F2[cc2]), acc);
+                        G[t] = acc;
+                    }
+                    __syncthreads();
+                    for (int t = tid; t < Q * d3; t += NT) {
+                        const int q = t / d3, c3 = t % d3;
+                        const int kx = min(kxg + xt * Q + q, Nx - 1);
+                        const int ox = kx <= (Nx >> 1) ? kx : Nx - kx;
+                        const float* f1 = sv.fac[m][0] + (int64_t)ox * d1;
+                        float acc = 0.f;
+                        for (int cc1 = 0; cc1 < d1; ++cc1) acc = fmaf(G[c3 * d1 + cc1], __ldg(&f1[cc1]), acc);
+                        H[t] = acc;
+                    }
+                    __syncthreads();
+                    for (int t = tid; t < NK * Q; t += NT) {
+                        const int kh = t / Q, q = t % Q;
+                        const float* f3 = sv.fac[m][2] + (int64_t)kh * d3;
+                        float acc = 0.f;
+                        for (int c3 = 0; c3 < d3; ++c3) acc = fmaf(H[q * d3 + c3], __ldg(&f3[c3]), acc);
+                        KV0[(m * NK + kh) * Q + q] = acc;
+                    }
+                }
+            }
         }
-        const float* KV = KV0 + ((s / nrhs) & 1) * (P::KV_b / sizeof(float));
+        const float* KV = tucker ? KV0 : KV0 + ((s / nrhs) & 1) * (P::KV_b / sizeof(float));
         mbar_wait(&bar[st], (uint32_t)((s >> 1) & 1));
         // forward level 1 (thread (c, n2, q)): FFT_R1 over n1 of x[R2 n1 + n2], twiddle W_N^{n2 k1}
         if (tid < NT1) {
@@ -1853,7 +1893,7 @@ void run_pass_c(svh_handle* h, const Geom& g, float2* X2, int nrhs, cudaStream_t
                 constexpr int Q2 = decltype(Qc)::value, R2 = N == 128 ? 4 : 8;
                 using P2 = ZTma2<N, Q2, R2>;
                 CUtensorMap tm2;
-                if (!(zform == 2 && sv.spec && g.nx % Q2 == 0 &&
+                if (!(zform == 2 && g.nx % Q2 == 0 &&
                       encode_tmap_c64_3d_box(&tm2, X2, (uint64_t)g.nx, (uint64_t)h->ny, (uint64_t)5 * nrhs * h->kz,
                                              (uint64_t)g.nx, (uint64_t)g.nx * h->ny, Q2, 1, (uint32_t)h->kz)))
                     return false;

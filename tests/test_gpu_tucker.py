@@ -42,6 +42,21 @@ def test_tucker_matvec_small(svh_lib, shape, tol):
     assert st["compression_ratio"] > 1.0
 
 
+# Nz = 128 / 256 / 512: Tucker expansion inside the TMA-staged z pass (k_ztma2)
+@pytest.mark.parametrize("shape", [(9, 5, 40), (6, 4, 100), (5, 3, 150)])
+def test_tucker_matvec_ztma(svh_lib, shape):
+    tol = 1e-6
+    case = svh_inputs.random_fill(shape, fill=0.5, seed=7 + sum(shape), n_mat=2)
+    lat = Lattice(case["mat_id"])
+    I = svh_inputs.currents(lat.K, 3, seed=6)
+    w = 2 * np.pi * case["freq"]
+    for go in (True, False):
+        ref = matvec_direct(lat, case["materials"], w, case["dx"], I, green_only=go)
+        got, st = gpu(svh_lib, case, I, tol, go)
+        for r in range(3):
+            assert rel_l2(got[r], ref[r]) <= tol + 1e-5, (rel_l2(got[r], ref[r]), st["ranks"])
+
+
 def test_tucker_config2_sampled(svh_lib):
     """BASELINE configs[1] with its Tucker tol 1e-6 (256x32x4 meander), 48 sampled voxels."""
     case = svh_inputs.config2()
