@@ -1449,7 +1449,7 @@ struct ZTma2 {
 };
 
 template <int N, int Q, int R2_>
-__global__ void __launch_bounds__(ZTma2<N, Q, R2_>::NT, (N == 128 || (N < 512 && Q == 4)) ? 2 : 1)
+__global__ void __launch_bounds__(ZTma2<N, Q, R2_>::NT, (N <= 128 || (N < 512 && Q == 4)) ? 2 : 1)
     k_ztma2(const __grid_constant__ CUtensorMap tmap, SpecView sv, const float2* __restrict__ tw, int Nx, int Ny,
             int Kz, float g, int nrhs, int ngroups, int tiles_x, const uint8_t* __restrict__ planeok, int kxg) {
     using P = ZTma2<N, Q, R2_>;
@@ -1814,6 +1814,28 @@ void run_pass_y(svh_handle* h, const Geom& g, const float2* in, float2* out, int
                h->d_rowmask, h->rowMW);
 }
 
+// k_ztma2 launch: false if the grid does not tile (x extent not a multiple of Q) or the
+// tensor map cannot be encoded (the caller then takes another pass-C kernel)
+template <int N, int Q2, int R2>
+bool launch_ztma2(svh_handle* h, const Geom& g, float2* X2, int nrhs, const SpecView& sv, cudaStream_t s) {
+    using P2 = ZTma2<N, Q2, R2>;
+    CUtensorMap tm2;
+    if (g.nx % Q2 != 0 ||
+        !encode_tmap_c64_3d_box(&tm2, X2, (uint64_t)g.nx, (uint64_t)h->ny, (uint64_t)5 * nrhs * h->kz, (uint64_t)g.nx,
+                                (uint64_t)g.nx * h->ny, Q2, 1, (uint32_t)h->kz))
+        return false;
+    const int tiles_x = g.nx / Q2;
+    const int ngroups = tiles_x * h->ny;
+    int dev = 0, nsm = 148, occ = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    prep(k_ztma2<N, Q2, R2>, P2::smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ztma2<N, Q2, R2>, P2::NT, P2::smem);
+    SVH_LAUNCH((k_ztma2<N, Q2, R2>), std::min(ngroups, nsm * std::max(occ, 1)), P2::NT, P2::smem, s, tm2, sv,
+               h->d_tw[2], h->nx, h->ny, h->kz, h->gscale, nrhs, ngroups, tiles_x, h->d_planeok, g.kx0);
+    return true;
+}
+
 template <int N>
 void run_pass_c(svh_handle* h, const Geom& g, float2* X2, int nrhs, cudaStream_t s) {
     SpecView sv{};
@@ -1843,6 +1865,9 @@ void run_pass_c(svh_handle* h, const Geom& g, float2* X2, int nrhs, cudaStream_t
                 return;
             }
             static const int zmac2 = getenv("SVH_ZMAC2") ? atoi(getenv("SVH_ZMAC2")) : 1;
+            if constexpr (N == 32) {
+                if (zmac2 == 3 && launch_ztma2<32, 16, 4>(h, g, X2, nrhs, sv, s)) return;
+            }
             if (zmac2 == 2 && sv.spec && N >= 4) {
                 const size_t smem2 = zmac2_smem<N, true>();
                 prep(k_zmac2<N, true>, smem2);
@@ -1863,6 +1888,10 @@ void run_pass_c(svh_handle* h, const Geom& g, float2* X2, int nrhs, cudaStream_t
                        (uint64_t)h->planemask, g.nx, g.kx0, zpre);
             return;
         }
+    }
+    if constexpr (N == 64) {
+        static const int z64 = getenv("SVH_Z64") ? atoi(getenv("SVH_Z64")) : 2;   // 0: k_freq_small (measured 1.8x slower)
+        if (z64 == 2 && launch_ztma2<64, 16, 4>(h, g, X2, nrhs, sv, s)) return;
     }
     if constexpr (N <= 64) {
         static const int cq = getenv("SVH_CQ") ? atoi(getenv("SVH_CQ")) : 32;
@@ -1889,31 +1918,14 @@ void run_pass_c(svh_handle* h, const Geom& g, float2* X2, int nrhs, cudaStream_t
         static const int zform = getenv("SVH_ZTMA") ? atoi(getenv("SVH_ZTMA")) : 2;
         if constexpr (N >= 128 && N <= 512) {
             static const int zq = getenv("SVH_ZQ") ? atoi(getenv("SVH_ZQ")) : 8;
-            auto launch2 = [&](auto Qc) -> bool {
-                constexpr int Q2 = decltype(Qc)::value, R2 = N == 128 ? 4 : 8;
-                using P2 = ZTma2<N, Q2, R2>;
-                CUtensorMap tm2;
-                if (!(zform == 2 && g.nx % Q2 == 0 &&
-                      encode_tmap_c64_3d_box(&tm2, X2, (uint64_t)g.nx, (uint64_t)h->ny, (uint64_t)5 * nrhs * h->kz,
-                                             (uint64_t)g.nx, (uint64_t)g.nx * h->ny, Q2, 1, (uint32_t)h->kz)))
-                    return false;
-                const int tiles_x = g.nx / Q2;
-                const int ngroups = tiles_x * h->ny;
-                int dev = 0, nsm = 148, occ = 1;
-                cudaGetDevice(&dev);
-                cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-                prep(k_ztma2<N, Q2, R2>, P2::smem);
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ztma2<N, Q2, R2>, P2::NT, P2::smem);
-                SVH_LAUNCH((k_ztma2<N, Q2, R2>), std::min(ngroups, nsm * std::max(occ, 1)), P2::NT, P2::smem, s, tm2,
-                           sv, h->d_tw[2], h->nx, h->ny, h->kz, h->gscale, nrhs, ngroups, tiles_x, h->d_planeok,
-                           g.kx0);
-                return true;
-            };
-            if constexpr (N == 512) {
-                if (launch2(std::integral_constant<int, 4>{})) return;
-            } else {
-                if (zq == 8 ? launch2(std::integral_constant<int, 8>{}) : launch2(std::integral_constant<int, 4>{}))
-                    return;
+            constexpr int R2 = N == 128 ? 4 : 8;
+            if (zform == 2) {
+                if constexpr (N == 512) {
+                    if (launch_ztma2<N, 4, R2>(h, g, X2, nrhs, sv, s)) return;
+                } else {
+                    if (zq == 8 ? launch_ztma2<N, 8, R2>(h, g, X2, nrhs, sv, s) : launch_ztma2<N, 4, R2>(h, g, X2, nrhs, sv, s))
+                        return;
+                }
             }
         }
         if constexpr (N >= 128 && N <= 512) {

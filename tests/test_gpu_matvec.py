@@ -228,7 +228,8 @@ def test_setup_rejects_bad_grids(svh_lib):
 # Pass C for 128 <= Nz <= 512 (k_ztma, TMA-staged z pass): Kz = 33..64 -> Nz = 128,
 # Kz = 65..128 -> 256, Kz = 129..256 -> 512, incl. Kz = N/2 exactly, a ragged kx tile edge
 # in the embedding and 3 RHS (the tile order is RHS-fastest); plus empty planes.
-ZSHAPES = [((9, 5, 40), 0.5), ((20, 3, 64), 0.5), ((5, 3, 128), 0.6), ((6, 4, 150), 0.5)]
+ZSHAPES = [((9, 5, 40), 0.5), ((20, 3, 64), 0.5), ((5, 3, 128), 0.6), ((6, 4, 150), 0.5),
+           ((12, 7, 12), 0.5), ((10, 6, 24), 0.5)]   # Nz = 32 / 64 (k_ztma2 opt-in there)
 
 
 @pytest.mark.parametrize("shape,fill", ZSHAPES)
