@@ -543,7 +543,7 @@ struct YTma {
 // TIN (forward only): load whole input tiles by TMA through tmap_in (X1 [plane][y][x]) and
 // zero the rows without voxels in registers, instead of the pruned cp.async row loads.
 template <int N, int DIR, int S, int QQ, bool TIN = false>
-__global__ void __launch_bounds__(fft_r1(N) * QQ, QQ == 4 ? 2 : 1)
+__global__ void __launch_bounds__(fft_r1(N) * QQ, (QQ == 4 && N <= 1024) ? 2 : 1)
     k_ytma(const float2* __restrict__ in, float2* __restrict__ out, const __grid_constant__ CUtensorMap tmap,
            const __grid_constant__ CUtensorMap tmap_in, const float2* __restrict__ tw, int Nx, int Kz, int Lin,
            int Lout, int ntiles, int tiles_x, const int32_t* __restrict__ planes, int nzp,
@@ -625,12 +625,17 @@ __global__ void __launch_bounds__(fft_r1(N) * QQ, QQ == 4 ? 2 : 1)
     };
     const int n2 = tid / Q, q1 = tid % Q;
     const bool ph1 = n2 < R2;
-    float2 tw1[R1];
+    // phase-1 twiddles W_N^{n2 k1}: loop-invariant, in registers; for R1 = 64 (N = 2048) there is
+    // no register room next to the 64-point transform, they are read from the (L1-resident) table
+    constexpr bool TW_REG = R1 < 64;
+    float2 tw1[TW_REG ? R1 : 1];
+    if constexpr (TW_REG) {
 #pragma unroll
-    for (int kk = 1; kk < R1; ++kk) {
-        float2 w = ph1 ? __ldg(&tw[n2 * kk]) : zero;
-        if (DIR > 0) w.y = -w.y;
-        tw1[kk] = w;
+        for (int kk = 1; kk < R1; ++kk) {
+            float2 w = ph1 ? __ldg(&tw[n2 * kk]) : zero;
+            if (DIR > 0) w.y = -w.y;
+            tw1[kk] = w;
+        }
     }
     const int k1 = tid / Q, q2 = tid % Q;
     int t = blockIdx.x;
@@ -666,7 +671,16 @@ __global__ void __launch_bounds__(fft_r1(N) * QQ, QQ == 4 ? 2 : 1)
             }
             reg_fft<R1, DIR, (DIR < 0)>(v);
 #pragma unroll
-            for (int kk = 1; kk < R1; ++kk) v[kk] = cmul(v[kk], tw1[kk]);
+            for (int kk = 1; kk < R1; ++kk) {
+                float2 w;
+                if constexpr (TW_REG) {
+                    w = tw1[kk];
+                } else {
+                    w = __ldg(&tw[n2 * kk]);
+                    if (DIR > 0) w.y = -w.y;
+                }
+                v[kk] = cmul(v[kk], w);
+            }
 #pragma unroll
             for (int kk = 0; kk < R1; ++kk) T[em_idx<N, Q>(n2 * R1 + kk, q1)] = v[kk];
         }
@@ -1730,7 +1744,8 @@ void run_pass_y(svh_handle* h, const Geom& g, const float2* in, float2* out, int
     static const bool pipe_fwd = getenv("SVH_PIPE_B") != nullptr;
     static const int ystage = getenv("SVH_YSTAGE") ? atoi(getenv("SVH_YSTAGE")) : 3;  // 0 = off; bit0 fwd, bit1 inv
     static const bool ytma = getenv("SVH_YTMA") == nullptr || atoi(getenv("SVH_YTMA")) != 0;
-    if constexpr (N >= 128 && N <= 1024) {
+    static const bool ytma2048 = getenv("SVH_YTMA2048") == nullptr || atoi(getenv("SVH_YTMA2048")) != 0;
+    if constexpr (N >= 128 && N <= 2048) {
         CUtensorMap tmap;
         const float2* x2 = DIR < 0 ? out : in;   // the X2 side of the pass
         static const int yq = getenv("SVH_YQ") ? atoi(getenv("SVH_YQ")) : 4;
@@ -1767,9 +1782,13 @@ void run_pass_y(svh_handle* h, const Geom& g, const float2* in, float2* out, int
                 go(k_ytma<N, DIR, 2, QQ, false>);
             return true;
         };
-        if (ytma && ((yq == 4 && launch(std::integral_constant<int, 4>{})) ||
-                     (yq != 4 && launch(std::integral_constant<int, 8>{}))))
-            return;
+        if constexpr (N == 2048) {
+            if (ytma && ytma2048 && launch(std::integral_constant<int, 4>{})) return;
+        } else {
+            if (ytma && ((yq == 4 && launch(std::integral_constant<int, 4>{})) ||
+                         (yq != 4 && launch(std::integral_constant<int, 8>{}))))
+                return;
+        }
     }
     if constexpr (N >= 128 && N <= 1024) {
         if (((DIR < 0 && (ystage & 1)) || (DIR > 0 && (ystage & 2))) && nx % 8 == 0) {

@@ -255,3 +255,18 @@ def test_matvec_ztma_empty_planes(svh_lib):
     got = gpu_matvec(svh_lib, case, I, green_only=True)
     for r in range(2):
         assert rel_l2(got[r], ref[r]) < TOL, (r, rel_l2(got[r], ref[r]))
+
+
+# 2048-point y axis (K_y = 513..1024): the TMA-ring strided passes k_ytma<2048> (twiddles from
+# the table instead of registers)
+@pytest.mark.parametrize("shape", [(3, 600, 2), (2, 1000, 2)])
+def test_matvec_y2048(svh_lib, shape):
+    case = svh_inputs.random_fill(shape, fill=0.5, seed=41 + sum(shape), n_mat=2)
+    lat = Lattice(case["mat_id"])
+    I = svh_inputs.currents(lat.K, nrhs=2, seed=8)
+    w = 2 * np.pi * case["freq"]
+    for go in (True, False):
+        ref = matvec_direct(lat, case["materials"], w, case["dx"], I, green_only=go)
+        got = gpu_matvec(svh_lib, case, I, green_only=go)
+        for r in range(2):
+            assert rel_l2(got[r], ref[r]) < TOL, (go, r, rel_l2(got[r], ref[r]))
