@@ -1687,7 +1687,9 @@ void prep(F* kern, size_t bytes) {
 // rows per CTA for the row passes (A/E)
 template <int N>
 constexpr int row_q() {
-    return fft_r2(N) == 1 ? 128 : (256 / fft_threads_per_pencil(N) > 0 ? 256 / fft_threads_per_pencil(N) : 1);
+    // N >= 2048: the 64-point first level needs ~190 registers per thread; 2 rows (128 threads)
+    // per CTA lets two CTAs share an SM and overlap one's loads with the other's barriers
+    return fft_r2(N) == 1 ? 128 : N >= 2048 ? 2 : (256 / fft_threads_per_pencil(N) > 0 ? 256 / fft_threads_per_pencil(N) : 1);
 }
 // pencils per CTA for the strided passes (B/D)
 template <int N>
