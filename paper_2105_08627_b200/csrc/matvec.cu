@@ -1687,9 +1687,10 @@ void prep(F* kern, size_t bytes) {
 // rows per CTA for the row passes (A/E)
 template <int N>
 constexpr int row_q() {
-    // N >= 2048: the 64-point first level needs ~190 registers per thread; 2 rows (128 threads)
-    // per CTA lets two CTAs share an SM and overlap one's loads with the other's barriers
-    return fft_r2(N) == 1 ? 128 : N >= 2048 ? 2 : (256 / fft_threads_per_pencil(N) > 0 ? 256 / fft_threads_per_pencil(N) : 1);
+    // N >= 2048: the 64-point first level needs ~170 registers per thread; one row (64 threads)
+    // per CTA lets several CTAs share an SM and overlap one's loads with the others' barriers
+    // (measured on 1024^2 grids: 4 rows/CTA A 7.4 / E 11.3 ms, 2 rows 5.0 / 7.5, 1 row 4.8 / 6.8)
+    return fft_r2(N) == 1 ? 128 : N >= 2048 ? 1 : (256 / fft_threads_per_pencil(N) > 0 ? 256 / fft_threads_per_pencil(N) : 1);
 }
 // pencils per CTA for the strided passes (B/D)
 template <int N>
