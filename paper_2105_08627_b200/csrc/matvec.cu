@@ -1490,12 +1490,26 @@ __global__ void __launch_bounds__(ZTma2<N, Q, R2_>::NT, (N <= 128 || (N < 512 &&
     // this CTA's tile sequence: column groups blockIdx.x, +gridDim.x, ...; all RHS of a group
     auto group_of = [&](int s) { return (int)blockIdx.x + (s / nrhs) * (int)gridDim.x; };
     // group -> (kx tile, ky), ordered so that the mirror images of a column (kx -> Nx - kx,
-    // ky -> Ny - ky), which read the same octant rows of the kernel spectra, run close together
-    // in time (consecutive groups for x, one tile row apart for y): those rows are then L2 hits
+    // ky -> Ny - ky), which read the same octant rows of the kernel spectra, are consecutive
+    // groups (run at the same time on neighbouring CTAs): those rows are fetched from HBM once
+    // and are L2 hits for the other three.  First the mirror quadruples {xs, tiles_x-1-xs} x
+    // {j, Ny-j} (j = 1 .. Ny/2-1), then the self-mirrored rows ky = 0 and Ny/2.
+    const int npair = (tiles_x >= 2 && Ny >= 4) ? ((Ny >> 1) - 1) * 2 * tiles_x : 0;
     auto column = [&](int grp, int& xt, int& ky) {
-        const int xi = grp % tiles_x, yi = grp / tiles_x;
+        if (grp < npair) {
+            const int ysl = grp / (2 * tiles_x), rem = grp % (2 * tiles_x);
+            const int xs = rem >> 2;
+            xt = (rem & 1) ? tiles_x - 1 - xs : xs;
+            ky = ((rem >> 1) & 1) ? Ny - (ysl + 1) : ysl + 1;
+            return;
+        }
+        const int g2 = grp - npair;
+        const int xi = g2 % tiles_x, yi = g2 / tiles_x;
         xt = (xi & 1) ? tiles_x - 1 - (xi >> 1) : (xi >> 1);
-        ky = yi == 0 ? 0 : yi == 1 ? (Ny >> 1) : ((yi & 1) ? Ny - (yi >> 1) : (yi >> 1));
+        if (npair > 0)
+            ky = yi ? (Ny >> 1) : 0;
+        else
+            ky = yi == 0 ? 0 : yi == 1 ? (Ny >> 1) : ((yi & 1) ? Ny - (yi >> 1) : (yi >> 1));
     };
     auto issue = [&](int s, int st) {
         const int grp = group_of(s), r = s % nrhs;
