@@ -51,7 +51,7 @@ extern "C" {
 #define SVH_ENCCL      -4   /* reserved: collective error (multi-GPU layer is in Python) */
 #define SVH_ENOCONV    -5   /* GMRES not converged: best iterate returned, stats flagged */
 #define SVH_EOPENPORT  -6   /* |I_port| below floor (open port) */
-#define SVH_ECACHE     -7   /* reserved: Toeplitz cache (Algorithm 2) mismatch */
+#define SVH_ECACHE     -7   /* Toeplitz cache (Algorithm 2): unreadable, corrupt (CRC-32), wrong version or too small */
 
 typedef struct svh_handle svh_handle;
 typedef void* svh_stream;   /* a cudaStream_t (0 = legacy default stream) */
@@ -74,7 +74,9 @@ typedef struct { int32_t n_plus; const svh_face_rect* plus; int32_t n_minus; con
 typedef struct {
     double  tucker_tol;   /* 0 = dense octant spectra; >0 = Tucker-compressed kernels (Alg. 1) */
     int32_t restart;      /* GMRES restart (50) */
-    double  rre;          /* relative residual target ||b - Ax|| / ||b|| (1e-8) */
+    double  rre;          /* relative residual target ||b - Ax|| / ||b|| on the true residual.  P:174 uses
+                             1e-8 (MATLAB double); the default here is 1e-6 because the complex64 matvec
+                             is only ~3e-7 accurate (reading G16) -- smaller targets stall */
     double  inner_tol;    /* Schur-complement inner solve tolerance (1e-8) */
     int32_t inner_maxit;  /* inner PCG iteration cap */
     int32_t max_iters;    /* total GMRES iteration cap */
@@ -102,7 +104,8 @@ typedef struct {
  * kernels carry relative error <= tol).  Errors: SVH_EINVAL, SVH_ECACHE (I/O), SVH_ECUDA. */
 int svh_kernel_cache_build(const char* path, const int32_t* nmax, double tol, int32_t device);
 
-/* Default options (P:95 tol 1e-8 when Tucker is on, P:174 restart 50, RRE 1e-8, P:166 inner 1e-8). */
+/* Default options: tucker_tol 0 (dense spectra; P:95 uses 1e-8 when Tucker is on), restart 50,
+ * rre 1e-6 (P:174 prints 1e-8; see rre above), inner_tol 1e-8, inner_maxit 200, max_iters 2000. */
 void svh_default_opts(svh_opts* o);
 
 /*

@@ -95,11 +95,3 @@ class Lattice:
         A = sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
                           shape=(self.M, 5 * self.K))
         return A.tocsr()  # duplicates (none within a column) summed per row entry
-
-    def boundary_faces(self):
-        """Boolean over nodes: True where only one side of the face is occupied."""
-        cnt = np.zeros(self.M, dtype=np.int64)
-        for axis in range(3):
-            for side in (-1, 1):
-                np.add.at(cnt, self.face_node(axis, self.coords, side), 1)
-        return cnt == 1

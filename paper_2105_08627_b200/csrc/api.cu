@@ -96,8 +96,10 @@ static void build_lattice(svh_handle* h) {
     // row occupancy words for the gather/scatter of passes A/E
     h->rowW = (kx + 31) / 32;
     const int64_t rows = (int64_t)ky * kz;
-    std::vector<int2> ri((size_t)rows * h->rowW);
-    std::vector<uint8_t> matp(std::max<int64_t>(1, h->K));
+    // one sentinel row at index `rows` (first word {0, K}): the packed segment of row r is
+    // [ri[r W].y, ri[(r + 1) W].y).  matp is padded for the 4-byte cp.async of pass E.
+    std::vector<int2> ri((size_t)(rows + 1) * h->rowW, make_int2(0, 0));
+    std::vector<uint8_t> matp(std::max<int64_t>(1, h->K) + 16, 0);
     int64_t run = 0;   // packed index of the next occupied voxel (x-fastest order)
     for (int64_t r = 0; r < rows; ++r)
         for (int w = 0; w < h->rowW; ++w) {
@@ -115,6 +117,7 @@ static void build_lattice(svh_handle* h) {
             }
             ri[(size_t)r * h->rowW + w] = make_int2((int)m, (int)first);
         }
+    for (int w = 0; w < h->rowW; ++w) ri[(size_t)rows * h->rowW + w] = make_int2(0, (int)run);
     // non-empty rows / planes (pass pruning)
     h->rowMW = (ky + 31) / 32;
     std::vector<uint32_t> rm((size_t)kz * h->rowMW, 0u);
@@ -250,6 +253,10 @@ int svh_setup(const svh_grid* grid, const uint8_t* mat_id, const svh_material* m
                 h->opts = *opts;
             else
                 svh_default_opts(&h->opts);
+            // the Hessenberg column of FGMRES lives in a fixed 4096-double device scratch
+            // (solve.cu: 16 + 2 (restart + 1) doubles)
+            SVH_CHECK(h->opts.restart >= 1 && h->opts.restart <= 2039, SVH_EINVAL, "restart must be in 1..2039");
+            SVH_CHECK(h->opts.tucker_tol >= 0 && h->opts.tucker_tol < 1, SVH_EINVAL, "tucker_tol must be in [0, 1)");
             h->mats.assign(mats, mats + n_mat);
             h->h_mat.assign(mat_id, mat_id + h->Kt);
             for (int64_t c = 0; c < h->Kt; ++c)

@@ -10,9 +10,13 @@
 // Delta-x^5 scaling of Alg. 2 line 6 is the j*omega*mu0*dx prefactor applied at matvec time
 // (App. B, reading G1), so the cached kernels are dx-independent.
 //
-// File "SVXT" v1 (little endian): char magic[4], u32 version, i32 nmax[3], f64 tol, then per
-// kernel q = 0..6: i32 d[3], f64 err, f64 U_a[nmax_a][d_a] (a = 0..2, column-major nmax_a x
-// d_a), f64 core[d3][d2][d1].
+// File "SVXT" v2 (little endian; the layout of SPEC S:236): header = char magic[4] "SVXT",
+// u32 version, f64 tol, u64 nmax[3], u32 block count (7); per block (kernel q = 0..6, in the
+// order K0, K1x, K1y, K1z, K2x, K2y, K2z): char tag[2] ("00", "1x", "1y", "1z", "2x", "2y", "2z"),
+// u64 ranks d[3], f64 U_a (a = 0..2, column-major nmax_a x d_a), f64 core (column-major
+// d1 x d2 x d3, i.e. c1 fastest); then a trailing u32 CRC-32 (IEEE 802.3, the zlib crc32) of
+// every preceding byte.  Restore refuses (SVH_ECACHE) a bad magic, version, block count, tag,
+// rank or CRC, a truncated file, and a cache smaller than the grid.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -34,7 +38,25 @@ void mode_products(const double* T, int Kx, int Ky, int Kz, const double* A, int
 
 namespace {
 
-constexpr uint32_t kVersion = 1;
+constexpr uint32_t kVersion = 2;
+const char* const kTags[7] = {"00", "1x", "1y", "1z", "2x", "2y", "2z"};
+
+uint32_t crc32_update(uint32_t crc, const void* data, size_t n) {
+    static uint32_t table[256];
+    static bool init = false;
+    if (!init) {
+        for (uint32_t i = 0; i < 256; ++i) {
+            uint32_t c = i;
+            for (int k = 0; k < 8; ++k) c = (c & 1u) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
+            table[i] = c;
+        }
+        init = true;
+    }
+    const unsigned char* p = static_cast<const unsigned char*>(data);
+    crc = ~crc;
+    for (size_t i = 0; i < n; ++i) crc = table[(crc ^ p[i]) & 0xFFu] ^ (crc >> 8);
+    return ~crc;
+}
 
 __global__ void k_unweight(const double* __restrict__ w, double* __restrict__ t, int Kx, int Ky, int Kz) {
     const int64_t Kt = (int64_t)Kx * Ky * Kz;
@@ -52,14 +74,27 @@ struct File {
     }
 };
 
-template <typename T>
-void put(FILE* f, const T* v, size_t n) {
-    SVH_CHECK(std::fwrite(v, sizeof(T), n, f) == n, SVH_ECACHE, "kernel cache: write failed");
-}
-template <typename T>
-void get(FILE* f, T* v, size_t n) {
-    SVH_CHECK(std::fread(v, sizeof(T), n, f) == n, SVH_ECACHE, "kernel cache: truncated file");
-}
+// writer that keeps the running CRC-32 of everything written
+struct Writer {
+    FILE* f;
+    uint32_t crc = 0;
+    template <typename T>
+    void put(const T* v, size_t n) {
+        SVH_CHECK(std::fwrite(v, sizeof(T), n, f) == n, SVH_ECACHE, "kernel cache: write failed");
+        crc = crc32_update(crc, v, sizeof(T) * n);
+    }
+};
+// reader over the whole file in memory (CRC checked before anything is parsed)
+struct Reader {
+    std::vector<unsigned char> buf;
+    size_t pos = 0, end = 0;
+    template <typename T>
+    void get(T* v, size_t n) {
+        SVH_CHECK(end - pos >= sizeof(T) * n, SVH_ECACHE, "kernel cache: truncated file");
+        std::memcpy(v, buf.data() + pos, sizeof(T) * n);
+        pos += sizeof(T) * n;
+    }
+};
 
 }  // namespace
 
@@ -77,37 +112,63 @@ void kernel_cache_build(const char* path, const int* nmax, double tol, int devic
     compute_kernels(h.get());
     File fo(path, "wb");
     SVH_CHECK(fo.f, SVH_ECACHE, std::string("kernel cache: cannot open ") + path);
-    put(fo.f, "SVXT", 4);
-    put(fo.f, &kVersion, 1);
-    put(fo.f, nmax, 3);
-    put(fo.f, &tol, 1);
+    Writer w{fo.f};
+    w.put("SVXT", 4);
+    w.put(&kVersion, 1);
+    w.put(&tol, 1);
+    const uint64_t n64[3] = {(uint64_t)nmax[0], (uint64_t)nmax[1], (uint64_t)nmax[2]};
+    w.put(n64, 3);
+    const uint32_t nblocks = 7;
+    w.put(&nblocks, 1);
     const int K3[3] = {h->kx, h->ky, h->kz};
-    tucker_hosvd_raw(h.get(), tol, [&](int, const int* d, const std::vector<double>* U, const double* dCore, double err) {
-        put(fo.f, d, 3);
-        put(fo.f, &err, 1);
-        for (int a = 0; a < 3; ++a) put(fo.f, U[a].data(), (size_t)K3[a] * d[a]);   // first d_a columns
+    tucker_hosvd_raw(h.get(), tol, [&](int q, const int* d, const std::vector<double>* U, const double* dCore, double) {
+        w.put(kTags[q], 2);
+        const uint64_t d64[3] = {(uint64_t)d[0], (uint64_t)d[1], (uint64_t)d[2]};
+        w.put(d64, 3);
+        for (int a = 0; a < 3; ++a) w.put(U[a].data(), (size_t)K3[a] * d[a]);   // first d_a columns
         std::vector<double> core((size_t)d[0] * d[1] * d[2]);
         SVH_CUDA(cudaMemcpy(core.data(), dCore, core.size() * sizeof(double), cudaMemcpyDeviceToHost));
-        put(fo.f, core.data(), core.size());
+        w.put(core.data(), core.size());
     });
+    const uint32_t crc = w.crc;
+    SVH_CHECK(std::fwrite(&crc, 4, 1, fo.f) == 1, SVH_ECACHE, "kernel cache: write failed");
     cudaFree(h->d_kern);
     h->d_kern = nullptr;
 }
 
 // h->d_kern [7][Kt] restored from the cache (replaces compute_kernels)
 void kernel_cache_restore(svh_handle* h, const char* path) {
-    File fi(path, "rb");
-    SVH_CHECK(fi.f, SVH_ECACHE, std::string("kernel cache: cannot open ") + path);
+    Reader rd;
+    {
+        File fi(path, "rb");
+        SVH_CHECK(fi.f, SVH_ECACHE, std::string("kernel cache: cannot open ") + path);
+        std::fseek(fi.f, 0, SEEK_END);
+        const long n = std::ftell(fi.f);
+        std::fseek(fi.f, 0, SEEK_SET);
+        SVH_CHECK(n >= 48, SVH_ECACHE, "kernel cache: truncated file");
+        rd.buf.resize((size_t)n);
+        SVH_CHECK(std::fread(rd.buf.data(), 1, (size_t)n, fi.f) == (size_t)n, SVH_ECACHE, "kernel cache: read failed");
+        rd.end = (size_t)n - 4;
+    }
     char magic[4];
-    uint32_t ver = 0;
-    int nmax[3];
+    uint32_t ver = 0, nblocks = 0, crc = 0;
+    uint64_t n64[3];
     double tol = 0;
-    get(fi.f, magic, 4);
+    rd.get(magic, 4);
     SVH_CHECK(std::memcmp(magic, "SVXT", 4) == 0, SVH_ECACHE, "kernel cache: not an SVXT file");
-    get(fi.f, &ver, 1);
+    rd.get(&ver, 1);
     SVH_CHECK(ver == kVersion, SVH_ECACHE, "kernel cache: version mismatch");
-    get(fi.f, nmax, 3);
-    get(fi.f, &tol, 1);
+    std::memcpy(&crc, rd.buf.data() + rd.end, 4);
+    SVH_CHECK(crc32_update(0, rd.buf.data(), rd.end) == crc, SVH_ECACHE, "kernel cache: checksum mismatch");
+    rd.get(&tol, 1);
+    rd.get(n64, 3);
+    rd.get(&nblocks, 1);
+    SVH_CHECK(nblocks == 7, SVH_ECACHE, "kernel cache: block count is not 7");
+    int nmax[3];
+    for (int a = 0; a < 3; ++a) {
+        SVH_CHECK(n64[a] >= 1 && n64[a] <= 2048, SVH_ECACHE, "kernel cache: corrupt N_max");
+        nmax[a] = (int)n64[a];
+    }
     const int K3[3] = {h->kx, h->ky, h->kz};
     for (int a = 0; a < 3; ++a)
         SVH_CHECK(K3[a] <= nmax[a], SVH_ECACHE, "kernel cache smaller than the grid (Alg. 2 needs Nmax >= K)");
@@ -125,14 +186,19 @@ void kernel_cache_restore(svh_handle* h, const char* path) {
         SVH_CUDA(cudaMalloc(&dW, Kt * sizeof(double)));
         size_t wcap = 0;
         for (int q = 0; q < 7; ++q) {
+            char tag[2];
+            rd.get(tag, 2);
+            SVH_CHECK(std::memcmp(tag, kTags[q], 2) == 0, SVH_ECACHE, "kernel cache: unexpected block tag");
+            uint64_t d64[3];
+            rd.get(d64, 3);
             int d[3];
-            double err = 0;
-            get(fi.f, d, 3);
-            get(fi.f, &err, 1);
             for (int a = 0; a < 3; ++a) {
-                SVH_CHECK(d[a] >= 1 && d[a] <= nmax[a], SVH_ECACHE, "kernel cache: corrupt ranks");
+                SVH_CHECK(d64[a] >= 1 && d64[a] <= (uint64_t)nmax[a], SVH_ECACHE, "kernel cache: corrupt ranks");
+                d[a] = (int)d64[a];
+            }
+            for (int a = 0; a < 3; ++a) {
                 std::vector<double> U((size_t)nmax[a] * d[a]), Ut((size_t)K3[a] * d[a]);
-                get(fi.f, U.data(), U.size());
+                rd.get(U.data(), U.size());
                 for (int j = 0; j < d[a]; ++j)   // trim: leading K_a rows of every column
                     std::memcpy(&Ut[(size_t)j * K3[a]], &U[(size_t)j * nmax[a]], K3[a] * sizeof(double));
                 cudaFree(dU[a]);
@@ -140,7 +206,7 @@ void kernel_cache_restore(svh_handle* h, const char* path) {
                 SVH_CUDA(cudaMemcpy(dU[a], Ut.data(), Ut.size() * sizeof(double), cudaMemcpyHostToDevice));
             }
             std::vector<double> core((size_t)d[0] * d[1] * d[2]);
-            get(fi.f, core.data(), core.size());
+            rd.get(core.data(), core.size());
             cudaFree(dCore);
             SVH_CUDA(cudaMalloc(&dCore, core.size() * sizeof(double)));
             SVH_CUDA(cudaMemcpy(dCore, core.data(), core.size() * sizeof(double), cudaMemcpyHostToDevice));

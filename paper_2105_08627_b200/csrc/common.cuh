@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
+#include <exception>
+#include <new>
 #include <string>
 
 #include "svh.h"
@@ -26,6 +28,21 @@ struct Error {
                                               + " (" + __FILE__ + ":" + std::to_string(__LINE__) + ")"}; \
         }                                                                                    \
     } while (0)
+
+// catch clauses of every extern "C" entry point: no C++ exception crosses the C-ABI
+#define SVH_C_ABI_CATCH                                                                   \
+    catch (const ::svh::Error& e) {                                                       \
+        ::svh::set_error(e.msg);                                                          \
+        return e.code;                                                                    \
+    }                                                                                     \
+    catch (const std::bad_alloc&) {                                                       \
+        ::svh::set_error("host allocation failed");                                       \
+        return SVH_ENOMEM;                                                                \
+    }                                                                                     \
+    catch (const std::exception& e) {                                                     \
+        ::svh::set_error(e.what());                                                       \
+        return SVH_EINVAL;                                                                \
+    }
 
 #define SVH_CHECK(cond, code, msg)                \
     do {                                          \

@@ -24,6 +24,8 @@
 
 #include "fft.cuh"
 #include "internal.h"
+#include "rowfft.cuh"
+#include "zpass.cuh"
 #include "tma.cuh"
 
 namespace svh {
@@ -754,14 +756,6 @@ __device__ __forceinline__ void mac5(float2 (&v)[5], float k0, float s1x, float 
     v[4] = cmul_i(C3, g);
 }
 
-struct SpecView {
-    const float* spec;   // dense [7][hz][hy][hx]; null in Tucker mode
-    int hx, hy, hz;
-    // Tucker mode (Eq. 10): factors [7][3] -> fp32 [h_i][d_i], cores [7] -> fp32 [d3][d2][d1]
-    const float* fac[7][3];
-    const float* core[7];
-    int rk[7][3];
-};
 
 // Tucker expansion of the 7 kernel spectra for a CTA tile (fixed ky, Q consecutive kx, all N kz)
 // into KV[m][kz][q]: G = core x2 F2[oy] (d3 x d1), H[q] = G x1 F1[ox_q] (d3), KV = H x3 F3[oz].
@@ -1691,11 +1685,16 @@ namespace {
 
 template <typename F>
 void prep(F* kern, size_t bytes) {
-    // every pass kernel gets the max shared-memory carveout; >48 KB needs opt-in
+    // every pass kernel gets the max shared-memory carveout; >48 KB needs opt-in.  The attributes
+    // are set once per (kernel, size): these driver calls cost host time on every launch otherwise.
+    static thread_local std::vector<std::pair<const void*, size_t>> done;
+    for (const auto& d : done)
+        if (d.first == (const void*)kern && d.second >= bytes) return;
     SVH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                   (int)cudaSharedmemCarveoutMaxShared));
     if (bytes > 48 * 1024)
         SVH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    done.emplace_back((const void*)kern, bytes);
 }
 
 // rows per CTA for the row passes (A/E)
@@ -1728,11 +1727,56 @@ static Geom whole_grid(const svh_handle* h) {
 }
 namespace {
 
+// persistent grid size for a kernel: min(work units, SMs x resident CTAs)
+// (occupancy queried once per (device, kernel, block, smem): the query costs host time)
+template <typename F>
+int persistent_grid(F kern, int nt, size_t smem, int64_t units) {
+    struct Rec {
+        int dev;
+        const void* k;
+        int nt;
+        size_t smem;
+        int ctas;
+    };
+    static thread_local std::vector<Rec> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int ctas = 0;
+    for (const auto& r : cache)
+        if (r.dev == dev && r.k == (const void*)kern && r.nt == nt && r.smem == smem) ctas = r.ctas;
+    if (ctas == 0) {
+        int nsm = 148, occ = 1;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, smem);
+        ctas = nsm * std::max(occ, 1);
+        cache.push_back(Rec{dev, (const void*)kern, nt, smem, ctas});
+    }
+    return (int)std::max<int64_t>(1, std::min<int64_t>(units, ctas));
+}
+
 template <int N>
 void run_pass_a(svh_handle* h, const Geom& g, const float2* in, float2* X1, bool packed, int nrhs, cudaStream_t s) {
-    constexpr int Q = row_q<N>();
     const int rows = g.kyl * h->kz;
     const int64_t Ktl = (int64_t)g.kyl * h->kz * h->kx;
+    if constexpr (N >= 128) {
+        using PL = RowPlan<N>;
+        const int nlist = g.nrows;
+        if (nlist == 0) return;
+        const int64_t units = (int64_t)((nlist + PL::RPC - 1) / PL::RPC) * 5 * nrhs;
+        const size_t smem = PL::smem + (size_t)PL::RPC * 2 * RowSlot<N>::A_b;
+        auto go = [&](auto kern) {
+            prep(kern, smem);
+            SVH_LAUNCH(kern, persistent_grid(kern, PL::NT, smem, units), PL::NT, smem, s, in, X1,
+                       h->d_rowinfo, h->rowW, g.rowlist, nlist, h->d_tw[0], h->kx, rows, h->K, Ktl, h->ky, g.kyl,
+                       g.y0, 5 * nrhs);
+        };
+        if (packed)
+            go(k_rowA<N, true>);
+        else
+            go(k_rowA<N, false>);
+        return;
+    }
+    constexpr int Q = row_q<N>();
     const int nt = fft_threads_per_pencil(N) * Q;
     const size_t smem = fft_r2(N) == 1 ? 0 : (size_t)Q * (N + N / fft_r1(N)) * sizeof(float2);
     const int nlist = g.nrows;
@@ -1887,6 +1931,34 @@ void run_pass_c(svh_handle* h, const Geom& g, float2* X2, int nrhs, cudaStream_t
                 sv.rk[m][a] = h->tucker.ranks[m][a];
             }
         }
+    if constexpr (N >= 64 && N <= 256) {
+        // 16 kx per tile: pass C's HBM pattern is Q*8-byte runs at the plane stride; a pure
+        // read-modify-write of that pattern reaches 2.4 / 4.2 / 5.4 TB/s for Q = 8 / 16 / 32
+        // (scripts/micro/zpattern.cu on B200), so the tile is as wide as shared memory allows
+        // (Q = 8 when high Tucker ranks leave no room for 16)
+        int dmax = 0;
+        if (h->use_tucker)
+            for (int m = 0; m < 7; ++m)
+                for (int a = 0; a < 3; ++a) dmax = std::max(dmax, sv.rk[m][a]);
+        auto launch = [&](auto Qc) -> bool {
+            constexpr int Q = decltype(Qc)::value;
+            constexpr int R2 = N == 256 ? 8 : 4;
+            using P = ZPlan<N, R2, Q>;
+            const size_t smem = P::smem(dmax);
+            if (g.nx % Q != 0 || smem > 227 * 1024) return false;
+            auto kern = k_zpass<N, R2, Q>;
+            prep(kern, smem);
+            const int64_t units = (int64_t)(h->ny / 2 + 1) * (g.nx / Q);
+            SVH_LAUNCH(kern, persistent_grid(kern, P::NT, smem, units), P::NT, smem, s, X2, sv, h->d_tw[2], h->nx,
+                       h->ny, h->kz, g.nx, g.kx0, h->gscale, nrhs, h->d_planeok, dmax);
+            return true;
+        };
+        if constexpr (N == 256) {
+            if (launch(std::integral_constant<int, 8>{}) || launch(std::integral_constant<int, 4>{})) return;
+        } else {
+            if (launch(std::integral_constant<int, 16>{}) || launch(std::integral_constant<int, 8>{})) return;
+        }
+    }
     static const bool zmac = getenv("SVH_ZMAC") == nullptr || atoi(getenv("SVH_ZMAC")) != 0;
     if constexpr (N >= 2 && N <= 32) {
         if (zmac) {
@@ -1999,15 +2071,32 @@ template <int N>
 void run_pass_e(svh_handle* h, const Geom& g, const float2* X1, const float2* in, float2* out, bool packed,
                 bool green_only,
                 int nrhs, cudaStream_t s) {
-    constexpr int Q = row_q<N>();
     const int rows = g.kyl * h->kz;
     const int64_t Ktl = (int64_t)g.kyl * h->kz * h->kx;
-    const int nt = fft_threads_per_pencil(N) * Q;
-    const size_t smem = fft_r2(N) == 1 ? 0 : (size_t)Q * (N + N / fft_r1(N)) * sizeof(float2);
     const int nzl = (int)h->mats.size() + 1;
     // packed output: only the non-empty rows; grid output: every row (empty ones get zeros)
     const int nlist = packed ? (int)h->n_rows_ne : rows;
     const int32_t* rl = packed ? h->d_rowlist : nullptr;
+    if constexpr (N >= 128) {
+        using PL = RowPlan<N>;
+        if (nlist == 0) return;
+        const int64_t units = (int64_t)((nlist + PL::RPC - 1) / PL::RPC) * 5 * nrhs;
+        const size_t smem = PL::smem + (size_t)PL::RPC * 2 * RowSlot<N>::E_b;
+        auto go = [&](auto kern) {
+            prep(kern, smem);
+            SVH_LAUNCH(kern, persistent_grid(kern, PL::NT, smem, units), PL::NT, smem, s, X1, out, in,
+                       h->d_rowinfo, h->rowW, rl, nlist, h->d_rowmask, h->rowMW, h->ky, h->d_matp, h->d_zloc, nzl,
+                       h->d_tw[0], h->kx, rows, h->K, Ktl, (int)green_only, g.kyl, g.y0, 5 * nrhs);
+        };
+        if (packed)
+            go(k_rowE<N, true>);
+        else
+            go(k_rowE<N, false>);
+        return;
+    }
+    constexpr int Q = row_q<N>();
+    const int nt = fft_threads_per_pencil(N) * Q;
+    const size_t smem = fft_r2(N) == 1 ? 0 : (size_t)Q * (N + N / fft_r1(N)) * sizeof(float2);
     dim3 grid((nlist + Q - 1) / Q, 5 * nrhs);
     if (packed) {
         prep(k_row_inv<N, Q, true>, smem);
@@ -2065,7 +2154,7 @@ int max_chunk(svh_handle* h) {
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
     const size_t per = (size_t)5 * h->kz * (h->ky + h->ny) * h->nx * sizeof(float2);
-    size_t budget = (size_t)(0.5 * (double)(fr + (size_t)h->ws_rhs * per));
+    size_t budget = (size_t)(0.75 * (double)(fr + (size_t)h->ws_rhs * per));
     return (int)std::max<size_t>(1, std::min<size_t>(64, budget / per));
 }
 

@@ -1656,10 +1656,8 @@ int svh_apply_system(svh_handle* h, const void* x, void* y, int32_t nrhs, svh_st
         cudaFree(zi);
         cudaFree(xin);
         return SVH_OK;
-    } catch (const Error& e) {
-        set_error(e.msg);
-        return e.code;
     }
+    SVH_C_ABI_CATCH
 }
 
 int svh_solve_columns(svh_handle* h, const svh_port* ports, int32_t n_ports, const int32_t* sel, int32_t n_sel,
@@ -1670,10 +1668,8 @@ int svh_solve_columns(svh_handle* h, const svh_port* ports, int32_t n_ports, con
         if (stats) std::memset(stats, 0, sizeof(*stats));
         solve_columns(h, ports, n_ports, sel, n_sel, Y_cols, stats);
         return SVH_OK;
-    } catch (const Error& e) {
-        set_error(e.msg);
-        return e.code;
     }
+    SVH_C_ABI_CATCH
 }
 
 int svh_solve(svh_handle* h, const svh_port* ports, int32_t n_ports, double* Z_port, double* L_H, double* R_ohm,
@@ -1705,10 +1701,8 @@ int svh_solve(svh_handle* h, const svh_port* ports, int32_t n_ports, double* Z_p
         const int c2 = svh_y_to_zl(Yr.data(), P, h->freq, Z_port, L_H, R_ohm);
         if (c2 != SVH_OK) return c2;
         return code;
-    } catch (const Error& e) {
-        set_error(e.msg);
-        return e.code;
     }
+    SVH_C_ABI_CATCH
 }
 
 int svh_y_to_zl(const double* Yp, int32_t P, double freq_hz, double* Z_port, double* L_H, double* R_ohm) {
@@ -1750,10 +1744,8 @@ int svh_y_to_zl(const double* Yp, int32_t P, double freq_hz, double* Z_port, dou
                 if (R_ohm) R_ohm[k] = z.real();
             }
         return SVH_OK;
-    } catch (const Error& e) {
-        set_error(e.msg);
-        return e.code;
     }
+    SVH_C_ABI_CATCH
 }
 
 }  // extern "C"

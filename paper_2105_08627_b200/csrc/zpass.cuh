@@ -1,0 +1,252 @@
+// Pass C of the matvec for 64 <= Nz <= 256 (Eq. 9; Tucker restoration P:89-101):
+// z-FFT of the 5 embedded current components, the 5 -> 5 moment-form MAC with the 7 kernel
+// spectra, inverse z-FFT and crop, in place on X2 = [rc][Kz][Ny][Nxs].
+//
+// Work unit = (oy, kx tile of Q columns): the rows ky = oy and Ny - oy share their raw kernel
+// spectra (K1y only flips sign, applied in the MAC), so the 7 x (N/2 + 1) x Q raw values are
+// built once per unit -- by the on-chip Tucker expansion (Eq. 10) or from the dense octant --
+// and used for both rows and every right-hand side.  A tile = one (RHS, row, kx tile).
+//
+// The z-FFT is split N = R1 x R2 (R1 = 16/32, R2 = 4/8):
+//   L1 (thread (c, n2, q)):  R1-point FFT over n1 of x[R2 n1 + n2] (inputs z >= N/2 are the zero
+//                            padding: R1/2 loads, straight from HBM into registers, prefetched one
+//                            tile ahead), written to the exchange buffer T;
+//   L2 (thread (k1, q)):     all 5 components: twiddle W_N^{n2 k1}, R2-point FFT -> kz = k1 + R1 k2,
+//                            MAC in registers, inverse R2-point FFT, twiddle W_N^{-n2 k1}, back to T;
+//   L1 inverse:              R1-point inverse FFT over k1 -> z = n2 + R2 n1, the kept z < Kz are
+//                            stored straight to HBM.
+// L1 needs no twiddles (compile-time constants); L2's R2-1 twiddles are per-thread constants.
+// Two barriers per tile; T is double-buffered so the next tile's L1 overlaps nothing it reads.
+#pragma once
+#include "fft.cuh"
+#include "tma.cuh"
+
+namespace svh {
+
+struct SpecView {
+    const float* spec;   // dense [7][hz][hy][hx]; null in Tucker mode
+    int hx, hy, hz;
+    // Tucker mode (Eq. 10): factors [7][3] -> fp32 [h_i][d_i], cores [7] -> fp32 [d3][d2][d1]
+    const float* fac[7][3];
+    const float* core[7];
+    int rk[7][3];
+};
+
+template <int N, int R2_, int Q_>
+struct ZPlan {
+    static constexpr int N_ = N, R2 = R2_, Q = Q_, R1 = N / R2_, NH = N / 2, NK = N / 2 + 1;
+    static constexpr int NL1 = 5 * R2 * Q, NL2 = R1 * Q;
+    static constexpr int NT = ((NL1 > NL2 ? NL1 : NL2) + 31) / 32 * 32;
+    static constexpr int TB = R1 * Q + Q;                 // one (c, n2) block of T, padded by Q
+    static constexpr int TE = 5 * R2 * TB;                // elements of one T buffer
+    static constexpr size_t T_b = (size_t)2 * TE * sizeof(float2);
+    static constexpr size_t KV_b = (size_t)7 * NK * Q * sizeof(float);
+    // Tucker scratch: G [7][d3][d1] and H [7][Q][d3] for ranks <= dmax
+    static size_t smem(int dmax) {
+        return T_b + KV_b + (size_t)7 * dmax * dmax * sizeof(float) + (size_t)7 * Q * dmax * sizeof(float);
+    }
+    static_assert(NL1 <= NT && NL2 <= NT, "z plan: one L1 and one L2 task per thread");
+};
+
+template <int N, int R2, int Q>
+__global__ void __launch_bounds__(ZPlan<N, R2, Q>::NT, ZPlan<N, R2, Q>::NT > 256 ? 1 : 2)
+    k_zpass(float2* __restrict__ X2, SpecView sv, const float2* __restrict__ tw, int Nx, int Ny, int Kz, int Nxs,
+            int kxg, float g, int nrhs, const uint8_t* __restrict__ planeok, int dmax) {
+    using P = ZPlan<N, R2, Q>;
+    constexpr int R1 = P::R1, NK = P::NK, TB = P::TB, TE = P::TE, NL1 = P::NL1, NL2 = P::NL2;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    float2* T = reinterpret_cast<float2*>(smraw);                       // [2][5][R2][TB]
+    float* KV = reinterpret_cast<float*>(smraw + P::T_b);               // [7][NK][Q] raw spectra
+    float* G = KV + 7 * NK * Q;                                         // [7][d3][d1]
+    float* H = G + 7 * dmax * dmax;                                     // [7][Q][d3]
+    const int tid = threadIdx.x;
+    const float2 zero = make_float2(0.f, 0.f);
+    const bool tucker = sv.spec == nullptr;
+    const int64_t plane = (int64_t)Nxs * Ny;
+    const int tiles_x = Nxs / Q;
+    const int nunits = (Ny / 2 + 1) * tiles_x;
+    // this CTA's contiguous chunk of units
+    const int u0 = (int)((int64_t)nunits * blockIdx.x / gridDim.x);
+    const int u1 = (int)((int64_t)nunits * (blockIdx.x + 1) / gridDim.x);
+    // L1 role
+    const bool l1 = tid < NL1;
+    const int c1 = tid / (R2 * Q), n2 = (tid / Q) % R2, q1 = tid % Q;
+    // L2 role and its twiddles W_N^{n2 k1}, n2 = 1 .. R2-1
+    const bool l2 = tid < NL2;
+    const int k1 = tid / Q, q2 = tid % Q;
+    float2 w2[R2];
+#pragma unroll
+    for (int m = 0; m < R2; ++m) w2[m] = l2 ? __ldg(&tw[(m * k1) & (N - 1)]) : zero;
+    // tile sequence inside a unit: row 0 / 1 (ky = oy, Ny - oy; one row if they coincide) x RHS
+    auto unit_rows = [&](int u) { const int oy = u / tiles_x; return (oy == 0 || 2 * oy == Ny) ? 1 : 2; };
+    // decode tile (u, i) -> ky, xt, r
+    auto tile_of = [&](int u, int i, int& ky, int& xt, int& r) {
+        const int oy = u / tiles_x;
+        xt = u % tiles_x;
+        const int row = i / nrhs;
+        r = i % nrhs;
+        ky = row == 0 ? oy : Ny - oy;
+    };
+    // L1 prefetch registers: the R1/2 live inputs of the next tile
+    float2 nx[R1 / 2];
+    auto load_tile = [&](int u, int i) {
+        int ky, xt, r;
+        tile_of(u, i, ky, xt, r);
+        const float2* src = X2 + ((int64_t)(r * 5 + c1) * Kz) * plane + (int64_t)ky * Nxs + xt * Q + q1;
+#pragma unroll
+        for (int n1 = 0; n1 < R1 / 2; ++n1) {
+            const int z = R2 * n1 + n2;
+            nx[n1] = (z < Kz && __ldg(&planeok[z])) ? src[(int64_t)z * plane] : zero;
+        }
+    };
+    int u = u0, i = 0;
+    if (u < u1 && l1) load_tile(u, 0);
+    int cur_oy = -1;
+    for (int s = 0; u < u1; ++s) {
+        float2* Tb = T + (s & 1) * TE;
+        int ky, xt, r;
+        tile_of(u, i, ky, xt, r);
+        const int oy = u / tiles_x;
+        if (i == 0) {
+            // the unit's raw kernel spectra KV[m][kh][q] (previous tile's L2 finished at its 2nd barrier)
+            if (tucker) {
+                if (oy != cur_oy) {
+                    // G_m = core_m x2 F2_m[oy]   ([d3][d1], once per oy)
+                    for (int m = 0; m < 7; ++m) {
+                        const int d1 = sv.rk[m][0], d2 = sv.rk[m][1], d3 = sv.rk[m][2];
+                        const float* C = sv.core[m];
+                        const float* F2 = sv.fac[m][1] + (int64_t)oy * d2;
+                        for (int t = tid; t < d3 * d1; t += P::NT) {
+                            const int c3 = t / d1, cc1 = t % d1;
+                            float acc = 0.f;
+                            for (int cc2 = 0; cc2 < d2; ++cc2)
+                                acc = fmaf(__ldg(&C[((int64_t)c3 * d2 + cc2) * d1 + cc1]), __ldg(&F2[cc2]), acc);
+                            G[m * dmax * dmax + t] = acc;
+                        }
+                    }
+                    cur_oy = oy;
+                    __syncthreads();
+                }
+                // H_m[q] = G_m x1 F1_m[ox_q]   ([Q][d3])
+                for (int m = 0; m < 7; ++m) {
+                    const int d1 = sv.rk[m][0], d3 = sv.rk[m][2];
+                    for (int t = tid; t < Q * d3; t += P::NT) {
+                        const int q = t / d3, c3 = t % d3;
+                        const int kx = kxg + xt * Q + q;
+                        const int ox = kx <= (Nx >> 1) ? kx : Nx - kx;
+                        const float* f1 = sv.fac[m][0] + (int64_t)ox * d1;
+                        const float* gm = G + m * dmax * dmax + c3 * d1;
+                        float acc = 0.f;
+                        for (int cc1 = 0; cc1 < d1; ++cc1) acc = fmaf(gm[cc1], __ldg(&f1[cc1]), acc);
+                        H[(m * Q + q) * dmax + c3] = acc;
+                    }
+                }
+                __syncthreads();
+                // KV_m[kh][q] = H_m[q] . F3_m[kh]
+                for (int t = tid; t < 7 * NK * Q; t += P::NT) {
+                    const int q = t % Q, rest = t / Q;
+                    const int kh = rest % NK, m = rest / NK;
+                    const int d3 = sv.rk[m][2];
+                    const float* f3 = sv.fac[m][2] + (int64_t)kh * d3;
+                    const float* hm = H + (m * Q + q) * dmax;
+                    float acc = 0.f;
+                    for (int c3 = 0; c3 < d3; ++c3) acc = fmaf(hm[c3], __ldg(&f3[c3]), acc);
+                    KV[t] = acc;
+                }
+            } else {
+                const int64_t pl = (int64_t)sv.hx * sv.hy * sv.hz;
+                for (int t = tid; t < 7 * NK * Q; t += P::NT) {
+                    const int q = t % Q, rest = t / Q;
+                    const int kh = rest % NK, m = rest / NK;
+                    const int kx = kxg + xt * Q + q;
+                    const int ox = kx <= (Nx >> 1) ? kx : Nx - kx;
+                    KV[t] = __ldg(&sv.spec[m * pl + ((int64_t)kh * sv.hy + oy) * sv.hx + ox]);
+                }
+            }
+            // published to L2 by the barrier after L1
+        }
+        // next tile of this CTA (prefetched into registers during this tile)
+        int un = u, in = i + 1;
+        if (in == unit_rows(u) * nrhs) {
+            ++un;
+            in = 0;
+        }
+        // L1 forward
+        if (l1) {
+            float2 v[R1];
+#pragma unroll
+            for (int n1 = 0; n1 < R1; ++n1) v[n1] = n1 < R1 / 2 ? nx[n1] : zero;
+            if (un < u1) load_tile(un, in);
+            reg_fft<R1, -1, true>(v);
+            float2* t1 = Tb + (c1 * R2 + n2) * TB + q1;
+#pragma unroll
+            for (int k = 0; k < R1; ++k) t1[k * Q] = v[k];
+        }
+        __syncthreads();
+        // L2: twiddle, R2-point FFT, MAC, inverse, twiddle
+        if (l2) {
+            const int kx = kxg + xt * Q + q2;
+            const float gx = kx <= (Nx >> 1) ? g : -g, gy = ky <= (Ny >> 1) ? g : -g;
+            float2 uu[5][R2];
+#pragma unroll
+            for (int c = 0; c < 5; ++c) {
+#pragma unroll
+                for (int m = 0; m < R2; ++m) {
+                    const float2 x = Tb[(c * R2 + m) * TB + k1 * Q + q2];
+                    uu[c][m] = m ? cmul(x, w2[m]) : x;
+                }
+                reg_fft<R2, -1>(uu[c]);
+            }
+#pragma unroll
+            for (int k2 = 0; k2 < R2; ++k2) {
+                const int kz = k1 + R1 * k2;
+                const int kh = kz <= (N >> 1) ? kz : N - kz;
+                const float s3 = kz <= (N >> 1) ? 1.f : -1.f;   // K1z is odd in kz
+                const float* kp = KV + kh * Q + q2;
+                // folded moment-form constants
+                const float f0 = g * kp[0 * NK * Q], f1 = gx * kp[1 * NK * Q], f2 = gy * kp[2 * NK * Q];
+                const float f3 = (-2.f * g) * s3 * kp[3 * NK * Q];
+                const float f4 = g * kp[4 * NK * Q], f5 = g * kp[5 * NK * Q], f6 = (4.f * g) * kp[6 * NK * Q];
+                const float2 Ix = uu[0][k2], Iy = uu[1][k2], Iz = uu[2][k2], I2 = uu[3][k2], I3 = uu[4][k2];
+                const float2 m1x = cadd(I2, I3), m1y = csub(I3, I2);
+                const float2 Qx = cfma_s(Ix, -f1, cmul_i(m1x, f4));
+                const float2 Qy = cfma_s(Iy, -f2, cmul_i(m1y, f5));
+                const float2 Qz = cfma_s(Iz, -f3, cmul_i(I3, f6));
+                uu[0][k2] = cfma_s(m1x, f1, cmul_i(Ix, f0));
+                uu[1][k2] = cfma_s(m1y, f2, cmul_i(Iy, f0));
+                uu[2][k2] = cfma_s(I3, f3, cmul_i(Iz, f0));
+                uu[3][k2] = csub(Qx, Qy);
+                uu[4][k2] = cadd(cadd(Qx, Qy), Qz);
+            }
+#pragma unroll
+            for (int c = 0; c < 5; ++c) {
+                reg_fft<R2, +1>(uu[c]);
+#pragma unroll
+                for (int m = 0; m < R2; ++m) {
+                    const float2 wc = make_float2(w2[m].x, -w2[m].y);
+                    Tb[(c * R2 + m) * TB + k1 * Q + q2] = m ? cmul(uu[c][m], wc) : uu[c][m];
+                }
+            }
+        }
+        __syncthreads();
+        // L1 inverse: z = n2 + R2 n1, kept z < Kz, straight to HBM
+        if (l1) {
+            float2 v[R1];
+            const float2* t1 = Tb + (c1 * R2 + n2) * TB + q1;
+#pragma unroll
+            for (int k = 0; k < R1; ++k) v[k] = t1[k * Q];
+            reg_fft<R1, +1>(v);
+            float2* dst = X2 + ((int64_t)(r * 5 + c1) * Kz) * plane + (int64_t)ky * Nxs + xt * Q + q1;
+#pragma unroll
+            for (int n1 = 0; n1 < R1 / 2; ++n1) {
+                const int z = n2 + R2 * n1;
+                if (z < Kz) dst[(int64_t)z * plane] = v[n1];
+            }
+        }
+        u = un;
+        i = in;
+        if (i == 0 && u < u1) __syncthreads();   // KV / G / H of the next unit are rewritten
+    }
+}
+
+}  // namespace svh

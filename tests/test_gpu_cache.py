@@ -59,3 +59,35 @@ def test_not_a_cache_is_refused(svh_lib, tmp_path):
     case = svh_inputs.random_fill((8, 8, 4), fill=0.5, seed=1)
     with pytest.raises(svh_lib.SvhError, match="not an SVXT"):
         svh_lib.setup_case(case, kernel_cache=str(bad))
+
+
+def test_cache_file_layout_and_crc(svh_lib, cache_file):
+    """The SVXT layout of SPEC S:236: magic, u32 version, f64 tol, u64 N_max[3], u32 block
+    count, per block a 2-byte tag and u64 ranks, f64 factors + core, trailing CRC-32 (zlib) of
+    every preceding byte."""
+    import struct
+    import zlib
+    b = open(cache_file, "rb").read()
+    assert b[:4] == b"SVXT"
+    ver, tol = struct.unpack_from("<Id", b, 4)
+    nmax = struct.unpack_from("<3Q", b, 16)
+    (nblk,) = struct.unpack_from("<I", b, 40)
+    assert (ver, nmax, nblk) == (2, (48, 40, 12), 7) and tol == 1e-10
+    pos = 44
+    for tag in (b"00", b"1x", b"1y", b"1z", b"2x", b"2y", b"2z"):
+        assert b[pos:pos + 2] == tag
+        d = struct.unpack_from("<3Q", b, pos + 2)
+        pos += 2 + 24 + 8 * (sum(n * r for n, r in zip(nmax, d)) + d[0] * d[1] * d[2])
+    assert pos == len(b) - 4
+    assert struct.unpack_from("<I", b, pos)[0] == zlib.crc32(b[:pos])
+
+
+def test_corrupt_cache_is_refused(svh_lib, cache_file, tmp_path):
+    """One flipped payload byte fails the CRC-32 (SPEC S:214 'checksum mismatch')."""
+    b = bytearray(open(cache_file, "rb").read())
+    b[len(b) // 2] ^= 0x40
+    bad = tmp_path / "flipped.svxt"
+    bad.write_bytes(bytes(b))
+    case = svh_inputs.random_fill((8, 8, 4), fill=0.5, seed=1)
+    with pytest.raises(svh_lib.SvhError, match="checksum"):
+        svh_lib.setup_case(case, kernel_cache=str(bad))

@@ -97,3 +97,37 @@ def test_ranks_nearly_constant_with_size():
         C, F = tucker.tucker_svd(tucker.weighted_toeplitz(K0), 1e-6)
         ranks.append(max(C.shape))
     assert abs(ranks[0] - ranks[1]) <= 3, ranks
+
+
+def test_embed_circulant_odd_sign_pinned():
+    """Reading G7 for an odd kernel, pinned to values the parity assumption does not produce:
+    every entry of the embedding of K1x (odd along x, even along y, z) equals the kernel
+    integrated directly at the SIGNED offset m (oracle quadrature at negative m_x), and the
+    circulant product reproduces the direct linear convolution y_l = sum_k K1x(l - k) I_k
+     -- a flipped sign or a transposed offset fails both."""
+    K = (4, 3, 2)
+    N = (8, 6, 4)
+    offs = np.array([(x, y, z) for x in range(K[0]) for y in range(K[1]) for z in range(K[2])])
+    K1x = kernels.seven_kernels(offs)[:, 1].reshape(K)
+    circ = tucker.embed_circulant(K1x, N, odd=(True, False, False))
+    signed = np.array([(x, y, z) for x in range(-K[0] + 1, K[0]) for y in range(-K[1] + 1, K[1])
+                       for z in range(-K[2] + 1, K[2])])
+    direct = kernels.seven_kernels(signed)[:, 1]
+    for m, val in zip(signed, direct):
+        assert np.isclose(circ[m[0] % N[0], m[1] % N[1], m[2] % N[2]], val, rtol=1e-12, atol=1e-16)
+    assert np.any(direct < 0) and np.any(direct > 0)
+    # the spectrum of an x-odd, y/z-even real sequence is purely imaginary
+    spec = np.fft.fftn(circ)
+    assert np.max(np.abs(spec.real)) < 1e-13 * np.max(np.abs(spec.imag))
+    # circulant product == direct linear convolution over the grid
+    rng = np.random.default_rng(3)
+    I = rng.standard_normal(K) + 1j * rng.standard_normal(K)
+    pad = np.zeros(N, dtype=complex)
+    pad[:K[0], :K[1], :K[2]] = I
+    y_fft = np.fft.ifftn(np.fft.fftn(pad) * spec)[:K[0], :K[1], :K[2]]
+    table = {tuple(m): v for m, v in zip(signed, direct)}
+    y_dir = np.zeros(K, dtype=complex)
+    for l in np.ndindex(*K):
+        for k in np.ndindex(*K):
+            y_dir[l] += table[(l[0] - k[0], l[1] - k[1], l[2] - k[2])] * I[k]
+    assert np.allclose(y_fft, y_dir, rtol=1e-12, atol=1e-15)
