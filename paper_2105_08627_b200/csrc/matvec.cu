@@ -26,6 +26,7 @@
 #include "internal.h"
 #include "rowfft.cuh"
 #include "zpass.cuh"
+#include "ypass.cuh"
 #include "tma.cuh"
 
 namespace svh {
@@ -1806,6 +1807,23 @@ void run_pass_y(svh_handle* h, const Geom& g, const float2* in, float2* out, int
     static const int ystage = getenv("SVH_YSTAGE") ? atoi(getenv("SVH_YSTAGE")) : 3;  // 0 = off; bit0 fwd, bit1 inv
     static const bool ytma = getenv("SVH_YTMA") == nullptr || atoi(getenv("SVH_YTMA")) != 0;
     static const bool ytma2048 = getenv("SVH_YTMA2048") == nullptr || atoi(getenv("SVH_YTMA2048")) != 0;
+    if constexpr (N == 1024 || N == 2048) {
+        // Stockham radix-16 pencils, TMA-staged input (ypass.cuh)
+        constexpr int Q = N == 2048 ? 4 : 8;
+        using P = YPlan<N, Q, DIR>;
+        CUtensorMap tin;
+        const int rows_in = DIR < 0 ? h->ky : h->ny;
+        if (nx % Q == 0 && encode_tmap_c64_3d(&tin, in, (uint64_t)nx, (uint64_t)rows_in, (uint64_t)5 * nrhs * h->kz,
+                                              (uint64_t)nx, (uint64_t)nx * rows_in, Q, P::BOX)) {
+            const int tiles_x = nx / Q;
+            const int ntiles = tiles_x * h->nzp * 5 * nrhs;
+            auto kern = k_ypass<N, Q, DIR>;
+            prep(kern, P::smem);
+            SVH_LAUNCH(kern, persistent_grid(kern, P::NT, P::smem, ntiles), P::NT, P::smem, s, out, tin, h->d_tw[1],
+                       nx, h->kz, Lin, Lout, ntiles, tiles_x, h->d_planes, h->nzp, h->d_rowmask, h->rowMW);
+            return;
+        }
+    }
     if constexpr (N >= 128 && N <= 2048) {
         CUtensorMap tmap;
         const float2* x2 = DIR < 0 ? out : in;   // the X2 side of the pass
@@ -1940,23 +1958,45 @@ void run_pass_c(svh_handle* h, const Geom& g, float2* X2, int nrhs, cudaStream_t
         if (h->use_tucker)
             for (int m = 0; m < 7; ++m)
                 for (int a = 0; a < 3; ++a) dmax = std::max(dmax, sv.rk[m][a]);
-        auto launch = [&](auto Qc) -> bool {
-            constexpr int Q = decltype(Qc)::value;
-            constexpr int R2 = N == 256 ? 8 : 4;
-            using P = ZPlan<N, R2, Q>;
-            const size_t smem = P::smem(dmax);
-            if (g.nx % Q != 0 || smem > 227 * 1024) return false;
-            auto kern = k_zpass<N, R2, Q>;
-            prep(kern, smem);
+        // plans: (R2, Q, threads): every thread runs TL1 = 5 R2 Q / threads L1 tasks and at most one
+        // L2 task; T double-buffered when shared memory allows
+        auto launch = [&](auto R2c, auto Qc, auto NTc) -> bool {
+            constexpr int R2 = decltype(R2c)::value, Q = decltype(Qc)::value, NT = decltype(NTc)::value;
+            using P = ZPlan<N, R2, Q, NT>;
+            if (g.nx % Q != 0) return false;
+            const int nbuf = P::smem(dmax, 2) <= 227 * 1024 ? 2 : 1;
+            const size_t smem = P::smem(dmax, nbuf);
+            if (smem > 227 * 1024) return false;
             const int64_t units = (int64_t)(h->ny / 2 + 1) * (g.nx / Q);
-            SVH_LAUNCH(kern, persistent_grid(kern, P::NT, smem, units), P::NT, smem, s, X2, sv, h->d_tw[2], h->nx,
-                       h->ny, h->kz, g.nx, g.kx0, h->gscale, nrhs, h->d_planeok, dmax);
+            auto go = [&](auto kern) {
+                prep(kern, smem);
+                SVH_LAUNCH(kern, persistent_grid(kern, NT, smem, units), NT, smem, s, X2, sv, h->d_tw[2], h->nx,
+                           h->ny, h->kz, g.nx, g.kx0, h->gscale, nrhs, h->d_planeok, dmax);
+            };
+            if (nbuf == 2)
+                go(k_zpass<N, R2, Q, NT, 2>);
+            else
+                go(k_zpass<N, R2, Q, NT, 1>);
             return true;
         };
-        if constexpr (N == 256) {
-            if (launch(std::integral_constant<int, 8>{}) || launch(std::integral_constant<int, 4>{})) return;
-        } else {
-            if (launch(std::integral_constant<int, 16>{}) || launch(std::integral_constant<int, 8>{})) return;
+        if constexpr (N == 128) {
+            if (launch(std::integral_constant<int, 8>{}, std::integral_constant<int, 16>{},
+                       std::integral_constant<int, 320>{}) ||
+                launch(std::integral_constant<int, 8>{}, std::integral_constant<int, 8>{},
+                       std::integral_constant<int, 160>{}))
+                return;
+        } else if constexpr (N == 64) {
+            if (launch(std::integral_constant<int, 4>{}, std::integral_constant<int, 16>{},
+                       std::integral_constant<int, 320>{}) ||
+                launch(std::integral_constant<int, 4>{}, std::integral_constant<int, 8>{},
+                       std::integral_constant<int, 160>{}))
+                return;
+        } else {   // N == 256
+            if (launch(std::integral_constant<int, 8>{}, std::integral_constant<int, 8>{},
+                       std::integral_constant<int, 320>{}) ||
+                launch(std::integral_constant<int, 8>{}, std::integral_constant<int, 4>{},
+                       std::integral_constant<int, 160>{}))
+                return;
         }
     }
     static const bool zmac = getenv("SVH_ZMAC") == nullptr || atoi(getenv("SVH_ZMAC")) != 0;
@@ -2081,7 +2121,7 @@ void run_pass_e(svh_handle* h, const Geom& g, const float2* X1, const float2* in
         using PL = RowPlan<N>;
         if (nlist == 0) return;
         const int64_t units = (int64_t)((nlist + PL::RPC - 1) / PL::RPC) * 5 * nrhs;
-        const size_t smem = PL::smem + (size_t)PL::RPC * 2 * RowSlot<N>::E_b;
+        const size_t smem = (size_t)PL::RPC * RowSlotE<N>::G_b;
         auto go = [&](auto kern) {
             prep(kern, smem);
             SVH_LAUNCH(kern, persistent_grid(kern, PL::NT, smem, units), PL::NT, smem, s, X1, out, in,

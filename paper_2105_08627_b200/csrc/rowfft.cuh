@@ -242,9 +242,20 @@ __global__ void __launch_bounds__(RowPlan<N>::NT, RowPlan<N>::MINB)
 // Pass E: inverse x-FFT + crop + local term z^b I^b + scatter to packed order (or
 // grid layout), over the rows rowlist[li] (packed output: the non-empty rows) or every row of
 // the (slab) grid (rowlist == nullptr, grid output: empty rows are written as zeros).  The
-// X1 row, the row's occupancy words, packed I segment and material ids are copied to shared
-// memory with cp.async one row-group ahead; the packed outputs are assembled in shared memory
-// and leave as one contiguous, coalesced segment.
+// row's occupancy words, packed I segment and material ids are copied to shared memory with
+// cp.async one row-group ahead, the X1 row as soon as the previous one has been read; the
+// packed outputs are assembled in place of the I segment and leave as one contiguous,
+// coalesced segment.  One FFT buffer (in place, one extra barrier) keeps a 2048-point row
+// group at ~52 KB of shared memory: four CTAs per SM.
+template <int N>
+struct RowSlotE {
+    static constexpr int W = (N / 2 + 31) / 32;
+    // small slot (double-buffered): RI [W] int2 | V [N/2] float2 | M [N/2 + 16] u8
+    static constexpr size_t S_b = (size_t)W * 8 + (size_t)(N / 2) * 8 + ((N / 2 + 16 + 15) / 16) * 16;
+    // per row group: B [PADN] float2 | X [N] float2 | 2 small slots
+    static constexpr size_t G_b = (size_t)RowPlan<N>::PADN * 8 + (size_t)N * 8 + 2 * S_b;
+};
+
 template <int N, bool PACKED>
 __global__ void __launch_bounds__(RowPlan<N>::NT, RowPlan<N>::MINB)
     k_rowE(const float2* __restrict__ X1, float2* __restrict__ out, const float2* __restrict__ in,
@@ -253,15 +264,14 @@ __global__ void __launch_bounds__(RowPlan<N>::NT, RowPlan<N>::MINB)
            const float2* __restrict__ zloc, int nzl, const float2* __restrict__ tw, int Kx, int rows, int64_t K,
            int64_t Kt, int green_only, int Kyl, int y0, int nrc) {
     using PL = RowPlan<N>;
-    using SL = RowSlot<N>;
+    using SL = RowSlotE<N>;
     constexpr int T = PL::T, RPC = PL::RPC, PADN = PL::PADN, RL = PL::RL, NS = PL::NS;
     extern __shared__ __align__(16) unsigned char smraw[];
-    __shared__ float2 zs[5 * 256];   // z^b of (material m, component c) at m*5 + c; nzl <= 256
-    for (int e = threadIdx.x; e < 5 * nzl; e += PL::NT) zs[e] = zloc[e];
     const int q = threadIdx.x / T, j = threadIdx.x % T;
-    float2* B0 = reinterpret_cast<float2*>(smraw) + q * 2 * PADN;
-    float2* B1 = B0 + PADN;
-    unsigned char* slots = smraw + PL::smem + (size_t)q * 2 * SL::E_b;
+    unsigned char* grp = smraw + (size_t)q * SL::G_b;
+    float2* B = reinterpret_cast<float2*>(grp);
+    float2* X = reinterpret_cast<float2*>(grp + (size_t)PADN * 8);
+    unsigned char* slots = grp + (size_t)PADN * 8 + (size_t)N * 8;
     const float2 zero = make_float2(0.f, 0.f);
     float2 w1[16];
 #pragma unroll
@@ -280,65 +290,69 @@ __global__ void __launch_bounds__(RowPlan<N>::NT, RowPlan<N>::MINB)
         const int z = row / Ky, y = row % Ky;
         return (__ldg(&rowmask[(int64_t)z * rowMW + (y >> 5)]) >> (y & 31)) & 1u;
     };
-    // packed segment of the row ([pre, pre + cnt)); grid layout: the row's Kx cells
     auto seg_of = [&](int row) -> int2 {
         if (row < 0) return make_int2(0, 0);
         if (PACKED) return row_segment(rowinfo, W, row);
         return make_int2(((row / Ky) * Kyl + row % Ky - y0) * Kx, Kx);
     };
-    auto issue = [&](int u, int2 sg, int b) {
+    auto issue_small = [&](int u, int2 sg, int b) {
         if (u < total) {
             int rc;
             const int row = row_at(u, rc);
             if (row >= 0) {
-                unsigned char* sl = slots + b * SL::E_b;
+                unsigned char* sl = slots + b * SL::S_b;
                 int2* RI = reinterpret_cast<int2*>(sl);
                 float2* V = reinterpret_cast<float2*>(sl + SL::W * 8);
-                float2* X = reinterpret_cast<float2*>(sl + SL::A_b);
-                uint32_t* Mw = reinterpret_cast<uint32_t*>(sl + SL::A_b + N * 8);
+                uint32_t* Mw = reinterpret_cast<uint32_t*>(sl + SL::W * 8 + (N / 2) * 8);
                 for (int e = j; e < W; e += T) cpa8(&RI[e], &rowinfo[(int64_t)row * W + e]);
-                if (is_live(row)) {
-                    const int lrow = (row / Ky) * Kyl + row % Ky - y0;
-                    const float2* xr = X1 + ((int64_t)rc * rows + lrow) * N;
-                    for (int e = j; e < N / 2; e += T) cpa16(&X[2 * e], &xr[2 * e]);
+                if (!green_only && is_live(row)) {
                     const float2* src = in + (PACKED ? (int64_t)rc * K : (int64_t)rc * Kt) + sg.x;
-                    if (!green_only) {
-                        for (int e = j; e < sg.y; e += T) cpa8(&V[e], &src[e]);
-                        if (PACKED) {   // material ids of the segment, 4-byte words (matp is padded)
-                            const int a0 = sg.x & ~3, nw = (sg.x + sg.y - a0 + 3) >> 2;
-                            for (int e = j; e < nw; e += T) cpa4(&Mw[e], matp + a0 + 4 * e);
-                        }
+                    for (int e = j; e < sg.y; e += T) cpa8(&V[e], &src[e]);
+                    if (PACKED) {   // material ids of the segment, 4-byte words (matp is padded)
+                        const int a0 = sg.x & ~3, nw = (sg.x + sg.y - a0 + 3) >> 2;
+                        for (int e = j; e < nw; e += T) cpa4(&Mw[e], matp + a0 + 4 * e);
                     }
                 }
             }
         }
         cpa_commit();
     };
-    __syncthreads();   // zs
+    auto issue_x = [&](int u) {
+        if (u < total) {
+            int rc;
+            const int row = row_at(u, rc);
+            if (is_live(row)) {
+                const int lrow = (row / Ky) * Kyl + row % Ky - y0;
+                const float2* xr = X1 + ((int64_t)rc * rows + lrow) * N;
+                for (int e = j; e < N / 2; e += T) cpa16(&X[2 * e], &xr[2 * e]);
+            }
+        }
+        cpa_commit();
+    };
     int u = blockIdx.x;
     int rc0;
     int2 sg_cur = seg_of(u < total ? row_at(u, rc0) : -1);
-    issue(u, sg_cur, 0);
+    issue_small(u, sg_cur, 0);
+    issue_x(u);
     int2 sg_next = seg_of(u + (int)gridDim.x < total ? row_at(u + gridDim.x, rc0) : -1);
     for (int k = 0; u < total; ++k, u += gridDim.x) {
         const int un = u + gridDim.x;
-        issue(un, sg_next, (k + 1) & 1);
+        cpa_wait0();
+        __syncthreads();   // this row's copies landed; every thread is done with the previous row
+        issue_small(un, sg_next, (k + 1) & 1);
         const int2 sg = sg_cur;
         sg_cur = sg_next;
         sg_next = seg_of(un + (int)gridDim.x < total ? row_at(un + gridDim.x, rc0) : -1);
-        cpa_wait1();
-        __syncthreads();
         int rc;
         const int row = row_at(u, rc);
         const int comp = rc % 5;
         const bool live = is_live(row);
-        const unsigned char* sl = slots + (k & 1) * SL::E_b;
+        unsigned char* sl = slots + (k & 1) * SL::S_b;
         const int2* RI = reinterpret_cast<const int2*>(sl);
-        const float2* V = reinterpret_cast<const float2*>(sl + SL::W * 8);
-        const float2* X = reinterpret_cast<const float2*>(sl + SL::A_b);
-        const uint8_t* Mb = sl + SL::A_b + N * 8 + (sg.x & 3);
-        // output element n (< Kx): local term + into the segment staging (B0 is free by then)
-        float2* S_out = B0;
+        float2* V = reinterpret_cast<float2*>(sl + SL::W * 8);
+        const uint8_t* Mb = sl + SL::W * 8 + (N / 2) * 8 + (sg.x & 3);
+        // output element n (< Kx): local term, into the segment staging in place of I (each
+        // position is read and written by one thread)
         auto put = [&](int n, float2 v) {
             if (row < 0 || n >= Kx) return;
             const int2 mp = RI[n >> 5];
@@ -346,56 +360,55 @@ __global__ void __launch_bounds__(RowPlan<N>::NT, RowPlan<N>::MINB)
             if (PACKED) {
                 if (!((bits >> b) & 1u)) return;
                 const int o = mp.y - sg.x + __popc(bits & ((1u << b) - 1u));
-                if (!green_only) v = cadd(v, cmul(zs[Mb[o] * 5 + comp], V[o]));
-                S_out[o] = v;
+                if (!green_only) v = cadd(v, cmul(__ldg(&zloc[Mb[o] * 5 + comp]), V[o]));
+                V[o] = v;
             } else {
                 if (!((bits >> b) & 1u)) {
-                    S_out[n] = zero;
+                    V[n] = zero;
                     return;
                 }
                 if (!green_only) {
                     const int idx = mp.y + __popc(bits & ((1u << b) - 1u));
-                    v = cadd(v, cmul(zs[__ldg(&matp[idx]) * 5 + comp], V[n]));
+                    v = cadd(v, cmul(__ldg(&zloc[__ldg(&matp[idx]) * 5 + comp]), V[n]));
                 }
-                S_out[n] = v;
+                V[n] = v;
             }
         };
-        // stage 0: radix 16, Ns = 1, all N inputs
+        // stage 0: radix 16, Ns = 1, all N inputs (from the X copy)
         {
             float2 v[16];
 #pragma unroll
             for (int r = 0; r < 16; ++r) v[r] = live ? X[j + r * (N / 16)] : zero;
             reg_fft<16, +1>(v);
 #pragma unroll
-            for (int r = 0; r < 16; ++r) B0[rpad(j * 16 + r)] = v[r];
+            for (int r = 0; r < 16; ++r) B[rpad(j * 16 + r)] = v[r];
         }
         __syncthreads();
+        issue_x(un);   // X is free: the next row's X1 row streams in during the remaining stages
         if constexpr (NS == 2) {
-            float2 vv[16 / RL][RL];
 #pragma unroll
             for (int i = 0; i < 16 / RL; ++i) {
                 const int t = j + i * T;
+                float2 v[RL];
 #pragma unroll
-                for (int r = 0; r < RL; ++r) vv[i][r] = B0[rpad(t + r * 16)];
+                for (int r = 0; r < RL; ++r) v[r] = B[rpad(t + r * 16)];
 #pragma unroll
-                for (int r = 1; r < RL; ++r) vv[i][r] = cmul(vv[i][r], tw_at<+1>(tw, (t * r) & (N - 1)));
-                reg_fft<RL, +1>(vv[i]);
+                for (int r = 1; r < RL; ++r) v[r] = cmul(v[r], tw_at<+1>(tw, (t * r) & (N - 1)));
+                reg_fft<RL, +1>(v);
+#pragma unroll
+                for (int r = 0; r < RL / 2; ++r) put(t + r * 16, v[r]);
             }
-            __syncthreads();   // B0 becomes the output staging
-#pragma unroll
-            for (int i = 0; i < 16 / RL; ++i)
-#pragma unroll
-                for (int r = 0; r < RL / 2; ++r) put(j + i * T + r * 16, vv[i][r]);
         } else {
             {
                 float2 v[16];
 #pragma unroll
-                for (int r = 0; r < 16; ++r) v[r] = B0[rpad(j + r * (N / 16))];
+                for (int r = 0; r < 16; ++r) v[r] = B[rpad(j + r * (N / 16))];
+                __syncthreads();   // in place: every stage-1 read before any stage-1 write
                 stage_twiddle<16, +1>(v, w1);
                 reg_fft<16, +1>(v);
                 const int base = (j >> 4) * 256 + (j & 15);
 #pragma unroll
-                for (int r = 0; r < 16; ++r) B1[rpad(base + r * 16)] = v[r];
+                for (int r = 0; r < 16; ++r) B[rpad(base + r * 16)] = v[r];
             }
             __syncthreads();
 #pragma unroll
@@ -403,7 +416,7 @@ __global__ void __launch_bounds__(RowPlan<N>::NT, RowPlan<N>::MINB)
                 const int t = j + i * T;
                 float2 v[RL];
 #pragma unroll
-                for (int r = 0; r < RL; ++r) v[r] = B1[rpad(t + r * (N / RL))];
+                for (int r = 0; r < RL; ++r) v[r] = B[rpad(t + r * (N / RL))];
 #pragma unroll
                 for (int r = 1; r < RL; ++r) v[r] = cmul(v[r], tw_at<+1>(tw, (t * r) & (N - 1)));
                 reg_fft<RL, +1>(v);
@@ -413,11 +426,9 @@ __global__ void __launch_bounds__(RowPlan<N>::NT, RowPlan<N>::MINB)
         }
         __syncthreads();   // the staged segment is complete
         if (row >= 0) {
-            const int cnt = sg.y;
             float2* dst = out + (PACKED ? (int64_t)rc * K : (int64_t)rc * Kt) + sg.x;
-            for (int e = j; e < cnt; e += T) dst[e] = S_out[e];
+            for (int e = j; e < sg.y; e += T) dst[e] = V[e];
         }
-        // B0 (staging) is rewritten by the next unit's stage 0 after its copy-wait barrier
     }
     cpa_wait0();
 }

@@ -45,7 +45,15 @@ struct CsrDev {
     int* ecol = nullptr;
     double* eval = nullptr;
     int* agg = nullptr;       // fine -> coarse aggregate (except coarsest level)
+    int* cptr = nullptr;      // members of aggregate I: cmem[cptr[I] .. cptr[I+1]) (ascending), for the
+    int* cmem = nullptr;      // deterministic (gather) restriction
     int nc = 0;
+    // K-cycle vectors of this level when it is the coarse level of a Krylov-accelerated step
+    double* kv1 = nullptr;
+    double* kw1 = nullptr;
+    double* kr2 = nullptr;
+    double* kv2 = nullptr;
+    double* kw2 = nullptr;
     double* vb = nullptr;     // level right-hand side (levels >= 1) [n][2]
     double* vx = nullptr;     // level solution (levels >= 1)
     double* tmp = nullptr;    // residual scratch
@@ -93,7 +101,10 @@ struct Solve {
     // graph is rebuilt whenever the AMG hierarchy is (port set change)
     cudaStream_t stream = nullptr;
     std::vector<std::pair<int, cudaGraphExec_t>> pcg_graphs;   // per vector-pair count NVP
-    double* d_pcg = nullptr;         // [8][2 nvp_cap]: rz, pq, rr, thr, alpha, beta, rz2, done
+    double* d_pcg = nullptr;         // [16][2 nvp_cap]: PCG scalars (k_fcg_* slot map)
+    double* d_kc = nullptr;          // [levels][8][2 nvp_cap]: K-cycle scalars per level
+    double* d_part = nullptr;        // deterministic-reduction partials
+    size_t part_cap = 0;
     int nvp_cap = 1;                 // vector pairs (ports) the level / work buffers hold
     int pcg_cap = 0;
     double t_matvec = 0, t_precond = 0;
@@ -344,16 +355,22 @@ __global__ void k_zero(double* __restrict__ x, int64_t n) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) x[i] = 0.0;
 }
-// restriction: rc[agg[i]] += r[i]
-__global__ void k_restrictV(int n, const int* __restrict__ agg, const double* __restrict__ r, double* __restrict__ rc,
-                            int sh) {
+// restriction: rc[I] = sum of r[i] over the members i of aggregate I, in ascending order (a
+// gather, not atomics: the result is bitwise independent of scheduling and of the batch width)
+__global__ void k_restrictG(int nc, const int* __restrict__ cptr, const int* __restrict__ cmem,
+                            const double* __restrict__ r, double* __restrict__ rc, int sh) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= (n << sh)) return;
-    const int i = t >> sh, p = t & ((1 << sh) - 1);
+    if (t >= (nc << sh)) return;
+    const int I = t >> sh, p = t & ((1 << sh) - 1);
     const int NVP = 1 << sh;
-    const int I = (agg[i] << sh) + p;
-    atomicAdd(&rc[2 * I], r[2 * t]);
-    atomicAdd(&rc[2 * I + 1], r[2 * t + 1]);
+    const double2* r2 = reinterpret_cast<const double2*>(r);
+    double a0 = 0, a1 = 0;
+    for (int k = cptr[I]; k < cptr[I + 1]; ++k) {
+        const double2 v = r2[(int64_t)cmem[k] * NVP + p];
+        a0 += v.x;
+        a1 += v.y;
+    }
+    reinterpret_cast<double2*>(rc)[t] = make_double2(a0, a1);
 }
 // prolongation: x[i] += ec[agg[i]]
 __global__ void k_prolongV(int n, const int* __restrict__ agg, const double* __restrict__ ec, double* __restrict__ x,
@@ -388,17 +405,38 @@ __global__ void k_denseV(int n, const double* __restrict__ Ci, const double* __r
         x[2 * wid + 1] = a1;
     }
 }
-// out[v] += sum_i a[i][v] b[i][v], v < NV = 2^(sh+1): with the grid stride a multiple of NV,
-// every thread keeps one fixed vector v = t & (NV-1); lanes of equal v reduce by shuffles
-__global__ void k_dotV(int n, const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ out,
-                       int sh) {
+// Deterministic dot products of NV = 2^(sh+1) real vectors stored [n][NV]: up to 3 pairs
+// (a_d, b_d) at once.  Block b of kDotBlocks sums rows [b n / G, (b+1) n / G); within a block,
+// lane l of the warp owning (d, v) sums rows lo + l, lo + l + 32, ... in order, then a fixed
+// shuffle tree.  The summation order of every vector depends only on n -- not on NV, the other
+// vectors or scheduling -- so a port's inner solve is bitwise the same alone or in a batch.
+constexpr int kDotBlocks = 128;
+__global__ void k_ddotP(int n, int nd, const double* __restrict__ a0, const double* __restrict__ b0,
+                        const double* __restrict__ a1, const double* __restrict__ b1, const double* __restrict__ a2,
+                        const double* __restrict__ b2, double* __restrict__ part, int sh) {
     const int NV = 2 << sh;
-    const int tot = n * NV;
-    const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lo = (int)((int64_t)n * blockIdx.x / gridDim.x), hi = (int)((int64_t)n * (blockIdx.x + 1) / gridDim.x);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int item = warp; item < nd * NV; item += nw) {
+        const int d = item / NV, v = item % NV;
+        const double* a = d == 0 ? a0 : d == 1 ? a1 : a2;
+        const double* b = d == 0 ? b0 : d == 1 ? b1 : b2;
+        double acc = 0;
+        for (int i = lo + lane; i < hi; i += 32) acc = fma(a[(int64_t)i * NV + v], b[(int64_t)i * NV + v], acc);
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffff, acc, o);
+        if (lane == 0) part[((int64_t)blockIdx.x * nd + d) * NV + v] = acc;
+    }
+}
+// out[d * ostride + v] = sum over blocks (ascending) of the partials
+__global__ void k_ddotF(int nb, int nd, const double* __restrict__ part, double* __restrict__ out, int ostride,
+                        int sh) {
+    const int NV = 2 << sh;
+    const int t = threadIdx.x;
+    if (t >= nd * NV) return;
+    const int d = t / NV, v = t % NV;
     double acc = 0;
-    for (int t = t0; t < tot; t += gridDim.x * blockDim.x) acc = fma(a[t], b[t], acc);
-    for (int o = 16; o >= NV; o >>= 1) acc += __shfl_xor_sync(0xffffffff, acc, o);
-    if ((threadIdx.x & 31) < NV && (threadIdx.x & 31) < 32) atomicAdd(&out[t0 & (NV - 1)], acc);
+    for (int b = 0; b < nb; ++b) acc += part[((int64_t)b * nd + d) * NV + v];
+    out[d * ostride + v] = acc;
 }
 // x += sign alpha_v y (per vector v)
 __global__ void k_axpyV(int n, const double* __restrict__ alpha, int sign, const double* __restrict__ y,
@@ -414,28 +452,62 @@ __global__ void k_xpbyV(int n, const double* __restrict__ z, const double* __res
     if (i >= (n << (sh + 1))) return;
     p[i] = z[i] + beta[i & ((2 << sh) - 1)] * p[i];
 }
-// PCG scalars on the device, pc = Solve::d_pcg laid out [slot][NV]: slots 0 rz, 1 pq, 2 rr,
-// 3 thr, 4 alpha, 5 beta, 6 rz2, 7 done -- NV independent real systems
-__global__ void k_pcg_alpha(double* pc, int NV) {
+// Flexible CG (FCG(1), the outer iteration AGMG pairs with its K-cycle: the preconditioner is a
+// nonlinear, varying operator) scalars on the device, pc = Solve::d_pcg laid out [slot][NV]:
+// 0 pq = p.Ap, 1 pr = p.r, 2 rr, 3 thr, 4 alpha, 5 beta, 6 zq = z.Ap, 7 done
+__global__ void k_fcg_alpha(double* pc, int NV) {
     const int v = threadIdx.x;
-    if (v < NV) pc[4 * NV + v] = (pc[7 * NV + v] != 0 || pc[NV + v] == 0) ? 0.0 : pc[v] / pc[NV + v];
+    if (v < NV) pc[4 * NV + v] = (pc[7 * NV + v] != 0 || pc[v] == 0) ? 0.0 : pc[NV + v] / pc[v];
 }
-__global__ void k_pcg_check(double* pc, int NV) {
+__global__ void k_fcg_check(double* pc, int NV) {
     const int v = threadIdx.x;
     if (v < NV && pc[2 * NV + v] <= pc[3 * NV + v]) pc[7 * NV + v] = 1.0;
 }
-__global__ void k_pcg_beta(double* pc, int NV) {
+__global__ void k_fcg_beta(double* pc, int NV) {
     const int v = threadIdx.x;
-    if (v < NV) {
-        pc[5 * NV + v] = (pc[7 * NV + v] != 0 || pc[v] == 0) ? 0.0 : pc[6 * NV + v] / pc[v];
-        pc[v] = pc[6 * NV + v];
-    }
+    if (v < NV) pc[5 * NV + v] = (pc[7 * NV + v] != 0 || pc[v] == 0) ? 0.0 : -pc[6 * NV + v] / pc[v];
 }
-
+// K-cycle (Notay-Vassilevski; AGMG): two FCG steps on the coarse level per visit.  Scalars of a
+// level at kc [slot][NV]: 0 rho1 = v1.w1, 1 alpha1 = v1.rc, 2 gamma = v2.w1, 3 beta = v2.w2,
+// 4 alpha2 = v2.r2.  r2 = rc - (alpha1 / rho1) w1
+__global__ void k_kc_r2(int n, const double* __restrict__ rc, const double* __restrict__ w1,
+                        const double* __restrict__ kc, double* __restrict__ r2, int sh) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int NV = 2 << sh;
+    if (i >= n * NV) return;
+    const int v = i & (NV - 1);
+    const double rho1 = kc[v], a1 = kc[NV + v];
+    const double c1 = rho1 != 0 ? a1 / rho1 : 0.0;
+    r2[i] = rc[i] - c1 * w1[i];
+}
+// x_fine += P (c1 v1 + c2 v2): ec = (a1/rho1 - gamma a2/(rho1 rho2)) v1 + (a2/rho2) v2,
+// rho2 = beta - gamma^2 / rho1; prolongation fused (x[i] += ec[agg[i]])
+__global__ void k_kc_prolong(int n, const int* __restrict__ agg, const double* __restrict__ v1,
+                             const double* __restrict__ v2, const double* __restrict__ kc, double* __restrict__ x,
+                             int sh) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int NV = 2 << sh;
+    if (t >= n * NV) return;
+    const int i = t / NV, v = t & (NV - 1);
+    const double rho1 = kc[v], a1 = kc[NV + v], gam = kc[2 * NV + v], bet = kc[3 * NV + v], a2 = kc[4 * NV + v];
+    double c1 = 0, c2 = 0;
+    if (rho1 != 0) {
+        const double rho2 = bet - gam * gam / rho1;
+        c1 = a1 / rho1;
+        if (rho2 > 1e-14 * fabs(bet)) {
+            c2 = a2 / rho2;
+            c1 -= gam * a2 / (rho1 * rho2);
+        }
+    }
+    const int64_t I = (int64_t)agg[i] * NV + v;
+    x[t] += c1 * v1[I] + c2 * v2[I];
+}
 // ---- complex Krylov helpers (double2 vectors of length n)
-// out[i] += sum_e conj(V_i[e]) w[e], i < m ; grid (blocks, m)
+// part[(i nblk + b)] = sum_{e in block b's grid-stride set} conj(V_i[e]) w[e], i < m; grid (nblk, m);
+// k_cdots_fin sums the blocks in order (deterministic: no atomics, fixed grid)
+constexpr int kCdotBlocks = 148;
 __global__ void k_cdots(int64_t n, const double2* __restrict__ V, int64_t ldv, const double2* __restrict__ w,
-                        double* __restrict__ out) {
+                        double2* __restrict__ part) {
     const int i = blockIdx.y;
     const double2* v = V + i * ldv;
     double sr = 0, si = 0;
@@ -455,18 +527,25 @@ __global__ void k_cdots(int64_t n, const double2* __restrict__ V, int64_t ldv, c
         sh[1][wp] = si;
     }
     __syncthreads();
-    if (wp == 0) {
-        sr = l < blockDim.x / 32 ? sh[0][l] : 0;
-        si = l < blockDim.x / 32 ? sh[1][l] : 0;
-        for (int o = 16; o > 0; o >>= 1) {
-            sr += __shfl_xor_sync(0xffffffff, sr, o);
-            si += __shfl_xor_sync(0xffffffff, si, o);
+    if (threadIdx.x == 0) {
+        double a = 0, b = 0;
+        for (int q = 0; q < (int)(blockDim.x / 32); ++q) {
+            a += sh[0][q];
+            b += sh[1][q];
         }
-        if (l == 0) {
-            atomicAdd(&out[2 * i], sr);
-            atomicAdd(&out[2 * i + 1], si);
-        }
+        part[(int64_t)i * gridDim.x + blockIdx.x] = make_double2(a, b);
     }
+}
+__global__ void k_cdots_fin(int nb, int m, const double2* __restrict__ part, double* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    double a = 0, b = 0;
+    for (int k = 0; k < nb; ++k) {
+        a += part[(int64_t)i * nb + k].x;
+        b += part[(int64_t)i * nb + k].y;
+    }
+    out[2 * i] = a;
+    out[2 * i + 1] = b;
 }
 // w -= sum_{i<m} V_i h_i   (h complex on device)
 __global__ void k_cupdate(int64_t n, const double2* __restrict__ V, int64_t ldv, const double* __restrict__ h, int m,
@@ -637,10 +716,15 @@ static void free_levels(Solve* S) {
         cudaFree(L.val);
         cudaFree(L.dinv);
         cudaFree(L.agg);
+        cudaFree(L.cptr);
+        cudaFree(L.cmem);
         cudaFree(L.ecol);
         cudaFree(L.eval);
+        for (double* k : {L.kv1, L.kw1, L.kr2, L.kv2, L.kw2}) cudaFree(k);
     }
     S->levels.clear();
+    cudaFree(S->d_kc);
+    S->d_kc = nullptr;
     cudaFree(S->d_cinv);
     S->d_cinv = nullptr;
     cudaFree(S->d_free);
@@ -664,6 +748,7 @@ void free_solve(svh_handle* h) {
     cudaFree(S->c64_in);
     cudaFree(S->c64_out);
     cudaFree(S->d_red);
+    cudaFree(S->d_part);
     cudaFree(S->d_pcg);
     if (S->stream) cudaStreamDestroy(S->stream);
     delete S;
@@ -834,6 +919,7 @@ CsrDev upload(const CsrHost& A) {
     SVH_CUDA(cudaMalloc(&d.vx, vb));
     SVH_CUDA(cudaMalloc(&d.tmp, vb));
     SVH_CUDA(cudaMalloc(&d.x2, vb));
+    for (double** k : {&d.kv1, &d.kw1, &d.kr2, &d.kv2, &d.kw2}) SVH_CUDA(cudaMalloc(k, vb));
     return d;
 }
 
@@ -922,6 +1008,18 @@ static void build_amg(svh_handle* h, const std::vector<int32_t>& fixed, int nvp)
         d.nc = n2;
         SVH_CUDA(cudaMalloc(&d.agg, A.n * sizeof(int)));
         SVH_CUDA(cudaMemcpy(d.agg, agg.data(), A.n * sizeof(int), cudaMemcpyHostToDevice));
+        // aggregate members (ascending) for the gather restriction
+        std::vector<int> cptr(n2 + 1, 0), cmem(A.n);
+        for (int i = 0; i < A.n; ++i) cptr[agg[i] + 1]++;
+        for (int I = 0; I < n2; ++I) cptr[I + 1] += cptr[I];
+        {
+            std::vector<int> pos(cptr.begin(), cptr.end() - 1);
+            for (int i = 0; i < A.n; ++i) cmem[pos[agg[i]]++] = i;
+        }
+        SVH_CUDA(cudaMalloc(&d.cptr, (n2 + 1) * sizeof(int)));
+        SVH_CUDA(cudaMalloc(&d.cmem, std::max(1, A.n) * sizeof(int)));
+        SVH_CUDA(cudaMemcpy(d.cptr, cptr.data(), (n2 + 1) * sizeof(int), cudaMemcpyHostToDevice));
+        SVH_CUDA(cudaMemcpy(d.cmem, cmem.data(), A.n * sizeof(int), cudaMemcpyHostToDevice));
         S->levels.push_back(d);
         CsrHost C = galerkin(A, agg, n2);
         if (n2 > 0.85 * A.n) {   // stalled coarsening: stop with a dense solve if small enough
@@ -932,6 +1030,8 @@ static void build_amg(svh_handle* h, const std::vector<int32_t>& fixed, int nvp)
         A.val.swap(C.val);
         A.n = C.n;
     }
+    SVH_CUDA(cudaMalloc(&S->d_kc, S->levels.size() * 8 * 2 * (size_t)S->nvp_cap * sizeof(double)));
+    SVH_CUDA(cudaMemset(S->d_kc, 0, S->levels.size() * 8 * 2 * (size_t)S->nvp_cap * sizeof(double)));
 }
 
 // ---------------------------------------------------------------------------
@@ -946,6 +1046,15 @@ static void ensure_work(svh_handle* h, int restart) {
         S->wsize = need;
     }
     if (!S->d_red) SVH_CUDA(cudaMalloc(&S->d_red, 4096 * sizeof(double)));
+    // reduction partials: k_ddotP (kDotBlocks x 3 dots x NV) and k_cdots (restart + 1 vectors x
+    // kCdotBlocks complex)
+    const size_t pneed = std::max((size_t)kDotBlocks * 3 * 2 * S->nvp_cap, (size_t)2 * (restart + 2) * kCdotBlocks);
+    if (S->part_cap < pneed) {
+        drop_pcg_graph(S);
+        cudaFree(S->d_part);
+        SVH_CUDA(cudaMalloc(&S->d_part, pneed * sizeof(double)));
+        S->part_cap = pneed;
+    }
     if (!S->c64_in) {
         SVH_CUDA(cudaMalloc(&S->c64_in, 5 * h->K * sizeof(float2)));
         SVH_CUDA(cudaMalloc(&S->c64_out, 5 * h->K * sizeof(float2)));
@@ -971,46 +1080,64 @@ static void apply_sys(svh_handle* h, const double2* x, double2* y, bool masked, 
                S->M);
 }
 
-// AMG cycle on level l: x = B^-1 b (x overwritten) for NVP vector pairs, V(2,2) l1-Jacobi,
-// W-cycle on the top levels
-static void vcycle(Solve* S, int l, const double* b, double* x, cudaStream_t s, int NVP) {
+// deterministic dot products (k_ddotP / k_ddotF): nd <= 3 pairs, results at out[d * ostride + v]
+static void ddot(Solve* S, int n, int nd, const double* a0, const double* b0, const double* a1, const double* b1,
+                 const double* a2, const double* b2, double* out, int ostride, int sh, cudaStream_t s) {
+    const int nb = std::min(kDotBlocks, std::max(1, (n + 255) / 256));   // a function of n only
+    SVH_LAUNCH(k_ddotP, nb, 256, 0, s, n, nd, a0, b0, a1, b1, a2, b2, S->d_part, sh);
+    SVH_LAUNCH(k_ddotF, 1, 128, 0, s, nb, nd, S->d_part, out, ostride, sh);
+}
+
+// AMG cycle on level l: x = B_l^-1 b for NVP vector pairs.  l1-Jacobi V(2,2) smoothing; the
+// coarse-grid correction of the top kKLevels levels is Krylov-accelerated (K-cycle, AGMG
+// P:166-168 / Notay-Vassilevski): two flexible-CG steps on the coarse system, each
+// preconditioned by the next level's cycle; below, one plain recursive call (V-cycle).  The
+// coarsest level is the exact dense solve.
+constexpr int kKLevels = 3;
+static void kcycle(Solve* S, int l, const double* b, double* x, cudaStream_t s, int NVP) {
     const int sh = __builtin_ctz(NVP);
+    const int NV = 2 * NVP;
     const CsrDev& L = S->levels[l];
     const int n = L.n;
     const int64_t nt = (int64_t)n * NVP;
-    if (l == (int)S->levels.size() - 1) {
+    const int last = (int)S->levels.size() - 1;
+    if (l == last) {
         SVH_LAUNCH(k_denseV, nblk(nt, 8), 256, 0, s, n, S->d_cinv, b, x, sh);
         return;
     }
     const CsrDev& C = S->levels[l + 1];
-    double* rc = C.vb;
-    double* ec = C.vx;
-    const int64_t ncv = 2LL * L.nc * NVP;
+    const int nc = L.nc;
+    const int64_t nct = (int64_t)nc * NVP;
     SVH_LAUNCH(k_jacobiV, nblk(nt), 256, 0, s, n, L.ellw, L.ecol, L.eval, L.dinv, b, (const double*)nullptr, x, sh);
     SVH_LAUNCH(k_jacobiV, nblk(nt), 256, 0, s, n, L.ellw, L.ecol, L.eval, L.dinv, b, x, L.x2, sh);
     SVH_LAUNCH(k_residV, nblk(nt), 256, 0, s, n, L.ellw, L.ecol, L.eval, b, L.x2, L.tmp, sh);
-    SVH_LAUNCH(k_zero, nblk(ncv), 256, 0, s, rc, ncv);
-    SVH_LAUNCH(k_restrictV, nblk(nt), 256, 0, s, n, L.agg, L.tmp, rc, sh);
-    vcycle(S, l + 1, rc, ec, s, NVP);
-    SVH_LAUNCH(k_prolongV, nblk(nt), 256, 0, s, n, L.agg, ec, L.x2, sh);
-    static const int wlev = getenv("SVH_AMG_W") ? atoi(getenv("SVH_AMG_W")) : 2;
-    if (l < wlev) {   // W-cycle on the top levels: second coarse-grid correction
-        SVH_LAUNCH(k_residV, nblk(nt), 256, 0, s, n, L.ellw, L.ecol, L.eval, b, L.x2, L.tmp, sh);
-        SVH_LAUNCH(k_zero, nblk(ncv), 256, 0, s, rc, ncv);
-        SVH_LAUNCH(k_restrictV, nblk(nt), 256, 0, s, n, L.agg, L.tmp, rc, sh);
-        vcycle(S, l + 1, rc, ec, s, NVP);
-        SVH_LAUNCH(k_prolongV, nblk(nt), 256, 0, s, n, L.agg, ec, L.x2, sh);
+    SVH_LAUNCH(k_restrictG, nblk(nct), 256, 0, s, nc, L.cptr, L.cmem, L.tmp, C.vb, sh);
+    if (l < kKLevels && l + 1 < last) {
+        double* kc = S->d_kc + (size_t)l * 8 * NV;
+        kcycle(S, l + 1, C.vb, C.kv1, s, NVP);
+        SVH_LAUNCH(k_spmvV, nblk(nct), 256, 0, s, nc, C.ellw, C.ecol, C.eval, C.kv1, C.kw1, sh);
+        ddot(S, nc, 2, C.kv1, C.kw1, C.kv1, C.vb, nullptr, nullptr, kc, NV, sh, s);
+        SVH_LAUNCH(k_kc_r2, nblk(2 * nct), 256, 0, s, nc, C.vb, C.kw1, kc, C.kr2, sh);
+        kcycle(S, l + 1, C.kr2, C.kv2, s, NVP);
+        SVH_LAUNCH(k_spmvV, nblk(nct), 256, 0, s, nc, C.ellw, C.ecol, C.eval, C.kv2, C.kw2, sh);
+        ddot(S, nc, 3, C.kv2, C.kw1, C.kv2, C.kw2, C.kv2, C.kr2, kc + 2 * NV, NV, sh, s);
+        SVH_LAUNCH(k_kc_prolong, nblk(2 * nt), 256, 0, s, n, L.agg, C.kv1, C.kv2, kc, L.x2, sh);
+    } else {
+        kcycle(S, l + 1, C.vb, C.vx, s, NVP);
+        SVH_LAUNCH(k_prolongV, nblk(nt), 256, 0, s, n, L.agg, C.vx, L.x2, sh);
     }
     SVH_LAUNCH(k_jacobiV, nblk(nt), 256, 0, s, n, L.ellw, L.ecol, L.eval, L.dinv, b, L.x2, x, sh);
     SVH_LAUNCH(k_jacobiV, nblk(nt), 256, 0, s, n, L.ellw, L.ecol, L.eval, L.dinv, b, x, L.x2, sh);
     SVH_CUDA(cudaMemcpyAsync(x, L.x2, 2 * (size_t)nt * sizeof(double), cudaMemcpyDeviceToDevice, s));
 }
 
-// PCG on S (level 0) for NV = 2 NVP real right-hand sides (re / im of NVP ports): x = S^-1 b
-// to relative tol per vector.  All scalars stay on the device; one iteration (SpMV, 3 dot
-// products, the scalar updates and the whole AMG cycle, ~250 kernels) is a CUDA graph captured
-// once per hierarchy and NVP and replayed, and the host reads the convergence flags every
-// kCheck iterations -- the solve is launch-latency bound otherwise (P:166 AGMG-CG; G15).
+// Flexible CG (FCG(1)) on S (level 0) for NV = 2 NVP real right-hand sides (re / im of NVP
+// ports), preconditioned by the K-cycle: x = S^-1 b to relative tol per vector (P:166 AGMG-CG;
+// G15).  All scalars stay on the device; one iteration (SpMV, 4 deterministic dots, scalar
+// updates and the whole cycle) is a CUDA graph captured once per hierarchy and NVP and replayed;
+// the host reads the convergence flags every kCheck iterations.  Vectors that converge freeze
+// (alpha = 0), and every reduction has a batch-independent order, so a port's result is
+// bitwise the same whichever ports share its batch (1-GPU vs sharded L bit for bit).
 static int pcgV(svh_handle* h, const double* b, double* x, double tol, int maxit, cudaStream_t s, int NVP) {
     Solve* S = h->solve;
     const CsrDev& A = S->levels[0];
@@ -1024,25 +1151,21 @@ static int pcgV(svh_handle* h, const double* b, double* x, double tol, int maxit
     double* p = S->wbuf[2];
     double* q = S->wbuf[3];
     double* pc = S->d_pcg;
-    auto dot = [&](const double* a, const double* bb, double* out) {
-        SVH_CUDA(cudaMemsetAsync(out, 0, NV * sizeof(double), s));
-        SVH_LAUNCH(k_dotV, 296, 256, 0, s, n, a, bb, out, sh);
-    };
     auto iteration = [&] {
         SVH_LAUNCH(k_spmvV, nblk(nt), 256, 0, s, n, A.ellw, A.ecol, A.eval, p, q, sh);
-        dot(p, q, pc + 1 * NV);
-        SVH_LAUNCH(k_pcg_alpha, 1, 64, 0, s, pc, NV);
+        ddot(S, n, 2, p, q, p, r, nullptr, nullptr, pc, NV, sh, s);   // pq, pr
+        SVH_LAUNCH(k_fcg_alpha, 1, 64, 0, s, pc, NV);
         SVH_LAUNCH(k_axpyV, nblk(nd), 256, 0, s, n, pc + 4 * NV, +1, p, x, sh);
         SVH_LAUNCH(k_axpyV, nblk(nd), 256, 0, s, n, pc + 4 * NV, -1, q, r, sh);
-        dot(r, r, pc + 2 * NV);
-        SVH_LAUNCH(k_pcg_check, 1, 64, 0, s, pc, NV);
-        vcycle(S, 0, r, z, s, NVP);
-        dot(r, z, pc + 6 * NV);
-        SVH_LAUNCH(k_pcg_beta, 1, 64, 0, s, pc, NV);
+        ddot(S, n, 1, r, r, nullptr, nullptr, nullptr, nullptr, pc + 2 * NV, NV, sh, s);
+        SVH_LAUNCH(k_fcg_check, 1, 64, 0, s, pc, NV);
+        kcycle(S, 0, r, z, s, NVP);
+        ddot(S, n, 1, z, q, nullptr, nullptr, nullptr, nullptr, pc + 6 * NV, NV, sh, s);
+        SVH_LAUNCH(k_fcg_beta, 1, 64, 0, s, pc, NV);
         SVH_LAUNCH(k_xpbyV, nblk(nd), 256, 0, s, n, z, pc + 5 * NV, p, sh);
     };
     // b.b -> thresholds thr = tol^2 b.b; vectors with b = 0 are done from the start
-    dot(b, b, pc + 2 * NV);
+    ddot(S, n, 1, b, b, nullptr, nullptr, nullptr, nullptr, pc + 2 * NV, NV, sh, s);
     std::vector<double> bn(NV);
     SVH_CUDA(cudaMemcpyAsync(bn.data(), pc + 2 * NV, NV * sizeof(double), cudaMemcpyDeviceToHost, s));
     SVH_CUDA(cudaStreamSynchronize(s));
@@ -1057,9 +1180,8 @@ static int pcgV(svh_handle* h, const double* b, double* x, double tol, int maxit
     if (!any) return 0;
     SVH_CUDA(cudaMemcpyAsync(pc, init.data(), init.size() * sizeof(double), cudaMemcpyHostToDevice, s));
     SVH_CUDA(cudaMemcpyAsync(r, b, nd * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    vcycle(S, 0, r, z, s, NVP);
+    kcycle(S, 0, r, z, s, NVP);
     SVH_CUDA(cudaMemcpyAsync(p, z, nd * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    dot(r, z, pc + 0 * NV);
     static const bool use_graph = getenv("SVH_NO_PCG_GRAPH") == nullptr;
     cudaGraphExec_t gx = nullptr;
     for (auto& gg : S->pcg_graphs)
@@ -1073,7 +1195,7 @@ static int pcgV(svh_handle* h, const double* b, double* x, double tol, int maxit
         cudaGraphDestroy(g);
         S->pcg_graphs.push_back({NVP, gx});
     }
-    constexpr int kCheck = 8;
+    constexpr int kCheck = 4;
     int it = 0;
     std::vector<double> done(NV);
     while (it < maxit) {
@@ -1113,8 +1235,8 @@ static void precond(svh_handle* h, const double2* in, double2* out, double tol, 
 
 static double cnorm(svh_handle* h, const double2* x, cudaStream_t s) {
     Solve* S = h->solve;
-    SVH_CUDA(cudaMemsetAsync(S->d_red, 0, 2 * sizeof(double), s));
-    SVH_LAUNCH(k_cdots, dim3(296, 1), 256, 0, s, S->N, x, 0, x, S->d_red);
+    SVH_LAUNCH(k_cdots, dim3(kCdotBlocks, 1), 256, 0, s, S->N, x, 0, x, reinterpret_cast<double2*>(S->d_part));
+    SVH_LAUNCH(k_cdots_fin, 1, 32, 0, s, kCdotBlocks, 1, reinterpret_cast<const double2*>(S->d_part), S->d_red);
     double v[2];
     SVH_CUDA(cudaMemcpyAsync(v, S->d_red, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
     SVH_CUDA(cudaStreamSynchronize(s));
@@ -1165,8 +1287,10 @@ static int fgmres(svh_handle* h, const double2* b, double2* x, double rre, int m
             // CGS2
             std::vector<cd> hj(j + 2, 0.0);
             for (int pass = 0; pass < 2; ++pass) {
-                SVH_CUDA(cudaMemsetAsync(hcol, 0, 2 * (j + 1) * sizeof(double), s));
-                SVH_LAUNCH(k_cdots, dim3(148, j + 1), 256, 0, s, N, V, N, w, hcol);
+                SVH_LAUNCH(k_cdots, dim3(kCdotBlocks, j + 1), 256, 0, s, N, V, N, w,
+                           reinterpret_cast<double2*>(S->d_part));
+                SVH_LAUNCH(k_cdots_fin, nblk(j + 1, 64), 64, 0, s, kCdotBlocks, j + 1,
+                           reinterpret_cast<const double2*>(S->d_part), hcol);
                 SVH_LAUNCH(k_cupdate, nblk(N), 256, 0, s, N, V, N, hcol, j + 1, w, 1.0);
                 std::vector<double> hv(2 * (j + 1));
                 SVH_CUDA(cudaMemcpyAsync(hv.data(), hcol, hv.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -1342,8 +1466,10 @@ static void fgmres_batch(svh_handle* h, BatchWork& W, int nb, double2* const* bb
                 double2* w = W.w(p);
                 std::vector<cd> hj(j + 2, 0.0);
                 for (int pass = 0; pass < 2; ++pass) {
-                    SVH_CUDA(cudaMemsetAsync(hcol, 0, 2 * (j + 1) * sizeof(double), s));
-                    SVH_LAUNCH(k_cdots, dim3(148, j + 1), 256, 0, s, N, V, N, w, hcol);
+                    SVH_LAUNCH(k_cdots, dim3(kCdotBlocks, j + 1), 256, 0, s, N, V, N, w,
+                               reinterpret_cast<double2*>(S->d_part));
+                    SVH_LAUNCH(k_cdots_fin, nblk(j + 1, 64), 64, 0, s, kCdotBlocks, j + 1,
+                               reinterpret_cast<const double2*>(S->d_part), hcol);
                     SVH_LAUNCH(k_cupdate, nblk(N), 256, 0, s, N, V, N, hcol, j + 1, w, 1.0);
                     std::vector<double> hv(2 * (j + 1));
                     SVH_CUDA(cudaMemcpyAsync(hv.data(), hcol, hv.size() * sizeof(double), cudaMemcpyDeviceToHost, s));

@@ -32,83 +32,102 @@ struct SpecView {
     int rk[7][3];
 };
 
-template <int N, int R2_, int Q_>
+template <int N, int R2_, int Q_, int NT_>
 struct ZPlan {
-    static constexpr int N_ = N, R2 = R2_, Q = Q_, R1 = N / R2_, NH = N / 2, NK = N / 2 + 1;
+    static constexpr int R2 = R2_, Q = Q_, R1 = N / R2_, NH = N / 2, NK = N / 2 + 1;
     static constexpr int NL1 = 5 * R2 * Q, NL2 = R1 * Q;
-    static constexpr int NT = ((NL1 > NL2 ? NL1 : NL2) + 31) / 32 * 32;
+    static constexpr int NT = NT_;
+    static constexpr int TL1 = NL1 / NT;                  // L1 tasks per thread
+    static_assert(NL1 % NT == 0 && NL2 <= NT && NT % 32 == 0, "z plan: balanced L1, one L2 task per thread");
     static constexpr int TB = R1 * Q + Q;                 // one (c, n2) block of T, padded by Q
     static constexpr int TE = 5 * R2 * TB;                // elements of one T buffer
-    static constexpr size_t T_b = (size_t)2 * TE * sizeof(float2);
-    static constexpr size_t KV_b = (size_t)7 * NK * Q * sizeof(float);
-    // Tucker scratch: G [7][d3][d1] and H [7][Q][d3] for ranks <= dmax
-    static size_t smem(int dmax) {
-        return T_b + KV_b + (size_t)7 * dmax * dmax * sizeof(float) + (size_t)7 * Q * dmax * sizeof(float);
+    static constexpr int KVS = 8;                         // floats per (kh, q) entry of KV (7 used)
+    static constexpr size_t KV_b = (size_t)NK * Q * KVS * sizeof(float);
+    // T (double-buffered when it fits) | KV [NK][Q][8] | Tucker scratch G [7][d3][d1], H [7][Q][d3]
+    static size_t smem(int dmax, int nbuf) {
+        return (size_t)nbuf * TE * sizeof(float2) + KV_b + (size_t)7 * dmax * dmax * sizeof(float) +
+               (size_t)7 * Q * dmax * sizeof(float);
     }
-    static_assert(NL1 <= NT && NL2 <= NT, "z plan: one L1 and one L2 task per thread");
 };
 
-template <int N, int R2, int Q>
-__global__ void __launch_bounds__(ZPlan<N, R2, Q>::NT, ZPlan<N, R2, Q>::NT > 256 ? 1 : 2)
+// NBUF = 2: T double-buffered (two barriers per tile); 1: single buffer (three barriers)
+template <int N, int R2, int Q, int NT, int NBUF>
+__global__ void __launch_bounds__(NT, 1)
     k_zpass(float2* __restrict__ X2, SpecView sv, const float2* __restrict__ tw, int Nx, int Ny, int Kz, int Nxs,
             int kxg, float g, int nrhs, const uint8_t* __restrict__ planeok, int dmax) {
-    using P = ZPlan<N, R2, Q>;
-    constexpr int R1 = P::R1, NK = P::NK, TB = P::TB, TE = P::TE, NL1 = P::NL1, NL2 = P::NL2;
+    using P = ZPlan<N, R2, Q, NT>;
+    constexpr int R1 = P::R1, NK = P::NK, TB = P::TB, TE = P::TE, TL1 = P::TL1, NL2 = P::NL2, KVS = P::KVS;
     extern __shared__ __align__(16) unsigned char smraw[];
-    float2* T = reinterpret_cast<float2*>(smraw);                       // [2][5][R2][TB]
-    float* KV = reinterpret_cast<float*>(smraw + P::T_b);               // [7][NK][Q] raw spectra
-    float* G = KV + 7 * NK * Q;                                         // [7][d3][d1]
-    float* H = G + 7 * dmax * dmax;                                     // [7][Q][d3]
+    float2* T = reinterpret_cast<float2*>(smraw);                                 // [NBUF][5][R2][TB]
+    float* KV = reinterpret_cast<float*>(smraw + (size_t)NBUF * TE * sizeof(float2));   // [NK][Q][8]
+    float* G = KV + NK * Q * KVS;                                                 // [7][d3][d1]
+    float* H = G + 7 * dmax * dmax;                                               // [7][Q][d3]
     const int tid = threadIdx.x;
     const float2 zero = make_float2(0.f, 0.f);
     const bool tucker = sv.spec == nullptr;
     const int64_t plane = (int64_t)Nxs * Ny;
     const int tiles_x = Nxs / Q;
     const int nunits = (Ny / 2 + 1) * tiles_x;
-    // this CTA's contiguous chunk of units
     const int u0 = (int)((int64_t)nunits * blockIdx.x / gridDim.x);
     const int u1 = (int)((int64_t)nunits * (blockIdx.x + 1) / gridDim.x);
-    // L1 role
-    const bool l1 = tid < NL1;
-    const int c1 = tid / (R2 * Q), n2 = (tid / Q) % R2, q1 = tid % Q;
+    // L1 tasks a = tid + k NT -> (c, n2, q); their element offsets and live-plane masks are
+    // per-thread constants
+    int tc[TL1], tq[TL1], tn2[TL1];
+    int64_t toff[TL1];
+    uint32_t live[TL1];
+#pragma unroll
+    for (int k = 0; k < TL1; ++k) {
+        const int a = tid + k * NT;
+        tc[k] = a / (R2 * Q);
+        tn2[k] = (a / Q) % R2;
+        tq[k] = a % Q;
+        toff[k] = (int64_t)tc[k] * Kz * plane + (int64_t)tn2[k] * plane + tq[k];
+        uint32_t m = 0;
+        for (int n1 = 0; n1 < R1 / 2; ++n1) {
+            const int z = R2 * n1 + tn2[k];
+            if (z < Kz && __ldg(&planeok[z])) m |= 1u << n1;
+        }
+        live[k] = m;
+    }
     // L2 role and its twiddles W_N^{n2 k1}, n2 = 1 .. R2-1
     const bool l2 = tid < NL2;
     const int k1 = tid / Q, q2 = tid % Q;
     float2 w2[R2];
 #pragma unroll
     for (int m = 0; m < R2; ++m) w2[m] = l2 ? __ldg(&tw[(m * k1) & (N - 1)]) : zero;
-    // tile sequence inside a unit: row 0 / 1 (ky = oy, Ny - oy; one row if they coincide) x RHS
     auto unit_rows = [&](int u) { const int oy = u / tiles_x; return (oy == 0 || 2 * oy == Ny) ? 1 : 2; };
-    // decode tile (u, i) -> ky, xt, r
-    auto tile_of = [&](int u, int i, int& ky, int& xt, int& r) {
+    // tile (u, i) -> element offset of (r, c = 0, z = 0, ky, xt * Q)
+    auto tile_base = [&](int u, int i, int& ky, int& xt, int& r) -> int64_t {
         const int oy = u / tiles_x;
         xt = u % tiles_x;
         const int row = i / nrhs;
         r = i % nrhs;
         ky = row == 0 ? oy : Ny - oy;
+        return (int64_t)r * 5 * Kz * plane + (int64_t)ky * Nxs + xt * Q;
     };
-    // L1 prefetch registers: the R1/2 live inputs of the next tile
-    float2 nx[R1 / 2];
-    auto load_tile = [&](int u, int i) {
-        int ky, xt, r;
-        tile_of(u, i, ky, xt, r);
-        const float2* src = X2 + ((int64_t)(r * 5 + c1) * Kz) * plane + (int64_t)ky * Nxs + xt * Q + q1;
+    const int64_t zstep = (int64_t)R2 * plane;
+    float2 nx[TL1][R1 / 2];   // prefetch of the next tile's live inputs
+    auto load_tile = [&](int64_t base) {
 #pragma unroll
-        for (int n1 = 0; n1 < R1 / 2; ++n1) {
-            const int z = R2 * n1 + n2;
-            nx[n1] = (z < Kz && __ldg(&planeok[z])) ? src[(int64_t)z * plane] : zero;
+        for (int k = 0; k < TL1; ++k) {
+            const float2* src = X2 + base + toff[k];
+#pragma unroll
+            for (int n1 = 0; n1 < R1 / 2; ++n1) nx[k][n1] = ((live[k] >> n1) & 1u) ? src[n1 * zstep] : zero;
         }
     };
     int u = u0, i = 0;
-    if (u < u1 && l1) load_tile(u, 0);
+    if (u < u1) {
+        int ky, xt, r;
+        load_tile(tile_base(u, 0, ky, xt, r));
+    }
     int cur_oy = -1;
     for (int s = 0; u < u1; ++s) {
-        float2* Tb = T + (s & 1) * TE;
+        float2* Tb = T + (NBUF == 2 ? (s & 1) * TE : 0);
         int ky, xt, r;
-        tile_of(u, i, ky, xt, r);
+        const int64_t base = tile_base(u, i, ky, xt, r);
         const int oy = u / tiles_x;
         if (i == 0) {
-            // the unit's raw kernel spectra KV[m][kh][q] (previous tile's L2 finished at its 2nd barrier)
+            // the unit's raw kernel spectra KV[kh][q][m] (the previous tile's L2 finished at its barrier)
             if (tucker) {
                 if (oy != cur_oy) {
                     // G_m = core_m x2 F2_m[oy]   ([d3][d1], once per oy)
@@ -116,71 +135,86 @@ __global__ void __launch_bounds__(ZPlan<N, R2, Q>::NT, ZPlan<N, R2, Q>::NT > 256
                         const int d1 = sv.rk[m][0], d2 = sv.rk[m][1], d3 = sv.rk[m][2];
                         const float* C = sv.core[m];
                         const float* F2 = sv.fac[m][1] + (int64_t)oy * d2;
-                        for (int t = tid; t < d3 * d1; t += P::NT) {
+                        for (int t = tid; t < d3 * d1; t += NT) {
                             const int c3 = t / d1, cc1 = t % d1;
+                            const float* cp = C + (int64_t)c3 * d2 * d1 + cc1;
                             float acc = 0.f;
-                            for (int cc2 = 0; cc2 < d2; ++cc2)
-                                acc = fmaf(__ldg(&C[((int64_t)c3 * d2 + cc2) * d1 + cc1]), __ldg(&F2[cc2]), acc);
+                            for (int cc2 = 0; cc2 < d2; ++cc2) acc = fmaf(__ldg(&cp[cc2 * d1]), __ldg(&F2[cc2]), acc);
                             G[m * dmax * dmax + t] = acc;
                         }
                     }
                     cur_oy = oy;
                     __syncthreads();
                 }
-                // H_m[q] = G_m x1 F1_m[ox_q]   ([Q][d3])
+                // H_m[q] = G_m x1 F1_m[ox_q]   ([Q][d3]); the kernel index m is the outer, uniform loop
+                // so the rank, the factor pointers and the index split stay out of the inner loops
+#pragma unroll 1
                 for (int m = 0; m < 7; ++m) {
                     const int d1 = sv.rk[m][0], d3 = sv.rk[m][2];
-                    for (int t = tid; t < Q * d3; t += P::NT) {
-                        const int q = t / d3, c3 = t % d3;
+                    const float* F1 = sv.fac[m][0];
+                    const float* Gm = G + m * dmax * dmax;
+                    float* Hm = H + m * Q * dmax;
+                    for (int t = tid; t < Q * d3; t += NT) {
+                        const int q = t / d3, c3 = t - q * d3;
                         const int kx = kxg + xt * Q + q;
                         const int ox = kx <= (Nx >> 1) ? kx : Nx - kx;
-                        const float* f1 = sv.fac[m][0] + (int64_t)ox * d1;
-                        const float* gm = G + m * dmax * dmax + c3 * d1;
+                        const float* f1 = F1 + (int64_t)ox * d1;
+                        const float* gm = Gm + c3 * d1;
                         float acc = 0.f;
+#pragma unroll 4
                         for (int cc1 = 0; cc1 < d1; ++cc1) acc = fmaf(gm[cc1], __ldg(&f1[cc1]), acc);
-                        H[(m * Q + q) * dmax + c3] = acc;
+                        Hm[q * dmax + c3] = acc;
                     }
                 }
                 __syncthreads();
-                // KV_m[kh][q] = H_m[q] . F3_m[kh]
-                for (int t = tid; t < 7 * NK * Q; t += P::NT) {
-                    const int q = t % Q, rest = t / Q;
-                    const int kh = rest % NK, m = rest / NK;
+                // KV[kh][q][m] = H_m[q] . F3_m[kh]
+#pragma unroll 1
+                for (int m = 0; m < 7; ++m) {
                     const int d3 = sv.rk[m][2];
-                    const float* f3 = sv.fac[m][2] + (int64_t)kh * d3;
-                    const float* hm = H + (m * Q + q) * dmax;
-                    float acc = 0.f;
-                    for (int c3 = 0; c3 < d3; ++c3) acc = fmaf(hm[c3], __ldg(&f3[c3]), acc);
-                    KV[t] = acc;
+                    const float* F3 = sv.fac[m][2];
+                    const float* Hm = H + m * Q * dmax;
+                    for (int t = tid; t < NK * Q; t += NT) {
+                        const int q = t % Q, kh = t / Q;
+                        const float* f3 = F3 + kh * d3;
+                        const float* hm = Hm + q * dmax;
+                        float acc = 0.f;
+#pragma unroll 4
+                        for (int c3 = 0; c3 < d3; ++c3) acc = fmaf(hm[c3], __ldg(&f3[c3]), acc);
+                        KV[t * KVS + m] = acc;
+                    }
                 }
             } else {
                 const int64_t pl = (int64_t)sv.hx * sv.hy * sv.hz;
-                for (int t = tid; t < 7 * NK * Q; t += P::NT) {
+                for (int t = tid; t < 7 * NK * Q; t += NT) {
                     const int q = t % Q, rest = t / Q;
                     const int kh = rest % NK, m = rest / NK;
                     const int kx = kxg + xt * Q + q;
                     const int ox = kx <= (Nx >> 1) ? kx : Nx - kx;
-                    KV[t] = __ldg(&sv.spec[m * pl + ((int64_t)kh * sv.hy + oy) * sv.hx + ox]);
+                    KV[(kh * Q + q) * KVS + m] = __ldg(&sv.spec[m * pl + ((int64_t)kh * sv.hy + oy) * sv.hx + ox]);
                 }
             }
             // published to L2 by the barrier after L1
         }
-        // next tile of this CTA (prefetched into registers during this tile)
+        // next tile of this CTA: its inputs are loaded into registers during this tile
         int un = u, in = i + 1;
         if (in == unit_rows(u) * nrhs) {
             ++un;
             in = 0;
         }
         // L1 forward
-        if (l1) {
+#pragma unroll
+        for (int k = 0; k < TL1; ++k) {
             float2 v[R1];
 #pragma unroll
-            for (int n1 = 0; n1 < R1; ++n1) v[n1] = n1 < R1 / 2 ? nx[n1] : zero;
-            if (un < u1) load_tile(un, in);
+            for (int n1 = 0; n1 < R1; ++n1) v[n1] = n1 < R1 / 2 ? nx[k][n1] : zero;
+            if (k == TL1 - 1 && un < u1) {
+                int kyn, xtn, rn;
+                load_tile(tile_base(un, in, kyn, xtn, rn));
+            }
             reg_fft<R1, -1, true>(v);
-            float2* t1 = Tb + (c1 * R2 + n2) * TB + q1;
+            float2* t1 = Tb + (tc[k] * R2 + tn2[k]) * TB + tq[k];
 #pragma unroll
-            for (int k = 0; k < R1; ++k) t1[k * Q] = v[k];
+            for (int kk = 0; kk < R1; ++kk) t1[kk * Q] = v[kk];
         }
         __syncthreads();
         // L2: twiddle, R2-point FFT, MAC, inverse, twiddle
@@ -202,11 +236,12 @@ __global__ void __launch_bounds__(ZPlan<N, R2, Q>::NT, ZPlan<N, R2, Q>::NT > 256
                 const int kz = k1 + R1 * k2;
                 const int kh = kz <= (N >> 1) ? kz : N - kz;
                 const float s3 = kz <= (N >> 1) ? 1.f : -1.f;   // K1z is odd in kz
-                const float* kp = KV + kh * Q + q2;
+                const float4 ka = *reinterpret_cast<const float4*>(KV + (kh * Q + q2) * KVS);
+                const float4 kb = *reinterpret_cast<const float4*>(KV + (kh * Q + q2) * KVS + 4);
                 // folded moment-form constants
-                const float f0 = g * kp[0 * NK * Q], f1 = gx * kp[1 * NK * Q], f2 = gy * kp[2 * NK * Q];
-                const float f3 = (-2.f * g) * s3 * kp[3 * NK * Q];
-                const float f4 = g * kp[4 * NK * Q], f5 = g * kp[5 * NK * Q], f6 = (4.f * g) * kp[6 * NK * Q];
+                const float f0 = g * ka.x, f1 = gx * ka.y, f2 = gy * ka.z;
+                const float f3 = (-2.f * g) * s3 * ka.w;
+                const float f4 = g * kb.x, f5 = g * kb.y, f6 = (4.f * g) * kb.z;
                 const float2 Ix = uu[0][k2], Iy = uu[1][k2], Iz = uu[2][k2], I2 = uu[3][k2], I3 = uu[4][k2];
                 const float2 m1x = cadd(I2, I3), m1y = csub(I3, I2);
                 const float2 Qx = cfma_s(Ix, -f1, cmul_i(m1x, f4));
@@ -230,22 +265,21 @@ __global__ void __launch_bounds__(ZPlan<N, R2, Q>::NT, ZPlan<N, R2, Q>::NT > 256
         }
         __syncthreads();
         // L1 inverse: z = n2 + R2 n1, kept z < Kz, straight to HBM
-        if (l1) {
+#pragma unroll
+        for (int k = 0; k < TL1; ++k) {
             float2 v[R1];
-            const float2* t1 = Tb + (c1 * R2 + n2) * TB + q1;
+            const float2* t1 = Tb + (tc[k] * R2 + tn2[k]) * TB + tq[k];
 #pragma unroll
-            for (int k = 0; k < R1; ++k) v[k] = t1[k * Q];
+            for (int kk = 0; kk < R1; ++kk) v[kk] = t1[kk * Q];
             reg_fft<R1, +1>(v);
-            float2* dst = X2 + ((int64_t)(r * 5 + c1) * Kz) * plane + (int64_t)ky * Nxs + xt * Q + q1;
+            float2* dst = X2 + base + toff[k];
 #pragma unroll
-            for (int n1 = 0; n1 < R1 / 2; ++n1) {
-                const int z = n2 + R2 * n1;
-                if (z < Kz) dst[(int64_t)z * plane] = v[n1];
-            }
+            for (int n1 = 0; n1 < R1 / 2; ++n1)
+                if (R2 * n1 + tn2[k] < Kz) dst[n1 * zstep] = v[n1];
         }
         u = un;
         i = in;
-        if (i == 0 && u < u1) __syncthreads();   // KV / G / H of the next unit are rewritten
+        if (NBUF == 1) __syncthreads();   // the next tile's L1 rewrites T
     }
 }
 

@@ -82,10 +82,18 @@ def solve_sharded(handle, ports, group=None):
 
 def slab_exchange(send, recv, P, group=None):
     """The all-to-all of the slab matvec: chunk p of ``send`` goes to rank p, chunk s of
-    ``recv`` comes from rank s (equal chunks; NCCL over NVLink on GPUs, gloo on CPU)."""
+    ``recv`` comes from rank s (equal chunks).  NCCL (NVLink) moves device buffers directly,
+    ordered on the current stream (no host synchronisation); a gloo group stages them through
+    host memory (the multi-process tests on one GPU)."""
     import torch.distributed as dist
     assert send.numel() % P == 0 and recv.numel() == send.numel()
-    dist.all_to_all_single(recv, send, group=group)
+    if dist.get_backend(group) == "nccl" or not send.is_cuda:
+        dist.all_to_all_single(recv, send, group=group)
+        return
+    hs = send.cpu()
+    hr = hs.new_empty(hs.shape)
+    dist.all_to_all_single(hr, hs, group=group)
+    recv.copy_(hr)
 
 
 def virtual_exchange(sends, recvs):
@@ -121,11 +129,11 @@ class SlabMatvec:
         nrhs = I_slab.shape[0]
         send, recv = self._buffers(nrhs, I_slab.device)
         out = torch.empty_like(I_slab)
+        # libsvh launches on the current stream; the collectives are ordered after it (NCCL) or
+        # synchronise through the host copy (gloo)
         self.h.slab_forward(self.rank, self.P, I_slab, send)
-        torch.cuda.current_stream().synchronize()
         slab_exchange(send, recv, self.P, self.group)
         self.h.slab_middle(self.rank, self.P, recv, send, nrhs)
-        torch.cuda.current_stream().synchronize()
         slab_exchange(send, recv, self.P, self.group)
         self.h.slab_backward(self.rank, self.P, recv, I_slab, out, green_only)
         return out
