@@ -184,9 +184,6 @@ static void destroy(svh_handle* h) {
     cudaFree(h->X1);
     cudaFree(h->X2);
     free_host_pipe(h);
-    for (auto st : h->streams) cudaStreamDestroy(st);
-    for (auto ev : h->stream_events) cudaEventDestroy(ev);
-    if (h->fork_event) cudaEventDestroy(h->fork_event);
     delete h;
 }
 

@@ -60,9 +60,6 @@ struct svh_handle {
     float2* X1 = nullptr;                // [chunk][5][kz][ky][nx]
     float2* X2 = nullptr;                // [chunk][5][kz][ny][nx]
     int ws_rhs = 0;
-    std::vector<cudaStream_t> streams;   // internal streams for concurrent RHS sub-batches
-    std::vector<cudaEvent_t> stream_events;
-    cudaEvent_t fork_event = nullptr;
     // host-buffer matvec pipeline (svh_matvec_host): double-buffered device slots, copy streams
     struct HostPipe {
         size_t cap = 0;                       // RHS per slot

@@ -303,10 +303,7 @@ __global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q)
     }
 }
 
-// Persistent, software-pipelined variant of the strided pass for N > 64: every CTA
-// loops over tiles; the input tile of the next iteration is copied HBM -> shared
-// memory with cp.async (16-byte LDGSTS, no register cost) while the current tile is
-// transformed, so a full tile of loads is always in flight per SM.
+// cp.async helpers (16-byte LDGSTS, no register cost) for the staged strided pass
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
@@ -314,221 +311,12 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 
-template <int N, int Q, int DIR>
-constexpr int colpipe_stage_rows() {
-    return DIR < 0 ? N / 2 : N;
-}
-template <int N, int Q, int DIR>
-constexpr size_t colpipe_smem() {
-    return (size_t)(2 * colpipe_stage_rows<N, Q, DIR>() * Q + em_size<N, Q>()) * sizeof(float2);
-}
-
-template <int N, int Q, int DIR>
-__global__ void __launch_bounds__(fft_threads_per_pencil(N) * Q, 1)
-    k_col_pipe(const float2* __restrict__ in, float2* __restrict__ out, const float2* __restrict__ tw, int Nx,
-               int Kz, int Lin, int Lout, int ntiles, int tiles_x, const int32_t* __restrict__ planes, int nzp,
-               const uint32_t* __restrict__ rowmask, int rowMW) {
-    constexpr int R1 = fft_r1(N), R2 = fft_r2(N);
-    constexpr int SR = colpipe_stage_rows<N, Q, DIR>();
-    constexpr int NT = fft_threads_per_pencil(N) * Q;
-    extern __shared__ float2 sm[];
-    float2* T = sm + 2 * SR * Q;
-    const float2 zero = make_float2(0.f, 0.f);
-    const int lin = min(Lin, SR);
-    // tile t -> (kx tile, non-empty plane, rhs*component)
-    auto tile_z = [&](int t) { return __ldg(&planes[(t / tiles_x) % nzp]); };
-    auto tile_rc = [&](int t) { return (t / tiles_x) / nzp; };
-    auto issue = [&](int t, int buf) {
-        const int z = tile_z(t), xt = t % tiles_x;
-        const float2* src = in + (((int64_t)tile_rc(t) * Kz + z) * Lin) * (int64_t)Nx + (int64_t)xt * Q;
-        float2* st = sm + buf * SR * Q;
-        for (int e = threadIdx.x; e < lin * (Q / 2); e += NT) {
-            const int j = e / (Q / 2), p = e % (Q / 2);
-            if (DIR > 0 || row_bit(rowmask, rowMW, z, j)) cp_async16(st + j * Q + 2 * p, src + (int64_t)j * Nx + 2 * p);
-        }
-    };
-    int t = blockIdx.x;
-    if (t < ntiles) issue(t, 0);
-    cp_async_commit();
-    for (int it = 0; t < ntiles; t += gridDim.x, ++it) {
-        const int buf = it & 1;
-        if (t + (int)gridDim.x < ntiles) issue(t + gridDim.x, buf ^ 1);
-        cp_async_commit();
-        cp_async_wait1();
-        __syncthreads();
-        const int z = tile_z(t);
-        const float2* st = sm + buf * SR * Q;
-        if (threadIdx.x < R2 * Q) {
-            const int n2 = threadIdx.x / Q, q = threadIdx.x % Q;
-            float2 v[R1];
-#pragma unroll
-            for (int n1 = 0; n1 < R1; ++n1) {
-                const int j = R2 * n1 + n2;
-                if (DIR < 0)
-                    v[n1] = (n1 < R1 / 2 && j < lin && row_bit(rowmask, rowMW, z, j)) ? st[j * Q + q] : zero;
-                else
-                    v[n1] = st[j * Q + q];
-            }
-            reg_fft<R1, DIR>(v);
-#pragma unroll
-            for (int k1 = 1; k1 < R1; ++k1) {
-                float2 w = __ldg(&tw[n2 * k1]);
-                if (DIR > 0) w.y = -w.y;
-                v[k1] = cmul(v[k1], w);
-            }
-#pragma unroll
-            for (int k1 = 0; k1 < R1; ++k1) T[em_idx<N, Q>(n2 * R1 + k1, q)] = v[k1];
-        }
-        __syncthreads();
-        if (threadIdx.x < R1 * Q) {
-            const int k1 = threadIdx.x / Q, q = threadIdx.x % Q;
-            const int xt = t % tiles_x;
-            float2* dst = out + (((int64_t)tile_rc(t) * Kz + z) * Lout) * (int64_t)Nx + (int64_t)xt * Q;
-            float2 u[R2];
-#pragma unroll
-            for (int n2 = 0; n2 < R2; ++n2) u[n2] = T[em_idx<N, Q>(n2 * R1 + k1, q)];
-            reg_fft<R2, DIR>(u);
-#pragma unroll
-            for (int k2 = 0; k2 < R2; ++k2) {
-                const int j = k1 + R1 * k2;
-                if (DIR < 0)
-                    dst[(int64_t)j * Nx + q] = u[k2];
-                else if (k2 < R2 / 2 && j < Lout && row_bit(rowmask, rowMW, z, j))
-                    dst[(int64_t)j * Nx + q] = u[k2];
-            }
-        }
-    }
-    cp_async_commit();
-}
-
-// Staged strided pass (B / D), the default for 128 <= N <= 1024.  One persistent CTA per
-// SM; tiles (Q consecutive kx of one non-empty plane of one (rhs, component)) stream
-// HBM -> shared memory through an S-deep cp.async ring (16-byte LDGSTS, no register
-// cost), so loads of the next S-1 tiles are in flight while the current one is
-// transformed.  Phase 1 (R1-point FFTs) reads the staged tile, phase 2 (R2-point FFTs)
-// stores straight to HBM.  The phase-1 twiddles W_N^(n2 k1) are loop-invariant per
-// thread and live in registers; rows holding no voxel are zero-filled in shared memory
-// (forward) or not stored (inverse) -- the pruning of k_col.
-template <int N, int Q, int DIR, int S>
-struct YStage {
-    static constexpr int R1 = fft_r1(N), R2 = fft_r2(N);
-    static constexpr int NT = R1 * Q;
-    static constexpr int SR = DIR < 0 ? N / 2 : N;
-    static constexpr int MW = (N / 2 + 31) / 32;
-    static constexpr size_t smem = (size_t)(S * SR * Q + em_size<N, Q>()) * sizeof(float2) + (size_t)S * MW * 4;
-};
-
-template <int N, int Q, int DIR, int S>
-__global__ void __launch_bounds__(fft_r1(N) * Q, 1)
-    k_ystage(const float2* __restrict__ in, float2* __restrict__ out, const float2* __restrict__ tw, int Nx,
-             int Kz, int Lin, int Lout, int ntiles, int tiles_x, const int32_t* __restrict__ planes, int nzp,
-             const uint32_t* __restrict__ rowmask, int rowMW) {
-    using P = YStage<N, Q, DIR, S>;
-    constexpr int R1 = P::R1, R2 = P::R2, NT = P::NT, SR = P::SR, MW = P::MW;
-    constexpr int NL = DIR < 0 ? R1 / 2 : R1;
-    extern __shared__ __align__(16) float2 sm[];
-    float2* stage = sm;
-    float2* T = sm + S * SR * Q;
-    uint32_t* M = reinterpret_cast<uint32_t*>(T + em_size<N, Q>());
-    const int tid = threadIdx.x;
-    const float2 zero = make_float2(0.f, 0.f);
-    const int lin = min(Lin, SR);
-    // rows lin..SR-1 of every stage are never copied: zero them once
-    for (int e = tid; e < S * (SR - lin) * Q; e += NT) {
-        const int st = e / ((SR - lin) * Q), r = e % ((SR - lin) * Q);
-        stage[st * SR * Q + lin * Q + r] = zero;
-    }
-    auto decode = [&](int t, int& z, int64_t& bin, int64_t& bout) {
-        const int xt = t % tiles_x, pr = t / tiles_x;
-        const int rc = pr / nzp;
-        z = __ldg(&planes[pr - rc * nzp]);
-        bin = ((int64_t)rc * Kz + z) * Lin * (int64_t)Nx + (int64_t)xt * Q;
-        bout = ((int64_t)rc * Kz + z) * Lout * (int64_t)Nx + (int64_t)xt * Q;
-    };
-    auto issue = [&](int t, int st) {
-        if (t < ntiles) {
-            int z;
-            int64_t bin, bout;
-            decode(t, z, bin, bout);
-            const uint32_t* pm = rowmask + (int64_t)z * rowMW;
-            if (tid < MW) M[st * MW + tid] = tid < rowMW ? __ldg(&pm[tid]) : 0u;
-            const float2* src = in + bin;
-            float2* dst = stage + st * SR * Q;
-            for (int e = tid; e < lin * (Q / 2); e += NT) {
-                const int j = e / (Q / 2), p2 = 2 * (e % (Q / 2));
-                if (DIR > 0 || ((__ldg(&pm[j >> 5]) >> (j & 31)) & 1u))
-                    cp_async16(dst + j * Q + p2, src + (int64_t)j * Nx + p2);
-                else
-                    *reinterpret_cast<float4*>(dst + j * Q + p2) = make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-        }
-        cp_async_commit();
-    };
-    // phase-1 role (n2, q1): twiddles W_N^(n2 k1), k1 = 1..R1-1, held in registers
-    const int n2 = tid / Q, q1 = tid % Q;
-    const bool ph1 = n2 < R2;
-    float2 tw1[R1];
-#pragma unroll
-    for (int kk = 1; kk < R1; ++kk) {
-        float2 w = ph1 ? __ldg(&tw[n2 * kk]) : zero;
-        if (DIR > 0) w.y = -w.y;
-        tw1[kk] = w;
-    }
-    const int k1 = tid / Q, q2 = tid % Q;   // phase-2 role
-    int t = blockIdx.x;
-#pragma unroll
-    for (int s = 0; s < S - 1; ++s) issue(t + s * (int)gridDim.x, s);
-    for (int i = 0; t < ntiles; ++i, t += gridDim.x) {
-        issue(t + (S - 1) * (int)gridDim.x, (i + S - 1) % S);
-        asm volatile("cp.async.wait_group %0;\n" ::"n"(S - 1));
-        __syncthreads();
-        const int st = i % S;
-        int z;
-        int64_t bin, bout;
-        decode(t, z, bin, bout);
-        if (ph1) {
-            const float2* src = stage + st * SR * Q;
-            float2 v[R1];
-#pragma unroll
-            for (int n1 = 0; n1 < R1; ++n1) v[n1] = n1 < NL ? src[(R2 * n1 + n2) * Q + q1] : zero;
-            reg_fft<R1, DIR, (DIR < 0)>(v);
-#pragma unroll
-            for (int kk = 1; kk < R1; ++kk) v[kk] = cmul(v[kk], tw1[kk]);
-#pragma unroll
-            for (int kk = 0; kk < R1; ++kk) T[em_idx<N, Q>(n2 * R1 + kk, q1)] = v[kk];
-        }
-        uint32_t keep = 0;   // inverse: which of this thread's output rows hold a voxel
-        if (DIR > 0) {
-#pragma unroll
-            for (int k2 = 0; k2 < R2 / 2; ++k2) {
-                const int j = k1 + R1 * k2;
-                if (j < Lout && ((M[st * MW + (j >> 5)] >> (j & 31)) & 1u)) keep |= 1u << k2;
-            }
-        }
-        __syncthreads();
-        float2 u[R2];
-#pragma unroll
-        for (int m = 0; m < R2; ++m) u[m] = T[em_idx<N, Q>(m * R1 + k1, q2)];
-        reg_fft<R2, DIR>(u);
-        float2* dst = out + bout + q2;
-#pragma unroll
-        for (int k2 = 0; k2 < R2; ++k2) {
-            const int off = (k1 + R1 * k2) * Nx;
-            if (DIR < 0)
-                dst[off] = u[k2];
-            else if (k2 < R2 / 2 && ((keep >> k2) & 1u))
-                dst[off] = u[k2];
-        }
-    }
-    asm volatile("cp.async.wait_group 0;\n" ::);
-}
-
-// TMA variant of the staged strided pass (default when the tensor map encodes).  X2 =
+// Staged strided pass (B / D) for 128 <= N <= 512.  X2 =
 // [plane p = rc*Kz + z][ky < Ny][kx < Nx] is described by ONE 3-D tensor map (box 8 kx x
 // 256 rows): the forward pass (B) stores its output tile with it, the inverse pass (D)
 // loads its input tile with it, one cp.async.bulk.tensor per 256-row box into an
-// mbarrier-tracked ring.  The other side keeps the pruned row traffic of k_ystage: B
-// loads only the rows holding a voxel (cp.async), D stores only those rows.
+// mbarrier-tracked ring.  The other side keeps the pruned row traffic: B loads only the rows
+// holding a voxel (cp.async, empty rows zero-filled in shared memory), D stores only those rows.
 template <int N, int DIR, int S, int QQ>
 struct YTma {
     static constexpr int Q = QQ;
@@ -543,18 +331,16 @@ struct YTma {
     static constexpr size_t smem = S * stage_b + T_b + O_b + (size_t)S * MW * 4 + S * 8 + 128;
 };
 
-// TIN (forward only): load whole input tiles by TMA through tmap_in (X1 [plane][y][x]) and
-// zero the rows without voxels in registers, instead of the pruned cp.async row loads.
-template <int N, int DIR, int S, int QQ, bool TIN = false>
+template <int N, int DIR, int S, int QQ>
 __global__ void __launch_bounds__(fft_r1(N) * QQ, (QQ == 4 && N <= 1024) ? 2 : 1)
     k_ytma(const float2* __restrict__ in, float2* __restrict__ out, const __grid_constant__ CUtensorMap tmap,
-           const __grid_constant__ CUtensorMap tmap_in, const float2* __restrict__ tw, int Nx, int Kz, int Lin,
+           const float2* __restrict__ tw, int Nx, int Kz, int Lin,
            int Lout, int ntiles, int tiles_x, const int32_t* __restrict__ planes, int nzp,
            const uint32_t* __restrict__ rowmask, int rowMW) {
     using P = YTma<N, DIR, S, QQ>;
     constexpr int Q = P::Q, R1 = P::R1, R2 = P::R2, NT = P::NT, SR = P::SR, MW = P::MW, BOX = P::BOX;
     constexpr int NL = DIR < 0 ? R1 / 2 : R1;
-    constexpr bool TMA_IN = DIR > 0 || TIN;
+    constexpr bool TMA_IN = DIR > 0;
     constexpr int BOXI = SR < 256 ? SR : 256;
     extern __shared__ __align__(128) unsigned char smraw[];
     float2* stage = reinterpret_cast<float2*>(smraw);
@@ -565,7 +351,7 @@ __global__ void __launch_bounds__(fft_r1(N) * QQ, (QQ == 4 && N <= 1024) ? 2 : 1
     const int tid = threadIdx.x;
     const float2 zero = make_float2(0.f, 0.f);
     const int lin = min(Lin, SR);
-    if (DIR < 0 && !TIN) {
+    if (DIR < 0) {
         for (int e = tid; e < S * (SR - lin) * Q; e += NT) {
             const int st = e / ((SR - lin) * Q), r = e % ((SR - lin) * Q);
             stage[st * SR * Q + lin * Q + r] = zero;
@@ -621,7 +407,7 @@ __global__ void __launch_bounds__(fft_r1(N) * QQ, (QQ == 4 && N <= 1024) ? 2 : 1
                 mbar_arrive_expect_tx(&bar[st], (uint32_t)P::stage_b);
 #pragma unroll
                 for (int b = 0; b < SR / BOXI; ++b)
-                    tma_load_3d(stage + st * SR * Q + b * BOXI * Q, DIR > 0 ? &tmap : &tmap_in, (t % tiles_x) * Q,
+                    tma_load_3d(stage + st * SR * Q + b * BOXI * Q, &tmap, (t % tiles_x) * Q,
                                 b * BOXI, p, &bar[st]);
             }
         }
@@ -668,9 +454,7 @@ __global__ void __launch_bounds__(fft_r1(N) * QQ, (QQ == 4 && N <= 1024) ? 2 : 1
 #pragma unroll
             for (int n1 = 0; n1 < R1; ++n1) {
                 const int j = R2 * n1 + n2;
-                bool live = n1 < NL;
-                if (TIN) live = live && ((M[st * MW + (j >> 5)] >> (j & 31)) & 1u);
-                v[n1] = live ? src[j * Q + q1] : zero;
+                v[n1] = n1 < NL ? src[j * Q + q1] : zero;
             }
             reg_fft<R1, DIR, (DIR < 0)>(v);
 #pragma unroll
@@ -717,7 +501,7 @@ __global__ void __launch_bounds__(fft_r1(N) * QQ, (QQ == 4 && N <= 1024) ? 2 : 1
         }
     }
     if (DIR < 0) {
-        if (!TIN) asm volatile("cp.async.wait_group 0;\n" ::);
+        asm volatile("cp.async.wait_group 0;\n" ::);
         __syncthreads();
         if (tid == 0) {
             if (pend_p >= 0) {
@@ -940,7 +724,7 @@ __global__ void __launch_bounds__(5 * Q)
 
 // Pass C, default for 2 <= Nz <= 32: 32 pencils (kx) x 5 components per CTA, one
 // thread per (component, pencil) for the z-FFTs in registers, the CTA loops over all
-// RHS (register prefetch of the next one).  Compared with k_freq_small:
+// RHS (register prefetch of the next one):
 //  * the prefactor j*omega*mu0*dx/(Nx Ny Nz) and the constants of the moment form are
 //    folded into the 7 kernel values once per CTA, so the MAC is 19 paired-FP32 ops;
 //  * the MAC points are split warp-uniformly (warp w takes kz = w, w+5, ...; lane = kx),
@@ -960,7 +744,7 @@ constexpr size_t zmac_smem() {
     return (size_t)zmac_s_f2<N>() * sizeof(float2) + (size_t)7 * N * 32 * sizeof(float);
 }
 
-template <int N, int PROBE = 0>
+template <int N>
 __global__ void __launch_bounds__(160, 3)
     k_zmac(float2* __restrict__ X2, SpecView sv, int Nx, int Ny, int Kz, float g, int nrhs, uint64_t pmask, int Nxs,
            int kxg, int zpre) {
@@ -1023,7 +807,7 @@ __global__ void __launch_bounds__(160, 3)
         float2 v[N];
 #pragma unroll
         for (int j = 0; j < N; ++j) v[j] = j < NH ? nxt[j] : zero;
-        if (PROBE != 2) reg_fft<N, -1, true>(v);
+        reg_fft<N, -1, true>(v);
 #pragma unroll
         for (int k = 0; k < N; ++k) S[(c * N + k) * Q + q] = v[k];
         __syncthreads();
@@ -1046,7 +830,7 @@ __global__ void __launch_bounds__(160, 3)
         float2* sp = S + w * Q + q;
         const float* kp = KV + w * Q + q;
 #pragma unroll 1
-        for (int k = w; k < N && PROBE != 1; k += 5, sp += 5 * Q, kp += 5 * Q) {
+        for (int k = w; k < N ; k += 5, sp += 5 * Q, kp += 5 * Q) {
             {
                 const float2 Ix = sp[0 * N * Q], Iy = sp[1 * N * Q], Iz = sp[2 * N * Q];
                 const float2 I2 = sp[3 * N * Q], I3 = sp[4 * N * Q];
@@ -1066,7 +850,7 @@ __global__ void __launch_bounds__(160, 3)
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < N; ++k) v[k] = S[(c * N + k) * Q + q];   // own column: no barrier before reuse
-        if (PROBE != 2) reg_fft<N, +1>(v);
+        reg_fft<N, +1>(v);
         float2* dst = col + r * rstride;
 #pragma unroll
         for (int j = 0; j < NH; ++j)
@@ -1079,22 +863,19 @@ __global__ void __launch_bounds__(160, 3)
 // next RHS is not staged in registers but bulk-prefetched into L2 (cp.async.bulk.prefetch), so
 // a CTA needs <= 96 registers / thread and ~55 KB of shared memory: 4 CTAs (20 warps) per SM
 // instead of 3.  Same arithmetic as k_zmac.
-template <int N, bool HALF = false>
+template <int N>
 constexpr size_t zmac2_smem() {
-    return (size_t)(HALF ? 5 * (N / 2) * 32 : zmac_s_f2<N>()) * sizeof(float2) +
-           (size_t)7 * (N / 2 + 1) * 32 * sizeof(float);
+    return (size_t)zmac_s_f2<N>() * sizeof(float2) + (size_t)7 * (N / 2 + 1) * 32 * sizeof(float);
 }
 
-// HALF: the spectra buffer holds kz < N/2 and then kz >= N/2 (MAC in two rounds, 4 barriers
-// per RHS instead of 2) -- 35 KB of shared memory, 5 CTAs (25 warps) per SM.
-template <int N, bool HALF = false>
-__global__ void __launch_bounds__(160, HALF ? 5 : 4)
+template <int N>
+__global__ void __launch_bounds__(160, 4)
     k_zmac2(float2* __restrict__ X2, SpecView sv, int Nx, int Ny, int Kz, float g, int nrhs, uint64_t pmask, int Nxs,
             int kxg) {
     constexpr int Q = 32, NH = N / 2, NK = N / 2 + 1;
-    constexpr int NS = HALF ? N / 2 : N;                 // kz rows held in S at a time
+    constexpr int NS = N;                                // kz rows held in S
     extern __shared__ float2 S[];
-    float* KV = reinterpret_cast<float*>(S + (HALF ? 5 * NS * Q : zmac_s_f2<N>()));   // [7][NK][Q]
+    float* KV = reinterpret_cast<float*>(S + zmac_s_f2<N>());   // [7][NK][Q]
     const int tid = threadIdx.x;
     const int c = tid >> 5, q = tid & 31;
     const int kx0 = blockIdx.x * Q;
@@ -1143,7 +924,7 @@ __global__ void __launch_bounds__(160, HALF ? 5 : 4)
         prefetch(r + 2);
         reg_fft<N, -1, true>(v);
 #pragma unroll
-        for (int hh = 0; hh < (HALF ? 2 : 1); ++hh) {
+        for (int hh = 0; hh < 1; ++hh) {
             const int k0 = hh * NS;   // kz rows [k0, k0 + NS) in S
 #pragma unroll
             for (int k = 0; k < NS; ++k) S[(c * NS + k) * Q + q] = v[k0 + k];
@@ -1290,151 +1071,9 @@ __global__ void __launch_bounds__(freq_big_threads<N>())
 // order for the moment-form MAC (mac5), and the inverse runs the transposed two-level
 // transform, cropped to z < Kz.  Rows of planes without voxels are read as zero (X2 there is
 // never written by pass B); their results are written but never read (pass D skips them).
-template <int N, int Q>
-struct ZTma {
-    static constexpr int R1 = fft_r1(N), R2 = fft_r2(N), R = R1 > R2 ? R1 : R2;
-    static constexpr int NT = 5 * R * Q, NH = N / 2, EM = em_size<N, Q>();
-    static constexpr int SLOT = 5 * NH * Q;   // float2 per ring slot (= spectrum rows kz < N/2)
-    static constexpr size_t stage_b = (size_t)SLOT * sizeof(float2);
-    static constexpr size_t T_b = ((size_t)5 * EM * sizeof(float2) + 127) / 128 * 128;
-    // ring slot x2, the upper-half spectrum rows, the transpose buffer, twiddles, plane flags
-    static constexpr size_t smem = 3 * stage_b + T_b + (size_t)N * sizeof(float2) + NH + 16 + 128;
-};
-
-template <int N, int Q>
-__global__ void __launch_bounds__(ZTma<N, Q>::NT, 1)
-    k_ztma(const __grid_constant__ CUtensorMap tmap, SpecView sv, const float2* __restrict__ tw, int Nx, int Ny,
-           int Kz, float g, int nrhs, int ntiles, int tiles_x, const uint8_t* __restrict__ planeok, int kxg) {
-    using P = ZTma<N, Q>;
-    constexpr int R1 = P::R1, R2 = P::R2, R = P::R, NT = P::NT, NH = P::NH, EM = P::EM, SLOT = P::SLOT;
-    extern __shared__ __align__(128) unsigned char smraw[];
-    float2* stage = reinterpret_cast<float2*>(smraw);                        // [2][5][NH][Q]
-    float2* hi = reinterpret_cast<float2*>(smraw + 2 * P::stage_b);          // [5][NH][Q], kz >= N/2
-    float2* T = reinterpret_cast<float2*>(smraw + 3 * P::stage_b);           // [5][EM]
-    float2* tws = reinterpret_cast<float2*>(smraw + 3 * P::stage_b + P::T_b);
-    uint8_t* pok = reinterpret_cast<uint8_t*>(tws + N);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + ((3 * P::stage_b + P::T_b + N * sizeof(float2) + NH + 7) / 8) * 8);
-    const int tid = threadIdx.x;
-    const float2 zero = make_float2(0.f, 0.f);
-    for (int j = tid; j < N; j += NT) tws[j] = __ldg(&tw[j]);
-    for (int j = tid; j < NH; j += NT) pok[j] = (j < Kz && __ldg(&planeok[j])) ? 1 : 0;
-    if (tid == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        mbar_fence_init();
-    }
-    __syncthreads();
-    auto issue = [&](int t, int st) {
-        if (t >= ntiles) return;
-        const int r = t % nrhs, rest = t / nrhs;
-        const int xt = rest % tiles_x, ky = rest / tiles_x;
-        mbar_arrive_expect_tx(&bar[st], (uint32_t)(5 * Kz * Q * sizeof(float2)));
-#pragma unroll
-        for (int c = 0; c < 5; ++c)
-            tma_load_3d(stage + st * SLOT + c * NH * Q, &tmap, xt * Q, ky, (r * 5 + c) * Kz, &bar[st]);
-    };
-    const int c = tid / (R * Q), j = (tid % (R * Q)) / Q, q = tid % Q;
-    float2* Tc = T + c * EM;
-    int t = blockIdx.x;
-    if (tid == 0) issue(t, 0);
-    for (int i = 0; t < ntiles; ++i, t += gridDim.x) {
-        const int st = i & 1;
-        float2* slot = stage + st * SLOT;
-        mbar_wait(&bar[st], (uint32_t)((i >> 1) & 1));
-        // forward, level 1 (thread n2 = j): FFT_R1 over n1 of x[R2 n1 + n2], twiddle W_N^{n2 k1}
-        if (j < R2) {
-            float2 v[R1];
-#pragma unroll
-            for (int n1 = 0; n1 < R1; ++n1) {
-                const int z = R2 * n1 + j;
-                v[n1] = (n1 < R1 / 2 && pok[z]) ? slot[(c * NH + z) * Q + q] : zero;
-            }
-            reg_fft<R1, -1, true>(v);
-#pragma unroll
-            for (int k1 = 1; k1 < R1; ++k1) v[k1] = cmul(v[k1], tws[j * k1]);
-#pragma unroll
-            for (int k1 = 0; k1 < R1; ++k1) Tc[em_idx<N, Q>(j * R1 + k1, q)] = v[k1];
-        }
-        __syncthreads();
-        if (tid == 0) {   // the other slot: its output store (tile i-1) must have left smem
-            tma_store_wait_read0();
-            issue(t + (int)gridDim.x, st ^ 1);
-        }
-        // forward, level 2 (thread k1 = j): FFT_R2 over n2 -> spectrum at kz = k1 + R1 k2,
-        // stored in natural order: kz < N/2 into the consumed slot, kz >= N/2 into hi
-        float2 u[R2];
-        if (j < R1) {
-#pragma unroll
-            for (int m = 0; m < R2; ++m) u[m] = Tc[em_idx<N, Q>(m * R1 + j, q)];
-            reg_fft<R2, -1>(u);
-#pragma unroll
-            for (int k2 = 0; k2 < R2; ++k2) {
-                const int kz = j + R1 * k2;
-                (kz < NH ? slot : hi)[(c * NH + (kz & (NH - 1))) * Q + q] = u[k2];
-            }
-        }
-        __syncthreads();
-        {
-            const int r = t % nrhs, rest = t / nrhs;
-            const int xt = rest % tiles_x, ky = rest / tiles_x;
-            for (int e = tid; e < N * Q; e += NT) {
-                const int kz = e / Q, qq = e % Q;
-                float kv[7];
-                kernel_values(sv, kxg + xt * Q + qq, ky, kz, Nx, Ny, N, kv);
-                float2* b = (kz < NH ? slot : hi) + (kz & (NH - 1)) * Q + qq;
-                float2 v5[5];
-#pragma unroll
-                for (int cc = 0; cc < 5; ++cc) v5[cc] = b[cc * NH * Q];
-                mac5(v5, kv[0], kv[1], kv[2], kv[3], kv[4], kv[5], kv[6], g);
-#pragma unroll
-                for (int cc = 0; cc < 5; ++cc) b[cc * NH * Q] = v5[cc];
-            }
-            (void)r;
-        }
-        __syncthreads();
-        // inverse, level 1 (thread k1 = j): IFFT_R2 over k2, twiddle W_N^{-n2 k1}
-        if (j < R1) {
-#pragma unroll
-            for (int k2 = 0; k2 < R2; ++k2) {
-                const int kz = j + R1 * k2;
-                u[k2] = (kz < NH ? slot : hi)[(c * NH + (kz & (NH - 1))) * Q + q];
-            }
-            reg_fft<R2, +1>(u);
-#pragma unroll
-            for (int n2 = 0; n2 < R2; ++n2) {
-                float2 w = tws[n2 * j];
-                w.y = -w.y;
-                Tc[em_idx<N, Q>(n2 * R1 + j, q)] = n2 ? cmul(u[n2], w) : u[n2];
-            }
-        }
-        __syncthreads();
-        // inverse, level 2 (thread n2 = j): IFFT_R1 over k1 -> z = n2 + R2 n1, cropped to z < Kz
-        if (j < R2) {
-            float2 v[R1];
-#pragma unroll
-            for (int k1 = 0; k1 < R1; ++k1) v[k1] = Tc[em_idx<N, Q>(j * R1 + k1, q)];
-            reg_fft<R1, +1>(v);
-#pragma unroll
-            for (int n1 = 0; n1 < R1 / 2; ++n1) {
-                const int z = j + R2 * n1;
-                if (z < Kz) slot[(c * NH + z) * Q + q] = v[n1];
-            }
-        }
-        fence_proxy_async_smem();
-        __syncthreads();
-        if (tid == 0) {
-            const int r = t % nrhs, rest = t / nrhs;
-            const int xt = rest % tiles_x, ky = rest / tiles_x;
-#pragma unroll
-            for (int cc = 0; cc < 5; ++cc) tma_store_3d(&tmap, xt * Q, ky, (r * 5 + cc) * Kz, slot + cc * NH * Q);
-            tma_store_commit();
-        }
-    }
-    if (tid == 0) tma_store_wait0();
-}
-
-// Pass C, second form (default for Nz = 128 .. 512): the same TMA ring and tiles as k_ztma,
-// but the z-FFT is split N = R1 x R2 with a SHORT second level (R2 = 4 / 8) so that one
+// Pass C for Nz = 512 (k_zpass covers 64..256): tiles of one RHS x Q kx x one ky arrive by
+// five cp.async.bulk.tensor loads (box Q x 1 x Kz) into a 2-slot mbarrier ring and leave by
+// five TMA stores.  The z-FFT is split N = R1 x R2 with a SHORT second level (R2 = 8) so that one
 // thread holds all 5 components of its (k1, q) column after the forward second level: the
 // moment-form MAC then runs in registers (no spectrum round trip through shared memory),
 // followed directly by the inverse first level, written back over the very elements the
@@ -1798,17 +1437,11 @@ template <int N, int DIR>
 void run_pass_y(svh_handle* h, const Geom& g, const float2* in, float2* out, int Lin, int Lout, int nrhs,
                 cudaStream_t s) {
     const int nx = g.nx;
-    constexpr int Q = col_q<N>();
-    // D (DIR = +1) runs the persistent cp.async-pipelined kernel; B the one-tile-per-CTA
-    // kernel (measured faster for the zero-padded forward direction).  SVH_NO_PIPE /
-    // SVH_PIPE_B flip these for experiments.
-    static const bool use_pipe = getenv("SVH_NO_PIPE") == nullptr;
-    static const bool pipe_fwd = getenv("SVH_PIPE_B") != nullptr;
-    static const int ystage = getenv("SVH_YSTAGE") ? atoi(getenv("SVH_YSTAGE")) : 3;  // 0 = off; bit0 fwd, bit1 inv
-    static const bool ytma = getenv("SVH_YTMA") == nullptr || atoi(getenv("SVH_YTMA")) != 0;
-    static const bool ytma2048 = getenv("SVH_YTMA2048") == nullptr || atoi(getenv("SVH_YTMA2048")) != 0;
-    if constexpr (N == 1024 || N == 2048) {
-        // Stockham radix-16 pencils, TMA-staged input (ypass.cuh)
+    if constexpr (N == 2048 && DIR > 0) {
+        // inverse 2048-point pencils: Stockham radix-16, TMA-staged input (ypass.cuh); measured
+        // 55 -> 34 ms on the 1024^2 x 64 grid (8 RHS).  For the forward pass and for 1024 points
+        // k_ytma (TMA-stored output tiles) measured faster (B 37.7 vs 43.9 ms; cfg4 B/D 3.2/2.4 vs
+        // 4.2/3.1 ms), so it stays the default there.
         constexpr int Q = N == 2048 ? 4 : 8;
         using P = YPlan<N, Q, DIR>;
         CUtensorMap tin;
@@ -1825,85 +1458,26 @@ void run_pass_y(svh_handle* h, const Geom& g, const float2* in, float2* out, int
         }
     }
     if constexpr (N >= 128 && N <= 2048) {
+        // TMA ring / TMA-stored tiles of 4 pencils (k_ytma)
+        constexpr int QQ = 4;
+        using P = YTma<N, DIR, 2, QQ>;
         CUtensorMap tmap;
         const float2* x2 = DIR < 0 ? out : in;   // the X2 side of the pass
-        static const int yq = getenv("SVH_YQ") ? atoi(getenv("SVH_YQ")) : 4;
-        static const bool btma = getenv("SVH_BTMA") ? atoi(getenv("SVH_BTMA")) != 0 : false;   // measured slower (more bytes)
-        auto launch = [&](auto Qc) -> bool {
-            constexpr int QQ = decltype(Qc)::value;
-            using P = YTma<N, DIR, 2, QQ>;
-            if (nx % QQ != 0 ||
-                !encode_tmap_c64_3d(&tmap, x2, (uint64_t)nx, (uint64_t)h->ny, (uint64_t)5 * nrhs * h->kz,
-                                    (uint64_t)nx, (uint64_t)nx * h->ny, QQ, P::BOX))
-                return false;
-            CUtensorMap tmap_in = tmap;
-            bool tin = false;
-            if (DIR < 0 && btma) {   // X1 [plane][y < Ky][x], box QQ x min(N/2, 256)
-                constexpr uint32_t BI = (N / 2) < 256 ? (N / 2) : 256;
-                tin = encode_tmap_c64_3d(&tmap_in, in, (uint64_t)nx, (uint64_t)h->ky, (uint64_t)5 * nrhs * h->kz,
-                                         (uint64_t)nx, (uint64_t)nx * h->ky, QQ, BI);
-            }
+        if (nx % QQ == 0 && encode_tmap_c64_3d(&tmap, x2, (uint64_t)nx, (uint64_t)h->ny, (uint64_t)5 * nrhs * h->kz,
+                                               (uint64_t)nx, (uint64_t)nx * h->ny, QQ, P::BOX)) {
             const int tiles_x = nx / QQ;
             const int ntiles = tiles_x * h->nzp * 5 * nrhs;
-            int dev = 0, nsm = 148, occ = 1;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-            auto go = [&](auto kern) {
-                prep(kern, P::smem);
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, P::NT, P::smem);
-                SVH_LAUNCH(kern, std::min(ntiles, nsm * std::max(occ, 1)), P::NT, P::smem, s, in, out, tmap, tmap_in,
-                           h->d_tw[1], nx, h->kz, Lin, Lout, ntiles, tiles_x, h->d_planes, h->nzp, h->d_rowmask,
-                           h->rowMW);
-            };
-            if (tin)
-                go(k_ytma<N, DIR, 2, QQ, true>);
-            else
-                go(k_ytma<N, DIR, 2, QQ, false>);
-            return true;
-        };
-        if constexpr (N == 2048) {
-            if (ytma && ytma2048 && launch(std::integral_constant<int, 4>{})) return;
-        } else {
-            if (ytma && ((yq == 4 && launch(std::integral_constant<int, 4>{})) ||
-                         (yq != 4 && launch(std::integral_constant<int, 8>{}))))
-                return;
-        }
-    }
-    if constexpr (N >= 128 && N <= 1024) {
-        if (((DIR < 0 && (ystage & 1)) || (DIR > 0 && (ystage & 2))) && nx % 8 == 0) {
-            constexpr int QS = 8, SS = DIR < 0 ? 3 : 2;
-            using P = YStage<N, QS, DIR, SS>;
-            const int tiles_x = nx / QS;
-            const int ntiles = tiles_x * h->nzp * 5 * nrhs;
-            int dev = 0, nsm = 148;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-            prep(k_ystage<N, QS, DIR, SS>, P::smem);
-            SVH_LAUNCH((k_ystage<N, QS, DIR, SS>), std::min(ntiles, nsm), P::NT, P::smem, s, in, out, h->d_tw[1],
-                       nx, h->kz, Lin, Lout, ntiles, tiles_x, h->d_planes, h->nzp, h->d_rowmask, h->rowMW);
+            auto kern = k_ytma<N, DIR, 2, QQ>;
+            prep(kern, P::smem);
+            SVH_LAUNCH(kern, persistent_grid(kern, P::NT, P::smem, ntiles), P::NT, P::smem, s, in, out, tmap,
+                       h->d_tw[1], nx, h->kz, Lin, Lout, ntiles, tiles_x, h->d_planes, h->nzp, h->d_rowmask,
+                       h->rowMW);
             return;
         }
     }
-    if constexpr (fft_r2(N) > 1 && Q >= 4 && colpipe_smem<N, 8, DIR>() <= 220 * 1024) {
-        const bool want = use_pipe && (DIR > 0 || pipe_fwd);
-        if (want && nx % 8 == 0) {
-            constexpr int QP = 8;
-            const int tiles_x = nx / QP;
-            const int ntiles = tiles_x * h->nzp * 5 * nrhs;
-            const size_t smem = colpipe_smem<N, QP, DIR>();
-            const int nt = fft_threads_per_pencil(N) * QP;
-            int dev = 0, nsm = 148;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-            int per_sm = (int)std::max<size_t>(1, (220 * 1024) / (smem + 1024));
-            per_sm = std::min(per_sm, std::max(1, 1024 / nt));
-            const int grid = std::min(ntiles, nsm * per_sm);
-            prep(k_col_pipe<N, QP, DIR>, smem);
-            SVH_LAUNCH((k_col_pipe<N, QP, DIR>), grid, nt, smem, s, in, out, h->d_tw[1], nx, h->kz, Lin, Lout,
-                       ntiles, tiles_x, h->d_planes, h->nzp, h->d_rowmask, h->rowMW);
-            return;
-        }
-    }
+    // generic one-tile-per-CTA pass: N <= 64 (one thread per pencil), N = 4096, and grids whose
+    // x extent does not tile (tested by the max-extent and tiny-grid parity tests)
+    constexpr int Q = col_q<N>();
     const int nt = fft_threads_per_pencil(N) * Q;
     const size_t smem = fft_r2(N) == 1 ? 0 : (size_t)em_size<N, Q>() * sizeof(float2);
     dim3 grid((nx + Q - 1) / Q, h->nzp, 5 * nrhs);
@@ -1999,102 +1573,35 @@ void run_pass_c(svh_handle* h, const Geom& g, float2* X2, int nrhs, cudaStream_t
                 return;
         }
     }
-    static const bool zmac = getenv("SVH_ZMAC") == nullptr || atoi(getenv("SVH_ZMAC")) != 0;
     if constexpr (N >= 2 && N <= 32) {
-        if (zmac) {
+        // one thread per (component, pencil) z-FFT in registers, 32 pencils x 5 components per CTA
+        dim3 grid((g.nx + 31) / 32, h->ny);
+        if (sv.spec) {
+            const size_t smem2 = zmac2_smem<N>();
+            prep(k_zmac2<N>, smem2);
+            SVH_LAUNCH((k_zmac2<N>), grid, 160, smem2, s, X2, sv, h->nx, h->ny, h->kz, h->gscale, nrhs,
+                       (uint64_t)h->planemask, g.nx, g.kx0);
+        } else {
             const size_t smem = zmac_smem<N>();
-            dim3 grid((g.nx + 31) / 32, h->ny);
-            static const int probe = getenv("SVH_ZPROBE") ? atoi(getenv("SVH_ZPROBE")) : 0;   // perf probes only
-            if (probe == 1 || probe == 2) {
-                auto kp = probe == 1 ? k_zmac<N, 1> : k_zmac<N, 2>;
-                prep(kp, smem);
-                SVH_LAUNCH(kp, grid, 160, smem, s, X2, sv, h->nx, h->ny, h->kz, h->gscale, nrhs, (uint64_t)h->planemask,
-                           g.nx, g.kx0, 1);
-                return;
-            }
-            static const int zmac2 = getenv("SVH_ZMAC2") ? atoi(getenv("SVH_ZMAC2")) : 1;
-            if constexpr (N == 32) {
-                if (zmac2 == 3 && launch_ztma2<32, 16, 4>(h, g, X2, nrhs, sv, s)) return;
-            }
-            if (zmac2 == 2 && sv.spec && N >= 4) {
-                const size_t smem2 = zmac2_smem<N, true>();
-                prep(k_zmac2<N, true>, smem2);
-                SVH_LAUNCH((k_zmac2<N, true>), grid, 160, smem2, s, X2, sv, h->nx, h->ny, h->kz, h->gscale, nrhs,
-                           (uint64_t)h->planemask, g.nx, g.kx0);
-                return;
-            }
-            if (zmac2 && sv.spec) {
-                const size_t smem2 = zmac2_smem<N>();
-                prep(k_zmac2<N>, smem2);
-                SVH_LAUNCH((k_zmac2<N>), grid, 160, smem2, s, X2, sv, h->nx, h->ny, h->kz, h->gscale, nrhs,
-                           (uint64_t)h->planemask, g.nx, g.kx0);
-                return;
-            }
-            static const int zpre = getenv("SVH_ZPRE") ? atoi(getenv("SVH_ZPRE")) : 1;
             prep(k_zmac<N>, smem);
             SVH_LAUNCH((k_zmac<N>), grid, 160, smem, s, X2, sv, h->nx, h->ny, h->kz, h->gscale, nrhs,
-                       (uint64_t)h->planemask, g.nx, g.kx0, zpre);
-            return;
+                       (uint64_t)h->planemask, g.nx, g.kx0, 1);
         }
+        return;
     }
-    if constexpr (N == 64) {
-        static const int z64 = getenv("SVH_Z64") ? atoi(getenv("SVH_Z64")) : 2;   // 0: k_freq_small (measured 1.8x slower)
-        if (z64 == 2 && launch_ztma2<64, 16, 4>(h, g, X2, nrhs, sv, s)) return;
+    if constexpr (N == 512) {
+        if (launch_ztma2<512, 4, 8>(h, g, X2, nrhs, sv, s)) return;
     }
     if constexpr (N <= 64) {
-        static const int cq = getenv("SVH_CQ") ? atoi(getenv("SVH_CQ")) : 32;
-        static const bool casync = getenv("SVH_CASYNC") != nullptr;
-        auto launch = [&](auto Qc, auto Ac) {
-            constexpr int Q = decltype(Qc)::value;
-            constexpr bool A = decltype(Ac)::value;
-            const size_t smem = freq_small_smem<N, Q, A>();
-            dim3 grid((g.nx + Q - 1) / Q, h->ny);
-            prep(k_freq_small<N, Q, A>, smem);
-            SVH_LAUNCH((k_freq_small<N, Q, A>), grid, 5 * Q, smem, s, X2, sv, h->nx, h->ny, h->kz, h->gscale,
-                       nrhs, (uint64_t)h->planemask, g.nx, g.kx0);
-        };
-        const bool async_ok = casync && g.nx % 32 == 0;
-        if (N >= 64 || cq == 16) {
-            if (async_ok) launch(std::integral_constant<int, 16>{}, std::true_type{});
-            else launch(std::integral_constant<int, 16>{}, std::false_type{});
-        } else {
-            if (async_ok) launch(std::integral_constant<int, 32>{}, std::true_type{});
-            else launch(std::integral_constant<int, 32>{}, std::false_type{});
-        }
+        // N = 1 and x extents that do not tile k_zpass: one thread per (component, pencil)
+        constexpr int Q = N >= 64 ? 16 : 32;
+        const size_t smem = freq_small_smem<N, Q, false>();
+        dim3 grid((g.nx + Q - 1) / Q, h->ny);
+        prep(k_freq_small<N, Q, false>, smem);
+        SVH_LAUNCH((k_freq_small<N, Q, false>), grid, 5 * Q, smem, s, X2, sv, h->nx, h->ny, h->kz, h->gscale, nrhs,
+                   (uint64_t)h->planemask, g.nx, g.kx0);
     } else {
-        static const bool ztma = getenv("SVH_ZTMA") == nullptr || atoi(getenv("SVH_ZTMA")) != 0;
-        static const int zform = getenv("SVH_ZTMA") ? atoi(getenv("SVH_ZTMA")) : 2;
-        if constexpr (N >= 128 && N <= 512) {
-            static const int zq = getenv("SVH_ZQ") ? atoi(getenv("SVH_ZQ")) : 8;
-            constexpr int R2 = N == 128 ? 4 : 8;
-            if (zform == 2) {
-                if constexpr (N == 512) {
-                    if (launch_ztma2<N, 4, R2>(h, g, X2, nrhs, sv, s)) return;
-                } else {
-                    if (zq == 8 ? launch_ztma2<N, 8, R2>(h, g, X2, nrhs, sv, s) : launch_ztma2<N, 4, R2>(h, g, X2, nrhs, sv, s))
-                        return;
-                }
-            }
-        }
-        if constexpr (N >= 128 && N <= 512) {
-            constexpr int QZ = N >= 512 ? 4 : 8;
-            using P = ZTma<N, QZ>;
-            CUtensorMap tmap;
-            if (ztma && sv.spec && g.nx % QZ == 0 &&
-                encode_tmap_c64_3d_box(&tmap, X2, (uint64_t)g.nx, (uint64_t)h->ny, (uint64_t)5 * nrhs * h->kz,
-                                       (uint64_t)g.nx, (uint64_t)g.nx * h->ny, QZ, 1, (uint32_t)h->kz)) {
-                const int tiles_x = g.nx / QZ;
-                const int ntiles = tiles_x * h->ny * nrhs;
-                int dev = 0, nsm = 148, occ = 1;
-                cudaGetDevice(&dev);
-                cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-                prep(k_ztma<N, QZ>, P::smem);
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ztma<N, QZ>, P::NT, P::smem);
-                SVH_LAUNCH((k_ztma<N, QZ>), std::min(ntiles, nsm * std::max(occ, 1)), P::NT, P::smem, s, tmap, sv,
-                           h->d_tw[2], h->nx, h->ny, h->kz, h->gscale, nrhs, ntiles, tiles_x, h->d_planeok, g.kx0);
-                return;
-            }
-        }
+        // generic shared-memory z pass: N >= 1024 and x extents that do not tile
         const int tpp = fft_threads_per_pencil(N);
         int Q = std::min(8, std::max(1, fft_max_threads(N) / (tpp * 5)));   // <= 8: Tucker H tile
         while (Q > 1 && (size_t)N * (5 * Q + 1) * sizeof(float2) > 160 * 1024) Q >>= 1;
@@ -2201,6 +1708,8 @@ int max_chunk(svh_handle* h) {
 // one sub-batch of nr RHS on stream s with workspace slices X1, X2
 static void matvec_batch(svh_handle* h, const float2* in, float2* out, float2* X1, float2* X2, int nr,
                          bool green_only, bool packed, cudaStream_t s) {
+    // SVH_SYNC_DEBUG (debugging aid, include/svh.h): synchronise after every pass and report the
+    // failing pass; it does not change which kernels run
     static const bool dbg = getenv("SVH_SYNC_DEBUG") != nullptr;
     auto tick = [&](int pass, bool begin) {
         if (dbg && !begin) {
@@ -2238,41 +1747,14 @@ static void matvec_batch(svh_handle* h, const float2* in, float2* out, float2* X
 }
 
 void matvec(svh_handle* h, const float2* I, float2* CC, int nrhs, bool green_only, bool packed, cudaStream_t s) {
+    // RHS chunks sized to the workspace budget (max_chunk); every pass fills the GPU on its own,
+    // so the chunks run back to back on the caller's stream
     const int chunk = std::min(nrhs, max_chunk(h));
     ensure_workspace(h, chunk);
     const int64_t per_rhs = 5 * (packed ? h->K : h->Kt);
-    const size_t x1_per = (size_t)5 * h->kz * h->ky * h->nx, x2_per = (size_t)5 * h->kz * h->ny * h->nx;
-    // optional RHS sub-batches on concurrent streams (SVH_STREAMS; measured no gain on B200
-    // for config 4 since every pass already fills the GPU, so the default is 1)
-    static const int nstreams = getenv("SVH_STREAMS") ? std::max(1, atoi(getenv("SVH_STREAMS"))) : 1;
     for (int r0 = 0; r0 < nrhs; r0 += chunk) {
         const int nr = std::min(chunk, nrhs - r0);
-        const int ns = std::min(nstreams, nr);
-        if (ns <= 1) {
-            matvec_batch(h, I + r0 * per_rhs, CC + r0 * per_rhs, h->X1, h->X2, nr, green_only, packed, s);
-            continue;
-        }
-        while ((int)h->streams.size() < ns) {
-            cudaStream_t st;
-            SVH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-            cudaEvent_t ev;
-            SVH_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-            h->streams.push_back(st);
-            h->stream_events.push_back(ev);
-        }
-        if (!h->fork_event) SVH_CUDA(cudaEventCreateWithFlags(&h->fork_event, cudaEventDisableTiming));
-        SVH_CUDA(cudaEventRecord(h->fork_event, s));
-        int off = 0;
-        for (int k = 0; k < ns; ++k) {
-            const int nk = nr / ns + (k < nr % ns ? 1 : 0);
-            cudaStream_t st = h->streams[k];
-            SVH_CUDA(cudaStreamWaitEvent(st, h->fork_event, 0));
-            matvec_batch(h, I + (r0 + off) * per_rhs, CC + (r0 + off) * per_rhs, h->X1 + off * x1_per,
-                         h->X2 + off * x2_per, nk, green_only, packed, st);
-            SVH_CUDA(cudaEventRecord(h->stream_events[k], st));
-            off += nk;
-        }
-        for (int k = 0; k < ns; ++k) SVH_CUDA(cudaStreamWaitEvent(s, h->stream_events[k], 0));
+        matvec_batch(h, I + r0 * per_rhs, CC + r0 * per_rhs, h->X1, h->X2, nr, green_only, packed, s);
     }
 }
 

@@ -830,9 +830,8 @@ int pairwise(const CsrHost& A, std::vector<int>& agg) {
         for (int p = A.rowptr[i]; p < A.rowptr[i + 1]; ++p) {
             const int j = A.col[p];
             if (j == i) continue;
-            static const bool neg = getenv("SVH_AMG_ABS") == nullptr;
-            // strength of connection: negative couplings (AGMG-style), or |a_ij| if SVH_AMG_ABS
-            const double a = neg ? -A.val[p] : std::fabs(A.val[p]);
+            // strength of connection: negative couplings (AGMG-style)
+            const double a = -A.val[p];
             const double s = a / std::sqrt(std::fabs(diag[i] * diag[j]) + 1e-300);
             rowmax = std::max(rowmax, s);
             if (agg[j] < 0 && s > bv) {
@@ -1182,11 +1181,10 @@ static int pcgV(svh_handle* h, const double* b, double* x, double tol, int maxit
     SVH_CUDA(cudaMemcpyAsync(r, b, nd * sizeof(double), cudaMemcpyDeviceToDevice, s));
     kcycle(S, 0, r, z, s, NVP);
     SVH_CUDA(cudaMemcpyAsync(p, z, nd * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    static const bool use_graph = getenv("SVH_NO_PCG_GRAPH") == nullptr;
     cudaGraphExec_t gx = nullptr;
     for (auto& gg : S->pcg_graphs)
         if (gg.first == NVP) gx = gg.second;
-    if (use_graph && !gx && s != nullptr) {
+    if (!gx && s != nullptr) {
         cudaGraph_t g = nullptr;
         SVH_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
         iteration();
@@ -1609,8 +1607,7 @@ static void solve_columns(svh_handle* h, const svh_port* ports, int P, const int
     PortSets ps = port_sets(h, ports, P);
     const int m = std::max(1, h->opts.restart);
     // batched multi-port solve (lockstep FGMRES, one shared PCG): batch size by memory, <= 16
-    static const int batch_env = getenv("SVH_SOLVE_BATCH") ? atoi(getenv("SVH_SOLVE_BATCH")) : 16;
-    int Bmax = std::min(nsel, std::max(1, std::min(16, batch_env)));
+    int Bmax = std::min(nsel, 16);
     if (Bmax > 1) {
         ensure_structure(h);
         size_t fr = 0, tt = 0;

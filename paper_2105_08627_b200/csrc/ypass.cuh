@@ -1,6 +1,6 @@
 // Strided passes B (forward y-FFT, zero-padded) and D (inverse y-FFT, cropped) of the matvec
 // (Eq. 9) for Ny = 1024 / 2048: the Stockham radix-16 FFT of rowfft.cuh applied to Q
-// pencils at once.
+// pencils at once.  Dispatched for the inverse 2048-point pass (matvec.cu run_pass_y).
 //
 // Tile = Q consecutive kx of one non-empty plane p = rc Kz + z.  Its input rows (B: the Ky rows
 // of X1, D: the Ny rows of X2) stream HBM -> shared memory by TMA (cp.async.bulk.tensor, box
