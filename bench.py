@@ -271,6 +271,10 @@ def cufft_reference(h, case, R, reps=3):
     import torch
     kz, ky, kx = h.shape
     nx, ny, nz = h.embedding
+    occ = torch.from_numpy(case["mat_id"] != 0).cuda()
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    I = torch.randn((5, kz, ky, kx), dtype=torch.complex64, device="cuda", generator=gen) * occ
+    ours = h.matvec_grid(I[None], green_only=True)[0]   # before the full-grid spectra take the memory
     K = torch.from_numpy(h.kernels()).cuda()            # fp64 [7][kz][ky][kx], m >= 0
     odd = [None, 2, 1, 0, None, None, None]             # K1x odd along x (tensor dim 2), ...
     spec = []
@@ -289,18 +293,23 @@ def cufft_reference(h, case, R, reps=3):
         spec.append(torch.fft.fftn(e).to(torch.complex64))
     w = 2 * np.pi * case["freq"]
     g = 1j * w * 4e-7 * np.pi * case["dx"]
-    occ = torch.from_numpy(case["mat_id"] != 0).cuda()
-    I = torch.randn((5, kz, ky, kx), dtype=torch.complex64, device="cuda") * occ
+    del K
 
     def one():
+        # component by component so the 2048^2 x 128 embedding fits next to the 7 spectra
         Ih = torch.fft.fftn(torch.nn.functional.pad(I, (0, nx - kx, 0, ny - ky, 0, nz - kz)), dim=(1, 2, 3))
-        m1 = [Ih[3] + Ih[4], Ih[4] - Ih[3], -2 * Ih[4]]
-        P0 = [spec[0] * Ih[c] + spec[1 + c] * m1[c] for c in range(3)]
-        P1 = [-spec[1 + c] * Ih[c] + spec[4 + c] * m1[c] for c in range(3)]
-        out = torch.stack(P0 + [P1[0] - P1[1], P1[0] + P1[1] - 2 * P1[2]])
-        return (g * torch.fft.ifftn(out, dim=(1, 2, 3)))[:, :kz, :ky, :kx]
+        res = torch.empty((5, kz, ky, kx), dtype=torch.complex64, device="cuda")
+        P1 = []
+        for c in range(3):
+            m1 = Ih[3] + Ih[4] if c == 0 else (Ih[4] - Ih[3] if c == 1 else -2 * Ih[4])
+            res[c] = (g * torch.fft.ifftn(spec[0] * Ih[c] + spec[1 + c] * m1))[:kz, :ky, :kx]
+            P1.append(-spec[1 + c] * Ih[c] + spec[4 + c] * m1)
+            del m1
+        del Ih
+        res[3] = (g * torch.fft.ifftn(P1[0] - P1[1]))[:kz, :ky, :kx]
+        res[4] = (g * torch.fft.ifftn(P1[0] + P1[1] - 2 * P1[2]))[:kz, :ky, :kx]
+        return res
     ref = one()
-    ours = h.matvec_grid(I[None], green_only=True)[0]
     rel = float(torch.linalg.norm((ref - ours)[:, occ]) / torch.linalg.norm(ours[:, occ]))
     del ref, ours
     torch.cuda.synchronize()
@@ -310,7 +319,7 @@ def cufft_reference(h, case, R, reps=3):
         one()
     e1.record()
     torch.cuda.synchronize()
-    del spec, K
+    del spec, I, occ
     torch.cuda.empty_cache()
     return e0.elapsed_time(e1) / reps, rel
 
@@ -503,18 +512,26 @@ def main():
 
     # ---- roofline of the dominant kernel (live per-pass CUDA events) ----
     peaks, peak_src = load_peaks()
-    pb = pass_bytes(h, R)
-    per_launch_ms = pass_ms / np.maximum(pass_n, 1)
-    dom = int(np.argmax(per_launch_ms))
+    # bytes and device time of each pass summed over the timed region (a step may run its RHS
+    # in several workspace chunks, i.e. several launches per pass)
+    pb = np.array(pass_bytes(h, R), dtype=np.float64)
+    pass_ms = np.asarray(pass_ms, dtype=np.float64)[:5]
+    pass_n = np.maximum(np.asarray(pass_n)[:5], 1)
+    per_launch_ms = pass_ms / pass_n
+    per_launch_bytes = pb * args.steps / pass_n
+    dom = int(np.argmax(pass_ms))
     names = ["A_x_fwd", "B_y_fwd", "C_z_mac", "D_y_inv", "E_x_inv"]
-    achieved = pb[dom] / (per_launch_ms[dom] / 1e3) / 1e9
+    achieved = per_launch_bytes[dom] / (per_launch_ms[dom] / 1e3) / 1e9
     peak = float(peaks["hbm_gbs"])
     matvec_bytes = sum(pb)
     roof = {"bound": "hbm", "kernel": names[dom], "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
-            "algorithmic_bytes_per_launch": int(pb[dom]),
-            "share_of_step": round(float(per_launch_ms[dom] / per_launch_ms.sum()), 4),
-            "passes_ms": {n: round(float(x), 4) for n, x in zip(names, per_launch_ms)},
+            "algorithmic_bytes_per_launch": int(per_launch_bytes[dom]),
+            "launches_per_step": int(pass_n[dom] // args.steps),
+            "share_of_step": round(float(pass_ms[dom] / pass_ms.sum()), 4),
+            "passes_ms_per_step": {n: round(float(x) / args.steps, 4) for n, x in zip(names, pass_ms)},
+            "passes_frac": {n: round(float(b) / (float(x) / args.steps / 1e3) / 1e9 / float(peaks["hbm_gbs"]), 4)
+                            for n, b, x in zip(names, pb, pass_ms)},
             "whole_matvec": {"bytes": int(matvec_bytes),
                              "achieved_GBs": round(matvec_bytes / (ms / 1e3) / 1e9, 1),
                              "frac": round(matvec_bytes / (ms / 1e3) / 1e9 / peak, 4)}}

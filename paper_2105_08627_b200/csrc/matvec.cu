@@ -1532,26 +1532,26 @@ void run_pass_c(svh_handle* h, const Geom& g, float2* X2, int nrhs, cudaStream_t
         if (h->use_tucker)
             for (int m = 0; m < 7; ++m)
                 for (int a = 0; a < 3; ++a) dmax = std::max(dmax, sv.rk[m][a]);
+        const bool fits = dmax <= kTuckerMaxRank;
         // plans: (R2, Q, threads): every thread runs TL1 = 5 R2 Q / threads L1 tasks and at most one
-        // L2 task; T double-buffered when shared memory allows
+        // L2 task.  Dense spectra: T double-buffered; Tucker: one T buffer, the freed shared memory
+        // holds the mode-3 factor rows and the expansion scratch (rank bucket 16 / 32)
         auto launch = [&](auto R2c, auto Qc, auto NTc) -> bool {
             constexpr int R2 = decltype(R2c)::value, Q = decltype(Qc)::value, NT = decltype(NTc)::value;
             using P = ZPlan<N, R2, Q, NT>;
-            if (g.nx % Q != 0) return false;
-            const int nbuf = P::smem(dmax, 2) <= 227 * 1024 ? 2 : 1;
-            const size_t smem = P::smem(dmax, nbuf);
-            if (smem > 227 * 1024) return false;
+            if (g.nx % Q != 0 || !fits) return false;
             const int64_t units = (int64_t)(h->ny / 2 + 1) * (g.nx / Q);
-            auto go = [&](auto kern) {
+            auto go = [&](auto kern, size_t smem) -> bool {
+                if (smem > 227 * 1024) return false;
                 prep(kern, smem);
                 SVH_LAUNCH(kern, persistent_grid(kern, NT, smem, units), NT, smem, s, X2, sv, h->d_tw[2], h->nx,
-                           h->ny, h->kz, g.nx, g.kx0, h->gscale, nrhs, h->d_planeok, dmax);
+                           h->ny, h->kz, g.nx, g.kx0, h->gscale, nrhs, h->d_planeok);
+                return true;
             };
-            if (nbuf == 2)
-                go(k_zpass<N, R2, Q, NT, 2>);
-            else
-                go(k_zpass<N, R2, Q, NT, 1>);
-            return true;
+            if (!h->use_tucker)
+                return go(k_zpass<N, R2, Q, NT, 2, 0>, P::smem(2, 0)) || go(k_zpass<N, R2, Q, NT, 1, 0>, P::smem(1, 0));
+            if (dmax <= 16) return go(k_zpass<N, R2, Q, NT, 1, 16>, P::smem(1, 16));
+            return go(k_zpass<N, R2, Q, NT, 1, 32>, P::smem(1, 32));
         };
         if constexpr (N == 128) {
             if (launch(std::integral_constant<int, 8>{}, std::integral_constant<int, 16>{},
@@ -1747,9 +1747,12 @@ static void matvec_batch(svh_handle* h, const float2* in, float2* out, float2* X
 }
 
 void matvec(svh_handle* h, const float2* I, float2* CC, int nrhs, bool green_only, bool packed, cudaStream_t s) {
-    // RHS chunks sized to the workspace budget (max_chunk); every pass fills the GPU on its own,
-    // so the chunks run back to back on the caller's stream
-    const int chunk = std::min(nrhs, max_chunk(h));
+    // RHS chunks sized to the workspace budget (max_chunk) and balanced (8 RHS with room for 7
+    // run as 4 + 4, not 7 + 1); every pass fills the GPU on its own, so the chunks run back to
+    // back on the caller's stream
+    const int maxc = std::max(1, std::min(nrhs, max_chunk(h)));
+    const int nch = (nrhs + maxc - 1) / maxc;
+    const int chunk = (nrhs + nch - 1) / nch;
     ensure_workspace(h, chunk);
     const int64_t per_rhs = 5 * (packed ? h->K : h->Kt);
     for (int r0 = 0; r0 < nrhs; r0 += chunk) {

@@ -23,6 +23,10 @@
 
 namespace svh {
 
+// largest Tucker rank the on-chip expansion handles (ranks of the 7 kernels, SURVEY 8(c) P15:
+// 10-21 for tol 1e-4 .. 1e-10); higher ranks take the generic z pass (k_freq_big)
+constexpr int kTuckerMaxRank = 32;
+
 struct SpecView {
     const float* spec;   // dense [7][hz][hy][hx]; null in Tucker mode
     int hx, hy, hz;
@@ -43,28 +47,31 @@ struct ZPlan {
     static constexpr int TE = 5 * R2 * TB;                // elements of one T buffer
     static constexpr int KVS = 8;                         // floats per (kh, q) entry of KV (7 used)
     static constexpr size_t KV_b = (size_t)NK * Q * KVS * sizeof(float);
-    // T (double-buffered when it fits) | KV [NK][Q][8] | Tucker scratch G [7][d3][d1], H [7][Q][d3]
-    static size_t smem(int dmax, int nbuf) {
-        return (size_t)nbuf * TE * sizeof(float2) + KV_b + (size_t)7 * dmax * dmax * sizeof(float) +
-               (size_t)7 * Q * dmax * sizeof(float);
+    // T (double-buffered in dense mode) | KV [NK][Q][8] | Tucker (rank bucket DM > 0): the
+    // mode-3 factor rows F3 [7][NK][DM], G [7][DM][DM + 1], H [7][Q][DM + 1] (zero-padded to DM)
+    static constexpr size_t smem(int nbuf, int DM) {
+        return (size_t)nbuf * TE * sizeof(float2) + KV_b +
+               (DM ? ((size_t)7 * NK * DM + (size_t)7 * DM * (DM + 1) + (size_t)7 * Q * (DM + 1)) * sizeof(float) : 0);
     }
 };
 
-// NBUF = 2: T double-buffered (two barriers per tile); 1: single buffer (three barriers)
-template <int N, int R2, int Q, int NT, int NBUF>
+// NBUF = 2: T double-buffered (two barriers per tile); 1: single buffer (three barriers).
+// DM = 0: dense octant spectra; 16 / 32: Tucker factors, ranks <= DM (zero-padded on chip).
+template <int N, int R2, int Q, int NT, int NBUF, int DM>
 __global__ void __launch_bounds__(NT, 1)
     k_zpass(float2* __restrict__ X2, SpecView sv, const float2* __restrict__ tw, int Nx, int Ny, int Kz, int Nxs,
-            int kxg, float g, int nrhs, const uint8_t* __restrict__ planeok, int dmax) {
+            int kxg, float g, int nrhs, const uint8_t* __restrict__ planeok) {
     using P = ZPlan<N, R2, Q, NT>;
     constexpr int R1 = P::R1, NK = P::NK, TB = P::TB, TE = P::TE, TL1 = P::TL1, NL2 = P::NL2, KVS = P::KVS;
+    constexpr int DP = DM + 1;   // padded row of G / H (conflict-free column reads)
     extern __shared__ __align__(16) unsigned char smraw[];
     float2* T = reinterpret_cast<float2*>(smraw);                                 // [NBUF][5][R2][TB]
     float* KV = reinterpret_cast<float*>(smraw + (size_t)NBUF * TE * sizeof(float2));   // [NK][Q][8]
-    float* G = KV + NK * Q * KVS;                                                 // [7][d3][d1]
-    float* H = G + 7 * dmax * dmax;                                               // [7][Q][d3]
+    float* F3s = KV + NK * Q * KVS;                                               // [7][NK][DM]
+    float* G = F3s + 7 * NK * DM;                                                 // [7][DM][DP]
+    float* H = G + 7 * DM * DP;                                                   // [7][Q][DP]
     const int tid = threadIdx.x;
     const float2 zero = make_float2(0.f, 0.f);
-    const bool tucker = sv.spec == nullptr;
     const int64_t plane = (int64_t)Nxs * Ny;
     const int tiles_x = Nxs / Q;
     const int nunits = (Ny / 2 + 1) * tiles_x;
@@ -95,6 +102,14 @@ __global__ void __launch_bounds__(NT, 1)
     float2 w2[R2];
 #pragma unroll
     for (int m = 0; m < R2; ++m) w2[m] = l2 ? __ldg(&tw[(m * k1) & (N - 1)]) : zero;
+    if constexpr (DM > 0) {
+        // the mode-3 factor rows of the octant (kh <= N/2) are the same for every unit: on chip once
+        for (int e = tid; e < 7 * NK * DM; e += NT) {
+            const int m = e / (NK * DM), rest = e - m * NK * DM, kh = rest / DM, c = rest - kh * DM;
+            const int d3 = sv.rk[m][2];
+            F3s[e] = c < d3 ? __ldg(&sv.fac[m][2][(int64_t)kh * d3 + c]) : 0.f;
+        }
+    }
     auto unit_rows = [&](int u) { const int oy = u / tiles_x; return (oy == 0 || 2 * oy == Ny) ? 1 : 2; };
     // tile (u, i) -> element offset of (r, c = 0, z = 0, ky, xt * Q)
     auto tile_base = [&](int u, int i, int& ky, int& xt, int& r) -> int64_t {
@@ -128,58 +143,57 @@ __global__ void __launch_bounds__(NT, 1)
         const int oy = u / tiles_x;
         if (i == 0) {
             // the unit's raw kernel spectra KV[kh][q][m] (the previous tile's L2 finished at its barrier)
-            if (tucker) {
+            if constexpr (DM > 0) {
                 if (oy != cur_oy) {
-                    // G_m = core_m x2 F2_m[oy]   ([d3][d1], once per oy)
-                    for (int m = 0; m < 7; ++m) {
+                    // G_m = core_m x2 F2_m[oy]   ([c3][c1], once per oy; zero outside the ranks)
+                    __syncthreads();   // (first unit: F3s; later: the previous unit's H reads of G)
+                    for (int t = tid; t < 7 * DM * DM; t += NT) {
+                        const int m = t / (DM * DM), rest = t - m * DM * DM, c3 = rest / DM, c1 = rest - c3 * DM;
                         const int d1 = sv.rk[m][0], d2 = sv.rk[m][1], d3 = sv.rk[m][2];
-                        const float* C = sv.core[m];
-                        const float* F2 = sv.fac[m][1] + (int64_t)oy * d2;
-                        for (int t = tid; t < d3 * d1; t += NT) {
-                            const int c3 = t / d1, cc1 = t % d1;
-                            const float* cp = C + (int64_t)c3 * d2 * d1 + cc1;
-                            float acc = 0.f;
+                        float acc = 0.f;
+                        if (c3 < d3 && c1 < d1) {
+                            const float* cp = sv.core[m] + (int64_t)c3 * d2 * d1 + c1;
+                            const float* F2 = sv.fac[m][1] + (int64_t)oy * d2;
                             for (int cc2 = 0; cc2 < d2; ++cc2) acc = fmaf(__ldg(&cp[cc2 * d1]), __ldg(&F2[cc2]), acc);
-                            G[m * dmax * dmax + t] = acc;
                         }
+                        G[(m * DM + c3) * DP + c1] = acc;
                     }
                     cur_oy = oy;
-                    __syncthreads();
                 }
-                // H_m[q] = G_m x1 F1_m[ox_q]   ([Q][d3]); the kernel index m is the outer, uniform loop
-                // so the rank, the factor pointers and the index split stay out of the inner loops
-#pragma unroll 1
-                for (int m = 0; m < 7; ++m) {
-                    const int d1 = sv.rk[m][0], d3 = sv.rk[m][2];
-                    const float* F1 = sv.fac[m][0];
-                    const float* Gm = G + m * dmax * dmax;
-                    float* Hm = H + m * Q * dmax;
-                    for (int t = tid; t < Q * d3; t += NT) {
-                        const int q = t / d3, c3 = t - q * d3;
-                        const int kx = kxg + xt * Q + q;
-                        const int ox = kx <= (Nx >> 1) ? kx : Nx - kx;
-                        const float* f1 = F1 + (int64_t)ox * d1;
-                        const float* gm = Gm + c3 * d1;
-                        float acc = 0.f;
+                __syncthreads();
+                // H_m[q] = G_m x1 F1_m[ox_q]: one task per (m, q), the factor row in registers
+                for (int t = tid; t < 7 * Q; t += NT) {
+                    const int m = t / Q, q = t - m * Q;
+                    const int d1 = sv.rk[m][0];
+                    const int kx = kxg + xt * Q + q;
+                    const int ox = kx <= (Nx >> 1) ? kx : Nx - kx;
+                    const float* f1 = sv.fac[m][0] + (int64_t)ox * d1;
+                    float fr[DM];
+#pragma unroll
+                    for (int c = 0; c < DM; ++c) fr[c] = c < d1 ? __ldg(&f1[c]) : 0.f;
+                    const float* Gm = G + m * DM * DP;
+                    float* hq = H + (m * Q + q) * DP;
 #pragma unroll 4
-                        for (int cc1 = 0; cc1 < d1; ++cc1) acc = fmaf(gm[cc1], __ldg(&f1[cc1]), acc);
-                        Hm[q * dmax + c3] = acc;
+                    for (int c3 = 0; c3 < DM; ++c3) {
+                        float acc = 0.f;
+#pragma unroll
+                        for (int c = 0; c < DM; ++c) acc = fmaf(Gm[c3 * DP + c], fr[c], acc);
+                        hq[c3] = acc;
                     }
                 }
                 __syncthreads();
-                // KV[kh][q][m] = H_m[q] . F3_m[kh]
+                // KV[kh][q][m] = F3_m[kh] . H_m[q]   (lanes run over q; both rows on chip)
 #pragma unroll 1
                 for (int m = 0; m < 7; ++m) {
-                    const int d3 = sv.rk[m][2];
-                    const float* F3 = sv.fac[m][2];
-                    const float* Hm = H + m * Q * dmax;
+                    const float* F3m = F3s + m * NK * DM;
+                    const float* Hm = H + m * Q * DP;
                     for (int t = tid; t < NK * Q; t += NT) {
                         const int q = t % Q, kh = t / Q;
-                        const float* f3 = F3 + kh * d3;
-                        const float* hm = Hm + q * dmax;
+                        const float* f3 = F3m + kh * DM;
+                        const float* hq = Hm + q * DP;
                         float acc = 0.f;
-#pragma unroll 4
-                        for (int c3 = 0; c3 < d3; ++c3) acc = fmaf(hm[c3], __ldg(&f3[c3]), acc);
+#pragma unroll
+                        for (int c = 0; c < DM; ++c) acc = fmaf(f3[c], hq[c], acc);
                         KV[t * KVS + m] = acc;
                     }
                 }

@@ -102,3 +102,27 @@ def test_floating_conductor_grounded():
     r = run(case)
     L_ref, _ = bar_closed_form(8, 1, 1, 0.25e-6, 0.0, 90e-9, 10e9)
     assert abs(r["L"][0, 0] - L_ref) < 0.05 * L_ref
+
+
+def test_iterative_oracle_equals_dense():
+    """solve_ports_iterative (GMRES + Eq. 12-15 Schur preconditioner + direct-sum Z, the oracle
+    used for config-2 golden values) reproduces the dense LU oracle (itself pinned by the P8-P13
+    closed forms) on a 2-port conductor and a non-uniform bar."""
+    import svh_inputs
+    from oracle.solve import solve_ports, solve_ports_iterative
+    mat = np.zeros((3, 6, 14), np.uint8)
+    mat[0, :, :] = 1
+    mat[2, 1:5, 2:12] = 2
+    mat[1, 2:4, 2:4] = 2
+    mat[0, 2:4, 6:8] = 0
+    ports = [{"plus": [(0, -1, (0, 0, 0), (1, 6, 1))], "minus": [(0, +1, (13, 0, 0), (14, 6, 1))]},
+             {"plus": [(0, +1, (11, 1, 2), (12, 5, 3))], "minus": [(0, +1, (13, 0, 0), (14, 6, 1))]}]
+    cases = [dict(mat_id=mat, dx=0.2e-6, materials=[(1.7e7, 90e-9), (0.0, 150e-9)], freq=5e9, ports=ports),
+             svh_inputs.bar(12, 3, 3, dx=0.25e-6, material=(0.0, 90e-9))]
+    for case in cases:
+        lat = Lattice(case["mat_id"])
+        w = 2 * np.pi * case["freq"]
+        ref = solve_ports(lat, case["materials"], w, case["dx"], case["ports"])
+        it = solve_ports_iterative(lat, case["materials"], w, case["dx"], case["ports"], rtol=1e-11)
+        assert all(i["code"] == 0 and i["rre"] < 1e-10 for i in it["info"]), it["info"]
+        assert np.max(np.abs(it["L"] - ref["L"])) < 1e-8 * np.max(np.abs(ref["L"]))
