@@ -84,6 +84,10 @@ typedef struct {
     int32_t verbose;      /* 0 quiet */
     const char* kernel_cache;  /* NULL: kernels by quadrature; else an SVXT file (svh_kernel_cache_build):
                                   the grid's Toeplitz tensors are restored from it (Alg. 2) */
+    int32_t plan;         /* matvec plan: 0 = auto = 5 = P5 (x | y | fused z | y | x, the only
+                             plan built); any other value -> SVH_EINVAL */
+    int32_t precision;    /* matvec arithmetic: 0 = complex64 (the only precision built; Krylov vectors are
+                             fp64); 1 = complex128 -> SVH_EINVAL (not built) */
 } svh_opts;
 
 typedef struct {

@@ -236,6 +236,17 @@ int svh_setup(const svh_grid* grid, const uint8_t* mat_id, const svh_material* m
             SVH_CHECK(!(std::isinf(mats[m].lambda_L_m) && mats[m].sigma_n_S_per_m <= 0), SVH_EINVAL,
                       "normal conductor needs sigma_n > 0");
         }
+        svh_opts o;
+        if (opts)
+            o = *opts;
+        else
+            svh_default_opts(&o);
+        // the Hessenberg column of FGMRES lives in a fixed 4096-double device scratch
+        // (solve.cu: 16 + 2 (restart + 1) doubles)
+        SVH_CHECK(o.restart >= 1 && o.restart <= 2039, SVH_EINVAL, "restart must be in 1..2039");
+        SVH_CHECK(o.tucker_tol >= 0 && o.tucker_tol < 1, SVH_EINVAL, "tucker_tol must be in [0, 1)");
+        SVH_CHECK(o.plan == 0 || o.plan == 5, SVH_EINVAL, "only the P5 matvec plan is built (plan 0 / 5)");
+        SVH_CHECK(o.precision == 0, SVH_EINVAL, "only the complex64 matvec is built (precision 0)");
         auto t0 = std::chrono::steady_clock::now();
         SVH_CUDA(cudaSetDevice(device));
         svh_handle* h = new svh_handle();
@@ -246,14 +257,7 @@ int svh_setup(const svh_grid* grid, const uint8_t* mat_id, const svh_material* m
             h->kz = grid->kz;
             h->dx = grid->dx_m;
             h->Kt = (int64_t)h->kx * h->ky * h->kz;
-            if (opts)
-                h->opts = *opts;
-            else
-                svh_default_opts(&h->opts);
-            // the Hessenberg column of FGMRES lives in a fixed 4096-double device scratch
-            // (solve.cu: 16 + 2 (restart + 1) doubles)
-            SVH_CHECK(h->opts.restart >= 1 && h->opts.restart <= 2039, SVH_EINVAL, "restart must be in 1..2039");
-            SVH_CHECK(h->opts.tucker_tol >= 0 && h->opts.tucker_tol < 1, SVH_EINVAL, "tucker_tol must be in [0, 1)");
+            h->opts = o;
             h->mats.assign(mats, mats + n_mat);
             h->h_mat.assign(mat_id, mat_id + h->Kt);
             for (int64_t c = 0; c < h->Kt; ++c)

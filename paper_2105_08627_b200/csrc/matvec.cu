@@ -1437,23 +1437,26 @@ template <int N, int DIR>
 void run_pass_y(svh_handle* h, const Geom& g, const float2* in, float2* out, int Lin, int Lout, int nrhs,
                 cudaStream_t s) {
     const int nx = g.nx;
-    if constexpr (N == 2048 && DIR > 0) {
-        // inverse 2048-point pencils: Stockham radix-16, TMA-staged input (ypass.cuh); measured
-        // 55 -> 34 ms on the 1024^2 x 64 grid (8 RHS).  For the forward pass and for 1024 points
-        // k_ytma (TMA-stored output tiles) measured faster (B 37.7 vs 43.9 ms; cfg4 B/D 3.2/2.4 vs
-        // 4.2/3.1 ms), so it stays the default there.
-        constexpr int Q = N == 2048 ? 4 : 8;
+    if constexpr (N == 2048) {
+        // 2048-point pencils: Stockham radix-16, TMA-staged input, TMA-stored output (B)
+        // (ypass.cuh).  For N <= 1024, k_ytma measured faster (cfg4 B/D 3.2/2.4 vs 4.2/3.1 ms).
+        constexpr int Q = 4;
         using P = YPlan<N, Q, DIR>;
-        CUtensorMap tin;
+        CUtensorMap tin, tout;
         const int rows_in = DIR < 0 ? h->ky : h->ny;
-        if (nx % Q == 0 && encode_tmap_c64_3d(&tin, in, (uint64_t)nx, (uint64_t)rows_in, (uint64_t)5 * nrhs * h->kz,
-                                              (uint64_t)nx, (uint64_t)nx * rows_in, Q, P::BOX)) {
+        const float2* x2 = DIR < 0 ? out : in;   // the X2 side of the pass
+        if (nx % Q == 0 &&
+            encode_tmap_c64_3d(&tin, in, (uint64_t)nx, (uint64_t)rows_in, (uint64_t)5 * nrhs * h->kz, (uint64_t)nx,
+                               (uint64_t)nx * rows_in, Q, P::BOX) &&
+            encode_tmap_c64_3d(&tout, x2, (uint64_t)nx, (uint64_t)h->ny, (uint64_t)5 * nrhs * h->kz, (uint64_t)nx,
+                               (uint64_t)nx * h->ny, Q, P::BOX)) {
             const int tiles_x = nx / Q;
             const int ntiles = tiles_x * h->nzp * 5 * nrhs;
             auto kern = k_ypass<N, Q, DIR>;
             prep(kern, P::smem);
-            SVH_LAUNCH(kern, persistent_grid(kern, P::NT, P::smem, ntiles), P::NT, P::smem, s, out, tin, h->d_tw[1],
-                       nx, h->kz, Lin, Lout, ntiles, tiles_x, h->d_planes, h->nzp, h->d_rowmask, h->rowMW);
+            SVH_LAUNCH(kern, persistent_grid(kern, P::NT, P::smem, ntiles), P::NT, P::smem, s, out, tin, tout,
+                       h->d_tw[1], nx, h->kz, Lin, Lout, ntiles, tiles_x, h->d_planes, h->nzp, h->d_rowmask,
+                       h->rowMW);
             return;
         }
     }

@@ -114,48 +114,64 @@ __global__ void __launch_bounds__(RowPlan<N>::NT, RowPlan<N>::MINB)
     for (int r = 0; r < 16; ++r) w1[r] = NS == 3 ? tw_at<-1>(tw, ((j & 15) * r * (N / 256)) & (N - 1)) : zero;
     const int groups = (nlist + RPC - 1) / RPC;
     const int total = groups * nrc;
-    auto row_at = [&](int u, int& rc) -> int {
-        rc = u / groups;
+    // bookkeeping loads (row list -> row-occupancy words) run two units ahead and are consumed
+    // one iteration after issue: no dependent L2 latency on the critical path of a row
+    auto row_load = [&](int u) -> int {
+        if (u >= total) return -1;
+        const int rc = u / groups;
         const int li = (u - rc * groups) * RPC + q;
         return li < nlist ? __ldg(&rowlist[li]) : -1;
     };
-    auto seg_of = [&](int row) -> int2 {
-        if (row < 0) return make_int2(0, 0);
-        if (PACKED) return row_segment(rowinfo, W, row);
-        return make_int2(((row / Ky) * Kyl + row % Ky - y0) * Kx, Kx);
+    auto seg_load = [&](int row, int& pre, int& nxt) {
+        if (row < 0) {
+            pre = nxt = 0;
+        } else if (PACKED) {
+            pre = __ldg(&rowinfo[(int64_t)row * W]).y;
+            nxt = __ldg(&rowinfo[(int64_t)(row + 1) * W]).y;
+        } else {
+            pre = ((row / Ky) * Kyl + row % Ky - y0) * Kx;
+            nxt = pre + Kx;
+        }
     };
-    // issue the copies of unit u (its row of this thread group) into slot b
-    auto issue = [&](int u, int2 sg, int b) {
-        if (u < total) {
-            int rc;
-            const int row = row_at(u, rc);
-            if (row >= 0) {
-                unsigned char* sl = slots + b * SL::A_b;
-                int2* RI = reinterpret_cast<int2*>(sl);
-                float2* V = reinterpret_cast<float2*>(sl + SL::W * 8);
-                if (PACKED)
-                    for (int e = j; e < W; e += T) cpa8(&RI[e], &rowinfo[(int64_t)row * W + e]);
-                const float2* src = in + (PACKED ? (int64_t)rc * K : (int64_t)rc * Kt) + sg.x;
-                for (int e = j; e < sg.y; e += T) cpa8(&V[e], &src[e]);
-            }
+    // issue the copies of unit u (row `row`, packed segment [pre, pre + cnt)) into slot b
+    auto issue = [&](int u, int row, int pre, int cnt, int b) {
+        if (row >= 0) {
+            const int rc = u / groups;
+            unsigned char* sl = slots + b * SL::A_b;
+            int2* RI = reinterpret_cast<int2*>(sl);
+            float2* V = reinterpret_cast<float2*>(sl + SL::W * 8);
+            if (PACKED)
+                for (int e = j; e < W; e += T) cpa8(&RI[e], &rowinfo[(int64_t)row * W + e]);
+            const float2* src = in + (PACKED ? (int64_t)rc * K : (int64_t)rc * Kt) + pre;
+            for (int e = j; e < cnt; e += T) cpa8(&V[e], &src[e]);
         }
         cpa_commit();
     };
+    const int G = gridDim.x;
     int u = blockIdx.x;
-    int rc0;
-    int2 sg_cur = seg_of(u < total ? row_at(u, rc0) : -1);
-    issue(u, sg_cur, 0);
-    int2 sg_next = seg_of(u + (int)gridDim.x < total ? row_at(u + gridDim.x, rc0) : -1);
-    for (int k = 0; u < total; ++k, u += gridDim.x) {
-        const int un = u + gridDim.x;
-        issue(un, sg_next, (k + 1) & 1);
-        const int2 sg = sg_cur;
-        sg_cur = sg_next;
-        sg_next = seg_of(un + (int)gridDim.x < total ? row_at(un + gridDim.x, rc0) : -1);
+    int row0 = row_load(u), pre0, nxt0;
+    seg_load(row0, pre0, nxt0);
+    issue(u, row0, pre0, nxt0 - pre0, 0);
+    int row1 = row_load(u + G), pre1, nxt1;
+    seg_load(row1, pre1, nxt1);
+    int row2 = row_load(u + 2 * G);
+    for (int k = 0; u < total; ++k, u += G) {
+        issue(u + G, row1, pre1, nxt1 - pre1, (k + 1) & 1);
+        int pre2, nxt2;
+        seg_load(row2, pre2, nxt2);
+        const int row3 = row_load(u + 3 * G);
+        const int row = row0;
+        const int2 sg = make_int2(pre0, nxt0 - pre0);
+        row0 = row1;
+        pre0 = pre1;
+        nxt0 = nxt1;
+        row1 = row2;
+        pre1 = pre2;
+        nxt1 = nxt2;
+        row2 = row3;
+        const int rc = u / groups;
         cpa_wait1();
         __syncthreads();
-        int rc;
-        const int row = row_at(u, rc);
         const int lrow = row >= 0 ? (row / Ky) * Kyl + row % Ky - y0 : 0;
         const unsigned char* sl = slots + (k & 1) * SL::A_b;
         const int2* RI = reinterpret_cast<const int2*>(sl);
@@ -278,75 +294,83 @@ __global__ void __launch_bounds__(RowPlan<N>::NT, RowPlan<N>::MINB)
     for (int r = 0; r < 16; ++r) w1[r] = NS == 3 ? tw_at<+1>(tw, ((j & 15) * r * (N / 256)) & (N - 1)) : zero;
     const int groups = (nlist + RPC - 1) / RPC;
     const int total = groups * nrc;
-    auto row_at = [&](int u, int& rc) -> int {
-        rc = u / groups;
+    // bookkeeping loads (row list -> row-occupancy words / row mask) run two units ahead and
+    // are consumed one iteration after issue (no dependent L2 latency on a row's critical path)
+    auto row_load = [&](int u) -> int {
+        if (u >= total) return -1;
+        const int rc = u / groups;
         const int li = (u - rc * groups) * RPC + q;
         if (li >= nlist) return -1;
         return rowlist ? __ldg(&rowlist[li]) : (li / Kyl) * Ky + y0 + li % Kyl;
     };
-    auto is_live = [&](int row) -> bool {
-        if (row < 0) return false;
-        if (rowlist) return true;
-        const int z = row / Ky, y = row % Ky;
-        return (__ldg(&rowmask[(int64_t)z * rowMW + (y >> 5)]) >> (y & 31)) & 1u;
+    auto seg_load = [&](int row, int& pre, int& nxt, uint32_t& lw) {
+        lw = 0;
+        if (row < 0) {
+            pre = nxt = 0;
+            return;
+        }
+        if (PACKED) {
+            pre = __ldg(&rowinfo[(int64_t)row * W]).y;
+            nxt = __ldg(&rowinfo[(int64_t)(row + 1) * W]).y;
+        } else {
+            pre = ((row / Ky) * Kyl + row % Ky - y0) * Kx;
+            nxt = pre + Kx;
+        }
+        lw = rowlist ? 1u : (__ldg(&rowmask[(int64_t)(row / Ky) * rowMW + ((row % Ky) >> 5)]) >> ((row % Ky) & 31));
     };
-    auto seg_of = [&](int row) -> int2 {
-        if (row < 0) return make_int2(0, 0);
-        if (PACKED) return row_segment(rowinfo, W, row);
-        return make_int2(((row / Ky) * Kyl + row % Ky - y0) * Kx, Kx);
-    };
-    auto issue_small = [&](int u, int2 sg, int b) {
-        if (u < total) {
-            int rc;
-            const int row = row_at(u, rc);
-            if (row >= 0) {
-                unsigned char* sl = slots + b * SL::S_b;
-                int2* RI = reinterpret_cast<int2*>(sl);
-                float2* V = reinterpret_cast<float2*>(sl + SL::W * 8);
-                uint32_t* Mw = reinterpret_cast<uint32_t*>(sl + SL::W * 8 + (N / 2) * 8);
-                for (int e = j; e < W; e += T) cpa8(&RI[e], &rowinfo[(int64_t)row * W + e]);
-                if (!green_only && is_live(row)) {
-                    const float2* src = in + (PACKED ? (int64_t)rc * K : (int64_t)rc * Kt) + sg.x;
-                    for (int e = j; e < sg.y; e += T) cpa8(&V[e], &src[e]);
-                    if (PACKED) {   // material ids of the segment, 4-byte words (matp is padded)
-                        const int a0 = sg.x & ~3, nw = (sg.x + sg.y - a0 + 3) >> 2;
-                        for (int e = j; e < nw; e += T) cpa4(&Mw[e], matp + a0 + 4 * e);
-                    }
+    auto issue_small = [&](int u, int row, int2 sg, bool live, int b) {
+        if (row >= 0) {
+            const int rc = u / groups;
+            unsigned char* sl = slots + b * SL::S_b;
+            int2* RI = reinterpret_cast<int2*>(sl);
+            float2* V = reinterpret_cast<float2*>(sl + SL::W * 8);
+            uint32_t* Mw = reinterpret_cast<uint32_t*>(sl + SL::W * 8 + (N / 2) * 8);
+            for (int e = j; e < W; e += T) cpa8(&RI[e], &rowinfo[(int64_t)row * W + e]);
+            if (!green_only && live) {
+                const float2* src = in + (PACKED ? (int64_t)rc * K : (int64_t)rc * Kt) + sg.x;
+                for (int e = j; e < sg.y; e += T) cpa8(&V[e], &src[e]);
+                if (PACKED) {   // material ids of the segment, 4-byte words (matp is padded)
+                    const int a0 = sg.x & ~3, nw = (sg.x + sg.y - a0 + 3) >> 2;
+                    for (int e = j; e < nw; e += T) cpa4(&Mw[e], matp + a0 + 4 * e);
                 }
             }
         }
         cpa_commit();
     };
-    auto issue_x = [&](int u) {
-        if (u < total) {
-            int rc;
-            const int row = row_at(u, rc);
-            if (is_live(row)) {
-                const int lrow = (row / Ky) * Kyl + row % Ky - y0;
-                const float2* xr = X1 + ((int64_t)rc * rows + lrow) * N;
-                for (int e = j; e < N / 2; e += T) cpa16(&X[2 * e], &xr[2 * e]);
-            }
+    auto issue_x = [&](int u, int row, bool live) {
+        if (live) {
+            const int rc = u / groups;
+            const int lrow = (row / Ky) * Kyl + row % Ky - y0;
+            const float2* xr = X1 + ((int64_t)rc * rows + lrow) * N;
+            for (int e = j; e < N / 2; e += T) cpa16(&X[2 * e], &xr[2 * e]);
         }
         cpa_commit();
     };
+    const int G = gridDim.x;
     int u = blockIdx.x;
-    int rc0;
-    int2 sg_cur = seg_of(u < total ? row_at(u, rc0) : -1);
-    issue_small(u, sg_cur, 0);
-    issue_x(u);
-    int2 sg_next = seg_of(u + (int)gridDim.x < total ? row_at(u + gridDim.x, rc0) : -1);
-    for (int k = 0; u < total; ++k, u += gridDim.x) {
-        const int un = u + gridDim.x;
+    int row0 = row_load(u), pre0, nxt0;
+    uint32_t lw0;
+    seg_load(row0, pre0, nxt0, lw0);
+    issue_small(u, row0, make_int2(pre0, nxt0 - pre0), (lw0 & 1u) != 0, 0);
+    issue_x(u, row0, row0 >= 0 && (lw0 & 1u));
+    int row1 = row_load(u + G), pre1, nxt1;
+    uint32_t lw1;
+    seg_load(row1, pre1, nxt1, lw1);
+    int row2 = row_load(u + 2 * G);
+    for (int k = 0; u < total; ++k, u += G) {
         cpa_wait0();
         __syncthreads();   // this row's copies landed; every thread is done with the previous row
-        issue_small(un, sg_next, (k + 1) & 1);
-        const int2 sg = sg_cur;
-        sg_cur = sg_next;
-        sg_next = seg_of(un + (int)gridDim.x < total ? row_at(un + gridDim.x, rc0) : -1);
-        int rc;
-        const int row = row_at(u, rc);
+        const bool live1 = row1 >= 0 && (lw1 & 1u);
+        issue_small(u + G, row1, make_int2(pre1, nxt1 - pre1), live1, (k + 1) & 1);
+        int pre2, nxt2;
+        uint32_t lw2;
+        seg_load(row2, pre2, nxt2, lw2);
+        const int row3 = row_load(u + 3 * G);
+        const int row = row0;
+        const int2 sg = make_int2(pre0, nxt0 - pre0);
+        const bool live = row0 >= 0 && (lw0 & 1u);
+        const int rc = u / groups;
         const int comp = rc % 5;
-        const bool live = is_live(row);
         unsigned char* sl = slots + (k & 1) * SL::S_b;
         const int2* RI = reinterpret_cast<const int2*>(sl);
         float2* V = reinterpret_cast<float2*>(sl + SL::W * 8);
@@ -384,7 +408,7 @@ __global__ void __launch_bounds__(RowPlan<N>::NT, RowPlan<N>::MINB)
             for (int r = 0; r < 16; ++r) B[rpad(j * 16 + r)] = v[r];
         }
         __syncthreads();
-        issue_x(un);   // X is free: the next row's X1 row streams in during the remaining stages
+        issue_x(u + G, row1, live1);   // X is free: the next row's X1 row streams in meanwhile
         if constexpr (NS == 2) {
 #pragma unroll
             for (int i = 0; i < 16 / RL; ++i) {
@@ -429,6 +453,15 @@ __global__ void __launch_bounds__(RowPlan<N>::NT, RowPlan<N>::MINB)
             float2* dst = out + (PACKED ? (int64_t)rc * K : (int64_t)rc * Kt) + sg.x;
             for (int e = j; e < sg.y; e += T) dst[e] = V[e];
         }
+        row0 = row1;
+        pre0 = pre1;
+        nxt0 = nxt1;
+        lw0 = lw1;
+        row1 = row2;
+        pre1 = pre2;
+        nxt1 = nxt2;
+        lw1 = lw2;
+        row2 = row3;
     }
     cpa_wait0();
 }

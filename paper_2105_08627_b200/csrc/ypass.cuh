@@ -1,14 +1,14 @@
 // Strided passes B (forward y-FFT, zero-padded) and D (inverse y-FFT, cropped) of the matvec
 // (Eq. 9) for Ny = 1024 / 2048: the Stockham radix-16 FFT of rowfft.cuh applied to Q
-// pencils at once.  Dispatched for the inverse 2048-point pass (matvec.cu run_pass_y).
+// pencils at once.
 //
 // Tile = Q consecutive kx of one non-empty plane p = rc Kz + z.  Its input rows (B: the Ky rows
 // of X1, D: the Ny rows of X2) stream HBM -> shared memory by TMA (cp.async.bulk.tensor, box
 // Q x 256 rows) into an S-deep mbarrier ring, so the next tiles' loads are in flight while this
 // one is transformed; stage 0 reads the dense staged tile, stages 1-2 run in place on one padded
 // work buffer W (element (i, q) at rpad(i) Q + q: conflict-free for every stage), and the last
-// stage stores straight from registers to HBM (B: all Ny rows of X2; D: the rows y < Ky that hold
-// a voxel, the only ones pass E reads).  B zeroes the staged rows that hold no voxel (pass A never
+// stage stores to HBM (B: all Ny rows of X2, staged in shared memory and written by TMA stores;
+// D: straight from registers, the rows y < Ky that hold a voxel, the only ones pass E reads).  B zeroes the staged rows that hold no voxel (pass A never
 // wrote them) and the rows Ky <= y < Ny/2 (outside the box: TMA zero fill).
 #pragma once
 #include "rowfft.cuh"
@@ -29,12 +29,15 @@ struct YPlan {
     static constexpr size_t stage_b = (size_t)SR * Q * sizeof(float2);
     static constexpr size_t W_b = (size_t)PADN * Q * sizeof(float2);
     static constexpr int MW = (N / 2 + 31) / 32;  // row-mask words of a plane (y < N/2)
-    static constexpr size_t smem = S * stage_b + W_b + (size_t)S * MW * 4 + S * 8 + 64;
+    // forward: the output tile (Ny rows x Q, dense) is staged for TMA stores
+    static constexpr size_t O_b = DIR < 0 ? (size_t)N * Q * sizeof(float2) : 0;
+    static constexpr size_t smem = S * stage_b + W_b + O_b + (size_t)S * MW * 4 + S * 8 + 64;
 };
 
 template <int N, int Q, int DIR>
 __global__ void __launch_bounds__(YPlan<N, Q, DIR>::NT, 1)
-    k_ypass(float2* __restrict__ out, const __grid_constant__ CUtensorMap tin, const float2* __restrict__ tw,
+    k_ypass(float2* __restrict__ out, const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
+            const float2* __restrict__ tw,
             int Nx, int Kz, int Lin, int Lout, int ntiles, int tiles_x, const int32_t* __restrict__ planes, int nzp,
             const uint32_t* __restrict__ rowmask, int rowMW) {
     using P = YPlan<N, Q, DIR>;
@@ -42,8 +45,10 @@ __global__ void __launch_bounds__(YPlan<N, Q, DIR>::NT, 1)
     extern __shared__ __align__(128) unsigned char smraw[];
     float2* stage = reinterpret_cast<float2*>(smraw);
     float2* W = reinterpret_cast<float2*>(smraw + S * P::stage_b);
-    uint32_t* M = reinterpret_cast<uint32_t*>(smraw + S * P::stage_b + P::W_b);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + ((S * P::stage_b + P::W_b + S * MW * 4 + 7) / 8) * 8);
+    float2* O = reinterpret_cast<float2*>(smraw + S * P::stage_b + P::W_b);
+    uint32_t* M = reinterpret_cast<uint32_t*>(smraw + S * P::stage_b + P::W_b + P::O_b);
+    uint64_t* bar =
+        reinterpret_cast<uint64_t*>(smraw + ((S * P::stage_b + P::W_b + P::O_b + S * MW * 4 + 7) / 8) * 8);
     const int tid = threadIdx.x;
     const int j = tid / Q, q = tid % Q;
     const float2 zero = make_float2(0.f, 0.f);
@@ -87,6 +92,7 @@ __global__ void __launch_bounds__(YPlan<N, Q, DIR>::NT, 1)
         int z, p, x0;
         decode(t, z, p, x0);
         mbar_wait(&bar[st], (uint32_t)((i / S) & 1));
+        if (DIR < 0 && tid == 0) tma_store_wait_read0();   // the previous tile's output left O
         __syncthreads();   // (also: the previous tile's stage-2 reads of W are done; M[st] visible)
         const float2* src = stage + st * SR * Q;
         const uint32_t* Ms = M + st * MW;
@@ -148,12 +154,22 @@ __global__ void __launch_bounds__(YPlan<N, Q, DIR>::NT, 1)
             for (int r = 0; r < RL; ++r) {
                 const int n = tt + r * (N / RL);
                 if (DIR < 0)
-                    dst[(int64_t)n * Nx] = v[r];
+                    O[n * Q + q] = v[r];
                 else if (r < RL / 2 && ((keep >> (i2 * RL + r)) & 1u))
                     dst[(int64_t)n * Nx] = v[r];
             }
         }
+        if (DIR < 0) {   // the whole output tile leaves by TMA stores (Ny / 256 boxes)
+            fence_proxy_async_smem();
+            __syncthreads();
+            if (tid == 0) {
+#pragma unroll
+                for (int b = 0; b < N / BOX; ++b) tma_store_3d(&tout, x0, b * BOX, p, O + b * BOX * Q);
+                tma_store_commit();
+            }
+        }
     }
+    if (DIR < 0 && tid == 0) tma_store_wait0();
 }
 
 }  // namespace svh

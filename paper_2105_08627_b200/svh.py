@@ -47,7 +47,8 @@ class Port(ctypes.Structure):
 class Opts(ctypes.Structure):
     _fields_ = [("tucker_tol", ctypes.c_double), ("restart", ctypes.c_int32), ("rre", ctypes.c_double),
                 ("inner_tol", ctypes.c_double), ("inner_maxit", ctypes.c_int32), ("max_iters", ctypes.c_int32),
-                ("rhs_chunk", ctypes.c_int32), ("verbose", ctypes.c_int32), ("kernel_cache", ctypes.c_char_p)]
+                ("rhs_chunk", ctypes.c_int32), ("verbose", ctypes.c_int32), ("kernel_cache", ctypes.c_char_p),
+                ("plan", ctypes.c_int32), ("precision", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):

@@ -47,3 +47,22 @@ def test_host_only_calls():
     code = L.svh_setup(ctypes.byref(g), mat, mats, 1, 1e9, None, 0, ctypes.byref(h))
     assert code == -1
     assert b"bad grid" in L.svh_last_error()
+
+
+def test_opts_validation_host_only():
+    """svh_opts is validated before any device work: restart range (the FGMRES Hessenberg
+    scratch), plan (only P5 is built) and precision (only complex64 is built)."""
+    from paper_2105_08627_b200 import svh
+    L = svh.lib()
+    g = svh.Grid(2, 1, 1, 1e-6)
+    mats = (svh.Material * 1)(svh.Material(1e7, 1e-7))
+    mat = (ctypes.c_uint8 * 2)(1, 1)
+    for field, bad, msg in (("restart", 5000, b"restart"), ("restart", 0, b"restart"), ("plan", 3, b"plan"),
+                            ("precision", 1, b"complex64"), ("tucker_tol", 1.5, b"tucker_tol")):
+        o = svh.Opts()
+        L.svh_default_opts(ctypes.byref(o))
+        setattr(o, field, bad)
+        h = ctypes.c_void_p()
+        code = L.svh_setup(ctypes.byref(g), mat, mats, 1, 1e9, ctypes.byref(o), 0, ctypes.byref(h))
+        assert code == -1, field
+        assert msg in L.svh_last_error(), (field, L.svh_last_error())
