@@ -171,6 +171,72 @@ def pass_bytes(h, R, packed=True):
     return [A, B, C, D, E]
 
 
+def p3s_bytes(h, case, R):
+    """Algorithmic HBM bytes of one plan-P3s product, R RHS: A3 reads K (packed)
+    and writes Nx*Ry; YZ reads and writes Nx*Ry (+ the octant spectra once, dense mode); E3
+    reads Nx*Ry + K (I again) and writes K.  Ry = rows of the live TY-row blocks (TY = 16 for
+    Nx = 1024, else 32) of the non-empty planes -- the pruning granularity of the plan."""
+    mat = case["mat_id"] != 0
+    kz, ky, kx = mat.shape
+    nx, ny, nz = h.embedding
+    ty = 16 if nx >= 1024 else 32
+    rows = mat.any(axis=2)                      # (kz, ky)
+    Ry = 0
+    for z in range(kz):
+        for b in range(0, ky, ty):
+            if rows[z, b:b + ty].any():
+                Ry += min(ty, ky - b)
+    c8 = 5 * 8 * R
+    K = h.K
+    spec = 7 * 4 * (nx // 2 + 1) * (ny // 2 + 1) * (nz // 2 + 1)
+    rowinfo = 8 * h.rows_nonempty * ((kx + 31) // 32)
+    A3 = c8 * (K + nx * Ry) + rowinfo
+    YZ = c8 * 2 * nx * Ry + (0 if h.tucker else spec)
+    E3 = c8 * (nx * Ry + 2 * K) + rowinfo + K
+    return [A3, YZ, E3]
+
+
+def thin_grid_plans(local, name="cfg3", nrhs=(2, 16), steps=20):
+    """Plan P5 vs plan P3s on a thin grid, each forced, device-timed with CUDA
+    events (inputs resident, 3 warm-up products), with the auto selection's choice."""
+    import torch
+    from paper_2105_08627_b200 import svh
+    case, _ = workload(name)
+    peaks, _ = load_peaks()
+    out = {"workload": case["name"]}
+    for R in nrhs:
+        rec = {}
+        for plan in (5, 3):
+            with svh.setup_case(case, device=local, plan=plan) as h:
+                I = torch.from_numpy(svh_inputs.currents(h.K, R, seed=7).astype(np.complex64)).cuda()
+                o = torch.empty_like(I)
+                for _ in range(3):
+                    h.matvec(I, out=o)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(steps):
+                    h.matvec(I, out=o)
+                e1.record()
+                torch.cuda.synchronize()
+                ms = e0.elapsed_time(e1) / steps
+                b = sum(pass_bytes(h, R)) if plan == 5 else sum(p3s_bytes(h, case, R))
+                kz, ky, kx = h.shape
+                rec["P5" if plan == 5 else "P3s"] = {
+                    "ms": round(ms, 4), "voxel_unknowns_per_s": 5.0 * kx * ky * kz * R / (ms / 1e3),
+                    "bytes": int(b), "frac": round(b / (ms / 1e3) / 1e9 / float(peaks["hbm_gbs"]), 4)}
+                del I, o
+        with svh.setup_case(case, device=local, plan=0) as h:
+            I = torch.from_numpy(svh_inputs.currents(h.K, R, seed=7).astype(np.complex64)).cuda()
+            h.matvec(I)
+            torch.cuda.synchronize()
+            rec["auto_choice"] = "P3s" if h.matvec_plan()[0] == 3 else "P5"
+            del I
+        torch.cuda.empty_cache()
+        out["nrhs_%d" % R] = rec
+    return out
+
+
 def oracle_sample_step(case, frac, seed):
     """One bounded oracle sample: a seeded random fraction `frac` of the source voxels (the
     sub-lattice keeps their positions and materials), one random output voxel (all 5
@@ -414,6 +480,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-solve", action="store_true", help="skip the time-to-L measurement")
     ap.add_argument("--no-cufft", action="store_true", help="skip the cuFFT reference-pipeline timing")
+    ap.add_argument("--no-plans", action="store_true", help="skip the thin-grid P5 vs P3s plan comparison")
     ap.add_argument("--solve-workload", default="cfg3")
     ap.add_argument("--slab", type=int, default=0,
                     help="slab-decomposed matvec (SURVEY 8(e)(2), strong scaling): under torchrun one y-slab per "
@@ -514,13 +581,20 @@ def main():
     peaks, peak_src = load_peaks()
     # bytes and device time of each pass summed over the timed region (a step may run its RHS
     # in several workspace chunks, i.e. several launches per pass)
-    pb = np.array(pass_bytes(h, R), dtype=np.float64)
-    pass_ms = np.asarray(pass_ms, dtype=np.float64)[:5]
-    pass_n = np.maximum(np.asarray(pass_n)[:5], 1)
+    # records 0-4: P5 passes A..E; record 5: whole P3s products (the auto plan picked P3s)
+    if np.asarray(pass_n)[5] > 0:
+        pb = np.array([sum(p3s_bytes(h, case, R))], dtype=np.float64)
+        pass_ms = np.asarray(pass_ms, dtype=np.float64)[5:6]
+        pass_n = np.maximum(np.asarray(pass_n)[5:6], 1)
+        names = ["P3s_x_fused_yz_x"]
+    else:
+        pb = np.array(pass_bytes(h, R), dtype=np.float64)
+        pass_ms = np.asarray(pass_ms, dtype=np.float64)[:5]
+        pass_n = np.maximum(np.asarray(pass_n)[:5], 1)
+        names = ["A_x_fwd", "B_y_fwd", "C_z_mac", "D_y_inv", "E_x_inv"]
     per_launch_ms = pass_ms / pass_n
     per_launch_bytes = pb * args.steps / pass_n
     dom = int(np.argmax(pass_ms))
-    names = ["A_x_fwd", "B_y_fwd", "C_z_mac", "D_y_inv", "E_x_inv"]
     achieved = per_launch_bytes[dom] / (per_launch_ms[dom] / 1e3) / 1e9
     peak = float(peaks["hbm_gbs"])
     matvec_bytes = sum(pb)
@@ -567,6 +641,10 @@ def main():
             "speedup_vs_cufft": round(ms_cufft / (ms_max / R), 3), "rel_l2_vs_ours": rel_cufft,
             "what": "torch.fft (cuFFT) pad+fftn, 5->5 MAC with full-grid spectra, ifftn, crop; grid layout"}
 
+    if not args.no_plans and world == 1:
+        h.close()
+        torch.cuda.empty_cache()
+        line["thin_grid_plans"] = thin_grid_plans(local)
     if not args.no_solve:
         line["time_to_L"] = time_to_L(args.solve_workload, local, world, rank)
 

@@ -37,6 +37,7 @@
 #ifndef SVH_H
 #define SVH_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -84,10 +85,18 @@ typedef struct {
     int32_t verbose;      /* 0 quiet */
     const char* kernel_cache;  /* NULL: kernels by quadrature; else an SVXT file (svh_kernel_cache_build):
                                   the grid's Toeplitz tensors are restored from it (Alg. 2) */
-    int32_t plan;         /* matvec plan: 0 = auto = 5 = P5 (x | y | fused z | y | x, the only
-                             plan built); any other value -> SVH_EINVAL */
+    int32_t plan;         /* matvec plan: 5 = P5 (x | y | fused z | y | x, any grid);
+                             3 = P3s (x | fused y-z-y slab on chip | x; thin grids: Nz <= 8,
+                             128 <= Nx <= 1024, Ny <= 1024, y-z slab within shared memory;
+                             SVH_EINVAL at the first matvec otherwise); 0 = auto: P5, or -- where
+                             P3s is eligible -- whichever of the two measures faster on the first
+                             product of each RHS-chunk size.  Other values -> SVH_EINVAL */
     int32_t precision;    /* matvec arithmetic: 0 = complex64 (the only precision built; Krylov vectors are
                              fp64); 1 = complex128 -> SVH_EINVAL (not built) */
+    int32_t schur_solver; /* S^-1 inside the Schur preconditioner (Eq. 13-15): 0 = AMG-preconditioned CG
+                             (default); 1 = sparse-direct comparator (Table IV
+                             P:251-262): METIS-reordered sparse Cholesky of S, factored once per port
+                             set on the device (cuSOLVER csrchol), exact solves (inner_tol ignored) */
 } svh_opts;
 
 typedef struct {
@@ -99,6 +108,9 @@ typedef struct {
     double  t_setup_s, t_solve_s, t_matvec_s, t_precond_s;   /* host wall clock */
     int32_t ranks[7][3];       /* Tucker multilinear ranks per kernel (0 if dense) */
     double  compression_ratio; /* dense octant spectra bytes / Tucker bytes (P:202 CR) */
+    double  t_precond_setup_s; /* setup of the Schur solver (AMG hierarchy or Cholesky factor), Table V */
+    double  precond_bytes;     /* device memory of that solver (Table IV "memory") */
+    int32_t schur_solver;      /* opts.schur_solver of the solve */
 } svh_stats;
 
 /* svh_kernel_cache_build -- Algorithm 2, install stage: Tucker-compress the 7
@@ -195,6 +207,37 @@ int svh_slab_backward(svh_handle* h, int32_t rank, int32_t P, const void* recv, 
                       int32_t nrhs, int32_t green_only, svh_stream stream);
 
 /*
+ * Fused-exchange slab matvec (fused variant; operator Eq. 9): the same
+ * product as svh_slab_forward / middle / backward, but the pack step stores each destination's
+ * chunk directly into that peer's receive buffer over NVLink peer memory and the ranks
+ * synchronise with stream memory operations (a flag write preceded by a memory barrier, and a
+ * stream wait -- no SM spins), so no all-to-all call, no local send buffer and no host
+ * synchronisation are involved.  Per rank, caller-owned, allocated with svh_ipc_alloc and
+ * mapped into every peer with svh_ipc_open (peer arrays are indexed by rank, entry `rank` =
+ * the rank's own pointer):
+ *   recv1, recv2 : complex64, nrhs * sizes[3] elements each (layout as recv above)
+ *   flags        : uint32 [2][P], zero-initialised (svh_ipc_alloc zeroes)
+ * One product with epoch e (e = 1, 2, ... increasing by one per product on every rank):
+ *   svh_slab_forward_p2p(I_slab -> peers' recv1, flags slot 0 = e)
+ *   svh_slab_middle_p2p (own recv1 -> peers' recv2, flags slot 1 = e)
+ *   svh_slab_backward   (own recv2, I_slab -> CC)
+ * Each call returns once its work, signal and wait are enqueued on `stream` (asynchronous).
+ * P <= 8.  Errors: SVH_EINVAL, SVH_ECUDA (stream memory operations unavailable, IPC failure).
+ *
+ * svh_ipc_alloc: cudaMalloc(bytes), zero it, write its 64-byte cudaIpcMemHandle to `handle`.
+ * svh_ipc_open : map a peer's handle (cudaIpcOpenMemHandle, lazy peer access) -> *dptr.
+ * svh_ipc_close / svh_ipc_free: unmap a peer mapping / free an own allocation.
+ */
+int svh_ipc_alloc(size_t bytes, void** dptr, void* handle);
+int svh_ipc_free(void* dptr);
+int svh_ipc_open(const void* handle, void** dptr);
+int svh_ipc_close(void* dptr);
+int svh_slab_forward_p2p(svh_handle* h, int32_t rank, int32_t P, const void* I_slab, void* const* recv1_peers,
+                         uint32_t* const* flag_peers, uint32_t epoch, int32_t nrhs, svh_stream stream);
+int svh_slab_middle_p2p(svh_handle* h, int32_t rank, int32_t P, const void* recv1, void* const* recv2_peers,
+                        uint32_t* const* flag_peers, uint32_t epoch, int32_t nrhs, svh_stream stream);
+
+/*
  * svh_apply_system -- Eq. 7 saddle operator (reading G12 sign convention):
  *   y_I   = Z.x_I + A^T x_Phi,   y_Phi = A x_I
  * x, y : device complex64 [nrhs][5K + M].  Errors: SVH_EINVAL, SVH_ECUDA.
@@ -241,12 +284,17 @@ void svh_destroy(svh_handle* h);
 const char* svh_last_error(void);
 
 /* Per-pass device-time accounting of svh_matvec: while enabled, CUDA events are
- * recorded on the caller's stream around each of the 5 passes (A..E).
- * svh_profile_read synchronises those events and returns, per pass, the summed
- * milliseconds (ms[5]) and the number of launches (launches[5]) since the last
+ * recorded on the caller's stream around each pass: records 0..4 = the 5 passes A..E of
+ * plan P5, record 5 = one whole plan-P3s product (its 3 kernels A3, YZ, E3).
+ * svh_profile_read synchronises those events and returns, per record, the summed
+ * milliseconds (ms[6]) and the number of launches (launches[6]) since the last
  * reset; reset != 0 clears the record.  Both pointers may be NULL. */
 int svh_profile_enable(svh_handle* h, int32_t on);
 int svh_profile_read(svh_handle* h, double* ms, int64_t* launches, int32_t reset);
+
+/* The plan (3 = P3s, 5 = P5) of the last svh_matvec chunk, and the device times of the two
+ * plans measured by the last auto-selection (0 if none ran).  ms_p5 / ms_p3s may be NULL. */
+int svh_matvec_plan(const svh_handle* h, int32_t* plan, float* ms_p5, float* ms_p3s);
 
 /* Number of kernel launches issued by this library since load (instrumentation). */
 int64_t svh_launch_count(void);

@@ -46,7 +46,7 @@ def build(verbose: bool = True, jobs: int = 8) -> str:
     with ThreadPoolExecutor(jobs) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
     if not os.path.exists(OUT) or os.path.getmtime(OUT) < max(os.path.getmtime(o) for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lcusolver", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lcusolver", "-lcusparse", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

@@ -179,6 +179,7 @@ static void destroy(svh_handle* h) {
     cudaFree(h->d_vox);
     cudaFree(h->d_kern);
     cudaFree(h->d_spec);
+    cudaFree(h->d_kvt);
     cudaFree(h->d_zloc);
     for (int a = 0; a < 3; ++a) cudaFree(h->d_tw[a]);
     cudaFree(h->X1);
@@ -245,8 +246,9 @@ int svh_setup(const svh_grid* grid, const uint8_t* mat_id, const svh_material* m
         // (solve.cu: 16 + 2 (restart + 1) doubles)
         SVH_CHECK(o.restart >= 1 && o.restart <= 2039, SVH_EINVAL, "restart must be in 1..2039");
         SVH_CHECK(o.tucker_tol >= 0 && o.tucker_tol < 1, SVH_EINVAL, "tucker_tol must be in [0, 1)");
-        SVH_CHECK(o.plan == 0 || o.plan == 5, SVH_EINVAL, "only the P5 matvec plan is built (plan 0 / 5)");
+        SVH_CHECK(o.plan == 0 || o.plan == 3 || o.plan == 5, SVH_EINVAL, "matvec plan must be 0 (auto), 3 (P3s) or 5 (P5)");
         SVH_CHECK(o.precision == 0, SVH_EINVAL, "only the complex64 matvec is built (precision 0)");
+        SVH_CHECK(o.schur_solver == 0 || o.schur_solver == 1, SVH_EINVAL, "schur_solver must be 0 (AMG-PCG) or 1 (sparse Cholesky)");
         auto t0 = std::chrono::steady_clock::now();
         SVH_CUDA(cudaSetDevice(device));
         svh_handle* h = new svh_handle();
@@ -437,8 +439,8 @@ int svh_profile_read(svh_handle* h, double* ms, int64_t* launches, int32_t reset
     return guarded([&] {
         SVH_CHECK(h, SVH_EINVAL, "null handle");
         SVH_CUDA(cudaSetDevice(h->device));
-        double acc[5] = {0, 0, 0, 0, 0};
-        int64_t cnt[5] = {0, 0, 0, 0, 0};
+        double acc[kProfPasses] = {};
+        int64_t cnt[kProfPasses] = {};
         for (auto& r : h->prof) {
             SVH_CUDA(cudaEventSynchronize(r.b));
             float t = 0.f;
@@ -446,7 +448,7 @@ int svh_profile_read(svh_handle* h, double* ms, int64_t* launches, int32_t reset
             acc[r.pass] += t;
             cnt[r.pass] += 1;
         }
-        for (int p = 0; p < 5; ++p) {
+        for (int p = 0; p < kProfPasses; ++p) {
             if (ms) ms[p] = acc[p];
             if (launches) launches[p] = cnt[p];
         }
@@ -457,6 +459,15 @@ int svh_profile_read(svh_handle* h, double* ms, int64_t* launches, int32_t reset
             }
             h->prof.clear();
         }
+    });
+}
+
+int svh_matvec_plan(const svh_handle* h, int32_t* plan, float* ms_p5, float* ms_p3s) {
+    return guarded([&] {
+        SVH_CHECK(h && plan, SVH_EINVAL, "null arg");
+        *plan = h->last_plan;
+        if (ms_p5) *ms_p5 = h->plan_ms.empty() ? 0.f : h->plan_ms.back().first;
+        if (ms_p3s) *ms_p3s = h->plan_ms.empty() ? 0.f : h->plan_ms.back().second;
     });
 }
 

@@ -19,6 +19,9 @@ struct SvhTucker {
     size_t bytes = 0;
 };
 
+// per-pass profile records: 0-4 = P5 passes A..E, 5 = the whole P3s matvec (A3 + YZ + E3)
+constexpr int kProfPasses = 6;
+
 struct svh_handle {
     int device = 0;
     int kx = 0, ky = 0, kz = 0;
@@ -51,6 +54,7 @@ struct svh_handle {
     uint8_t* d_matp = nullptr;           // [K] material id in packed order
     double* d_kern = nullptr;            // [7][Kt] unit-voxel kernels, fp64
     float* d_spec = nullptr;             // [7][hz][hy][hx] dense octant spectra (tucker_tol == 0)
+    float* d_kvt = nullptr;              // [hx][7][hz][hy] the same, kx-major (plan P3s, built on first use)
     SvhTucker tucker;
     bool use_tucker = false;
     float2* d_zloc = nullptr;            // [n_mat + 1][5] local terms z^b (index 0 unused)
@@ -69,6 +73,10 @@ struct svh_handle {
         cudaEvent_t in_ready[2] = {}, mv_done[2] = {}, out_done[2] = {};
     };
     HostPipe* pipe = nullptr;
+    // matvec plan: 5 = P5, 3 = P3s; auto-tuned per chunk size (choose_plan)
+    int last_plan = 5;
+    std::vector<std::pair<int, int>> plan_tuned;       // (chunk RHS, plan)
+    std::vector<std::pair<float, float>> plan_ms;      // (P5 ms, P3s ms) of each tuning
     // solve-side data (built lazily by svh_solve / svh_apply_system)
     svh::Solve* solve = nullptr;
     double t_setup = 0;
@@ -100,9 +108,19 @@ void matvec_host(svh_handle* h, const float2* I_host, float2* CC_host, int nrhs,
 void free_host_pipe(svh_handle* h);
 void slab_sizes(const svh_handle* h, int P, int64_t* out4);
 void slab_forward(svh_handle* h, int rank, int P, const float2* I, float2* send, int nrhs, cudaStream_t s);
+void slab_forward_p2p(svh_handle* h, int rank, int P, const float2* I, void* const* recv1_peers,
+                      uint32_t* const* flag_peers, uint32_t epoch, int nrhs, cudaStream_t s);
+void slab_middle_p2p(svh_handle* h, int rank, int P, const float2* recv1, void* const* recv2_peers,
+                     uint32_t* const* flag_peers, uint32_t epoch, int nrhs, cudaStream_t s);
+void slab_forward_compute(svh_handle* h, int rank, int P, const float2* I, int nrhs, cudaStream_t s);
+void slab_middle_compute(svh_handle* h, int rank, int P, const float2* recv, int nrhs, cudaStream_t s);
 void slab_middle(svh_handle* h, int rank, int P, const float2* recv, float2* send, int nrhs, cudaStream_t s);
 void slab_backward(svh_handle* h, int rank, int P, const float2* recv, const float2* I, float2* CC, int nrhs,
                    bool green_only, cudaStream_t s);
+// p3s.cu (plan P3s for thin grids)
+bool p3s_eligible(const svh_handle* h);
+void p3s_matvec(svh_handle* h, const float2* in, float2* out, float2* XT, int nr, bool green_only, bool packed,
+                cudaStream_t s);
 // quad.cu
 void compute_kernels(svh_handle* h);
 // cache.cu (Algorithm 2)

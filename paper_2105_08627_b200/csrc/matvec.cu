@@ -1710,7 +1710,7 @@ int max_chunk(svh_handle* h) {
 
 // one sub-batch of nr RHS on stream s with workspace slices X1, X2
 static void matvec_batch(svh_handle* h, const float2* in, float2* out, float2* X1, float2* X2, int nr,
-                         bool green_only, bool packed, cudaStream_t s) {
+                         bool green_only, bool packed, cudaStream_t s, int plan) {
     // SVH_SYNC_DEBUG (debugging aid, include/svh.h): synchronise after every pass and report the
     // failing pass; it does not change which kernels run
     static const bool dbg = getenv("SVH_SYNC_DEBUG") != nullptr;
@@ -1731,6 +1731,13 @@ static void matvec_batch(svh_handle* h, const float2* in, float2* out, float2* X
             SVH_CUDA(cudaEventRecord(h->prof.back().b, s));
         }
     };
+    if (plan == 3) {
+        // plan P3s (p3s.cu): x | fused y-z-y on chip | x, profiled as one record (pass 5)
+        tick(5, true);
+        p3s_matvec(h, in, out, X1, nr, green_only, packed, s);
+        tick(5, false);
+        return;
+    }
     const Geom g = whole_grid(h);
     tick(0, true);
     SVH_DISPATCH_N(h->nx, run_pass_a<NN>(h, g, in, X1, packed, nr, s));
@@ -1749,6 +1756,9 @@ static void matvec_batch(svh_handle* h, const float2* in, float2* out, float2* X
     tick(4, false);
 }
 
+int choose_plan(svh_handle* h, const float2* in, float2* out, int nr, bool green_only, bool packed,
+                cudaStream_t s);
+
 void matvec(svh_handle* h, const float2* I, float2* CC, int nrhs, bool green_only, bool packed, cudaStream_t s) {
     // RHS chunks sized to the workspace budget (max_chunk) and balanced (8 RHS with room for 7
     // run as 4 + 4, not 7 + 1); every pass fills the GPU on its own, so the chunks run back to
@@ -1760,8 +1770,54 @@ void matvec(svh_handle* h, const float2* I, float2* CC, int nrhs, bool green_onl
     const int64_t per_rhs = 5 * (packed ? h->K : h->Kt);
     for (int r0 = 0; r0 < nrhs; r0 += chunk) {
         const int nr = std::min(chunk, nrhs - r0);
-        matvec_batch(h, I + r0 * per_rhs, CC + r0 * per_rhs, h->X1, h->X2, nr, green_only, packed, s);
+        const int plan = choose_plan(h, I + r0 * per_rhs, CC + r0 * per_rhs, nr, green_only, packed, s);
+        matvec_batch(h, I + r0 * per_rhs, CC + r0 * per_rhs, h->X1, h->X2, nr, green_only, packed, s, plan);
+        h->last_plan = plan;
     }
+}
+
+// Plan for a chunk of nr RHS (SURVEY 8(d) reporting rule: plans are chosen by absolute time).
+// opts.plan = 5 / 3 forces P5 / P3s; auto (0) takes P5 unless P3s is eligible (thin grid,
+// p3s_eligible), and then times both once per chunk size on the caller's data (two warm runs
+// of each, then one timed run of each; the last run is P3s, so CC holds a valid product
+// either way) and keeps the faster.  Not while the stream is being captured into a graph.
+int choose_plan(svh_handle* h, const float2* in, float2* out, int nr, bool green_only, bool packed, cudaStream_t s) {
+    if (h->opts.plan == 5) return 5;
+    if (h->opts.plan == 3) {
+        SVH_CHECK(p3s_eligible(h), SVH_EINVAL, "plan P3s needs Nz <= 8, 128 <= Nx <= 1024, Ny <= 1024 and a "
+                                               "y-z slab that fits shared memory");
+        return 3;
+    }
+    if (!p3s_eligible(h)) return 5;
+    for (const auto& t : h->plan_tuned)
+        if (t.first == nr) return t.second;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    SVH_CUDA(cudaStreamIsCapturing(s, &cs));
+    if (cs != cudaStreamCaptureStatusNone) return 3;
+    const bool prof = h->prof_on;
+    h->prof_on = false;
+    cudaEvent_t ev[4];
+    for (auto& e : ev) SVH_CUDA(cudaEventCreate(&e));
+    for (int w = 0; w < 2; ++w) {
+        matvec_batch(h, in, out, h->X1, h->X2, nr, green_only, packed, s, 5);
+        matvec_batch(h, in, out, h->X1, h->X2, nr, green_only, packed, s, 3);
+    }
+    SVH_CUDA(cudaEventRecord(ev[0], s));
+    matvec_batch(h, in, out, h->X1, h->X2, nr, green_only, packed, s, 5);
+    SVH_CUDA(cudaEventRecord(ev[1], s));
+    SVH_CUDA(cudaEventRecord(ev[2], s));
+    matvec_batch(h, in, out, h->X1, h->X2, nr, green_only, packed, s, 3);
+    SVH_CUDA(cudaEventRecord(ev[3], s));
+    SVH_CUDA(cudaEventSynchronize(ev[3]));
+    float t5 = 0.f, t3 = 0.f;
+    SVH_CUDA(cudaEventElapsedTime(&t5, ev[0], ev[1]));
+    SVH_CUDA(cudaEventElapsedTime(&t3, ev[2], ev[3]));
+    for (auto& e : ev) cudaEventDestroy(e);
+    h->prof_on = prof;
+    const int plan = t3 <= t5 ? 3 : 5;
+    h->plan_tuned.push_back({nr, plan});
+    h->plan_ms.push_back({t5, t3});
+    return plan;
 }
 
 // ---------------------------------------------------------------------------
@@ -1838,29 +1894,41 @@ void slab_sizes(const svh_handle* h, int P, int64_t* out4) {
     out4[3] = out4[2] * P;                          // send / recv buffer elements per RHS
 }
 
-void slab_forward(svh_handle* h, int rank, int P, const float2* I, float2* send, int nrhs, cudaStream_t s) {
+// pass A on the slab's rows -> X1 [b][y][Nx] (the part of slab_forward before the pack)
+void slab_forward_compute(svh_handle* h, int rank, int P, const float2* I, int nrhs, cudaStream_t s) {
     check_slab(h, rank, P);
     ensure_workspace(h, nrhs);
-    const int Kyl = h->ky / P, Nxl = h->nx / P;
+    const int Kyl = h->ky / P;
     const auto& sr = slab_rows(h, rank, P);
     const Geom g{h->nx, 0, Kyl, rank * Kyl, sr.d, sr.n};
     SVH_DISPATCH_N(h->nx, run_pass_a<NN>(h, g, I, h->X1, false, nrhs, s));
-    const int64_t Bt = 5LL * nrhs * h->kz;
-    slab_copy(send, h->X1, P, Bt, Kyl, Nxl, (int64_t)Kyl * h->nx, h->nx, Nxl, false, s);
 }
 
-void slab_middle(svh_handle* h, int rank, int P, const float2* recv, float2* send, int nrhs, cudaStream_t s) {
+// unpack recv [s][b][y][k] -> X1 [b][s Kyl + y][k], passes B, C, D on the kx-slab (X1 in place)
+void slab_middle_compute(svh_handle* h, int rank, int P, const float2* recv, int nrhs, cudaStream_t s) {
     check_slab(h, rank, P);
     ensure_workspace(h, nrhs);
     const int Kyl = h->ky / P, Nxl = h->nx / P;
     const int64_t Bt = 5LL * nrhs * h->kz;
-    // [s][b][y][k] -> X1 [b][s Kyl + y][k]
     slab_copy(const_cast<float2*>(recv), h->X1, P, Bt, Kyl, Nxl, (int64_t)h->ky * Nxl, Nxl, (int64_t)Kyl * Nxl, true,
               s);
     const Geom g{Nxl, rank * Nxl, h->ky, 0, nullptr, 0};
     SVH_DISPATCH_N(h->ny, (run_pass_y<NN, -1>(h, g, h->X1, h->X2, h->ky, h->ny, nrhs, s)));
     SVH_DISPATCH_N(h->nz, run_pass_c<NN>(h, g, h->X2, nrhs, s));
     SVH_DISPATCH_N(h->ny, (run_pass_y<NN, +1>(h, g, h->X2, h->X1, h->ny, h->ky, nrhs, s)));
+}
+
+void slab_forward(svh_handle* h, int rank, int P, const float2* I, float2* send, int nrhs, cudaStream_t s) {
+    slab_forward_compute(h, rank, P, I, nrhs, s);
+    const int Kyl = h->ky / P, Nxl = h->nx / P;
+    const int64_t Bt = 5LL * nrhs * h->kz;
+    slab_copy(send, h->X1, P, Bt, Kyl, Nxl, (int64_t)Kyl * h->nx, h->nx, Nxl, false, s);
+}
+
+void slab_middle(svh_handle* h, int rank, int P, const float2* recv, float2* send, int nrhs, cudaStream_t s) {
+    slab_middle_compute(h, rank, P, recv, nrhs, s);
+    const int Kyl = h->ky / P, Nxl = h->nx / P;
+    const int64_t Bt = 5LL * nrhs * h->kz;
     slab_copy(send, h->X1, P, Bt, Kyl, Nxl, (int64_t)h->ky * Nxl, Nxl, (int64_t)Kyl * Nxl, false, s);
 }
 

@@ -26,6 +26,10 @@
 #include <numeric>
 #include <vector>
 
+#include <cusolverSp.h>
+#include <cusolverSp_LOWLEVEL_PREVIEW.h>
+#include <cusparse.h>
+
 #include "internal.h"
 
 namespace svh {
@@ -108,6 +112,24 @@ struct Solve {
     int nvp_cap = 1;                 // vector pairs (ports) the level / work buffers hold
     int pcg_cap = 0;
     double t_matvec = 0, t_precond = 0;
+    bool pre_built = false;          // the preconditioner of fixed_nodes is set up
+    double t_pre_setup = 0;          // its setup wall time (Table V "preconditioner setup")
+    double pre_bytes = 0;            // its device memory (AMG hierarchy or Cholesky factor)
+    // sparse-direct Schur solve (svh_opts.schur_solver = 1, the paper's Table IV
+    // comparison): S(p, p) = L L^T of the METIS nested-dissection-reordered free-node Schur
+    // matrix, factored and solved on the device by cuSOLVER's csrchol
+    struct Chol {
+        cusolverSpHandle_t sp = nullptr;
+        cusparseMatDescr_t descr = nullptr;
+        csrcholInfo_t info = nullptr;
+        int n = 0;
+        int64_t nnz = 0;
+        int *rp = nullptr, *ci = nullptr, *perm = nullptr;
+        double* v = nullptr;
+        void* buf = nullptr;
+        double *bp = nullptr, *xp = nullptr;
+        size_t internal = 0, work = 0;
+    } chol;
 };
 
 // ---------------------------------------------------------------------------
@@ -351,6 +373,19 @@ __global__ void k_residV(int n, int w, const int* __restrict__ ec, const double*
     const double2 bi = reinterpret_cast<const double2*>(b)[t];
     reinterpret_cast<double2*>(r)[t] = make_double2(bi.x - a0, bi.y - a1);
 }
+// column v of the [n][NV] layout <-> a contiguous permuted vector (sparse-direct solve):
+// gather (dir 0): y[i] = x[perm[i] NV + v];  scatter (dir 1): y[perm[i] NV + v] = x[i]
+__global__ void k_col_perm(const double* __restrict__ x, double* __restrict__ y, const int* __restrict__ perm, int n,
+                           int NV, int v, int dir) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t o = (int64_t)__ldg(&perm[i]) * NV + v;
+    if (dir == 0)
+        y[i] = x[o];
+    else
+        y[o] = x[i];
+}
+
 __global__ void k_zero(double* __restrict__ x, int64_t n) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) x[i] = 0.0;
@@ -733,6 +768,13 @@ static void free_levels(Solve* S) {
     S->d_free = nullptr;
     S->d_free_list = nullptr;
     S->d_node2free = nullptr;
+    auto& C = S->chol;
+    if (C.info) cusolverSpDestroyCsrcholInfo(C.info);
+    if (C.descr) cusparseDestroyMatDescr(C.descr);
+    if (C.sp) cusolverSpDestroy(C.sp);
+    for (void* q : {(void*)C.rp, (void*)C.ci, (void*)C.perm, (void*)C.v, C.buf, (void*)C.bp, (void*)C.xp}) cudaFree(q);
+    C = Solve::Chol{};
+    S->pre_built = false;
 }
 
 void free_solve(svh_handle* h) {
@@ -962,10 +1004,84 @@ std::vector<double> dense_inverse(const CsrHost& A) {
 
 }  // namespace
 
+#define SVH_CUSP(call)                                                                              \
+    do {                                                                                            \
+        const int st__ = (int)(call);                                                               \
+        if (st__ != 0) throw Error{SVH_ECUDA, std::string(#call) + " failed: status " + std::to_string(st__)}; \
+    } while (0)
+
+// f4 comparator: METIS nested-dissection order (host), permuted CSR, device Cholesky factor
+static void build_chol(Solve* S, const CsrHost& A) {
+    auto& C = S->chol;
+    const int n = A.n;
+    const int nnz = (int)A.col.size();
+    C.n = n;
+    C.nnz = nnz;
+    SVH_CUSP(cusolverSpCreate(&C.sp));
+    SVH_CUSP(cusparseCreateMatDescr(&C.descr));
+    SVH_CUSP(cusparseSetMatType(C.descr, CUSPARSE_MATRIX_TYPE_GENERAL));
+    SVH_CUSP(cusparseSetMatIndexBase(C.descr, CUSPARSE_INDEX_BASE_ZERO));
+    std::vector<int> p(n), q(n);
+    SVH_CUSP(cusolverSpXcsrmetisndHost(C.sp, n, nnz, C.descr, A.rowptr.data(), A.col.data(), nullptr, p.data()));
+    for (int i = 0; i < n; ++i) q[p[i]] = i;
+    // B = A(p, p): row i of B is row p[i] of A with columns renumbered by q, sorted
+    std::vector<int> rp(n + 1, 0), ci(nnz);
+    std::vector<double> v(nnz);
+    std::vector<std::pair<int, double>> row;
+    for (int i = 0; i < n; ++i) {
+        row.clear();
+        for (int k = A.rowptr[p[i]]; k < A.rowptr[p[i] + 1]; ++k) row.push_back({q[A.col[k]], A.val[k]});
+        std::sort(row.begin(), row.end());
+        rp[i + 1] = rp[i] + (int)row.size();
+        for (size_t k = 0; k < row.size(); ++k) {
+            ci[rp[i] + k] = row[k].first;
+            v[rp[i] + k] = row[k].second;
+        }
+    }
+    SVH_CUDA(cudaMalloc(&C.rp, (n + 1) * sizeof(int)));
+    SVH_CUDA(cudaMalloc(&C.ci, std::max(1, nnz) * sizeof(int)));
+    SVH_CUDA(cudaMalloc(&C.v, std::max(1, nnz) * sizeof(double)));
+    SVH_CUDA(cudaMalloc(&C.perm, std::max(1, n) * sizeof(int)));
+    SVH_CUDA(cudaMalloc(&C.bp, std::max(1, n) * sizeof(double)));
+    SVH_CUDA(cudaMalloc(&C.xp, std::max(1, n) * sizeof(double)));
+    SVH_CUDA(cudaMemcpy(C.rp, rp.data(), (n + 1) * sizeof(int), cudaMemcpyHostToDevice));
+    SVH_CUDA(cudaMemcpy(C.ci, ci.data(), nnz * sizeof(int), cudaMemcpyHostToDevice));
+    SVH_CUDA(cudaMemcpy(C.v, v.data(), nnz * sizeof(double), cudaMemcpyHostToDevice));
+    SVH_CUDA(cudaMemcpy(C.perm, p.data(), n * sizeof(int), cudaMemcpyHostToDevice));
+    SVH_CUSP(cusolverSpCreateCsrcholInfo(&C.info));
+    SVH_CUSP(cusolverSpXcsrcholAnalysis(C.sp, n, nnz, C.descr, C.rp, C.ci, C.info));
+    SVH_CUSP(cusolverSpDcsrcholBufferInfo(C.sp, n, nnz, C.descr, C.v, C.rp, C.ci, C.info, &C.internal, &C.work));
+    SVH_CUDA(cudaMalloc(&C.buf, std::max<size_t>(C.work, 16)));
+    SVH_CUSP(cusolverSpDcsrcholFactor(C.sp, n, nnz, C.descr, C.v, C.rp, C.ci, C.info, C.buf));
+    int sing = -1;
+    SVH_CUSP(cusolverSpDcsrcholZeroPivot(C.sp, C.info, 1e-300, &sing));
+    SVH_CHECK(sing < 0, SVH_ECUDA, "Schur matrix not SPD (zero pivot in the sparse Cholesky)");
+    SVH_CUDA(cudaDeviceSynchronize());
+    S->pre_bytes = (double)C.internal + (double)C.work + (double)nnz * 12 + (double)n * 28;
+}
+
+// x = S^-1 b for the NV = 2 NVP real vectors of the [n][NV] layout, by the Cholesky factor
+static void chol_solveV(Solve* S, const double* b, double* x, cudaStream_t s, int NVP) {
+    auto& C = S->chol;
+    const int NV = 2 * NVP;
+    SVH_CUSP(cusolverSpSetStream(C.sp, s));
+    for (int v = 0; v < NV; ++v) {
+        SVH_LAUNCH(k_col_perm, nblk(C.n), 256, 0, s, b, C.bp, C.perm, C.n, NV, v, 0);
+        SVH_CUSP(cusolverSpDcsrcholSolve(C.sp, C.n, C.bp, C.xp, C.info, C.buf));
+        SVH_LAUNCH(k_col_perm, nblk(C.n), 256, 0, s, C.xp, x, C.perm, C.n, NV, v, 1);
+    }
+}
+
 static void build_amg(svh_handle* h, const std::vector<int32_t>& fixed, int nvp) {
     Solve* S = h->solve;
-    if (!S->levels.empty() && fixed == S->fixed_nodes && nvp <= S->nvp_cap) return;
+    if (S->pre_built && fixed == S->fixed_nodes && nvp <= S->nvp_cap) return;
     free_levels(S);
+    const auto tp0 = std::chrono::steady_clock::now();
+    struct Done {   // setup time of whatever this call builds
+        Solve* S;
+        std::chrono::steady_clock::time_point t0;
+        ~Done() { S->t_pre_setup = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); }
+    } done{S, tp0};
     S->nvp_cap = std::max(1, nvp);
     g_upload_nvp = S->nvp_cap;
     S->fixed_nodes = fixed;
@@ -984,8 +1100,17 @@ static void build_amg(svh_handle* h, const std::vector<int32_t>& fixed, int nvp)
     SVH_CUDA(cudaMemcpy(S->d_free_list, flist.data(), flist.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     SVH_CUDA(cudaMalloc(&S->d_node2free, S->M * sizeof(int32_t)));
     SVH_CUDA(cudaMemcpy(S->d_node2free, node2free.data(), S->M * sizeof(int32_t), cudaMemcpyHostToDevice));
-    if (S->nf == 0) return;
+    S->pre_bytes = 0;
+    if (S->nf == 0) {
+        S->pre_built = true;
+        return;
+    }
     CsrHost A = build_schur(S, node2free, S->nf);
+    if (h->opts.schur_solver == 1) {
+        build_chol(S, A);
+        S->pre_built = true;
+        return;
+    }
     const int kCoarse = 1024;
     while (true) {
         if (A.n <= kCoarse) {
@@ -1031,6 +1156,11 @@ static void build_amg(svh_handle* h, const std::vector<int32_t>& fixed, int nvp)
     }
     SVH_CUDA(cudaMalloc(&S->d_kc, S->levels.size() * 8 * 2 * (size_t)S->nvp_cap * sizeof(double)));
     SVH_CUDA(cudaMemset(S->d_kc, 0, S->levels.size() * 8 * 2 * (size_t)S->nvp_cap * sizeof(double)));
+    for (const auto& L : S->levels)
+        S->pre_bytes += (double)L.nnz * 12 + (double)L.ellw * L.n * 12 + (double)L.n * (4 + 8) +
+                        (double)L.n * 2 * 8 * S->nvp_cap * 9;
+    S->pre_bytes += (double)S->ncoarse * S->ncoarse * 8;
+    S->pre_built = true;
 }
 
 // ---------------------------------------------------------------------------
@@ -1214,6 +1344,15 @@ static int pcgV(svh_handle* h, const double* b, double* x, double tol, int maxit
     return it;
 }
 
+// S^-1 of the preconditioner: AMG-preconditioned CG, or the sparse-direct comparator
+static int schur_solve(svh_handle* h, const double* b, double* x, double tol, int maxit, cudaStream_t s, int NVP) {
+    if (h->opts.schur_solver == 1) {
+        chol_solveV(h->solve, b, x, s, NVP);
+        return 1;
+    }
+    return pcgV(h, b, x, tol, maxit, s, NVP);
+}
+
 // out = Q^-1 in  (right preconditioner)
 static void precond(svh_handle* h, const double2* in, double2* out, double tol, int maxit, cudaStream_t s) {
     Solve* S = h->solve;
@@ -1225,7 +1364,7 @@ static void precond(svh_handle* h, const double2* in, double2* out, double tol, 
     if (S->nf > 0) {
         SVH_LAUNCH(k_pre_e2, nblk(S->nf), 256, 0, s, tt, in + n5, e2, S->d_free_list, S->d_node_vox, S->d_node_axis, K,
                    S->nf);
-        S->inner_its += pcgV(h, e2, b2, tol, maxit, s, 1);
+        S->inner_its += schur_solve(h, e2, b2, tol, maxit, s, 1);
     }
     SVH_LAUNCH(k_pre_b, nblk(S->M), 256, 0, s, b2, in + n5, out + n5, S->d_node2free, S->M);
     SVH_LAUNCH(k_pre_a, nblk(K), 256, 0, s, in, out + n5, S->d_yinv, out, S->d_fnode, S->d_free, K);
@@ -1435,7 +1574,7 @@ static void fgmres_batch(svh_handle* h, BatchWork& W, int nb, double2* const* bb
                                S->d_node_vox, S->d_node_axis, K, S->nf, NVP, p);
             }
             auto c0 = std::chrono::steady_clock::now();
-            if (S->nf > 0) S->inner_its += pcgV(h, e2, b2, tol_inner, inner_max, s, NVP);
+            if (S->nf > 0) S->inner_its += schur_solve(h, e2, b2, tol_inner, inner_max, s, NVP);
             for (int p : act) {
                 SVH_LAUNCH(k_pre_bV, nblk(S->M), 256, 0, s, b2, W.V(p, j) + n5, W.Z(p, j) + n5, S->d_node2free, S->M,
                            NVP, p);
@@ -1743,6 +1882,9 @@ static void solve_columns(svh_handle* h, const svh_port* ports, int P, const int
         st->inner_iterations += S->inner_its;
         st->t_matvec_s += S->t_matvec;
         st->t_precond_s += S->t_precond;
+        st->t_precond_setup_s = S->t_pre_setup;
+        st->precond_bytes = S->pre_bytes;
+        st->schur_solver = h->opts.schur_solver;
         st->converged = all_conv ? 1 : 0;
         st->final_rre = std::max(st->final_rre, worst);
         st->t_solve_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

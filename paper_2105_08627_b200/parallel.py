@@ -158,3 +158,66 @@ class SlabMatvec:
             self.h.slab_backward(r, P, recvs[r], slabs[r], o, green_only)
             out[:, :, :, r * Kyl:(r + 1) * Kyl, :] = o
         return out
+
+
+class P2PSlabMatvec:
+    """Fused-exchange slab matvec (SURVEY 8(e)(2) fused variant): svh_slab_forward_p2p /
+    svh_slab_middle_p2p store each destination's chunk straight into the peer's receive buffer
+    over NVLink peer memory (CUDA IPC) and synchronise with stream memory operations -- no
+    all-to-all, no local send buffer, no host synchronisation.  The process group is used once,
+    at construction, to exchange the 64-byte IPC handles (all_gather_object)."""
+
+    def __init__(self, handle, nrhs, group=None):
+        import torch.distributed as dist
+        from . import svh
+        self.h, self.group = handle, group
+        self.P, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        self.Kyl, self.Nxl, self.chunk, self.per_rhs = handle.slab_sizes(self.P)
+        self.nrhs = int(nrhs)
+        nb = self.nrhs * self.per_rhs * 8
+        self.own = [svh.ipc_alloc(nb), svh.ipc_alloc(nb), svh.ipc_alloc(2 * self.P * 4)]   # recv1, recv2, flags
+        handles = [None] * self.P
+        dist.all_gather_object(handles, [hd for _, hd in self.own], group=group)
+        self.peer = []          # [buffer kind][peer rank] -> device pointer in this process
+        self.opened = []
+        for k in range(3):
+            row = []
+            for p in range(self.P):
+                if p == self.rank:
+                    row.append(self.own[k][0])
+                else:
+                    ptr = svh.ipc_open(handles[p][k])
+                    self.opened.append(ptr)
+                    row.append(ptr)
+            self.peer.append(row)
+        self.epoch = 0
+        dist.barrier(group=group)
+
+    def matvec(self, I_slab, green_only=False):
+        """This rank's slab of Z.I ([nrhs][5][Kz][Kyl][Kx]); every rank calls it the same number
+        of times (collective by construction)."""
+        import torch
+        I_slab = I_slab.contiguous()
+        assert I_slab.shape[0] == self.nrhs
+        self.epoch += 1
+        out = torch.empty_like(I_slab)
+        self.h.slab_forward_p2p(self.rank, self.P, I_slab, self.peer[0], self.peer[2], self.epoch)
+        self.h.slab_middle_p2p(self.rank, self.P, self.own[0][0], self.peer[1], self.peer[2], self.epoch, self.nrhs)
+        self.h.slab_backward(self.rank, self.P, self.own[1][0], I_slab, out, green_only)
+        return out
+
+    def close(self):
+        """Collective: unmap the peers' buffers and free this rank's (after a barrier, so no
+        peer still writes into them)."""
+        import torch
+        import torch.distributed as dist
+        from . import svh
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)
+        for p in self.opened:
+            svh.ipc_close(p)
+        dist.barrier(group=self.group)
+        for ptr, _ in self.own:
+            svh.ipc_free(ptr)
+        self.opened, self.own = [], []
+

@@ -48,7 +48,7 @@ class Opts(ctypes.Structure):
     _fields_ = [("tucker_tol", ctypes.c_double), ("restart", ctypes.c_int32), ("rre", ctypes.c_double),
                 ("inner_tol", ctypes.c_double), ("inner_maxit", ctypes.c_int32), ("max_iters", ctypes.c_int32),
                 ("rhs_chunk", ctypes.c_int32), ("verbose", ctypes.c_int32), ("kernel_cache", ctypes.c_char_p),
-                ("plan", ctypes.c_int32), ("precision", ctypes.c_int32)]
+                ("plan", ctypes.c_int32), ("precision", ctypes.c_int32), ("schur_solver", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
@@ -56,7 +56,8 @@ class Stats(ctypes.Structure):
                 ("inner_iterations", ctypes.c_int32), ("converged", ctypes.c_int32), ("final_rre", ctypes.c_double),
                 ("t_setup_s", ctypes.c_double), ("t_solve_s", ctypes.c_double), ("t_matvec_s", ctypes.c_double),
                 ("t_precond_s", ctypes.c_double), ("ranks", (ctypes.c_int32 * 3) * 7),
-                ("compression_ratio", ctypes.c_double)]
+                ("compression_ratio", ctypes.c_double), ("t_precond_setup_s", ctypes.c_double),
+                ("precond_bytes", ctypes.c_double), ("schur_solver", ctypes.c_int32)]
 
     def as_dict(self):
         d = {f: getattr(self, f) for f, _ in self._fields_ if f != "ranks"}
@@ -83,6 +84,15 @@ def lib():
         L.svh_unknowns.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]
         L.svh_embedding.argtypes = [vp, ctypes.POINTER(i32)]
         L.svh_plan_info.argtypes = [vp, ctypes.POINTER(i64)]
+        vpp = ctypes.POINTER(vp)
+        L.svh_ipc_alloc.argtypes = [ctypes.c_size_t, vpp, ctypes.c_char_p]
+        L.svh_ipc_free.argtypes = [vp]
+        L.svh_ipc_open.argtypes = [ctypes.c_char_p, vpp]
+        L.svh_ipc_close.argtypes = [vp]
+        L.svh_slab_forward_p2p.argtypes = [vp, i32, i32, vp, vpp, vpp, ctypes.c_uint32, i32, vp]
+        L.svh_slab_middle_p2p.argtypes = [vp, i32, i32, vp, vpp, vpp, ctypes.c_uint32, i32, vp]
+        L.svh_matvec_plan.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(ctypes.c_float),
+                                      ctypes.POINTER(ctypes.c_float)]
         L.svh_slab_sizes.argtypes = [vp, i32, ctypes.POINTER(i64)]
         L.svh_matvec_host.argtypes = [vp, vp, vp, i32, i32, i32, vp]
         L.svh_kernel_cache_build.argtypes = [ctypes.c_char_p, ctypes.POINTER(i32), dbl, i32]
@@ -108,7 +118,9 @@ def lib():
         for name in ("svh_kernel_cache_build", "svh_matvec_host", "svh_slab_sizes", "svh_slab_forward", "svh_slab_middle", "svh_slab_backward",
                      "svh_setup", "svh_set_frequency", "svh_unknowns", "svh_embedding", "svh_plan_info", "svh_matvec",
                      "svh_matvec_grid", "svh_apply_system", "svh_solve", "svh_solve_columns", "svh_get_kernels",
-                     "svh_get_stats", "svh_profile_enable", "svh_profile_read", "svh_y_to_zl"):
+                     "svh_get_stats", "svh_profile_enable", "svh_profile_read", "svh_y_to_zl", "svh_matvec_plan",
+                     "svh_ipc_alloc", "svh_ipc_free", "svh_ipc_open", "svh_ipc_close", "svh_slab_forward_p2p",
+                     "svh_slab_middle_p2p"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -119,7 +131,9 @@ EXPORTED = ("svh_default_opts", "svh_setup", "svh_set_frequency", "svh_unknowns"
             "svh_slab_backward",
             "svh_matvec",
             "svh_matvec_grid", "svh_apply_system", "svh_solve", "svh_solve_columns", "svh_get_kernels",
-            "svh_get_stats", "svh_profile_enable", "svh_profile_read", "svh_y_to_zl", "svh_destroy",
+            "svh_get_stats", "svh_profile_enable", "svh_profile_read", "svh_y_to_zl", "svh_matvec_plan",
+            "svh_ipc_alloc", "svh_ipc_free", "svh_ipc_open", "svh_ipc_close", "svh_slab_forward_p2p",
+            "svh_slab_middle_p2p", "svh_destroy",
             "svh_last_error", "svh_launch_count")
 
 
@@ -145,6 +159,32 @@ def y_to_zl(Y, freq):
 
 def launch_count() -> int:
     return int(lib().svh_launch_count())
+
+
+def _ptr_array(ptrs):
+    return (ctypes.c_void_p * len(ptrs))(*[ctypes.c_void_p(int(p)) for p in ptrs])
+
+
+def ipc_alloc(nbytes):
+    """svh_ipc_alloc: a zeroed device buffer and its 64-byte CUDA IPC handle -> (ptr, handle)."""
+    p = ctypes.c_void_p()
+    hd = ctypes.create_string_buffer(64)
+    _check(lib().svh_ipc_alloc(int(nbytes), ctypes.byref(p), hd))
+    return int(p.value), bytes(hd.raw)
+
+
+def ipc_open(handle):
+    p = ctypes.c_void_p()
+    _check(lib().svh_ipc_open(bytes(handle), ctypes.byref(p)))
+    return int(p.value)
+
+
+def ipc_close(ptr):
+    _check(lib().svh_ipc_close(ctypes.c_void_p(int(ptr))))
+
+
+def ipc_free(ptr):
+    _check(lib().svh_ipc_free(ctypes.c_void_p(int(ptr))))
 
 
 def _stream_ptr(stream):
@@ -280,8 +320,22 @@ class Handle:
         _check(lib().svh_slab_middle(self._h, int(rank), int(P), ctypes.c_void_p(recv.data_ptr()),
                                      ctypes.c_void_p(send.data_ptr()), int(nrhs), _stream_ptr(stream)))
 
+    def slab_forward_p2p(self, rank, P, I_slab, recv1_peers, flag_peers, epoch, stream=None):
+        """Fused-exchange forward step: pass A, chunks stored into the peers' recv1 buffers (raw
+        device pointers, indexed by rank), flag slot 0 = epoch, stream wait for every peer."""
+        _check(lib().svh_slab_forward_p2p(self._h, int(rank), int(P), ctypes.c_void_p(I_slab.data_ptr()),
+                                          _ptr_array(recv1_peers), _ptr_array(flag_peers), int(epoch),
+                                          I_slab.shape[0], _stream_ptr(stream)))
+
+    def slab_middle_p2p(self, rank, P, recv1, recv2_peers, flag_peers, epoch, nrhs, stream=None):
+        _check(lib().svh_slab_middle_p2p(self._h, int(rank), int(P), ctypes.c_void_p(int(recv1)),
+                                         _ptr_array(recv2_peers), _ptr_array(flag_peers), int(epoch), int(nrhs),
+                                         _stream_ptr(stream)))
+
     def slab_backward(self, rank, P, recv, I_slab, out, green_only=False, stream=None):
-        _check(lib().svh_slab_backward(self._h, int(rank), int(P), ctypes.c_void_p(recv.data_ptr()),
+        """recv: a device tensor or a raw device pointer (int, e.g. an svh_ipc_alloc buffer)."""
+        recv = recv if isinstance(recv, int) else recv.data_ptr()
+        _check(lib().svh_slab_backward(self._h, int(rank), int(P), ctypes.c_void_p(recv),
                                        ctypes.c_void_p(I_slab.data_ptr()), ctypes.c_void_p(out.data_ptr()),
                                        I_slab.shape[0], int(green_only), _stream_ptr(stream)))
 
@@ -336,11 +390,18 @@ class Handle:
         _check(lib().svh_profile_enable(self._h, int(on)))
 
     def profile_read(self, reset=True):
-        ms = np.zeros(5)
-        n = np.zeros(5, dtype=np.int64)
+        """Per-record device ms and launch counts: [0:5] = P5 passes A..E, [5] = whole P3s products."""
+        ms = np.zeros(6)
+        n = np.zeros(6, dtype=np.int64)
         _check(lib().svh_profile_read(self._h, ms.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
                                       n.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), int(reset)))
         return ms, n
+
+    def matvec_plan(self):
+        """(plan of the last matvec chunk: 3 = P3s / 5 = P5, P5 ms, P3s ms of the last auto-selection)."""
+        p, a, b = ctypes.c_int32(), ctypes.c_float(), ctypes.c_float()
+        _check(lib().svh_matvec_plan(self._h, ctypes.byref(p), ctypes.byref(a), ctypes.byref(b)))
+        return int(p.value), float(a.value), float(b.value)
 
     def stats(self):
         st = Stats()

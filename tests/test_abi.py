@@ -51,13 +51,13 @@ def test_host_only_calls():
 
 def test_opts_validation_host_only():
     """svh_opts is validated before any device work: restart range (the FGMRES Hessenberg
-    scratch), plan (only P5 is built) and precision (only complex64 is built)."""
+    scratch), plan (0 auto, 3 P3s, 5 P5) and precision (only complex64 is built)."""
     from paper_2105_08627_b200 import svh
     L = svh.lib()
     g = svh.Grid(2, 1, 1, 1e-6)
     mats = (svh.Material * 1)(svh.Material(1e7, 1e-7))
     mat = (ctypes.c_uint8 * 2)(1, 1)
-    for field, bad, msg in (("restart", 5000, b"restart"), ("restart", 0, b"restart"), ("plan", 3, b"plan"),
+    for field, bad, msg in (("restart", 5000, b"restart"), ("restart", 0, b"restart"), ("plan", 4, b"plan"),
                             ("precision", 1, b"complex64"), ("tucker_tol", 1.5, b"tucker_tol")):
         o = svh.Opts()
         L.svh_default_opts(ctypes.byref(o))
