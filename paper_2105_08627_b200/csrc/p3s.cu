@@ -23,6 +23,7 @@
 // column stays in shared memory in the two-level order (ky = k1 + R1 k2 at position R2 k1 + k2),
 // which every step reads and writes in place (no read/write hazard inside a step).
 #include <algorithm>
+#include <vector>
 #include <cuda_runtime.h>
 
 #include "fft.cuh"
@@ -479,20 +480,34 @@ __global__ void __launch_bounds__(512, 1)
     }
 }
 
+// kernel attributes and resident-CTA counts are queried once per (device, kernel, size): these
+// driver calls cost host time on every launch otherwise, and a P3s product on a thin grid is
+// only ~0.5 ms of device work
+struct AttrRec {
+    int dev;
+    const void* k;
+    size_t smem;
+    int ctas;
+};
 template <typename F>
-void prep_attr(F* kern, size_t bytes) {
-    SVH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                  (int)cudaSharedmemCarveoutMaxShared));
-    SVH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-}
-
-template <typename F>
-int grid_for(F kern, int nt, size_t smem, int64_t units) {
-    int dev = 0, nsm = 148, occ = 1;
+int grid_for(F* kern, int nt, size_t smem, int64_t units) {
+    static thread_local std::vector<AttrRec> cache;
+    int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, smem);
-    return (int)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)nsm * std::max(occ, 1)));
+    int ctas = 0;
+    for (const auto& r : cache)
+        if (r.dev == dev && r.k == (const void*)kern && r.smem == smem) ctas = r.ctas;
+    if (ctas == 0) {
+        SVH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                      (int)cudaSharedmemCarveoutMaxShared));
+        SVH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int nsm = 148, occ = 1;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, smem);
+        ctas = nsm * std::max(occ, 1);
+        cache.push_back(AttrRec{dev, (const void*)kern, smem, ctas});
+    }
+    return (int)std::max<int64_t>(1, std::min<int64_t>(units, ctas));
 }
 
 P3Planes planes_of(const svh_handle* h) {
@@ -563,7 +578,6 @@ void run_a3(svh_handle* h, const P3Planes& pl, const float2* in, float2* XT, boo
     const int64_t ntiles = (int64_t)5 * nr * pl.Pn * nyb;
     const size_t smem = (size_t)TY * p3_rs<NX>() * sizeof(float2);
     auto go = [&](auto kern) {
-        prep_attr(kern, smem);
         SVH_LAUNCH(kern, grid_for(kern, NT, smem, ntiles), NT, smem, s, in, XT, h->d_rowinfo, h->rowW, h->d_rowmask,
                    h->rowMW, pl, h->d_tw[0], h->kx, h->ky, h->K, h->Kt, (int)ntiles, nyb);
     };
@@ -582,7 +596,6 @@ void run_e3(svh_handle* h, const P3Planes& pl, const float2* XT, const float2* i
     const size_t smem = (size_t)TY * p3_rs<NX>() * sizeof(float2);
     const int nzl = (int)h->mats.size() + 1;
     auto go = [&](auto kern) {
-        prep_attr(kern, smem);
         SVH_LAUNCH(kern, grid_for(kern, NT, smem, ntiles), NT, smem, s, XT, out, in, h->d_rowinfo, h->rowW,
                    h->d_rowmask, h->rowMW, pl, h->d_matp, h->d_zloc, nzl, h->d_tw[0], h->kx, h->ky, h->kz, h->K,
                    h->Kt, (int)green_only, (int)ntiles, nyb);
@@ -618,7 +631,6 @@ void run_yz(svh_handle* h, const P3Planes& pl, float2* XT, int TY, int nr, cudaS
     }
     auto go = [&](auto kern, bool kvg) {
         const size_t smem = P3YZ<NY, NZ>::smem(pl.Pn, h->use_tucker, kvg);
-        prep_attr(kern, smem);
         SVH_LAUNCH(kern, grid_for(kern, 512, smem, h->nx), 512, smem, s, XT, sv, h->d_kvt, h->d_tw[1], h->nx, h->ky,
                    h->kz, h->d_rowmask, h->rowMW, pl, TY, h->gscale, nr);
     };

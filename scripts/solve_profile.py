@@ -30,7 +30,14 @@ def main():
         h = svh.setup_case(case, tucker_tol=0.0, inner_tol=a.inner_tol, rre=a.rre, schur_solver=a.schur)
         torch.cuda.synchronize()
         t1 = time.perf_counter()
-        res = h.solve(case["ports"])
+        try:
+            res = h.solve(case["ports"])
+        except svh.SvhError as e:   # e.g. the sparse-direct factor does not fit one GPU (cfg4)
+            print(json.dumps({"workload": case["name"], "K": h.K, "M": h.M, "schur_solver": a.schur,
+                              "error": str(e)}), flush=True)
+            h.close()
+            torch.cuda.empty_cache()
+            continue
         t2 = time.perf_counter()
         st = res["stats"]
         print(json.dumps({"workload": case["name"], "K": h.K, "M": h.M, "ports": len(case["ports"]),

@@ -59,7 +59,7 @@ def test_direct_multiport_vs_oracle(svh_lib):
 
 def test_direct_config2_golden(svh_lib):
     case = svh_inputs.config2()
-    pt = GOLDEN["points"][2]
+    pt = GOLDEN["points"][-1]
     with svh_lib.setup_case(case, rre=1e-7, schur_solver=1) as h:
         h.set_frequency(pt["freq_hz"])
         res = h.solve(case["ports"])
