@@ -20,7 +20,7 @@ OBJ = os.path.join(HERE, "_build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-         "-I", INC, "-I", CSRC, "-Xptxas", "-warn-spills"]
+         "-I", INC, "-I", CSRC, "-Xptxas", "-warn-spills", "-Xcompiler", "-Wno-deprecated-declarations"]
 
 
 def _newest_header():

@@ -121,9 +121,6 @@ void slab_backward(svh_handle* h, int rank, int P, const float2* recv, const flo
 bool p3s_eligible(const svh_handle* h);
 void p3s_matvec(svh_handle* h, const float2* in, float2* out, float2* XT, int nr, bool green_only, bool packed,
                 cudaStream_t s);
-// zblk.cu (pass C on the blocked X2 layout of the 2048-point y passes)
-bool zblk_supported(const svh_handle* h);
-void run_zblk(svh_handle* h, float2* X2, int nrhs, cudaStream_t s);
 // quad.cu
 void compute_kernels(svh_handle* h);
 // cache.cu (Algorithm 2)

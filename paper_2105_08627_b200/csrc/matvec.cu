@@ -1361,10 +1361,9 @@ struct Geom {
     int kyl, y0;              // rows of the row passes
     const int32_t* rowlist;   // pass A: non-empty global rows z*Ky + y (ascending)
     int nrows;
-    bool blk = false;         // X2 in the blocked layout [rc][ky][kx/8][z][kx%8] (ypass.cuh, zblk.cu)
 };
 static Geom whole_grid(const svh_handle* h) {
-    return Geom{h->nx, 0, h->ky, 0, h->d_rowlist, (int)h->n_rows_ne, zblk_supported(h)};
+    return Geom{h->nx, 0, h->ky, 0, h->d_rowlist, (int)h->n_rows_ne};
 }
 namespace {
 
@@ -1446,35 +1445,18 @@ void run_pass_y(svh_handle* h, const Geom& g, const float2* in, float2* out, int
         CUtensorMap tin, tout;
         const int rows_in = DIR < 0 ? h->ky : h->ny;
         const float2* x2 = DIR < 0 ? out : in;   // the X2 side of the pass
-        // blocked X2 (g.blk): a 4-D map (kx % 8, z, kx / 8, rc Ny + ky), box (Q, 1, 1, BOX)
-        auto x2map = [&](CUtensorMap* m) -> bool {
-            if (!g.blk)
-                return encode_tmap_c64_3d(m, x2, (uint64_t)nx, (uint64_t)h->ny, (uint64_t)5 * nrhs * h->kz,
-                                          (uint64_t)nx, (uint64_t)nx * h->ny, Q, P::BOX);
-            const uint64_t d[4] = {(uint64_t)kZB, (uint64_t)h->kz, (uint64_t)nx / kZB, (uint64_t)5 * nrhs * h->ny};
-            const uint64_t st[3] = {(uint64_t)kZB, (uint64_t)kZB * h->kz, (uint64_t)nx * h->kz};
-            const uint32_t b[4] = {(uint32_t)Q, 1, 1, (uint32_t)P::BOX};
-            return encode_tmap_c64_4d(m, x2, d, st, b);
-        };
-        const bool ok = nx % Q == 0 &&
-                        (DIR < 0 ? encode_tmap_c64_3d(&tin, in, (uint64_t)nx, (uint64_t)rows_in,
-                                                      (uint64_t)5 * nrhs * h->kz, (uint64_t)nx,
-                                                      (uint64_t)nx * rows_in, Q, P::BOX) && x2map(&tout)
-                                 : x2map(&tin) && x2map(&tout));
-        SVH_CHECK(ok || !g.blk, SVH_ECUDA, "blocked X2 layout: tensor map encoding failed");
-        if (ok) {
+        if (nx % Q == 0 &&
+            encode_tmap_c64_3d(&tin, in, (uint64_t)nx, (uint64_t)rows_in, (uint64_t)5 * nrhs * h->kz, (uint64_t)nx,
+                               (uint64_t)nx * rows_in, Q, P::BOX) &&
+            encode_tmap_c64_3d(&tout, x2, (uint64_t)nx, (uint64_t)h->ny, (uint64_t)5 * nrhs * h->kz, (uint64_t)nx,
+                               (uint64_t)nx * h->ny, Q, P::BOX)) {
             const int tiles_x = nx / Q;
             const int ntiles = tiles_x * h->nzp * 5 * nrhs;
-            auto go = [&](auto kern) {
-                prep(kern, P::smem);
-                SVH_LAUNCH(kern, persistent_grid(kern, P::NT, P::smem, ntiles), P::NT, P::smem, s, out, tin, tout,
-                           h->d_tw[1], nx, h->kz, Lin, Lout, ntiles, tiles_x, h->d_planes, h->nzp, h->d_rowmask,
-                           h->rowMW);
-            };
-            if (g.blk)
-                go(k_ypass<N, Q, DIR, true>);
-            else
-                go(k_ypass<N, Q, DIR, false>);
+            auto kern = k_ypass<N, Q, DIR>;
+            prep(kern, P::smem);
+            SVH_LAUNCH(kern, persistent_grid(kern, P::NT, P::smem, ntiles), P::NT, P::smem, s, out, tin, tout,
+                       h->d_tw[1], nx, h->kz, Lin, Lout, ntiles, tiles_x, h->d_planes, h->nzp, h->d_rowmask,
+                       h->rowMW);
             return;
         }
     }
@@ -1531,10 +1513,6 @@ bool launch_ztma2(svh_handle* h, const Geom& g, float2* X2, int nrhs, const Spec
 
 template <int N>
 void run_pass_c(svh_handle* h, const Geom& g, float2* X2, int nrhs, cudaStream_t s) {
-    if (g.blk) {   // blocked X2 layout (2048-point y passes): contiguous z tiles (zblk.cu)
-        run_zblk(h, X2, nrhs, s);
-        return;
-    }
     SpecView sv{};
     sv.spec = h->use_tucker ? nullptr : h->d_spec;
     sv.hx = h->hx;

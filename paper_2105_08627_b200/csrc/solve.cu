@@ -440,26 +440,53 @@ __global__ void k_denseV(int n, const double* __restrict__ Ci, const double* __r
         x[2 * wid + 1] = a1;
     }
 }
-// Deterministic dot products of NV = 2^(sh+1) real vectors stored [n][NV]: up to 3 pairs
-// (a_d, b_d) at once.  Block b of kDotBlocks sums rows [b n / G, (b+1) n / G); within a block,
-// lane l of the warp owning (d, v) sums rows lo + l, lo + l + 32, ... in order, then a fixed
-// shuffle tree.  The summation order of every vector depends only on n -- not on NV, the other
-// vectors or scheduling -- so a port's inner solve is bitwise the same alone or in a batch.
-constexpr int kDotBlocks = 128;
-__global__ void k_ddotP(int n, int nd, const double* __restrict__ a0, const double* __restrict__ b0,
-                        const double* __restrict__ a1, const double* __restrict__ b1, const double* __restrict__ a2,
-                        const double* __restrict__ b2, double* __restrict__ part, int sh) {
-    const int NV = 2 << sh;
+// Deterministic dot products of NV = 2^(SH+1) real vectors stored [n][NV]: up to 3 pairs
+// (a_d, b_d) at once.  Block b of G (G a function of n only) sums rows [b n / G, (b+1) n / G);
+// thread t of the block sums rows lo + t, lo + t + 256, ... in order for every vector v (its
+// row's NV values are one contiguous 8 NV-byte run: the block reads the range coalesced, each
+// vector once per pair), then a fixed shuffle tree per warp and the 8 warps in order.  The
+// summation order of every vector depends only on n -- not on NV, the other vectors or
+// scheduling -- so a port's inner solve is bitwise the same alone or in a batch.
+constexpr int kDotBlocks = 592;
+constexpr int kDotThreads = 256;
+template <int SH>
+__global__ void __launch_bounds__(kDotThreads)
+    k_ddotP(int n, int nd, const double* __restrict__ a0, const double* __restrict__ b0,
+            const double* __restrict__ a1, const double* __restrict__ b1, const double* __restrict__ a2,
+            const double* __restrict__ b2, double* __restrict__ part) {
+    constexpr int NV = 2 << SH;
+    __shared__ double red[kDotThreads / 32][NV];
     const int lo = (int)((int64_t)n * blockIdx.x / gridDim.x), hi = (int)((int64_t)n * (blockIdx.x + 1) / gridDim.x);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int item = warp; item < nd * NV; item += nw) {
-        const int d = item / NV, v = item % NV;
-        const double* a = d == 0 ? a0 : d == 1 ? a1 : a2;
-        const double* b = d == 0 ? b0 : d == 1 ? b1 : b2;
-        double acc = 0;
-        for (int i = lo + lane; i < hi; i += 32) acc = fma(a[(int64_t)i * NV + v], b[(int64_t)i * NV + v], acc);
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffff, acc, o);
-        if (lane == 0) part[((int64_t)blockIdx.x * nd + d) * NV + v] = acc;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int d = 0; d < nd; ++d) {
+        const double2* a = reinterpret_cast<const double2*>(d == 0 ? a0 : d == 1 ? a1 : a2);
+        const double2* b = reinterpret_cast<const double2*>(d == 0 ? b0 : d == 1 ? b1 : b2);
+        double acc[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+        for (int i = lo + (int)threadIdx.x; i < hi; i += kDotThreads) {
+#pragma unroll
+            for (int v2 = 0; v2 < NV / 2; ++v2) {
+                const double2 x = __ldg(&a[(int64_t)i * (NV / 2) + v2]);
+                const double2 y = __ldg(&b[(int64_t)i * (NV / 2) + v2]);
+                acc[2 * v2] = fma(x.x, y.x, acc[2 * v2]);
+                acc[2 * v2 + 1] = fma(x.y, y.y, acc[2 * v2 + 1]);
+            }
+        }
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+            for (int o = 16; o > 0; o >>= 1) acc[v] += __shfl_xor_sync(0xffffffff, acc[v], o);
+        if (lane == 0)
+#pragma unroll
+            for (int v = 0; v < NV; ++v) red[warp][v] = acc[v];
+        __syncthreads();
+        if (threadIdx.x < NV) {
+            double t = 0.0;
+#pragma unroll
+            for (int w = 0; w < kDotThreads / 32; ++w) t += red[w][threadIdx.x];
+            part[((int64_t)blockIdx.x * nd + d) * NV + threadIdx.x] = t;
+        }
+        __syncthreads();
     }
 }
 // out[d * ostride + v] = sum over blocks (ascending) of the partials
@@ -1212,8 +1239,15 @@ static void apply_sys(svh_handle* h, const double2* x, double2* y, bool masked, 
 // deterministic dot products (k_ddotP / k_ddotF): nd <= 3 pairs, results at out[d * ostride + v]
 static void ddot(Solve* S, int n, int nd, const double* a0, const double* b0, const double* a1, const double* b1,
                  const double* a2, const double* b2, double* out, int ostride, int sh, cudaStream_t s) {
-    const int nb = std::min(kDotBlocks, std::max(1, (n + 255) / 256));   // a function of n only
-    SVH_LAUNCH(k_ddotP, nb, 256, 0, s, n, nd, a0, b0, a1, b1, a2, b2, S->d_part, sh);
+    const int nb = std::min(kDotBlocks, std::max(1, (n + 1023) / 1024));   // a function of n only
+    switch (sh) {
+        case 0: SVH_LAUNCH(k_ddotP<0>, nb, kDotThreads, 0, s, n, nd, a0, b0, a1, b1, a2, b2, S->d_part); break;
+        case 1: SVH_LAUNCH(k_ddotP<1>, nb, kDotThreads, 0, s, n, nd, a0, b0, a1, b1, a2, b2, S->d_part); break;
+        case 2: SVH_LAUNCH(k_ddotP<2>, nb, kDotThreads, 0, s, n, nd, a0, b0, a1, b1, a2, b2, S->d_part); break;
+        case 3: SVH_LAUNCH(k_ddotP<3>, nb, kDotThreads, 0, s, n, nd, a0, b0, a1, b1, a2, b2, S->d_part); break;
+        case 4: SVH_LAUNCH(k_ddotP<4>, nb, kDotThreads, 0, s, n, nd, a0, b0, a1, b1, a2, b2, S->d_part); break;
+        default: throw Error{SVH_EINVAL, "ddot: at most 16 vector pairs"};
+    }
     SVH_LAUNCH(k_ddotF, 1, 128, 0, s, nb, nd, S->d_part, out, ostride, sh);
 }
 

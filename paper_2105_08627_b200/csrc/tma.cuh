@@ -64,40 +64,6 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
-// 4-D tiled TMA load / store (the blocked X2 layout of the 2048-point y passes, zblk.cu)
-__device__ __forceinline__ void tma_load_4d(void* smem_dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
-                                            uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
-        "[%6];\n" ::"r"(smem_u32(smem_dst)),
-        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, int c0, int c1, int c2, int c3,
-                                             const void* smem_src) {
-    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4}], [%5];\n" ::"l"(map),
-                 "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(smem_src))
-                 : "memory");
-}
-// 1-D bulk copies (contiguous, 16-byte multiples): global -> shared on an mbarrier, shared ->
-// global in the issuing thread's bulk group
-__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                     smem_u32(smem_dst)),
-                 "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, uint32_t bytes) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst), "r"(smem_u32(smem_src)),
-                 "r"(bytes)
-                 : "memory");
-}
-// wait until at most N of the issuing thread's committed bulk groups are still reading shared memory
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-    asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory");
-}
-
 // host: encode a 3-D tensor map of 8-byte elements (complex64) with a [box0, box1, 1] box.
 // dims/strides in elements; returns false if the driver entry point is unavailable.
 bool encode_tmap_c64_3d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
@@ -106,9 +72,5 @@ bool encode_tmap_c64_3d(CUtensorMap* map, const void* base, uint64_t d0, uint64_
 bool encode_tmap_c64_3d_box(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
                             uint64_t stride1_elems, uint64_t stride2_elems, uint32_t box0, uint32_t box1,
                             uint32_t box2);
-
-// host: 4-D tensor map of complex64, dims d[0..3] (elements), strides s[0..2] of dims 1..3
-// (elements), box b[0..3]
-bool encode_tmap_c64_4d(CUtensorMap* map, const void* base, const uint64_t* d, const uint64_t* s, const uint32_t* b);
 
 }  // namespace svh

@@ -45,17 +45,4 @@ bool encode_tmap_c64_3d_box(CUtensorMap* map, const void* base, uint64_t d0, uin
     return r == CUDA_SUCCESS;
 }
 
-bool encode_tmap_c64_4d(CUtensorMap* map, const void* base, const uint64_t* d, const uint64_t* s, const uint32_t* b) {
-    EncodeFn fn = encode_fn();
-    if (!fn) return false;
-    const cuuint64_t dims[4] = {d[0], d[1], d[2], d[3]};
-    const cuuint64_t strides[3] = {s[0] * 8, s[1] * 8, s[2] * 8};
-    const cuuint32_t box[4] = {b[0], b[1], b[2], b[3]};
-    const cuuint32_t estr[4] = {1, 1, 1, 1};
-    const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(base), dims, strides, box, estr,
-                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS;
-}
-
 }  // namespace svh

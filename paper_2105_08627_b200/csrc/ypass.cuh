@@ -34,11 +34,7 @@ struct YPlan {
     static constexpr size_t smem = S * stage_b + W_b + O_b + (size_t)S * MW * 4 + S * 8 + 64;
 };
 
-// kx block of the blocked X2 layout (BLK): X2 = [rc][ky][kx / kZB][z][kx % kZB], so the z
-// pencils of kZB consecutive kx at one (rc, ky) are one contiguous run (pass C, zblk.cu)
-constexpr int kZB = 8;
-
-template <int N, int Q, int DIR, bool BLK = false>
+template <int N, int Q, int DIR>
 __global__ void __launch_bounds__(YPlan<N, Q, DIR>::NT, 1)
     k_ypass(float2* __restrict__ out, const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
             const float2* __restrict__ tw,
@@ -68,13 +64,6 @@ __global__ void __launch_bounds__(YPlan<N, Q, DIR>::NT, 1)
         p = rc * Kz + z;
         x0 = xt * Q;
     };
-    // X2-side box coordinates: 3-D (kx, row, plane) or, blocked, 4-D (kx % kZB, z, kx / kZB, rc N + row)
-    auto x2_load = [&](float2* dst, int x0, int row, int p, int z, uint64_t* b) {
-        if constexpr (BLK)
-            tma_load_4d(dst, &tin, x0 % kZB, z, x0 / kZB, (p / Kz) * N + row, b);
-        else
-            tma_load_3d(dst, &tin, x0, row, p, b);
-    };
     // thread 0: TMA of tile t into slot st (+ the plane's row-mask words)
     auto issue = [&](int t, int st) {
         if (t >= ntiles) return;
@@ -82,12 +71,7 @@ __global__ void __launch_bounds__(YPlan<N, Q, DIR>::NT, 1)
         decode(t, z, p, x0);
         mbar_arrive_expect_tx(&bar[st], (uint32_t)P::stage_b);
 #pragma unroll
-        for (int b = 0; b < SR / BOX; ++b) {
-            if (DIR > 0)
-                x2_load(stage + st * SR * Q + b * BOX * Q, x0, b * BOX, p, z, &bar[st]);
-            else
-                tma_load_3d(stage + st * SR * Q + b * BOX * Q, &tin, x0, b * BOX, p, &bar[st]);
-        }
+        for (int b = 0; b < SR / BOX; ++b) tma_load_3d(stage + st * SR * Q + b * BOX * Q, &tin, x0, b * BOX, p, &bar[st]);
     };
     auto load_mask = [&](int t, int st) {
         if (t >= ntiles) return;
@@ -180,12 +164,7 @@ __global__ void __launch_bounds__(YPlan<N, Q, DIR>::NT, 1)
             __syncthreads();
             if (tid == 0) {
 #pragma unroll
-                for (int b = 0; b < N / BOX; ++b) {
-                    if constexpr (BLK)
-                        tma_store_4d(&tout, x0 % kZB, z, x0 / kZB, (p / Kz) * N + b * BOX, O + b * BOX * Q);
-                    else
-                        tma_store_3d(&tout, x0, b * BOX, p, O + b * BOX * Q);
-                }
+                for (int b = 0; b < N / BOX; ++b) tma_store_3d(&tout, x0, b * BOX, p, O + b * BOX * Q);
                 tma_store_commit();
             }
         }

@@ -164,9 +164,9 @@ def test_bench_grid_tucker_vs_dense(svh_lib):
     assert rel_l2(outs[(1e-4, True)], outs[(0.0, True)]) > 1e-8
 
 
-# Blocked X2 layout (Ny = 2048 with Nz = 64 / 128: the 2048-point y passes store z tiles
-# contiguously and pass C moves them by bulk copies, zblk.cu): 48 sampled observers, every
-# source, dense and Tucker spectra, empty planes (layered) included.
+# Ny = 2048 with Nz = 64 / 128 (the 2048-point y passes feeding the z pass of the headline
+# grid's extents at test size): 48 sampled observers, every source, dense and Tucker spectra,
+# empty planes (layered) included.
 BLOCKED = [((2, 600, 40), 0.0), ((3, 520, 20), 0.0), ((2, 600, 40), 1e-6), ((4, 530, 33), 1e-4)]
 
 
@@ -179,7 +179,7 @@ def test_blocked_layout_vs_oracle(svh_lib, shape, tol):
 
 
 def test_blocked_layout_layered(svh_lib):
-    """Empty planes and rows on the blocked path (pass B skips empty planes; pass C masks them)."""
+    """Empty planes and rows at Ny = 2048, Nz = 128 (pass B skips empty planes; pass C masks them)."""
     case = svh_inputs.layered((6, 560, 36))
     lat = Lattice(case["mat_id"])
     rows = np.sort(np.random.default_rng(4).choice(lat.K, 48, replace=False))
