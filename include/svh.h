@@ -91,8 +91,10 @@ typedef struct {
                              SVH_EINVAL at the first matvec otherwise); 0 = auto: P5, or -- where
                              P3s is eligible -- whichever of the two measures faster on the first
                              product of each RHS-chunk size.  Other values -> SVH_EINVAL */
-    int32_t precision;    /* matvec arithmetic: 0 = complex64 (the only precision built; Krylov vectors are
-                             fp64); 1 = complex128 -> SVH_EINVAL (not built) */
+    int32_t precision;    /* matvec arithmetic: 0 = complex64 (the FFT passes; Krylov vectors are fp64);
+                             1 = complex128 build: dense fp64 spectra are kept, svh_matvec_z is available and
+                             svh_solve runs its operator in fp64 (tight rre, e.g. 1e-8 / 1e-10 as the paper's
+                             MATLAB double); requires tucker_tol = 0, else SVH_EINVAL */
     int32_t schur_solver; /* S^-1 inside the Schur preconditioner (Eq. 13-15): 0 = AMG-preconditioned CG
                              (default); 1 = sparse-direct comparator (Table IV
                              P:251-262): METIS-reordered sparse Cholesky of S, factored once per port
@@ -178,6 +180,16 @@ int svh_matvec_host(svh_handle* h, const void* I_host, void* CC_host, int32_t nr
 /* Same operator on the lattice layout: complex64 [nrhs][5][kz][ky][kx]; input
  * values at empty voxels are ignored (treated as 0); output is 0 there. */
 int svh_matvec_grid(svh_handle* h, const void* I, void* CC, int32_t nrhs, int32_t green_only, svh_stream stream);
+
+/*
+ * svh_matvec_z -- the complex128 build of Eq. 9 (SURVEY 8(b) precision c128, 8(c) c.5): the same
+ * operator as svh_matvec in double precision with the fp64 dense spectra (plain full-embedding
+ * FFT passes; a reference / tight-solve path, not the throughput path).
+ *   I, CC : device complex128 [nrhs][5][K] (packed voxel order); must not alias.
+ * Errors: SVH_EINVAL (bad args, or the handle was not set up with opts.precision = 1), SVH_ENOMEM,
+ * SVH_ECUDA.  Asynchronous w.r.t. the host.
+ */
+int svh_matvec_z(svh_handle* h, const void* I, void* CC, int32_t nrhs, int32_t green_only, svh_stream stream);
 
 /*
  * Slab-decomposed matvec (the operator is Eq. 9 as in svh_matvec_grid,

@@ -28,6 +28,7 @@ static int next_pow2_embed(int K) {
 void update_local_terms(svh_handle* h) {
     const int nm = (int)h->mats.size();
     std::vector<float2> z((size_t)(nm + 1) * 5, make_float2(0.f, 0.f));
+    std::vector<double2> z64((size_t)(nm + 1) * 5, make_double2(0.0, 0.0));
     const double w = h->omega;
     const double div[5] = {1, 1, 1, 6, 2};
     for (int m = 0; m < nm; ++m) {
@@ -43,11 +44,20 @@ void update_local_terms(svh_handle* h) {
             b = lam * lam / den;
         }
         for (int c = 0; c < 5; ++c)
-            z[(size_t)(m + 1) * 5 + c] = make_float2((float)(a / (div[c] * h->dx)), (float)(w * kMu0 * b / (div[c] * h->dx)));
+        {
+            z64[(size_t)(m + 1) * 5 + c] = make_double2(a / (div[c] * h->dx), w * kMu0 * b / (div[c] * h->dx));
+            z[(size_t)(m + 1) * 5 + c] = make_float2((float)z64[(size_t)(m + 1) * 5 + c].x,
+                                                     (float)z64[(size_t)(m + 1) * 5 + c].y);
+        }
     }
     if (!h->d_zloc) SVH_CUDA(cudaMalloc(&h->d_zloc, z.size() * sizeof(float2)));
     SVH_CUDA(cudaMemcpy(h->d_zloc, z.data(), z.size() * sizeof(float2), cudaMemcpyHostToDevice));
     h->gscale = (float)(w * kMu0 * h->dx / ((double)h->nx * h->ny * h->nz));
+    h->gscale64 = w * kMu0 * h->dx / ((double)h->nx * h->ny * h->nz);
+    if (h->opts.precision == 1) {
+        if (!h->d_zloc64) SVH_CUDA(cudaMalloc(&h->d_zloc64, z64.size() * sizeof(double2)));
+        SVH_CUDA(cudaMemcpy(h->d_zloc64, z64.data(), z64.size() * sizeof(double2), cudaMemcpyHostToDevice));
+    }
 }
 
 static void make_twiddles(svh_handle* h) {
@@ -60,6 +70,15 @@ static void make_twiddles(svh_handle* h) {
         }
         SVH_CUDA(cudaMalloc(&h->d_tw[a], t.size() * sizeof(float2)));
         SVH_CUDA(cudaMemcpy(h->d_tw[a], t.data(), t.size() * sizeof(float2), cudaMemcpyHostToDevice));
+        if (h->opts.precision == 1) {
+            std::vector<double2> t64(N3[a]);
+            for (int j = 0; j < N3[a]; ++j) {
+                const double th = -2.0 * M_PI * j / N3[a];
+                t64[j] = make_double2(std::cos(th), std::sin(th));
+            }
+            SVH_CUDA(cudaMalloc(&h->d_tw64[a], t64.size() * sizeof(double2)));
+            SVH_CUDA(cudaMemcpy(h->d_tw64[a], t64.data(), t64.size() * sizeof(double2), cudaMemcpyHostToDevice));
+        }
     }
 }
 
@@ -180,6 +199,10 @@ static void destroy(svh_handle* h) {
     cudaFree(h->d_kern);
     cudaFree(h->d_spec);
     cudaFree(h->d_kvt);
+    cudaFree(h->d_spec64);
+    cudaFree(h->d_zloc64);
+    cudaFree(h->W64);
+    for (int a = 0; a < 3; ++a) cudaFree(h->d_tw64[a]);
     cudaFree(h->d_zloc);
     for (int a = 0; a < 3; ++a) cudaFree(h->d_tw[a]);
     cudaFree(h->X1);
@@ -247,7 +270,9 @@ int svh_setup(const svh_grid* grid, const uint8_t* mat_id, const svh_material* m
         SVH_CHECK(o.restart >= 1 && o.restart <= 2039, SVH_EINVAL, "restart must be in 1..2039");
         SVH_CHECK(o.tucker_tol >= 0 && o.tucker_tol < 1, SVH_EINVAL, "tucker_tol must be in [0, 1)");
         SVH_CHECK(o.plan == 0 || o.plan == 3 || o.plan == 5, SVH_EINVAL, "matvec plan must be 0 (auto), 3 (P3s) or 5 (P5)");
-        SVH_CHECK(o.precision == 0, SVH_EINVAL, "only the complex64 matvec is built (precision 0)");
+        SVH_CHECK(o.precision == 0 || o.precision == 1, SVH_EINVAL, "precision must be 0 (complex64) or 1 (complex128)");
+        SVH_CHECK(o.precision == 0 || o.tucker_tol == 0, SVH_EINVAL,
+                  "the complex128 build uses dense spectra (tucker_tol = 0)");
         SVH_CHECK(o.schur_solver == 0 || o.schur_solver == 1, SVH_EINVAL, "schur_solver must be 0 (AMG-PCG) or 1 (sparse Cholesky)");
         auto t0 = std::chrono::steady_clock::now();
         SVH_CUDA(cudaSetDevice(device));
@@ -468,6 +493,14 @@ int svh_matvec_plan(const svh_handle* h, int32_t* plan, float* ms_p5, float* ms_
         *plan = h->last_plan;
         if (ms_p5) *ms_p5 = h->plan_ms.empty() ? 0.f : h->plan_ms.back().first;
         if (ms_p3s) *ms_p3s = h->plan_ms.empty() ? 0.f : h->plan_ms.back().second;
+    });
+}
+
+int svh_matvec_z(svh_handle* h, const void* I, void* CC, int32_t nrhs, int32_t green_only, svh_stream stream) {
+    return guarded([&] {
+        SVH_CHECK(h && I && CC && nrhs >= 1 && I != CC, SVH_EINVAL, "bad matvec args");
+        SVH_CUDA(cudaSetDevice(h->device));
+        matvec_z(h, (const double2*)I, (double2*)CC, nrhs, green_only != 0, (cudaStream_t)stream);
     });
 }
 

@@ -58,6 +58,14 @@ struct svh_handle {
     SvhTucker tucker;
     bool use_tucker = false;
     float2* d_zloc = nullptr;            // [n_mat + 1][5] local terms z^b (index 0 unused)
+    // complex128 build (opts.precision = 1, matvec64.cu): fp64 octant spectra, local terms,
+    // prefactor, twiddles and the embedding workspace
+    double* d_spec64 = nullptr;          // [7][hz][hy][hx]
+    double2* d_zloc64 = nullptr;         // [n_mat + 1][5]
+    double gscale64 = 0;
+    double2* d_tw64[3] = {nullptr, nullptr, nullptr};
+    double2* W64 = nullptr;
+    size_t w64_bytes = 0;
     float2* d_tw[3] = {nullptr, nullptr, nullptr};  // W_N^j tables per axis
     float gscale = 0;                    // omega * mu0 * dx / (nx ny nz)
     // matvec workspace
@@ -121,6 +129,8 @@ void slab_backward(svh_handle* h, int rank, int P, const float2* recv, const flo
 bool p3s_eligible(const svh_handle* h);
 void p3s_matvec(svh_handle* h, const float2* in, float2* out, float2* XT, int nr, bool green_only, bool packed,
                 cudaStream_t s);
+// matvec64.cu (complex128 build)
+void matvec_z(svh_handle* h, const double2* I, double2* CC, int nrhs, bool green_only, cudaStream_t s);
 // quad.cu
 void compute_kernels(svh_handle* h);
 // cache.cu (Algorithm 2)

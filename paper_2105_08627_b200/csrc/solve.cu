@@ -99,6 +99,7 @@ struct Solve {
     int64_t N = 0;
     float2* c64_in = nullptr;
     float2* c64_out = nullptr;
+    double2* z_out = nullptr;        // complex128 build: Z.x of apply_sys
     double* d_red = nullptr;         // reduction scratch
     int inner_its = 0;
     // PCG with device-side scalars, one CUDA graph per iteration (V-cycle included); the
@@ -184,7 +185,9 @@ __global__ void k_to_c64(const double2* __restrict__ x, float2* __restrict__ y, 
 }
 
 // y_I = ZI (c64 result) + A^T F Phi ; y_Phi = F A I + (1 - F) Phi
-__global__ void k_sys_I(const float2* __restrict__ zi, const double2* __restrict__ x, double2* __restrict__ y,
+// ZT = float2 (the complex64 matvec) or double2 (the complex128 build)
+template <typename ZT>
+__global__ void k_sys_I(const ZT* __restrict__ zi, const double2* __restrict__ x, double2* __restrict__ y,
                         const int32_t* __restrict__ fnode, const uint8_t* __restrict__ free_, int64_t K) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= K) return;
@@ -192,7 +195,7 @@ __global__ void k_sys_I(const float2* __restrict__ zi, const double2* __restrict
     apply_AT_voxel(x + 5 * K, free_, fnode + 6 * k, o);
 #pragma unroll
     for (int c = 0; c < 5; ++c) {
-        const float2 z = zi[c * K + k];
+        const ZT z = zi[c * K + k];
         y[c * K + k] = make_double2((double)z.x + o[c].x, (double)z.y + o[c].y);
     }
 }
@@ -356,6 +359,31 @@ __global__ void k_jacobiV(int n, int w, const int* __restrict__ ec, const double
     reinterpret_cast<double2*>(xo)[t] = o;
 }
 // r = b - A x
+// the first two l1-Jacobi sweeps from a zero guess in one pass: x1 = D^-1 b, x2 = x1 + D^-1 (b - A x1)
+// with x1 formed on the fly at the neighbours (the same operations, in the same order, as two
+// k_jacobiV launches)
+__global__ void k_jacobi2V(int n, int w, const int* __restrict__ ec, const double* __restrict__ ev,
+                           const double* __restrict__ dinv, const double* __restrict__ b, double* __restrict__ xo,
+                           int sh) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (n << sh)) return;
+    const int i = t >> sh, p = t & ((1 << sh) - 1);
+    const int NVP = 1 << sh;
+    const double2* b2 = reinterpret_cast<const double2*>(b);
+    double a0 = 0, a1 = 0;
+    for (int k = 0; k < w; ++k) {
+        const double v = __ldg(&ev[(int64_t)k * n + i]);
+        const int j = __ldg(&ec[(int64_t)k * n + i]);
+        const double dj = __ldg(&dinv[j]);
+        const double2 bj = b2[(int64_t)j * NVP + p];
+        a0 = fma(v, dj * bj.x, a0);
+        a1 = fma(v, dj * bj.y, a1);
+    }
+    const double2 bi = b2[t];
+    const double d = dinv[i];
+    const double2 xi = make_double2(d * bi.x, d * bi.y);
+    reinterpret_cast<double2*>(xo)[t] = make_double2(xi.x + d * (bi.x - a0), xi.y + d * (bi.y - a1));
+}
 __global__ void k_residV(int n, int w, const int* __restrict__ ec, const double* __restrict__ ev,
                          const double* __restrict__ b, const double* __restrict__ x, double* __restrict__ r, int sh) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -489,16 +517,20 @@ __global__ void __launch_bounds__(kDotThreads)
         __syncthreads();
     }
 }
-// out[d * ostride + v] = sum over blocks (ascending) of the partials
+// out[d * ostride + v] = sum of the block partials in a fixed order: warp w takes items (d, v)
+// w, w + 4, ...; lane l sums blocks l, l + 32, ... ascending, then a fixed shuffle tree
+// (independent of NV and of the other vectors, like k_ddotP)
 __global__ void k_ddotF(int nb, int nd, const double* __restrict__ part, double* __restrict__ out, int ostride,
                         int sh) {
     const int NV = 2 << sh;
-    const int t = threadIdx.x;
-    if (t >= nd * NV) return;
-    const int d = t / NV, v = t % NV;
-    double acc = 0;
-    for (int b = 0; b < nb; ++b) acc += part[((int64_t)b * nd + d) * NV + v];
-    out[d * ostride + v] = acc;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int t = warp; t < nd * NV; t += nw) {
+        const int d = t / NV, v = t % NV;
+        double acc = 0;
+        for (int b = lane; b < nb; b += 32) acc += part[((int64_t)b * nd + d) * NV + v];
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffff, acc, o);
+        if (lane == 0) out[d * ostride + v] = acc;
+    }
 }
 // x += sign alpha_v y (per vector v)
 __global__ void k_axpyV(int n, const double* __restrict__ alpha, int sign, const double* __restrict__ y,
@@ -816,6 +848,7 @@ void free_solve(svh_handle* h) {
     cudaFree(S->d_krylov);
     cudaFree(S->c64_in);
     cudaFree(S->c64_out);
+    cudaFree(S->z_out);
     cudaFree(S->d_red);
     cudaFree(S->d_part);
     cudaFree(S->d_pcg);
@@ -1229,9 +1262,15 @@ static void ensure_work(svh_handle* h, int restart) {
 static void apply_sys(svh_handle* h, const double2* x, double2* y, bool masked, cudaStream_t s) {
     Solve* S = h->solve;
     const int64_t K = h->K, n5 = 5 * K;
-    SVH_LAUNCH(k_to_c64, nblk(n5), 256, 0, s, x, S->c64_in, n5);
-    matvec(h, S->c64_in, S->c64_out, 1, false, true, s);
-    SVH_LAUNCH(k_sys_I, nblk(K), 256, 0, s, S->c64_out, x, y, S->d_fnode, masked ? S->d_free : nullptr, K);
+    if (h->opts.precision == 1) {   // complex128 build: the operator in fp64 end to end
+        if (!S->z_out) SVH_CUDA(cudaMalloc(&S->z_out, n5 * sizeof(double2)));
+        matvec_z(h, x, S->z_out, 1, false, s);
+        SVH_LAUNCH(k_sys_I<double2>, nblk(K), 256, 0, s, S->z_out, x, y, S->d_fnode, masked ? S->d_free : nullptr, K);
+    } else {
+        SVH_LAUNCH(k_to_c64, nblk(n5), 256, 0, s, x, S->c64_in, n5);
+        matvec(h, S->c64_in, S->c64_out, 1, false, true, s);
+        SVH_LAUNCH(k_sys_I<float2>, nblk(K), 256, 0, s, S->c64_out, x, y, S->d_fnode, masked ? S->d_free : nullptr, K);
+    }
     SVH_LAUNCH(k_sys_Phi, nblk(S->M), 256, 0, s, x, y, S->d_node_vox, S->d_node_axis, masked ? S->d_free : nullptr, K,
                S->M);
 }
@@ -1248,7 +1287,7 @@ static void ddot(Solve* S, int n, int nd, const double* a0, const double* b0, co
         case 4: SVH_LAUNCH(k_ddotP<4>, nb, kDotThreads, 0, s, n, nd, a0, b0, a1, b1, a2, b2, S->d_part); break;
         default: throw Error{SVH_EINVAL, "ddot: at most 16 vector pairs"};
     }
-    SVH_LAUNCH(k_ddotF, 1, 128, 0, s, nb, nd, S->d_part, out, ostride, sh);
+    SVH_LAUNCH(k_ddotF, 1, 1024, 0, s, nb, nd, S->d_part, out, ostride, sh);
 }
 
 // AMG cycle on level l: x = B_l^-1 b for NVP vector pairs.  l1-Jacobi V(2,2) smoothing; the
@@ -1271,8 +1310,7 @@ static void kcycle(Solve* S, int l, const double* b, double* x, cudaStream_t s, 
     const CsrDev& C = S->levels[l + 1];
     const int nc = L.nc;
     const int64_t nct = (int64_t)nc * NVP;
-    SVH_LAUNCH(k_jacobiV, nblk(nt), 256, 0, s, n, L.ellw, L.ecol, L.eval, L.dinv, b, (const double*)nullptr, x, sh);
-    SVH_LAUNCH(k_jacobiV, nblk(nt), 256, 0, s, n, L.ellw, L.ecol, L.eval, L.dinv, b, x, L.x2, sh);
+    SVH_LAUNCH(k_jacobi2V, nblk(nt), 256, 0, s, n, L.ellw, L.ecol, L.eval, L.dinv, b, L.x2, sh);
     SVH_LAUNCH(k_residV, nblk(nt), 256, 0, s, n, L.ellw, L.ecol, L.eval, b, L.x2, L.tmp, sh);
     SVH_LAUNCH(k_restrictG, nblk(nct), 256, 0, s, nc, L.cptr, L.cmem, L.tmp, C.vb, sh);
     if (l < kKLevels && l + 1 < last) {
@@ -1289,9 +1327,9 @@ static void kcycle(Solve* S, int l, const double* b, double* x, cudaStream_t s, 
         kcycle(S, l + 1, C.vb, C.vx, s, NVP);
         SVH_LAUNCH(k_prolongV, nblk(nt), 256, 0, s, n, L.agg, C.vx, L.x2, sh);
     }
-    SVH_LAUNCH(k_jacobiV, nblk(nt), 256, 0, s, n, L.ellw, L.ecol, L.eval, L.dinv, b, L.x2, x, sh);
-    SVH_LAUNCH(k_jacobiV, nblk(nt), 256, 0, s, n, L.ellw, L.ecol, L.eval, L.dinv, b, x, L.x2, sh);
-    SVH_CUDA(cudaMemcpyAsync(x, L.x2, 2 * (size_t)nt * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    // post-smoothing: L.x2 -> L.tmp (free since the restriction) -> x
+    SVH_LAUNCH(k_jacobiV, nblk(nt), 256, 0, s, n, L.ellw, L.ecol, L.eval, L.dinv, b, L.x2, L.tmp, sh);
+    SVH_LAUNCH(k_jacobiV, nblk(nt), 256, 0, s, n, L.ellw, L.ecol, L.eval, L.dinv, b, L.tmp, x, sh);
 }
 
 // Flexible CG (FCG(1)) on S (level 0) for NV = 2 NVP real right-hand sides (re / im of NVP
@@ -1526,6 +1564,8 @@ struct BatchWork {
     double2* kry = nullptr;   // per port: V (m+1), Z (m), w, r   -> (2m+3) N
     float2* cin = nullptr;    // [B][5K] complex64 operator input / output
     float2* cout = nullptr;
+    double2* zin = nullptr;   // [B][5K] complex128 build
+    double2* zout = nullptr;
     double2* base(int p) const { return kry + (size_t)p * (2 * m + 3) * N; }
     double2* V(int p, int j) const { return base(p) + (size_t)j * N; }
     double2* Z(int p, int j) const { return base(p) + (size_t)(m + 1 + j) * N; }
@@ -1535,8 +1575,11 @@ struct BatchWork {
         cudaFree(kry);
         cudaFree(cin);
         cudaFree(cout);
+        cudaFree(zin);
+        cudaFree(zout);
         kry = nullptr;
         cin = cout = nullptr;
+        zin = zout = nullptr;
     }
 };
 
@@ -1618,11 +1661,22 @@ static void fgmres_batch(svh_handle* h, BatchWork& W, int nb, double2* const* bb
             SVH_CUDA(cudaStreamSynchronize(s));
             auto c1 = std::chrono::steady_clock::now();
             // ---- operator, one matvec over the batch: w = A Z_j
-            for (int p : act) SVH_LAUNCH(k_to_c64, nblk(n5), 256, 0, s, W.Z(p, j), W.cin + (size_t)p * n5, n5);
-            matvec(h, W.cin, W.cout, nb, false, true, s);
+            if (h->opts.precision == 1) {   // complex128 build: fp64 operator on the stacked Z_j
+                for (int p : act)
+                    SVH_CUDA(cudaMemcpyAsync(W.zin + (size_t)p * n5, W.Z(p, j), n5 * sizeof(double2),
+                                             cudaMemcpyDeviceToDevice, s));
+                matvec_z(h, W.zin, W.zout, nb, false, s);
+            } else {
+                for (int p : act) SVH_LAUNCH(k_to_c64, nblk(n5), 256, 0, s, W.Z(p, j), W.cin + (size_t)p * n5, n5);
+                matvec(h, W.cin, W.cout, nb, false, true, s);
+            }
             for (int p : act) {
-                SVH_LAUNCH(k_sys_I, nblk(K), 256, 0, s, W.cout + (size_t)p * n5, W.Z(p, j), W.w(p), S->d_fnode,
-                           S->d_free, K);
+                if (h->opts.precision == 1)
+                    SVH_LAUNCH(k_sys_I<double2>, nblk(K), 256, 0, s, W.zout + (size_t)p * n5, W.Z(p, j), W.w(p),
+                               S->d_fnode, S->d_free, K);
+                else
+                    SVH_LAUNCH(k_sys_I<float2>, nblk(K), 256, 0, s, W.cout + (size_t)p * n5, W.Z(p, j), W.w(p),
+                               S->d_fnode, S->d_free, K);
                 SVH_LAUNCH(k_sys_Phi, nblk(S->M), 256, 0, s, W.Z(p, j), W.w(p), S->d_node_vox, S->d_node_axis,
                            S->d_free, K, S->M);
             }
@@ -1850,6 +1904,11 @@ static void solve_columns(svh_handle* h, const svh_port* ports, int P, const int
             SVH_CUDA(cudaMalloc(&W.cin, (size_t)Bmax * 5 * h->K * sizeof(float2)));
             SVH_CUDA(cudaMalloc(&W.cout, (size_t)Bmax * 5 * h->K * sizeof(float2)));
             SVH_CUDA(cudaMemsetAsync(W.cin, 0, (size_t)Bmax * 5 * h->K * sizeof(float2), s));
+            if (h->opts.precision == 1) {
+                SVH_CUDA(cudaMalloc(&W.zin, (size_t)Bmax * 5 * h->K * sizeof(double2)));
+                SVH_CUDA(cudaMalloc(&W.zout, (size_t)Bmax * 5 * h->K * sizeof(double2)));
+                SVH_CUDA(cudaMemsetAsync(W.zin, 0, (size_t)Bmax * 5 * h->K * sizeof(double2), s));
+            }
             for (int p = 0; p < Bmax; ++p) {
                 SVH_CUDA(cudaMalloc(&bbs[p], N * sizeof(double2)));
                 SVH_CUDA(cudaMalloc(&xs[p], N * sizeof(double2)));

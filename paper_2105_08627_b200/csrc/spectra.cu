@@ -130,12 +130,14 @@ void compute_spectra(svh_handle* h) {
     SVH_CUDA(cudaMalloc(&w2, n2 * sizeof(double)));
     SVH_CUDA(cudaMalloc(&wo, no * sizeof(double)));
     SVH_CUDA(cudaMalloc(&h->d_spec, 7 * no * sizeof(float)));
+    if (h->opts.precision == 1) SVH_CUDA(cudaMalloc(&h->d_spec64, 7 * no * sizeof(double)));   // complex128 build
     // kernel order K0, K1x, K1y, K1z, K2x, K2y, K2z; odd axis of K1c is c
     for (int q = 0; q < 7; ++q) {
         const int odd_axis = (q >= 1 && q <= 3) ? q - 1 : -1;
         mode_products(h->d_kern + q * h->Kt, h->kx, h->ky, h->kz, dC[0][odd_axis == 0], H3[0],
                       dC[1][odd_axis == 1], H3[1], dC[2][odd_axis == 2], H3[2], w1, w2, wo);
         SVH_LAUNCH(k_to_f32, dim3((unsigned)((no + 255) / 256)), 256, 0, 0, wo, h->d_spec + q * no, no);
+        if (h->d_spec64) SVH_CUDA(cudaMemcpy(h->d_spec64 + q * no, wo, no * sizeof(double), cudaMemcpyDeviceToDevice));
     }
     SVH_CUDA(cudaDeviceSynchronize());
     cudaFree(w1);

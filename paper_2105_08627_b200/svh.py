@@ -91,6 +91,7 @@ def lib():
         L.svh_ipc_close.argtypes = [vp]
         L.svh_slab_forward_p2p.argtypes = [vp, i32, i32, vp, vpp, vpp, ctypes.c_uint32, i32, vp]
         L.svh_slab_middle_p2p.argtypes = [vp, i32, i32, vp, vpp, vpp, ctypes.c_uint32, i32, vp]
+        L.svh_matvec_z.argtypes = [vp, vp, vp, i32, i32, vp]
         L.svh_matvec_plan.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(ctypes.c_float),
                                       ctypes.POINTER(ctypes.c_float)]
         L.svh_slab_sizes.argtypes = [vp, i32, ctypes.POINTER(i64)]
@@ -120,7 +121,7 @@ def lib():
                      "svh_matvec_grid", "svh_apply_system", "svh_solve", "svh_solve_columns", "svh_get_kernels",
                      "svh_get_stats", "svh_profile_enable", "svh_profile_read", "svh_y_to_zl", "svh_matvec_plan",
                      "svh_ipc_alloc", "svh_ipc_free", "svh_ipc_open", "svh_ipc_close", "svh_slab_forward_p2p",
-                     "svh_slab_middle_p2p"):
+                     "svh_slab_middle_p2p", "svh_matvec_z"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -133,7 +134,7 @@ EXPORTED = ("svh_default_opts", "svh_setup", "svh_set_frequency", "svh_unknowns"
             "svh_matvec_grid", "svh_apply_system", "svh_solve", "svh_solve_columns", "svh_get_kernels",
             "svh_get_stats", "svh_profile_enable", "svh_profile_read", "svh_y_to_zl", "svh_matvec_plan",
             "svh_ipc_alloc", "svh_ipc_free", "svh_ipc_open", "svh_ipc_close", "svh_slab_forward_p2p",
-            "svh_slab_middle_p2p", "svh_destroy",
+            "svh_slab_middle_p2p", "svh_matvec_z", "svh_destroy",
             "svh_last_error", "svh_launch_count")
 
 
@@ -284,6 +285,18 @@ class Handle:
         _check(lib().svh_matvec(self._h, ctypes.c_void_p(Ib.data_ptr()), ctypes.c_void_p(o.data_ptr()),
                                 Ib.shape[0], int(green_only), _stream_ptr(stream)))
         return o[0] if squeeze and out is None else o
+
+    def matvec_z(self, I, out=None, green_only=False, stream=None):
+        """svh_matvec_z: the complex128 build (handle set up with precision=1); I: complex128
+        [nrhs][5][K] (or [5][K]) on the device."""
+        import torch
+        Ib = I.unsqueeze(0) if I.dim() == 2 else I
+        assert Ib.dtype == torch.complex128 and Ib.is_cuda and Ib.shape[1:] == (5, self.K)
+        Ib = Ib.contiguous()
+        o = torch.empty_like(Ib) if out is None else out
+        _check(lib().svh_matvec_z(self._h, ctypes.c_void_p(Ib.data_ptr()), ctypes.c_void_p(o.data_ptr()),
+                                  Ib.shape[0], int(green_only), _stream_ptr(stream)))
+        return o if I.dim() == 3 else o[0]
 
     def matvec_host(self, I_host, out_host, green_only=False, chunk=0, stream=None):
         """End-to-end product on host tensors (complex64 [nrhs, 5, K], pinned for overlap):

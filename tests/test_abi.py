@@ -51,14 +51,16 @@ def test_host_only_calls():
 
 def test_opts_validation_host_only():
     """svh_opts is validated before any device work: restart range (the FGMRES Hessenberg
-    scratch), plan (0 auto, 3 P3s, 5 P5) and precision (only complex64 is built)."""
+    scratch), plan (0 auto, 3 P3s, 5 P5), precision (0 / 1; the complex128 build needs dense
+    spectra) and the Schur solver."""
     from paper_2105_08627_b200 import svh
     L = svh.lib()
     g = svh.Grid(2, 1, 1, 1e-6)
     mats = (svh.Material * 1)(svh.Material(1e7, 1e-7))
     mat = (ctypes.c_uint8 * 2)(1, 1)
     for field, bad, msg in (("restart", 5000, b"restart"), ("restart", 0, b"restart"), ("plan", 4, b"plan"),
-                            ("precision", 1, b"complex64"), ("tucker_tol", 1.5, b"tucker_tol")):
+                            ("precision", 2, b"precision"), ("tucker_tol", 1.5, b"tucker_tol"),
+                            ("schur_solver", 2, b"schur_solver")):
         o = svh.Opts()
         L.svh_default_opts(ctypes.byref(o))
         setattr(o, field, bad)
@@ -66,3 +68,9 @@ def test_opts_validation_host_only():
         code = L.svh_setup(ctypes.byref(g), mat, mats, 1, 1e9, ctypes.byref(o), 0, ctypes.byref(h))
         assert code == -1, field
         assert msg in L.svh_last_error(), (field, L.svh_last_error())
+    o = svh.Opts()
+    L.svh_default_opts(ctypes.byref(o))
+    o.precision, o.tucker_tol = 1, 1e-6
+    h = ctypes.c_void_p()
+    assert L.svh_setup(ctypes.byref(g), mat, mats, 1, 1e9, ctypes.byref(o), 0, ctypes.byref(h)) == -1
+    assert b"complex128" in L.svh_last_error()
