@@ -1553,10 +1553,8 @@ void run_pass_c(svh_handle* h, const Geom& g, float2* X2, int nrhs, cudaStream_t
             };
             if (!h->use_tucker)
                 return go(k_zpass<N, R2, Q, NT, 2, 0>, P::smem(2, 0)) || go(k_zpass<N, R2, Q, NT, 1, 0>, P::smem(1, 0));
-            // Tucker: two T buffers (two barriers per tile) when they fit, F3 rows then from L1/L2
-            if (dmax <= 16)
-                return go(k_zpass<N, R2, Q, NT, 2, 16>, P::smem(2, 16)) || go(k_zpass<N, R2, Q, NT, 1, 16>, P::smem(1, 16));
-            return go(k_zpass<N, R2, Q, NT, 2, 32>, P::smem(2, 32)) || go(k_zpass<N, R2, Q, NT, 1, 32>, P::smem(1, 32));
+            if (dmax <= 16) return go(k_zpass<N, R2, Q, NT, 1, 16>, P::smem(1, 16));
+            return go(k_zpass<N, R2, Q, NT, 1, 32>, P::smem(1, 32));
         };
         if constexpr (N == 128) {
             if (launch(std::integral_constant<int, 8>{}, std::integral_constant<int, 16>{},

@@ -47,14 +47,11 @@ struct ZPlan {
     static constexpr int TE = 5 * R2 * TB;                // elements of one T buffer
     static constexpr int KVS = 8;                         // floats per (kh, q) entry of KV (7 used)
     static constexpr size_t KV_b = (size_t)NK * Q * KVS * sizeof(float);
-    // T (double-buffered when it fits) | KV [NK][Q][8] | Tucker (rank bucket DM > 0): the
-    // mode-3 factor rows F3 [7][NK][DM] (single-buffered T only; with two T buffers they are
-    // read from L1/L2), G [7][DM][DM + 1], H [7][Q][DM + 1] (zero-padded to DM)
+    // T (double-buffered in dense mode) | KV [NK][Q][8] | Tucker (rank bucket DM > 0): the
+    // mode-3 factor rows F3 [7][NK][DM], G [7][DM][DM + 1], H [7][Q][DM + 1] (zero-padded to DM)
     static constexpr size_t smem(int nbuf, int DM) {
         return (size_t)nbuf * TE * sizeof(float2) + KV_b +
-               (DM ? ((nbuf == 1 ? (size_t)7 * NK * DM : 0) + (size_t)7 * DM * (DM + 1) + (size_t)7 * Q * (DM + 1)) *
-                         sizeof(float)
-                   : 0);
+               (DM ? ((size_t)7 * NK * DM + (size_t)7 * DM * (DM + 1) + (size_t)7 * Q * (DM + 1)) * sizeof(float) : 0);
     }
 };
 
@@ -70,9 +67,8 @@ __global__ void __launch_bounds__(NT, 1)
     extern __shared__ __align__(16) unsigned char smraw[];
     float2* T = reinterpret_cast<float2*>(smraw);                                 // [NBUF][5][R2][TB]
     float* KV = reinterpret_cast<float*>(smraw + (size_t)NBUF * TE * sizeof(float2));   // [NK][Q][8]
-    constexpr bool F3S = NBUF == 1;                                               // F3 rows on chip
-    float* F3s = KV + NK * Q * KVS;                                               // [7][NK][DM] (F3S)
-    float* G = F3s + (F3S ? 7 * NK * DM : 0);                                     // [7][DM][DP]
+    float* F3s = KV + NK * Q * KVS;                                               // [7][NK][DM]
+    float* G = F3s + 7 * NK * DM;                                                 // [7][DM][DP]
     float* H = G + 7 * DM * DP;                                                   // [7][Q][DP]
     const int tid = threadIdx.x;
     const float2 zero = make_float2(0.f, 0.f);
@@ -106,7 +102,7 @@ __global__ void __launch_bounds__(NT, 1)
     float2 w2[R2];
 #pragma unroll
     for (int m = 0; m < R2; ++m) w2[m] = l2 ? __ldg(&tw[(m * k1) & (N - 1)]) : zero;
-    if constexpr (DM > 0 && F3S) {
+    if constexpr (DM > 0) {
         // the mode-3 factor rows of the octant (kh <= N/2) are the same for every unit: on chip once
         for (int e = tid; e < 7 * NK * DM; e += NT) {
             const int m = e / (NK * DM), rest = e - m * NK * DM, kh = rest / DM, c = rest - kh * DM;
@@ -191,20 +187,13 @@ __global__ void __launch_bounds__(NT, 1)
                 for (int m = 0; m < 7; ++m) {
                     const float* F3m = F3s + m * NK * DM;
                     const float* Hm = H + m * Q * DP;
-                    const int d3 = sv.rk[m][2];
                     for (int t = tid; t < NK * Q; t += NT) {
                         const int q = t % Q, kh = t / Q;
+                        const float* f3 = F3m + kh * DM;
                         const float* hq = Hm + q * DP;
                         float acc = 0.f;
-                        if constexpr (F3S) {
-                            const float* f3 = F3m + kh * DM;
 #pragma unroll
-                            for (int c = 0; c < DM; ++c) acc = fmaf(f3[c], hq[c], acc);
-                        } else {   // the row F3_m[kh] from global (L1-resident: 7 x NK x d3 floats)
-                            const float* f3 = sv.fac[m][2] + (int64_t)kh * d3;
-#pragma unroll
-                            for (int c = 0; c < DM; ++c) acc = fmaf(c < d3 ? __ldg(&f3[c]) : 0.f, hq[c], acc);
-                        }
+                        for (int c = 0; c < DM; ++c) acc = fmaf(f3[c], hq[c], acc);
                         KV[t * KVS + m] = acc;
                     }
                 }
