@@ -868,7 +868,7 @@ const double kFlux[5][6] = {{-1, 1, 0, 0, 0, 0},
                             {0.5, 0.5, -0.5, -0.5, 0, 0},
                             {0.5, 0.5, 0.5, 0.5, -1, -1}};
 
-CsrHost build_schur(const Solve* S, const std::vector<int32_t>& node2free, int nf) {
+CsrHost build_schur(const Solve* S, const std::vector<int32_t>& node2free, const std::vector<int32_t>& flist, int nf) {
     // rows by free node: neighbours are faces of the <= 2 adjacent voxels
     CsrHost A;
     A.n = nf;
@@ -881,8 +881,8 @@ CsrHost build_schur(const Solve* S, const std::vector<int32_t>& node2free, int n
     std::vector<int> slot(nf, 0);
     const int64_t K = S->K;
     int f = 0;
-    for (int64_t r = 0; r < S->M; ++r) {
-        if (node2free[r] < 0) continue;
+    for (int fi = 0; fi < nf; ++fi) {   // row f = free index f (node flist[f])
+        const int64_t r = flist[fi];
         const int row_start = (int)cols.size();
         for (int side = 0; side < 2; ++side) {
             const int32_t k = S->node_vox[2 * r + side];
@@ -1147,12 +1147,28 @@ static void build_amg(svh_handle* h, const std::vector<int32_t>& fixed, int nvp)
     S->fixed_nodes = fixed;
     std::vector<uint8_t> fr(S->M, 1);
     for (int32_t r : fixed) fr[r] = 0;
+    // free nodes numbered in voxel order (key: the lower packed voxel index of the face, then the
+    // axis), not by face family: the <= 11 couplings of a row of S are then a few positions
+    // apart except across y rows / z planes, so the level-0 gathers of the PCG and the cycle
+    // stay in L1/L2, and the pairwise aggregation sweeps the lattice in a spatial order
     std::vector<int32_t> node2free(S->M, -1), flist;
-    for (int64_t r = 0; r < S->M; ++r)
-        if (fr[r]) {
-            node2free[r] = (int32_t)flist.size();
-            flist.push_back((int32_t)r);
-        }
+    {   // counting sort by key = 3 v + axis (stable in node id)
+        const int64_t nk = 3 * S->K + 3;
+        std::vector<int64_t> cnt(nk + 1, 0);
+        std::vector<int32_t> key(S->M, -1);
+        for (int64_t r = 0; r < S->M; ++r)
+            if (fr[r]) {
+                const int32_t a = S->node_vox[2 * r], b = S->node_vox[2 * r + 1];
+                const int64_t v = a < 0 ? b : (b < 0 ? a : std::min(a, b));
+                key[r] = (int32_t)(v * 3 + S->node_axis[r]);
+                ++cnt[key[r] + 1];
+            }
+        for (int64_t k = 0; k < nk; ++k) cnt[k + 1] += cnt[k];
+        flist.assign(cnt[nk], 0);
+        for (int64_t r = 0; r < S->M; ++r)
+            if (key[r] >= 0) flist[cnt[key[r]]++] = (int32_t)r;
+        for (size_t f = 0; f < flist.size(); ++f) node2free[flist[f]] = (int32_t)f;
+    }
     S->nf = (int)flist.size();
     SVH_CUDA(cudaMalloc(&S->d_free, S->M));
     SVH_CUDA(cudaMemcpy(S->d_free, fr.data(), S->M, cudaMemcpyHostToDevice));
@@ -1165,7 +1181,7 @@ static void build_amg(svh_handle* h, const std::vector<int32_t>& fixed, int nvp)
         S->pre_built = true;
         return;
     }
-    CsrHost A = build_schur(S, node2free, S->nf);
+    CsrHost A = build_schur(S, node2free, flist, S->nf);
     if (h->opts.schur_solver == 1) {
         build_chol(S, A);
         S->pre_built = true;
