@@ -92,8 +92,7 @@ __global__ void __launch_bounds__(YPlan<N, Q, DIR>::NT, 1)
         int z, p, x0;
         decode(t, z, p, x0);
         mbar_wait(&bar[st], (uint32_t)((i / S) & 1));
-        if (DIR < 0 && tid == 0) tma_store_wait_read0();   // the previous tile's output left O
-        __syncthreads();   // (also: the previous tile's stage-2 reads of W are done; M[st] visible)
+        __syncthreads();   // the previous tile's stage-2 reads of W are done; M[st] visible
         const float2* src = stage + st * SR * Q;
         const uint32_t* Ms = M + st * MW;
         // stage 0: radix 16, Ns = 1; rows n = j + r N/16
@@ -138,6 +137,9 @@ __global__ void __launch_bounds__(YPlan<N, Q, DIR>::NT, 1)
 #pragma unroll
             for (int r = 0; r < 16; ++r) W[rpad(base + r * 16) * Q + q] = v[r];
         }
+        // forward: the previous tile's TMA stores must have read O before stage 2 rewrites it --
+        // waited for only here, so stages 0-1 of this tile overlap the drain of those stores
+        if (DIR < 0 && tid == 0) tma_store_wait_read0();
         __syncthreads();
         // stage 2 (last): radix RL, Ns = 256, tasks tt = j + i2 T; outputs tt + r N/RL
         float2* dst = out + (int64_t)p * Lout * Nx + x0 + q;
