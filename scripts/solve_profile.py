@@ -48,6 +48,7 @@ def main():
                           "schur_solver": ["amg_pcg", "sparse_cholesky"][a.schur],
                           "t_precond_setup_s": round(st["t_precond_setup_s"], 3),
                           "precond_MB": round(st["precond_bytes"] / 1e6, 1),
+                          "amg_levels": st["amg_levels"], "amg_op_complexity": round(st["amg_op_complexity"], 3),
                           "final_rre": st["final_rre"],
                           "L_pH_diag": [round(float(x) * 1e12, 5) for x in res["L"].diagonal()]}), flush=True)
         h.close()
