@@ -113,6 +113,8 @@ typedef struct {
     double  t_precond_setup_s; /* setup of the Schur solver (AMG hierarchy or Cholesky factor), Table V */
     double  precond_bytes;     /* device memory of that solver (Table IV "memory") */
     int32_t schur_solver;      /* opts.schur_solver of the solve */
+    int32_t amg_levels;        /* levels of the AMG hierarchy (built on the device; 0 for schur_solver 1) */
+    double  amg_op_complexity; /* AMG operator complexity: sum of level nonzeros / level-0 nonzeros */
 } svh_stats;
 
 /* svh_kernel_cache_build -- Algorithm 2, install stage: Tucker-compress the 7

@@ -26,6 +26,10 @@
 #include <numeric>
 #include <vector>
 
+#include <mutex>
+
+#include <cub/cub.cuh>
+#include <cusolverDn.h>
 #include <cusolverSp.h>
 #include <cusolverSp_LOWLEVEL_PREVIEW.h>
 #include <cusparse.h>
@@ -39,9 +43,6 @@ using cd = std::complex<double>;
 struct CsrDev {
     int n = 0;
     int64_t nnz = 0;
-    int* rowptr = nullptr;
-    int* col = nullptr;
-    double* val = nullptr;
     double* dinv = nullptr;   // l1-Jacobi: 1 / sum_j |a_ij|
     // ELL copy used by the SpMV-type kernels: column-major [ellw][n] (entry k of row i at
     // k*n + i, so a warp's loads of one k are coalesced); padding col = i, val = 0
@@ -49,8 +50,8 @@ struct CsrDev {
     int* ecol = nullptr;
     double* eval = nullptr;
     int* agg = nullptr;       // fine -> coarse aggregate (except coarsest level)
-    int* cptr = nullptr;      // members of aggregate I: cmem[cptr[I] .. cptr[I+1]) (ascending), for the
-    int* cmem = nullptr;      // deterministic (gather) restriction
+    int* cmem = nullptr;      // [nc][4] members of each aggregate (-1 padded), for the
+                              // deterministic (gather) restriction
     int nc = 0;
     // K-cycle vectors of this level when it is the coarse level of a Krylov-accelerated step
     double* kv1 = nullptr;
@@ -116,6 +117,8 @@ struct Solve {
     bool pre_built = false;          // the preconditioner of fixed_nodes is set up
     double t_pre_setup = 0;          // its setup wall time (Table V "preconditioner setup")
     double pre_bytes = 0;            // its device memory (AMG hierarchy or Cholesky factor)
+    int64_t nnz0 = 0;                // AMG level-0 nonzeros
+    double op_complexity = 0;        // AMG operator complexity: sum of level nonzeros / nnz0
     // sparse-direct Schur solve (svh_opts.schur_solver = 1, the paper's Table IV
     // comparison): S(p, p) = L L^T of the METIS nested-dissection-reordered free-node Schur
     // matrix, factored and solved on the device by cuSOLVER's csrchol
@@ -418,18 +421,21 @@ __global__ void k_zero(double* __restrict__ x, int64_t n) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) x[i] = 0.0;
 }
-// restriction: rc[I] = sum of r[i] over the members i of aggregate I, in ascending order (a
-// gather, not atomics: the result is bitwise independent of scheduling and of the batch width)
-__global__ void k_restrictG(int nc, const int* __restrict__ cptr, const int* __restrict__ cmem,
-                            const double* __restrict__ r, double* __restrict__ rc, int sh) {
+// restriction: rc[I] = sum of r[i] over the (<= 4) members i of aggregate I, in their fixed
+// order (a gather, not atomics: the result is bitwise independent of scheduling and of the
+// batch width)
+__global__ void k_restrictG(int nc, const int* __restrict__ mem4, const double* __restrict__ r,
+                            double* __restrict__ rc, int sh) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= (nc << sh)) return;
     const int I = t >> sh, p = t & ((1 << sh) - 1);
     const int NVP = 1 << sh;
     const double2* r2 = reinterpret_cast<const double2*>(r);
     double a0 = 0, a1 = 0;
-    for (int k = cptr[I]; k < cptr[I + 1]; ++k) {
-        const double2 v = r2[(int64_t)cmem[k] * NVP + p];
+    for (int k = 0; k < 4; ++k) {
+        const int m = mem4[4 * I + k];
+        if (m < 0) break;
+        const double2 v = r2[(int64_t)m * NVP + p];
         a0 += v.x;
         a1 += v.y;
     }
@@ -805,12 +811,8 @@ static void free_levels(Solve* S) {
         cudaFree(L.vx);
         cudaFree(L.tmp);
         cudaFree(L.x2);
-        cudaFree(L.rowptr);
-        cudaFree(L.col);
-        cudaFree(L.val);
         cudaFree(L.dinv);
         cudaFree(L.agg);
-        cudaFree(L.cptr);
         cudaFree(L.cmem);
         cudaFree(L.ecol);
         cudaFree(L.eval);
@@ -858,217 +860,419 @@ void free_solve(svh_handle* h) {
 }
 
 // ---------------------------------------------------------------------------
-// host: AMG setup on the free-node Schur complement S = F A Y^-1 A^T F
-namespace {
-
-// flux coefficients of the 5 bases on the 6 faces (-x,+x,-y,+y,-z,+z)
-const double kFlux[5][6] = {{-1, 1, 0, 0, 0, 0},
-                            {0, 0, -1, 1, 0, 0},
-                            {0, 0, 0, 0, -1, 1},
-                            {0.5, 0.5, -0.5, -0.5, 0, 0},
-                            {0.5, 0.5, 0.5, 0.5, -1, -1}};
-
-CsrHost build_schur(const Solve* S, const std::vector<int32_t>& node2free, const std::vector<int32_t>& flist, int nf) {
-    // rows by free node: neighbours are faces of the <= 2 adjacent voxels
-    CsrHost A;
-    A.n = nf;
-    A.rowptr.assign(nf + 1, 0);
-    std::vector<int> cols;
-    std::vector<double> vals;
-    cols.reserve((size_t)nf * 11);
-    vals.reserve((size_t)nf * 11);
-    std::vector<int> mark(nf, -1);
-    std::vector<int> slot(nf, 0);
-    const int64_t K = S->K;
-    int f = 0;
-    for (int fi = 0; fi < nf; ++fi) {   // row f = free index f (node flist[f])
-        const int64_t r = flist[fi];
-        const int row_start = (int)cols.size();
-        for (int side = 0; side < 2; ++side) {
-            const int32_t k = S->node_vox[2 * r + side];
-            if (k < 0) continue;
-            const int32_t* fn = &S->fnode[6 * k];
-            int pr = -1;
-            for (int q = 0; q < 6; ++q)
-                if (fn[q] == r) pr = q;
-            for (int q = 0; q < 6; ++q) {
-                const int cf = node2free[fn[q]];
-                if (cf < 0) continue;
-                double v = 0;
-                for (int b = 0; b < 5; ++b) v += kFlux[b][pr] * kFlux[b][q] * S->yinv[b * K + k];
-                if (mark[cf] != f) {
-                    mark[cf] = f;
-                    slot[cf] = (int)cols.size();
-                    cols.push_back(cf);
-                    vals.push_back(v);
-                } else {
-                    vals[slot[cf]] += v;
-                }
-            }
-        }
-        (void)row_start;
-        ++f;
-        A.rowptr[f] = (int)cols.size();
-    }
-    A.col.swap(cols);
-    A.val.swap(vals);
-    return A;
-}
-
-// one pass of pairwise aggregation: returns agg map and number of aggregates
-int pairwise(const CsrHost& A, std::vector<int>& agg) {
-    const int n = A.n;
-    agg.assign(n, -1);
-    int nc = 0;
-    std::vector<double> diag(n, 0.0);
-    for (int i = 0; i < n; ++i)
-        for (int p = A.rowptr[i]; p < A.rowptr[i + 1]; ++p)
-            if (A.col[p] == i) diag[i] = A.val[p];
-    for (int i = 0; i < n; ++i) {
-        if (agg[i] >= 0) continue;
-        // strongest coupling by |a_ij| / sqrt(a_ii a_jj) among unaggregated neighbours
-        int best = -1;
-        double bv = 0.0, rowmax = 0.0;
-        for (int p = A.rowptr[i]; p < A.rowptr[i + 1]; ++p) {
-            const int j = A.col[p];
-            if (j == i) continue;
-            // strength of connection: negative couplings (AGMG-style)
-            const double a = -A.val[p];
-            const double s = a / std::sqrt(std::fabs(diag[i] * diag[j]) + 1e-300);
-            rowmax = std::max(rowmax, s);
-            if (agg[j] < 0 && s > bv) {
-                bv = s;
-                best = j;
-            }
-        }
-        agg[i] = nc;
-        if (best >= 0 && bv >= 0.25 * rowmax) agg[best] = nc;
-        ++nc;
-    }
-    return nc;
-}
-
-CsrHost galerkin(const CsrHost& A, const std::vector<int>& agg, int nc) {
-    // members of each aggregate
-    std::vector<int> cnt(nc + 1, 0), mem(A.n);
-    for (int i = 0; i < A.n; ++i) cnt[agg[i] + 1]++;
-    for (int I = 0; I < nc; ++I) cnt[I + 1] += cnt[I];
-    std::vector<int> pos(cnt.begin(), cnt.end() - 1);
-    for (int i = 0; i < A.n; ++i) mem[pos[agg[i]]++] = i;
-    CsrHost C;
-    C.n = nc;
-    C.rowptr.assign(nc + 1, 0);
-    std::vector<int> mark(nc, -1), slot(nc, 0);
-    for (int I = 0; I < nc; ++I) {
-        for (int q = cnt[I]; q < cnt[I + 1]; ++q) {
-            const int i = mem[q];
-            for (int p = A.rowptr[i]; p < A.rowptr[i + 1]; ++p) {
-                const int J = agg[A.col[p]];
-                if (mark[J] != I) {
-                    mark[J] = I;
-                    slot[J] = (int)C.col.size();
-                    C.col.push_back(J);
-                    C.val.push_back(A.val[p]);
-                } else {
-                    C.val[slot[J]] += A.val[p];
-                }
-            }
-        }
-        C.rowptr[I + 1] = (int)C.col.size();
-    }
-    return C;
-}
-
-int g_upload_nvp = 1;   // vector pairs the level buffers are sized for (set by build_amg)
-CsrDev upload(const CsrHost& A) {
-    CsrDev d;
-    d.n = A.n;
-    d.nnz = (int64_t)A.col.size();
-    std::vector<double> dinv(A.n, 0.0);
-    for (int i = 0; i < A.n; ++i) {
-        double s = 0;
-        for (int p = A.rowptr[i]; p < A.rowptr[i + 1]; ++p) s += std::fabs(A.val[p]);
-        dinv[i] = s > 0 ? 1.0 / s : 0.0;
-    }
-    SVH_CUDA(cudaMalloc(&d.rowptr, (A.n + 1) * sizeof(int)));
-    SVH_CUDA(cudaMalloc(&d.col, std::max<size_t>(1, A.col.size()) * sizeof(int)));
-    SVH_CUDA(cudaMalloc(&d.val, std::max<size_t>(1, A.val.size()) * sizeof(double)));
-    SVH_CUDA(cudaMalloc(&d.dinv, std::max(1, A.n) * sizeof(double)));
-    SVH_CUDA(cudaMemcpy(d.rowptr, A.rowptr.data(), (A.n + 1) * sizeof(int), cudaMemcpyHostToDevice));
-    SVH_CUDA(cudaMemcpy(d.col, A.col.data(), A.col.size() * sizeof(int), cudaMemcpyHostToDevice));
-    SVH_CUDA(cudaMemcpy(d.val, A.val.data(), A.val.size() * sizeof(double), cudaMemcpyHostToDevice));
-    SVH_CUDA(cudaMemcpy(d.dinv, dinv.data(), A.n * sizeof(double), cudaMemcpyHostToDevice));
-    int w = 1;
-    for (int i = 0; i < A.n; ++i) w = std::max(w, A.rowptr[i + 1] - A.rowptr[i]);
-    std::vector<int> ec((size_t)w * std::max(1, A.n));
-    std::vector<double> ev((size_t)w * std::max(1, A.n), 0.0);
-    for (int i = 0; i < A.n; ++i) {
-        int k = 0;
-        for (int p = A.rowptr[i]; p < A.rowptr[i + 1]; ++p, ++k) {
-            ec[(size_t)k * A.n + i] = A.col[p];
-            ev[(size_t)k * A.n + i] = A.val[p];
-        }
-        for (; k < w; ++k) ec[(size_t)k * A.n + i] = i;
-    }
-    d.ellw = w;
-    SVH_CUDA(cudaMalloc(&d.ecol, ec.size() * sizeof(int)));
-    SVH_CUDA(cudaMalloc(&d.eval, ev.size() * sizeof(double)));
-    SVH_CUDA(cudaMemcpy(d.ecol, ec.data(), ec.size() * sizeof(int), cudaMemcpyHostToDevice));
-    SVH_CUDA(cudaMemcpy(d.eval, ev.data(), ev.size() * sizeof(double), cudaMemcpyHostToDevice));
-    const size_t vb = (size_t)2 * std::max(1, A.n) * sizeof(double) * g_upload_nvp;
-    SVH_CUDA(cudaMalloc(&d.vb, vb));
-    SVH_CUDA(cudaMalloc(&d.vx, vb));
-    SVH_CUDA(cudaMalloc(&d.tmp, vb));
-    SVH_CUDA(cudaMalloc(&d.x2, vb));
-    for (double** k : {&d.kv1, &d.kw1, &d.kr2, &d.kv2, &d.kw2}) SVH_CUDA(cudaMalloc(k, vb));
-    return d;
-}
-
-// dense SPD inverse (Cholesky, then solve for the identity); returns row-major
-std::vector<double> dense_inverse(const CsrHost& A) {
-    const int n = A.n;
-    std::vector<double> L((size_t)n * n, 0.0);
-    for (int i = 0; i < n; ++i)
-        for (int p = A.rowptr[i]; p < A.rowptr[i + 1]; ++p) L[(size_t)i * n + A.col[p]] = A.val[p];
-    // Cholesky in place (lower)
-    for (int j = 0; j < n; ++j) {
-        double d = L[(size_t)j * n + j];
-        for (int k = 0; k < j; ++k) d -= L[(size_t)j * n + k] * L[(size_t)j * n + k];
-        SVH_CHECK(d > 0, SVH_ECUDA, "coarse Schur matrix not SPD");
-        d = std::sqrt(d);
-        L[(size_t)j * n + j] = d;
-        for (int i = j + 1; i < n; ++i) {
-            double s = L[(size_t)i * n + j];
-            for (int k = 0; k < j; ++k) s -= L[(size_t)i * n + k] * L[(size_t)j * n + k];
-            L[(size_t)i * n + j] = s / d;
-        }
-    }
-    std::vector<double> inv((size_t)n * n, 0.0), col(n);
-    for (int c = 0; c < n; ++c) {
-        std::fill(col.begin(), col.end(), 0.0);
-        col[c] = 1.0;
-        for (int i = 0; i < n; ++i) {
-            double s = col[i];
-            for (int k = 0; k < i; ++k) s -= L[(size_t)i * n + k] * col[k];
-            col[i] = s / L[(size_t)i * n + i];
-        }
-        for (int i = n - 1; i >= 0; --i) {
-            double s = col[i];
-            for (int k = i + 1; k < n; ++k) s -= L[(size_t)k * n + i] * col[k];
-            col[i] = s / L[(size_t)i * n + i];
-        }
-        for (int i = 0; i < n; ++i) inv[(size_t)i * n + c] = col[i];
-    }
-    return inv;
-}
-
-}  // namespace
-
+// AMG setup on the device (the paper's AGMG): the free-node Schur
+// complement S = F A Y^-1 A^T F is assembled straight into the level-0 ELL, then each level is
+// coarsened by double pairwise aggregation (two matching passes, aggregates of <= 4 nodes) with
+// the Galerkin product P^T A P of the piecewise-constant prolongation after each pass.  Every
+// step is deterministic (a function of the matrix only, no atomics in any value), so every rank
+// of a sharded solve builds the bitwise-same hierarchy.
 #define SVH_CUSP(call)                                                                              \
     do {                                                                                            \
         const int st__ = (int)(call);                                                               \
         if (st__ != 0) throw Error{SVH_ECUDA, std::string(#call) + " failed: status " + std::to_string(st__)}; \
     } while (0)
+
+namespace {
+
+// flux coefficients of the 5 bases on the 6 faces (-x,+x,-y,+y,-z,+z)
+__constant__ double c_flux[5][6] = {{-1, 1, 0, 0, 0, 0},
+                                    {0, 0, -1, 1, 0, 0},
+                                    {0, 0, 0, 0, -1, 1},
+                                    {0.5, 0.5, -0.5, -0.5, 0, 0},
+                                    {0.5, 0.5, 0.5, 0.5, -1, -1}};
+constexpr int kSchurW = 11;   // <= 6 faces of each of the <= 2 voxels of a face, the face itself once
+
+// row fi of S (free node r = flist[fi]): couplings to the free faces of its <= 2 voxels,
+// S_rq = sum_b flux_b(r) flux_b(q) / Y_b(k) (Eq. 13-14); ELL column-major, l1 row sums
+__global__ void k_schur_ell(int nf, const int32_t* __restrict__ flist, const int32_t* __restrict__ node_vox,
+                            const int32_t* __restrict__ fnode, const int32_t* __restrict__ node2free,
+                            const double* __restrict__ yinv, int64_t K, int* __restrict__ ecol,
+                            double* __restrict__ eval, double* __restrict__ dinv,
+                            unsigned long long* __restrict__ nnz) {
+    const int fi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (fi >= nf) return;
+    const int32_t r = flist[fi];
+    int cols[kSchurW];
+    double vals[kSchurW];
+    int cnt = 0;
+    for (int side = 0; side < 2; ++side) {
+        const int32_t k = node_vox[2 * r + side];
+        if (k < 0) continue;
+        const int32_t* fn = fnode + 6 * (int64_t)k;
+        int pr = 0;
+        for (int q = 0; q < 6; ++q)
+            if (fn[q] == r) pr = q;
+        double y[5];
+        for (int b = 0; b < 5; ++b) y[b] = yinv[b * K + k];
+        for (int q = 0; q < 6; ++q) {
+            const int cf = node2free[fn[q]];
+            if (cf < 0) continue;
+            double v = 0;
+            for (int b = 0; b < 5; ++b) v += c_flux[b][pr] * c_flux[b][q] * y[b];
+            int j = 0;
+            while (j < cnt && cols[j] != cf) ++j;
+            if (j < cnt) {
+                vals[j] += v;
+            } else if (cnt < kSchurW) {
+                cols[cnt] = cf;
+                vals[cnt++] = v;
+            }
+        }
+    }
+    double s = 0;
+    for (int j = 0; j < kSchurW; ++j) {
+        const bool on = j < cnt;
+        ecol[(int64_t)j * nf + fi] = on ? cols[j] : fi;
+        eval[(int64_t)j * nf + fi] = on ? vals[j] : 0.0;
+        s += on ? fabs(vals[j]) : 0.0;
+    }
+    dinv[fi] = s > 0 ? 1.0 / s : 0.0;
+    atomicAdd(nnz, (unsigned long long)cnt);   // a count (order-independent)
+}
+
+__global__ void k_ell_diag(int n, int w, const int* __restrict__ ecol, const double* __restrict__ eval,
+                           double* __restrict__ diag) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double d = 0;
+    for (int k = 0; k < w; ++k)
+        if (ecol[(int64_t)k * n + i] == i) d += eval[(int64_t)k * n + i];
+    diag[i] = d;
+}
+
+// strength of connection (AGMG-style, negative couplings): s_ij = -a_ij / sqrt(|a_ii a_jj|)
+__device__ __forceinline__ double strength(double a, double di, double dj) {
+    return -a / sqrt(fabs(di * dj) + 1e-300);
+}
+__global__ void k_ell_smax(int n, int w, const int* __restrict__ ecol, const double* __restrict__ eval,
+                           const double* __restrict__ diag, double* __restrict__ smax) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double m = 0;
+    for (int k = 0; k < w; ++k) {
+        const int j = ecol[(int64_t)k * n + i];
+        if (j != i) m = fmax(m, strength(eval[(int64_t)k * n + i], diag[i], diag[j]));
+    }
+    smax[i] = m;
+}
+
+// edge tie-break: equal strengths are common on a uniform lattice; a hash of the (unordered)
+// pair makes every edge key distinct, so the heaviest remaining edge is always mutually
+// preferred and each matching round pairs a constant fraction of the nodes
+__device__ __forceinline__ uint32_t edge_hash(uint32_t a, uint32_t b) {
+    if (a > b) { const uint32_t t = a; a = b; b = t; }
+    uint32_t h = a * 0x9E3779B1u ^ (b * 0x85EBCA77u + 0x7F4A7C15u);
+    h ^= h >> 16; h *= 0x85EBCA6Bu; h ^= h >> 13; h *= 0xC2B2AE35u; h ^= h >> 16;
+    return h;
+}
+// matching round, step 1: every unmatched node proposes to its strongest unmatched neighbour
+// with s_ij >= 0.25 max_k s_ik (s_ij > 0); none -> it stays a singleton
+__global__ void k_match_pref(int n, int w, const int* __restrict__ ecol, const double* __restrict__ eval,
+                             const double* __restrict__ diag, const double* __restrict__ smax,
+                             const int* __restrict__ mate, int* __restrict__ pref) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (mate[i] >= 0) {
+        pref[i] = -1;
+        return;
+    }
+    int best = -1;
+    double bs = 0;
+    uint32_t bh = 0;
+    const double thr = 0.25 * smax[i];
+    for (int k = 0; k < w; ++k) {
+        const int j = ecol[(int64_t)k * n + i];
+        if (j == i || mate[j] >= 0) continue;
+        const double s = strength(eval[(int64_t)k * n + i], diag[i], diag[j]);
+        if (!(s > 0) || s < thr) continue;
+        const uint32_t hh = edge_hash(i, j);
+        if (best < 0 || s > bs || (s == bs && hh > bh)) {
+            best = j;
+            bs = s;
+            bh = hh;
+        }
+    }
+    pref[i] = best;
+}
+// step 2: mutual proposals are matched; a node with no proposal is final as a singleton
+__global__ void k_match_commit(int n, const int* __restrict__ pref, int* __restrict__ mate,
+                               unsigned int* __restrict__ left) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || mate[i] >= 0) return;
+    const int p = pref[i];
+    if (p < 0)
+        mate[i] = i;
+    else if (pref[p] == i)
+        mate[i] = p;
+    else
+        atomicAdd(left, 1u);   // a count only (the result does not depend on its order)
+}
+__global__ void k_match_final(int n, int* __restrict__ mate, int* __restrict__ lead) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (mate[i] < 0) mate[i] = i;
+    lead[i] = mate[i] >= i ? 1 : 0;   // the lower node of a pair (or a singleton) opens an aggregate
+}
+// aggregates numbered in the order of their lowest node (keeps the spatial order of the rows)
+__global__ void k_match_number(int n, const int* __restrict__ mate, const int* __restrict__ id,
+                               int* __restrict__ agg, int* __restrict__ mem) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int m = mate[i];
+    const int I = id[min(i, m)];
+    agg[i] = I;
+    if (m >= i) {
+        mem[2 * I] = i;
+        mem[2 * I + 1] = m > i ? m : -1;
+    }
+}
+// Galerkin row I of P^T A P (aggregates of <= 2 nodes): the members' rows in order, columns
+// mapped to aggregates, duplicates summed in first-appearance order; rows land in a [nc][2w]
+// scratch, their lengths in cnt
+__global__ void k_gal_rows(int nc, int n, int w, const int* __restrict__ mem, const int* __restrict__ ecol,
+                           const double* __restrict__ eval, const int* __restrict__ agg, int* __restrict__ scol,
+                           double* __restrict__ sval, int* __restrict__ cnt, int* __restrict__ wmax,
+                           unsigned long long* __restrict__ nnz) {
+    const int I = blockIdx.x * blockDim.x + threadIdx.x;
+    if (I >= nc) return;
+    int* rc = scol + (int64_t)I * 2 * w;
+    double* rv = sval + (int64_t)I * 2 * w;
+    int c = 0;
+    for (int q = 0; q < 2; ++q) {
+        const int m = mem[2 * I + q];
+        if (m < 0) continue;
+        for (int k = 0; k < w; ++k) {
+            const double v = eval[(int64_t)k * n + m];
+            if (v == 0.0) continue;   // ELL padding (and exact zeros)
+            const int J = agg[ecol[(int64_t)k * n + m]];
+            int j = 0;
+            while (j < c && rc[j] != J) ++j;
+            if (j < c) {
+                rv[j] += v;
+            } else {
+                rc[c] = J;
+                rv[c++] = v;
+            }
+        }
+    }
+    cnt[I] = c;
+    atomicMax(wmax, c);
+    atomicAdd(nnz, (unsigned long long)c);
+}
+__global__ void k_gal_ell(int nc, int w2, int wc, const int* __restrict__ scol, const double* __restrict__ sval,
+                          const int* __restrict__ cnt, int* __restrict__ ecol, double* __restrict__ eval,
+                          double* __restrict__ dinv) {
+    const int I = blockIdx.x * blockDim.x + threadIdx.x;
+    if (I >= nc) return;
+    const int c = cnt[I];
+    double s = 0;
+    for (int k = 0; k < wc; ++k) {
+        const bool on = k < c;
+        const double v = on ? sval[(int64_t)I * w2 + k] : 0.0;
+        ecol[(int64_t)k * nc + I] = on ? scol[(int64_t)I * w2 + k] : I;
+        eval[(int64_t)k * nc + I] = v;
+        s += fabs(v);
+    }
+    dinv[I] = s > 0 ? 1.0 / s : 0.0;
+}
+// double-pairwise composition: agg = agg2[agg1], members (<= 4, fixed width, -1 padded)
+__global__ void k_compose(int n, int n2, const int* __restrict__ agg1, const int* __restrict__ agg2,
+                          const int* __restrict__ mem1, const int* __restrict__ mem2, int* __restrict__ agg,
+                          int* __restrict__ mem4) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) agg[t] = agg2[agg1[t]];
+    if (t < n2) {
+        int o = 0;
+        for (int a = 0; a < 2; ++a) {
+            const int c1 = mem2[2 * t + a];
+            for (int b = 0; b < 2; ++b) {
+                const int f = c1 >= 0 ? mem1[2 * c1 + b] : -1;
+                if (f >= 0) mem4[4 * t + o++] = f;
+            }
+        }
+        for (; o < 4; ++o) mem4[4 * t + o] = -1;
+    }
+}
+// dense copy of a small ELL matrix (coarsest level), column-major n x n
+__global__ void k_ell_dense(int n, int w, const int* __restrict__ ecol, const double* __restrict__ eval,
+                            double* __restrict__ D) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int k = 0; k < w; ++k) {
+        const double v = eval[(int64_t)k * n + i];
+        if (v != 0.0) D[(int64_t)ecol[(int64_t)k * n + i] * n + i] += v;
+    }
+}
+__global__ void k_eye(int n, double* __restrict__ B) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < (int64_t)n * n) B[t] = (t / n == t % n) ? 1.0 : 0.0;
+}
+
+// device scratch for one level's setup (freed on scope exit, also on a throw)
+struct DevBuf {
+    std::vector<void*> p;
+    template <class T>
+    T* get(size_t n) {
+        void* q = nullptr;
+        SVH_CUDA(cudaMalloc(&q, std::max<size_t>(1, n) * sizeof(T)));
+        p.push_back(q);
+        return (T*)q;
+    }
+    ~DevBuf() {
+        for (void* q : p) cudaFree(q);
+    }
+};
+
+// an ELL matrix on the device (level operator before its vectors are attached)
+struct Ell {
+    int n = 0, w = 0;
+    int64_t nnz = 0;
+    int* col = nullptr;
+    double* val = nullptr;
+    double* dinv = nullptr;
+};
+void free_ell(Ell& A) {
+    cudaFree(A.col);
+    cudaFree(A.val);
+    cudaFree(A.dinv);
+    A = Ell{};
+}
+
+// one pairwise matching pass on A: agg[n], mem[2 nc] (caller-allocated, nc <= n); returns nc
+int pairwise_dev(const Ell& A, int* agg, int* mem, cudaStream_t s) {
+    const int n = A.n;
+    DevBuf B;
+    double* diag = B.get<double>(n);
+    double* smax = B.get<double>(n);
+    int* mate = B.get<int>(n);
+    int* pref = B.get<int>(n);
+    int* lead = B.get<int>(n + 1);
+    int* id = B.get<int>(n + 1);
+    unsigned int* left = B.get<unsigned int>(1);
+    const unsigned g = nblk(n);
+    SVH_LAUNCH(k_ell_diag, g, 256, 0, s, n, A.w, A.col, A.val, diag);
+    SVH_LAUNCH(k_ell_smax, g, 256, 0, s, n, A.w, A.col, A.val, diag, smax);
+    SVH_CUDA(cudaMemsetAsync(mate, 0xff, n * sizeof(int), s));
+    for (int round = 0; round < 12; ++round) {
+        SVH_CUDA(cudaMemsetAsync(left, 0, sizeof(unsigned int), s));
+        SVH_LAUNCH(k_match_pref, g, 256, 0, s, n, A.w, A.col, A.val, diag, smax, mate, pref);
+        SVH_LAUNCH(k_match_commit, g, 256, 0, s, n, pref, mate, left);
+        unsigned int h_left = 0;
+        SVH_CUDA(cudaMemcpyAsync(&h_left, left, sizeof(h_left), cudaMemcpyDeviceToHost, s));
+        SVH_CUDA(cudaStreamSynchronize(s));
+        if (h_left == 0) break;
+    }
+    SVH_LAUNCH(k_match_final, g, 256, 0, s, n, mate, lead);
+    size_t tb = 0;
+    SVH_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, lead, id, n + 1, s));
+    void* tmp = B.get<char>(tb);
+    SVH_CUDA(cudaMemsetAsync(lead + n, 0, sizeof(int), s));
+    SVH_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, lead, id, n + 1, s));
+    int nc = 0;
+    SVH_CUDA(cudaMemcpyAsync(&nc, id + n, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SVH_CUDA(cudaStreamSynchronize(s));
+    SVH_LAUNCH(k_match_number, g, 256, 0, s, n, mate, id, agg, mem);
+    return nc;
+}
+
+// C = P^T A P for the pairwise aggregates (agg, mem) of A
+Ell galerkin_dev(const Ell& A, const int* agg, const int* mem, int nc, cudaStream_t s) {
+    DevBuf B;
+    const int w2 = 2 * A.w;
+    int* scol = B.get<int>((size_t)nc * w2);
+    double* sval = B.get<double>((size_t)nc * w2);
+    int* cnt = B.get<int>(nc);
+    int* wmax = B.get<int>(1);
+    unsigned long long* nnz = B.get<unsigned long long>(1);
+    SVH_CUDA(cudaMemsetAsync(wmax, 0, sizeof(int), s));
+    SVH_CUDA(cudaMemsetAsync(nnz, 0, sizeof(unsigned long long), s));
+    SVH_LAUNCH(k_gal_rows, nblk(nc), 256, 0, s, nc, A.n, A.w, mem, A.col, A.val, agg, scol, sval, cnt, wmax, nnz);
+    int wc = 0;
+    unsigned long long h_nnz = 0;
+    SVH_CUDA(cudaMemcpyAsync(&wc, wmax, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SVH_CUDA(cudaMemcpyAsync(&h_nnz, nnz, sizeof(h_nnz), cudaMemcpyDeviceToHost, s));
+    SVH_CUDA(cudaStreamSynchronize(s));
+    Ell C;
+    C.n = nc;
+    C.w = std::max(1, wc);
+    C.nnz = (int64_t)h_nnz;
+    SVH_CUDA(cudaMalloc(&C.col, (size_t)C.w * std::max(1, nc) * sizeof(int)));
+    SVH_CUDA(cudaMalloc(&C.val, (size_t)C.w * std::max(1, nc) * sizeof(double)));
+    SVH_CUDA(cudaMalloc(&C.dinv, std::max(1, nc) * sizeof(double)));
+    SVH_LAUNCH(k_gal_ell, nblk(nc), 256, 0, s, nc, w2, C.w, scol, sval, cnt, C.col, C.val, C.dinv);
+    return C;
+}
+
+int g_upload_nvp = 1;   // vector pairs the level buffers are sized for (set by build_amg)
+// a level of the hierarchy: takes ownership of A's arrays, attaches the cycle's vectors
+CsrDev make_level(Ell& A) {
+    CsrDev d;
+    d.n = A.n;
+    d.nnz = A.nnz;
+    d.ellw = A.w;
+    d.ecol = A.col;
+    d.eval = A.val;
+    d.dinv = A.dinv;
+    A = Ell{};
+    const size_t vb = (size_t)2 * std::max(1, d.n) * sizeof(double) * g_upload_nvp;
+    for (double** k : {&d.vb, &d.vx, &d.tmp, &d.x2, &d.kv1, &d.kw1, &d.kr2, &d.kv2, &d.kw2})
+        SVH_CUDA(cudaMalloc(k, vb));
+    return d;
+}
+
+// host CSR copy of an ELL matrix (the sparse-direct comparator factors level 0 on the host side)
+CsrHost ell_to_host(const Ell& A) {
+    std::vector<int> ec((size_t)A.w * A.n);
+    std::vector<double> ev((size_t)A.w * A.n);
+    SVH_CUDA(cudaMemcpy(ec.data(), A.col, ec.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    SVH_CUDA(cudaMemcpy(ev.data(), A.val, ev.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    CsrHost H;
+    H.n = A.n;
+    H.rowptr.assign(A.n + 1, 0);
+    for (int i = 0; i < A.n; ++i) {
+        for (int k = 0; k < A.w; ++k) {
+            const double v = ev[(size_t)k * A.n + i];
+            if (v == 0.0) continue;
+            H.col.push_back(ec[(size_t)k * A.n + i]);
+            H.val.push_back(v);
+        }
+        H.rowptr[i + 1] = (int)H.col.size();
+    }
+    return H;
+}
+
+// inverse of the (small, SPD) coarsest matrix on the device: Cholesky (potrf) + potrs on I
+double* dense_inverse_dev(const Ell& A, cudaStream_t s) {
+    static cusolverDnHandle_t hs = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] { cusolverDnCreate(&hs); });
+    SVH_CHECK(hs != nullptr, SVH_ECUDA, "cusolverDnCreate failed");
+    const int n = A.n;
+    DevBuf B;
+    double* D = B.get<double>((size_t)n * n);
+    int* info = B.get<int>(1);
+    double* inv = nullptr;
+    SVH_CUDA(cudaMalloc(&inv, (size_t)std::max(1, n) * n * sizeof(double)));
+    SVH_CUDA(cudaMemsetAsync(D, 0, (size_t)n * n * sizeof(double), s));
+    SVH_LAUNCH(k_ell_dense, nblk(n), 256, 0, s, n, A.w, A.col, A.val, D);
+    SVH_LAUNCH(k_eye, nblk((int64_t)n * n), 256, 0, s, n, inv);
+    SVH_CUSP(cusolverDnSetStream(hs, s));
+    int lw = 0;
+    SVH_CUSP(cusolverDnDpotrf_bufferSize(hs, CUBLAS_FILL_MODE_LOWER, n, D, n, &lw));
+    double* work = B.get<double>(lw);
+    SVH_CUSP(cusolverDnDpotrf(hs, CUBLAS_FILL_MODE_LOWER, n, D, n, work, lw, info));
+    SVH_CUSP(cusolverDnDpotrs(hs, CUBLAS_FILL_MODE_LOWER, n, n, D, n, inv, n, info));
+    int h_info = 0;
+    SVH_CUDA(cudaMemcpyAsync(&h_info, info, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SVH_CUDA(cudaStreamSynchronize(s));
+    if (h_info != 0) {
+        cudaFree(inv);
+        throw Error{SVH_ECUDA, "coarse Schur matrix not SPD"};
+    }
+    return inv;   // symmetric: row-major = column-major
+}
+
+}  // namespace
 
 // f4 comparator: METIS nested-dissection order (host), permuted CSR, device Cholesky factor
 static void build_chol(Solve* S, const CsrHost& A) {
@@ -1181,55 +1385,72 @@ static void build_amg(svh_handle* h, const std::vector<int32_t>& fixed, int nvp)
         S->pre_built = true;
         return;
     }
-    CsrHost A = build_schur(S, node2free, flist, S->nf);
+    cudaStream_t s = nullptr;
+    Ell A;
+    A.n = S->nf;
+    A.w = kSchurW;
+    SVH_CUDA(cudaMalloc(&A.col, (size_t)A.w * A.n * sizeof(int)));
+    SVH_CUDA(cudaMalloc(&A.val, (size_t)A.w * A.n * sizeof(double)));
+    SVH_CUDA(cudaMalloc(&A.dinv, (size_t)A.n * sizeof(double)));
+    {
+        DevBuf B;
+        unsigned long long* dn = B.get<unsigned long long>(1);
+        SVH_CUDA(cudaMemsetAsync(dn, 0, sizeof(*dn), s));
+        SVH_LAUNCH(k_schur_ell, nblk(A.n), 256, 0, s, A.n, S->d_free_list, S->d_node_vox, S->d_fnode,
+                   S->d_node2free, S->d_yinv, S->K, A.col, A.val, A.dinv, dn);
+        unsigned long long hn = 0;
+        SVH_CUDA(cudaMemcpyAsync(&hn, dn, sizeof(hn), cudaMemcpyDeviceToHost, s));
+        SVH_CUDA(cudaStreamSynchronize(s));
+        A.nnz = (int64_t)hn;
+    }
+    struct EllGuard {   // frees whichever level operators are still owned here on a throw
+        Ell* a[2];
+        ~EllGuard() {
+            for (Ell* e : a) free_ell(*e);
+        }
+    };
+    Ell A1;
+    EllGuard guard{{&A, &A1}};
     if (h->opts.schur_solver == 1) {
-        build_chol(S, A);
+        build_chol(S, ell_to_host(A));
         S->pre_built = true;
         return;
     }
+    S->nnz0 = A.nnz;
+    S->op_complexity = 0;
     const int kCoarse = 1024;
     while (true) {
         if (A.n <= kCoarse) {
-            auto inv = dense_inverse(A);
+            S->d_cinv = dense_inverse_dev(A, s);
             S->ncoarse = A.n;
-            SVH_CUDA(cudaMalloc(&S->d_cinv, inv.size() * sizeof(double)));
-            SVH_CUDA(cudaMemcpy(S->d_cinv, inv.data(), inv.size() * sizeof(double), cudaMemcpyHostToDevice));
-            CsrDev d = upload(A);
-            S->levels.push_back(d);
+            S->levels.push_back(make_level(A));
             break;
         }
-        std::vector<int> a1, a2;
-        const int n1 = pairwise(A, a1);
-        CsrHost A1 = galerkin(A, a1, n1);
-        const int n2 = pairwise(A1, a2);
-        std::vector<int> agg(A.n);
-        for (int i = 0; i < A.n; ++i) agg[i] = a2[a1[i]];
-        CsrDev d = upload(A);
+        DevBuf B;
+        int* agg1 = B.get<int>(A.n);
+        int* mem1 = B.get<int>(2 * (size_t)A.n);
+        const int n1 = pairwise_dev(A, agg1, mem1, s);
+        A1 = galerkin_dev(A, agg1, mem1, n1, s);
+        int* agg2 = B.get<int>(n1);
+        int* mem2 = B.get<int>(2 * (size_t)n1);
+        const int n2 = pairwise_dev(A1, agg2, mem2, s);
+        Ell C = galerkin_dev(A1, agg2, mem2, n2, s);
+        free_ell(A1);
+        const int n = A.n;
+        CsrDev d = make_level(A);
         d.nc = n2;
-        SVH_CUDA(cudaMalloc(&d.agg, A.n * sizeof(int)));
-        SVH_CUDA(cudaMemcpy(d.agg, agg.data(), A.n * sizeof(int), cudaMemcpyHostToDevice));
-        // aggregate members (ascending) for the gather restriction
-        std::vector<int> cptr(n2 + 1, 0), cmem(A.n);
-        for (int i = 0; i < A.n; ++i) cptr[agg[i] + 1]++;
-        for (int I = 0; I < n2; ++I) cptr[I + 1] += cptr[I];
-        {
-            std::vector<int> pos(cptr.begin(), cptr.end() - 1);
-            for (int i = 0; i < A.n; ++i) cmem[pos[agg[i]]++] = i;
-        }
-        SVH_CUDA(cudaMalloc(&d.cptr, (n2 + 1) * sizeof(int)));
-        SVH_CUDA(cudaMalloc(&d.cmem, std::max(1, A.n) * sizeof(int)));
-        SVH_CUDA(cudaMemcpy(d.cptr, cptr.data(), (n2 + 1) * sizeof(int), cudaMemcpyHostToDevice));
-        SVH_CUDA(cudaMemcpy(d.cmem, cmem.data(), A.n * sizeof(int), cudaMemcpyHostToDevice));
+        SVH_CUDA(cudaMalloc(&d.agg, n * sizeof(int)));
+        SVH_CUDA(cudaMalloc(&d.cmem, 4 * (size_t)std::max(1, n2) * sizeof(int)));
+        SVH_LAUNCH(k_compose, nblk(std::max(n, n2)), 256, 0, s, n, n2, agg1, agg2, mem1, mem2, d.agg, d.cmem);
         S->levels.push_back(d);
-        CsrHost C = galerkin(A, agg, n2);
-        if (n2 > 0.85 * A.n) {   // stalled coarsening: stop with a dense solve if small enough
-            SVH_CHECK(C.n <= 8192, SVH_ECUDA, "AMG coarsening stalled");
+        A = C;
+        if (n2 > 0.85 * n) {   // stalled coarsening: stop with a dense solve if small enough
+            SVH_CHECK(A.n <= 8192, SVH_ECUDA, "AMG coarsening stalled");
         }
-        A.rowptr.swap(C.rowptr);
-        A.col.swap(C.col);
-        A.val.swap(C.val);
-        A.n = C.n;
     }
+    SVH_CUDA(cudaDeviceSynchronize());
+    for (const auto& L : S->levels) S->op_complexity += (double)L.nnz;
+    S->op_complexity /= std::max<double>(1.0, (double)S->nnz0);
     SVH_CUDA(cudaMalloc(&S->d_kc, S->levels.size() * 8 * 2 * (size_t)S->nvp_cap * sizeof(double)));
     SVH_CUDA(cudaMemset(S->d_kc, 0, S->levels.size() * 8 * 2 * (size_t)S->nvp_cap * sizeof(double)));
     for (const auto& L : S->levels)
@@ -1328,7 +1549,7 @@ static void kcycle(Solve* S, int l, const double* b, double* x, cudaStream_t s, 
     const int64_t nct = (int64_t)nc * NVP;
     SVH_LAUNCH(k_jacobi2V, nblk(nt), 256, 0, s, n, L.ellw, L.ecol, L.eval, L.dinv, b, L.x2, sh);
     SVH_LAUNCH(k_residV, nblk(nt), 256, 0, s, n, L.ellw, L.ecol, L.eval, b, L.x2, L.tmp, sh);
-    SVH_LAUNCH(k_restrictG, nblk(nct), 256, 0, s, nc, L.cptr, L.cmem, L.tmp, C.vb, sh);
+    SVH_LAUNCH(k_restrictG, nblk(nct), 256, 0, s, nc, L.cmem, L.tmp, C.vb, sh);
     if (l < kKLevels && l + 1 < last) {
         double* kc = S->d_kc + (size_t)l * 8 * NV;
         kcycle(S, l + 1, C.vb, C.kv1, s, NVP);
@@ -1994,6 +2215,8 @@ static void solve_columns(svh_handle* h, const svh_port* ports, int P, const int
         st->t_precond_setup_s = S->t_pre_setup;
         st->precond_bytes = S->pre_bytes;
         st->schur_solver = h->opts.schur_solver;
+        st->amg_levels = h->opts.schur_solver == 1 ? 0 : (int32_t)S->levels.size();
+        st->amg_op_complexity = h->opts.schur_solver == 1 ? 0.0 : S->op_complexity;
         st->converged = all_conv ? 1 : 0;
         st->final_rre = std::max(st->final_rre, worst);
         st->t_solve_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

@@ -57,7 +57,8 @@ class Stats(ctypes.Structure):
                 ("t_setup_s", ctypes.c_double), ("t_solve_s", ctypes.c_double), ("t_matvec_s", ctypes.c_double),
                 ("t_precond_s", ctypes.c_double), ("ranks", (ctypes.c_int32 * 3) * 7),
                 ("compression_ratio", ctypes.c_double), ("t_precond_setup_s", ctypes.c_double),
-                ("precond_bytes", ctypes.c_double), ("schur_solver", ctypes.c_int32)]
+                ("precond_bytes", ctypes.c_double), ("schur_solver", ctypes.c_int32),
+                ("amg_levels", ctypes.c_int32), ("amg_op_complexity", ctypes.c_double)]
 
     def as_dict(self):
         d = {f: getattr(self, f) for f, _ in self._fields_ if f != "ranks"}

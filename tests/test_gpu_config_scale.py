@@ -62,3 +62,29 @@ def test_config3_sigma0_zero_frequency_independence(svh_lib):
     L1 = _cfg3_L(svh_lib, case, freq=1e9)["L"]
     L10 = _cfg3_L(svh_lib, case, freq=10e9)["L"]
     assert np.max(np.abs(L1 - L10)) <= 1e-4 * np.max(np.abs(L10))                # P11
+
+
+def test_config2_amg_hierarchy_on_device(svh_lib):
+    """H11: the AMG hierarchy is built on the device (double pairwise aggregation, Galerkin
+    products, dense coarsest inverse), is deterministic (two setups give the bitwise-same
+    solve) and coarsens like AGMG's double pairwise scheme: several levels, operator complexity
+    well below 2 (aggregates of <= 4 nodes), and a bounded number of inner iterations per
+    preconditioner apply at the paper's inner solver."""
+    case = svh_inputs.config2()
+    pt = GOLDEN["points"][0]
+    res = []
+    for _ in range(2):
+        with svh_lib.setup_case(case, tucker_tol=0.0, rre=1e-7) as h:
+            h.set_frequency(pt["freq_hz"])
+            res.append(h.solve(case["ports"]))
+    a, b = res
+    assert a["code"] == 0 and b["code"] == 0
+    st = a["stats"]
+    assert st["amg_levels"] >= 3, st
+    assert 1.0 < st["amg_op_complexity"] < 2.0, st
+    assert st["t_precond_setup_s"] > 0
+    assert np.array_equal(a["Y"], b["Y"])                     # deterministic hierarchy and solve
+    assert abs(float(a["L"][0, 0]) - pt["L_H"]) <= L_TOL * abs(pt["L_H"])
+    # inner PCG iterations per preconditioner apply (one apply per GMRES iteration + 1)
+    per_apply = st["inner_iterations"] / max(1, st["total_iterations"] + 1)
+    assert per_apply <= 30, st
