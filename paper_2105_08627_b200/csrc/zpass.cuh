@@ -77,10 +77,10 @@ __global__ void __launch_bounds__(NT, 1)
     const int nunits = (Ny / 2 + 1) * tiles_x;
     const int u0 = (int)((int64_t)nunits * blockIdx.x / gridDim.x);
     const int u1 = (int)((int64_t)nunits * (blockIdx.x + 1) / gridDim.x);
-    // L1 tasks a = tid + k NT -> (c, n2, q); their element offsets and live-plane masks are
-    // per-thread constants
+    // L1 tasks a = tid + k NT -> (c, n2, q); their element pointers (tile base added per tile)
+    // and live-plane masks are per-thread constants
     int tc[TL1], tq[TL1], tn2[TL1];
-    int64_t toff[TL1];
+    float2* pk[TL1];
     uint32_t live[TL1];
 #pragma unroll
     for (int k = 0; k < TL1; ++k) {
@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(NT, 1)
         tc[k] = a / (R2 * Q);
         tn2[k] = (a / Q) % R2;
         tq[k] = a % Q;
-        toff[k] = (int64_t)tc[k] * Kz * plane + (int64_t)tn2[k] * plane + tq[k];
+        pk[k] = X2 + ((int64_t)tc[k] * Kz * plane + (int64_t)tn2[k] * plane + tq[k]);
         uint32_t m = 0;
         for (int n1 = 0; n1 < R1 / 2; ++n1) {
             const int z = R2 * n1 + tn2[k];
@@ -96,6 +96,11 @@ __global__ void __launch_bounds__(NT, 1)
         }
         live[k] = m;
     }
+    // CTA-uniform fast paths: every kept plane z < Kz = N/2 exists (unpredicated stores) and
+    // is non-empty (unpredicated loads)
+    const bool full_z = Kz == P::NH;
+    bool dense_z = full_z;
+    for (int z = 0; z < Kz; ++z) dense_z = dense_z && __ldg(&planeok[z]) != 0;
     // L2 role and its twiddles W_N^{n2 k1}, n2 = 1 .. R2-1
     const bool l2 = tid < NL2;
     const int k1 = tid / Q, q2 = tid % Q;
@@ -110,38 +115,51 @@ __global__ void __launch_bounds__(NT, 1)
             F3s[e] = c < d3 ? __ldg(&sv.fac[m][2][(int64_t)kh * d3 + c]) : 0.f;
         }
     }
-    auto unit_rows = [&](int u) { const int oy = u / tiles_x; return (oy == 0 || 2 * oy == Ny) ? 1 : 2; };
-    // tile (u, i) -> element offset of (r, c = 0, z = 0, ky, xt * Q)
-    auto tile_base = [&](int u, int i, int& ky, int& xt, int& r) -> int64_t {
-        const int oy = u / tiles_x;
-        xt = u % tiles_x;
-        const int row = i / nrhs;
-        r = i % nrhs;
-        ky = row == 0 ? oy : Ny - oy;
-        return (int64_t)r * 5 * Kz * plane + (int64_t)ky * Nxs + xt * Q;
+    // tile walk without divisions: unit u = (oy, xt); within a unit the row (ky = oy, then
+    // Ny - oy) and, fastest, the RHS r.  base = element offset of (r, c = 0, z = 0, ky, xt * Q)
+    const int64_t rstride = (int64_t)5 * Kz * plane;
+    auto rows_of = [&](int o) { return (o == 0 || 2 * o == Ny) ? 1 : 2; };
+    auto base_of = [&](int o, int x, int rw, int rr) -> int64_t {
+        return (int64_t)rr * rstride + (int64_t)(rw == 0 ? o : Ny - o) * Nxs + x * Q;
     };
     const int64_t zstep = (int64_t)R2 * plane;
     float2 nx[TL1][R1 / 2];   // prefetch of the next tile's live inputs
-    auto load_tile = [&](int64_t base) {
+    auto load_tile = [&](int64_t b) {
 #pragma unroll
         for (int k = 0; k < TL1; ++k) {
-            const float2* src = X2 + base + toff[k];
+            const float2* src = pk[k] + b;
+            if (dense_z) {
 #pragma unroll
-            for (int n1 = 0; n1 < R1 / 2; ++n1) nx[k][n1] = ((live[k] >> n1) & 1u) ? src[n1 * zstep] : zero;
+                for (int n1 = 0; n1 < R1 / 2; ++n1) {
+                    nx[k][n1] = *src;
+                    src += zstep;
+                }
+            } else {
+#pragma unroll
+                for (int n1 = 0; n1 < R1 / 2; ++n1) {
+                    nx[k][n1] = ((live[k] >> n1) & 1u) ? *src : zero;
+                    src += zstep;
+                }
+            }
         }
     };
-    int u = u0, i = 0;
+    int u = u0, oy = u0 / tiles_x, xt = u0 - (u0 / tiles_x) * tiles_x, row = 0, r = 0;
+    // folded moment-form constants, applied once per unit when KV is built:
+    // g K0, gx K1x, g K1y (its ky sign at use), -2g K1z (its kz sign at use), g K2x, g K2y, 4g K2z
+    auto kv_scale = [&](int m, int q) -> float {
+        const int kx = kxg + xt * Q + q;
+        return m == 1 ? (kx <= (Nx >> 1) ? g : -g) : m == 3 ? -2.f * g : m == 6 ? 4.f * g : g;
+    };
+    int64_t base = 0;
     if (u < u1) {
-        int ky, xt, r;
-        load_tile(tile_base(u, 0, ky, xt, r));
+        base = base_of(oy, xt, 0, 0);
+        load_tile(base);
     }
     int cur_oy = -1;
     for (int s = 0; u < u1; ++s) {
         float2* Tb = T + (NBUF == 2 ? (s & 1) * TE : 0);
-        int ky, xt, r;
-        const int64_t base = tile_base(u, i, ky, xt, r);
-        const int oy = u / tiles_x;
-        if (i == 0) {
+        const int ky = row == 0 ? oy : Ny - oy;
+        if (row == 0 && r == 0) {
             // the unit's raw kernel spectra KV[kh][q][m] (the previous tile's L2 finished at its barrier)
             if constexpr (DM > 0) {
                 if (oy != cur_oy) {
@@ -182,19 +200,32 @@ __global__ void __launch_bounds__(NT, 1)
                     }
                 }
                 __syncthreads();
-                // KV[kh][q][m] = F3_m[kh] . H_m[q]   (lanes run over q; both rows on chip)
+                // KV[kh][q][m] = F3_m[kh] . H_m[q]: a thread keeps its column's H row in registers
+                // (q = tid mod Q is fixed, NT is a multiple of Q) and walks kh; F3 rows by 16-byte loads
+                static_assert(NT % Q == 0 && DM % 4 == 0, "KV build: fixed column per thread");
+                {
+                    const int q = tid % Q;
 #pragma unroll 1
-                for (int m = 0; m < 7; ++m) {
-                    const float* F3m = F3s + m * NK * DM;
-                    const float* Hm = H + m * Q * DP;
-                    for (int t = tid; t < NK * Q; t += NT) {
-                        const int q = t % Q, kh = t / Q;
-                        const float* f3 = F3m + kh * DM;
-                        const float* hq = Hm + q * DP;
-                        float acc = 0.f;
+                    for (int m = 0; m < 7; ++m) {
+                        const float* F3m = F3s + m * NK * DM;
+                        const float* hq = H + (m * Q + q) * DP;
+                        const float sc = kv_scale(m, q);
+                        float hr[DM];
 #pragma unroll
-                        for (int c = 0; c < DM; ++c) acc = fmaf(f3[c], hq[c], acc);
-                        KV[t * KVS + m] = acc;
+                        for (int c = 0; c < DM; ++c) hr[c] = hq[c];
+                        for (int kh = tid / Q; kh < NK; kh += NT / Q) {
+                            const float4* f3 = reinterpret_cast<const float4*>(F3m + kh * DM);
+                            float acc = 0.f;
+#pragma unroll
+                            for (int c4 = 0; c4 < DM / 4; ++c4) {
+                                const float4 f = f3[c4];
+                                acc = fmaf(f.x, hr[4 * c4], acc);
+                                acc = fmaf(f.y, hr[4 * c4 + 1], acc);
+                                acc = fmaf(f.z, hr[4 * c4 + 2], acc);
+                                acc = fmaf(f.w, hr[4 * c4 + 3], acc);
+                            }
+                            KV[(kh * Q + q) * KVS + m] = sc * acc;
+                        }
                     }
                 }
             } else {
@@ -204,37 +235,43 @@ __global__ void __launch_bounds__(NT, 1)
                     const int kh = rest % NK, m = rest / NK;
                     const int kx = kxg + xt * Q + q;
                     const int ox = kx <= (Nx >> 1) ? kx : Nx - kx;
-                    KV[(kh * Q + q) * KVS + m] = __ldg(&sv.spec[m * pl + ((int64_t)kh * sv.hy + oy) * sv.hx + ox]);
+                    KV[(kh * Q + q) * KVS + m] =
+                        kv_scale(m, q) * __ldg(&sv.spec[m * pl + ((int64_t)kh * sv.hy + oy) * sv.hx + ox]);
                 }
             }
             // published to L2 by the barrier after L1
         }
-        // next tile of this CTA: its inputs are loaded into registers during this tile
-        int un = u, in = i + 1;
-        if (in == unit_rows(u) * nrhs) {
-            ++un;
-            in = 0;
+        // next tile of this CTA
+        int un = u, oyn = oy, xtn = xt, rown = row, rn = r + 1;
+        if (rn == nrhs) {
+            rn = 0;
+            if (++rown == rows_of(oy)) {
+                rown = 0;
+                ++un;
+                if (++xtn == tiles_x) {
+                    xtn = 0;
+                    ++oyn;
+                }
+            }
         }
+        const int64_t basen = base_of(oyn, xtn, rown, rn);
         // L1 forward
 #pragma unroll
         for (int k = 0; k < TL1; ++k) {
             float2 v[R1];
 #pragma unroll
             for (int n1 = 0; n1 < R1; ++n1) v[n1] = n1 < R1 / 2 ? nx[k][n1] : zero;
-            if (k == TL1 - 1 && un < u1) {
-                int kyn, xtn, rn;
-                load_tile(tile_base(un, in, kyn, xtn, rn));
-            }
             reg_fft<R1, -1, true>(v);
             float2* t1 = Tb + (tc[k] * R2 + tn2[k]) * TB + tq[k];
 #pragma unroll
             for (int kk = 0; kk < R1; ++kk) t1[kk * Q] = v[kk];
         }
+        // the next tile's inputs: in flight during L2 and the inverse L1 of this tile
+        if (un < u1) load_tile(basen);
         __syncthreads();
         // L2: twiddle, R2-point FFT, MAC, inverse, twiddle
         if (l2) {
-            const int kx = kxg + xt * Q + q2;
-            const float gx = kx <= (Nx >> 1) ? g : -g, gy = ky <= (Ny >> 1) ? g : -g;
+            const uint32_t sy = ky <= (Ny >> 1) ? 0u : 0x80000000u;   // K1y is odd in ky
             float2 uu[5][R2];
 #pragma unroll
             for (int c = 0; c < 5; ++c) {
@@ -249,13 +286,13 @@ __global__ void __launch_bounds__(NT, 1)
             for (int k2 = 0; k2 < R2; ++k2) {
                 const int kz = k1 + R1 * k2;
                 const int kh = kz <= (N >> 1) ? kz : N - kz;
-                const float s3 = kz <= (N >> 1) ? 1.f : -1.f;   // K1z is odd in kz
+                const uint32_t s3 = kz <= (N >> 1) ? 0u : 0x80000000u;   // K1z is odd in kz
                 const float4 ka = *reinterpret_cast<const float4*>(KV + (kh * Q + q2) * KVS);
                 const float4 kb = *reinterpret_cast<const float4*>(KV + (kh * Q + q2) * KVS + 4);
-                // folded moment-form constants
-                const float f0 = g * ka.x, f1 = gx * ka.y, f2 = gy * ka.z;
-                const float f3 = (-2.f * g) * s3 * ka.w;
-                const float f4 = g * kb.x, f5 = g * kb.y, f6 = (4.f * g) * kb.z;
+                // the constants were folded into KV; only the two odd-axis signs are applied here
+                const float f0 = ka.x, f1 = ka.y, f2 = __uint_as_float(__float_as_uint(ka.z) ^ sy);
+                const float f3 = __uint_as_float(__float_as_uint(ka.w) ^ s3);
+                const float f4 = kb.x, f5 = kb.y, f6 = kb.z;
                 const float2 Ix = uu[0][k2], Iy = uu[1][k2], Iz = uu[2][k2], I2 = uu[3][k2], I3 = uu[4][k2];
                 const float2 m1x = cadd(I2, I3), m1y = csub(I3, I2);
                 const float2 Qx = cfma_s(Ix, -f1, cmul_i(m1x, f4));
@@ -286,13 +323,27 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
             for (int kk = 0; kk < R1; ++kk) v[kk] = t1[kk * Q];
             reg_fft<R1, +1>(v);
-            float2* dst = X2 + base + toff[k];
+            float2* dst = pk[k] + base;
+            if (full_z) {
 #pragma unroll
-            for (int n1 = 0; n1 < R1 / 2; ++n1)
-                if (R2 * n1 + tn2[k] < Kz) dst[n1 * zstep] = v[n1];
+                for (int n1 = 0; n1 < R1 / 2; ++n1) {
+                    *dst = v[n1];
+                    dst += zstep;
+                }
+            } else {
+#pragma unroll
+                for (int n1 = 0; n1 < R1 / 2; ++n1) {
+                    if (R2 * n1 + tn2[k] < Kz) *dst = v[n1];
+                    dst += zstep;
+                }
+            }
         }
         u = un;
-        i = in;
+        oy = oyn;
+        xt = xtn;
+        row = rown;
+        r = rn;
+        base = basen;
         if (NBUF == 1) __syncthreads();   // the next tile's L1 rewrites T
     }
 }
