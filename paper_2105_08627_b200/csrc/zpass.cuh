@@ -16,7 +16,8 @@
 //   L1 inverse:              R1-point inverse FFT over k1 -> z = n2 + R2 n1, the kept z < Kz are
 //                            stored straight to HBM.
 // L1 needs no twiddles (compile-time constants); L2's R2-1 twiddles are per-thread constants.
-// Two barriers per tile; T is double-buffered so the next tile's L1 overlaps nothing it reads.
+// Two barriers per tile: a thread's forward L1 of the next tile rewrites only the T pencils its own
+// inverse L1 has just read, so one T buffer needs no third barrier.
 #pragma once
 #include "fft.cuh"
 #include "tma.cuh"
@@ -55,7 +56,7 @@ struct ZPlan {
     }
 };
 
-// NBUF = 2: T double-buffered (two barriers per tile); 1: single buffer (three barriers).
+// NBUF = 2: T double-buffered; 1: single buffer (two barriers per tile either way).
 // DM = 0: dense octant spectra; 16 / 32: Tucker factors, ranks <= DM (zero-padded on chip).
 template <int N, int R2, int Q, int NT, int NBUF, int DM>
 __global__ void __launch_bounds__(NT, 1)
@@ -344,7 +345,8 @@ __global__ void __launch_bounds__(NT, 1)
         row = rown;
         r = rn;
         base = basen;
-        if (NBUF == 1) __syncthreads();   // the next tile's L1 rewrites T
+        // no barrier here even with one T buffer: the next tile's forward L1 writes, task by task,
+        // exactly the T pencils (c, n2, q) this thread has just read in the inverse L1
     }
 }
 
