@@ -500,7 +500,11 @@ int grid_for(F* kern, int nt, size_t smem, int64_t units) {
     if (ctas == 0) {
         SVH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                       (int)cudaSharedmemCarveoutMaxShared));
-        SVH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        // the attribute is sticky per kernel: never lower it below a size cached earlier
+        size_t top = smem;
+        for (const auto& r : cache)
+            if (r.dev == dev && r.k == (const void*)kern) top = std::max(top, r.smem);
+        SVH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)top));
         int nsm = 148, occ = 1;
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, smem);

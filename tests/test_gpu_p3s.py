@@ -144,3 +144,13 @@ def test_p3s_rejects_ineligible(svh_lib, shape, tucker):
         I = torch.zeros((1, 5, h.K), dtype=torch.complex64, device="cuda")
         h.matvec(I)
         assert h.matvec_plan()[0] == 5
+
+
+def test_p3s_shared_memory_attribute_is_not_lowered(svh_lib):
+    """One k_p3_yz instantiation (Nx 128, Ny 512, Nz 8) run with 4, then 3, then 4 non-empty
+    planes in one process: its slab is 82 KB, 61 KB, 82 KB of dynamic shared memory.  The
+    opt-in size attribute is sticky per kernel, so the cached launch set-up must never lower it
+    (the third product would fail to launch)."""
+    for kz, seed in ((4, 1), (3, 2), (4, 3)):
+        case = svh_inputs.random_fill((64, 200, kz), fill=0.5, seed=700 + kz, n_mat=2)
+        _check(svh_lib, case, 1, seed)
